@@ -1,0 +1,280 @@
+"""Pins for the CPU oracle (oracle/btree_oracle.c) against what the paper and
+the mathematics fix -- not against the oracle itself.
+
+Each test names the passage (P:n = PAPER.md line n) or the closed form it
+checks.  CPU only; the whole file runs in well under a minute.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_1910_02639_b200 import datagen
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                   "paper_worked_examples.json")))
+
+
+# ---- Eq. 2 / Eq. 3 worked example --------------------------------
+def test_eq2_eq3_worked_example(oracle):
+    g = GOLD["eq2_eq3_worked_example"]
+    c = [oracle.cell_coord(x, g["lo"], g["hi"], g["b"]) for x in g["x"]]
+    assert c == g["coords"]
+    assert oracle.cell_id(*c, g["b"]) == g["j"]
+    assert g["b"] ** 3 == g["ncells"]
+
+
+def test_eq2_clamps_and_faces(oracle):
+    # x at the min face -> 0; x at the max face maps to b and is clamped to b-1 (R8)
+    assert oracle.cell_coord(0.0, 0.0, 5.0, 10) == 0
+    assert oracle.cell_coord(5.0, 0.0, 5.0, 10) == 9
+    assert oracle.cell_coord(-1.0, 0.0, 5.0, 10) == 0
+    assert oracle.cell_coord(7.0, 0.0, 5.0, 10) == 9
+    # monotone in x on a fine sweep straddling every face (lemma L2)
+    xs = np.linspace(-0.1, 5.1, 20001)
+    cs = [oracle.cell_coord(float(x), 0.0, 5.0, 7) for x in xs]
+    assert all(a <= b for a, b in zip(cs, cs[1:]))
+    assert set(cs) == set(range(7))
+    # zero-extent box (degenerate axis): still monotone, NaN (0/0) -> 0
+    assert oracle.cell_coord(1.0, 1.0, 1.0, 4) == 0
+    assert oracle.cell_coord(0.5, 1.0, 1.0, 4) == 0
+    assert oracle.cell_coord(1.5, 1.0, 1.0, 4) == 3
+
+
+def test_eq3_corners(oracle):
+    for b in (2, 3, 10, 81):
+        assert oracle.cell_id(0, 0, 0, b) == 0
+        assert oracle.cell_id(b - 1, b - 1, b - 1, b) == b ** 3 - 1
+        assert oracle.cell_id(1, 0, 0, b) == 1
+        assert oracle.cell_id(0, 1, 0, b) == b
+        assert oracle.cell_id(0, 0, 1, b) == b * b
+
+
+# ---- Eq. 1 ------------------------------------------------------
+def test_eq1_branching_factor(oracle):
+    for n, s, b in GOLD["eq1_examples"]["cases"]:
+        assert oracle.branching_factor(n, s) == b, (n, s)
+
+
+def test_eq1_is_smallest_integer_root(oracle):
+    rng = np.random.default_rng(7)
+    for _ in range(2000):
+        s = int(rng.integers(1, 200))
+        n = int(rng.integers(s + 1, 10 ** 7))
+        b = oracle.branching_factor(n, s)
+        assert b >= 2
+        assert b ** 3 * s >= n
+        assert b == 2 or (b - 1) ** 3 * s < n
+
+
+# ---- Eq. 4 ------------------------------------------------------
+def test_eq4_ratio(oracle):
+    for c in GOLD["eq4_examples"]["cases"]:
+        assert oracle.ratio(c["counts"], c["alpha"], c["s"]) == c["r"]
+
+
+# ---- Eq. 5 / Fig. 1 ----------------------------------
+def test_eq5_fig1_range(oracle):
+    g = GOLD["fig1_search_range"]
+    rx = oracle.search_range(g["x"][0], g["R"], g["lo"], g["hi"], g["b"])
+    ry = oracle.search_range(g["x"][1], g["R"], g["lo"], g["hi"], g["b"])
+    assert list(rx) == g["range_x"]
+    assert list(ry) == g["range_y"]
+    # radius >= box side -> whole range; tiny radius at a cell centre -> one cell
+    assert oracle.search_range(3.0, 10.0, 0.0, 6.0, 6) == (0, 5)
+    assert oracle.search_range(2.5, 0.1, 0.0, 6.0, 6) == (2, 2)
+
+
+# ---- root box (reading R9) ---------------------------------------
+def test_root_box_strictly_contains(oracle):
+    pos = np.array([[0.0, 0.0, 0.0], [1.0, 1.0, 1.0]])
+    lo, hi = oracle.root_box(pos)
+    assert np.all(lo < 0.0) and np.all(hi > 1.0)
+    assert np.allclose(lo, -1e-9, rtol=1e-6) and np.allclose(hi, 1 + 1e-9, rtol=1e-12)
+    lo, hi = oracle.root_box(np.zeros((1, 3)))
+    assert np.all(hi - lo >= 2e-12)
+
+
+# ---- predicate and closed forms ---------------------------------------------
+def test_boundary_is_strict(oracle):
+    pos = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    h = np.array([0.5, 0.5])  # d^2 = 1 = (2h)^2 -> not neighbors (strict <)
+    for counts in (oracle.brute_force(pos, h)[0], oracle.Tree(pos, 1).count(h)):
+        assert list(counts) == [0, 0]
+    h = np.array([np.nextafter(0.5, 1.0), 0.5])  # (2h)^2 = 1 + 2^-51 > 1
+    for counts in (oracle.brute_force(pos, h)[0], oracle.Tree(pos, 1).count(h)):
+        assert list(counts) == [1, 0]  # gather: asymmetric for unequal h (R13)
+
+
+def _lattice_expected(m, r2max):
+    """Exact neighbor count of every point of an integer m^3 lattice for the
+    criterion |d|^2 <= r2max (integers), by enumerating integer offsets."""
+    offs = [(a, b, c) for a in range(-3, 4) for b in range(-3, 4) for c in range(-3, 4)
+            if 0 < a * a + b * b + c * c <= r2max]
+    idx = np.arange(m)
+    gx, gy, gz = np.meshgrid(idx, idx, idx, indexing="ij")
+    P = np.stack([gx.ravel(), gy.ravel(), gz.ravel()], axis=1)
+    cnt = np.zeros(len(P), dtype=np.int64)
+    for a, b, c in offs:
+        q = P + np.array([a, b, c])
+        cnt += np.all((q >= 0) & (q < m), axis=1)
+    return cnt
+
+
+@pytest.mark.parametrize("two_h,r2max,interior", [(2.5, 6, 80), (1.01, 1, 6), (1.9, 3, 26)])
+def test_lattice_closed_form(oracle, two_h, r2max, interior):
+    m = 9
+    pos = datagen.lattice(m, 1.0)
+    h = np.full(len(pos), two_h / 2)
+    exp = _lattice_expected(m, r2max)
+    bf = oracle.brute_force(pos, h)[0]
+    assert np.array_equal(bf, exp)
+    for s in (1, 8, 64):
+        assert np.array_equal(oracle.Tree(pos, s).count(h), exp)
+    centre = (m // 2) * (m * m + m + 1)
+    assert exp[centre] == interior
+
+
+def test_brute_force_vs_scipy_ckdtree(oracle):
+    """Independent library arithmetic: scipy's cKDTree (<= with its own
+    arithmetic).  Sets agree except pairs within a relative band 1e-12 of
+    the threshold, which we exclude from the comparison."""
+    cKDTree = pytest.importorskip("scipy.spatial").cKDTree
+    for seed, hh in ((1, (0.03, 0.08)), (2, (0.05, 0.05))):
+        pos, h = datagen.uniform(3000, seed, *hh)
+        c, off, idx = oracle.brute_force(pos, h)
+        kd = cKDTree(pos)
+        for i in range(0, 3000, 7):
+            mine = set(idx[off[i]:off[i + 1]].tolist())
+            theirs = set(kd.query_ball_point(pos[i], 2 * h[i])) - {i}
+            for j in mine ^ theirs:
+                d2 = float(np.sum((pos[i] - pos[j]) ** 2))
+                assert abs(d2 - (2 * h[i]) ** 2) <= 1e-12 * (2 * h[i]) ** 2, (i, j)
+
+
+# ---- tree walk vs brute force ----------------------------------------------
+def _assert_same(a, b):
+    ca, oa, ia = a
+    cb, ob, ib = b
+    assert np.array_equal(ca, cb)
+    assert np.array_equal(oa, ob)
+    assert np.array_equal(ia, ib)
+
+
+@pytest.mark.parametrize("case", ["uniform", "varh", "clustered", "boundary", "lattice"])
+def test_tree_walk_equals_brute_force(oracle, case):
+    if case == "uniform":
+        pos, h = datagen.uniform(4000, 11, 0.04)
+    elif case == "varh":
+        pos, h = datagen.uniform(4000, 12, 0.01, 0.08)
+    elif case == "clustered":
+        pos, h = datagen.clustered(5000, 13, h=0.01)
+    elif case == "boundary":
+        pos, h = datagen.near_boundary(64, 64, 14)
+    else:
+        pos = datagen.lattice(12, 0.01, 0.005)
+        h = np.full(len(pos), 0.015)
+    ref = oracle.brute_force(pos, h)
+    for s, beta in ((64, 0.5), (8, 0.5), (1, 0.1), (2, 1.0)):
+        _assert_same(oracle.Tree(pos, s, beta).neighbors(h), ref)
+
+
+def test_invariance_over_s_beta_alpha(oracle):
+    pos, h = datagen.clustered(6000, 21, h=0.015)
+    ref = oracle.Tree(pos, 64).neighbors(h)
+    for s in (1, 2, 8, 64, 4096):
+        for beta in (0.1, 0.5, 1.0):
+            for alpha in (0.0, 0.5):
+                _assert_same(oracle.Tree(pos, s, beta, alpha).neighbors(h), ref)
+
+
+def test_symmetry_constant_h_and_self_excluded(oracle):
+    pos, h = datagen.uniform(3000, 31, 0.05)
+    c, off, idx = oracle.Tree(pos, 16).neighbors(h)
+    rows = np.repeat(np.arange(len(pos)), c)
+    assert not np.any(rows == idx)
+    pairs = set(zip(rows.tolist(), idx.tolist()))
+    assert all((j, i) in pairs for i, j in pairs)
+    assert c.sum() == off[-1] == idx.size
+
+
+def test_permutation_invariance_and_monotone_h(oracle):
+    pos, h = datagen.clustered(4000, 41, h=0.02)
+    c, off, idx = oracle.Tree(pos, 32).neighbors(h)
+    rng = np.random.default_rng(5)
+    p = rng.permutation(len(pos))
+    c2, off2, idx2 = oracle.Tree(pos[p], 32).neighbors(h[p])
+    inv = np.argsort(p)
+    for i in range(0, len(pos), 13):
+        k = inv[i]
+        mapped = np.sort(p[idx2[off2[k]:off2[k + 1]]])
+        assert np.array_equal(mapped, idx[off[i]:off[i + 1]])
+    cbig = oracle.Tree(pos, 32).count(h * 1.1)
+    assert np.all(cbig >= c)
+
+
+# ---- build structure (Alg. 1, Table II best case) --
+def test_partition_and_bucket_bound(oracle):
+    pos, h = datagen.clustered(20000, 51, h=0.01)
+    for s in (1, 8, 64):
+        t = oracle.Tree(pos, s)
+        perm, lb, lc, ld = t.order()
+        assert np.array_equal(np.sort(perm), np.arange(len(pos)))
+        assert lc.sum() == len(pos)
+        assert np.all(lc >= 1) and np.all(lc <= s)
+        assert np.array_equal(lb[1:], np.cumsum(lc)[:-1])
+        for b0, c in zip(lb[:200], lc[:200]):  # leaves keep ascending original index
+            seg = perm[b0:b0 + c]
+            assert np.all(np.diff(seg) > 0)
+        st = t.stats()
+        assert st["leaves"] == len(lc) and st["overfull"] == 0
+
+
+@pytest.mark.parametrize("m", [4, 8, 16])
+def test_even_lattice_best_case_depth_one(oracle, m):
+    t = oracle.Tree(datagen.lattice(m, 1.0), 8)
+    st = t.stats()
+    assert st["depth"] == 1 and st["halvings"] == 0 and st["nodes"] == 1
+    assert st["root_b"] == m // 2 and st["leaves"] == (m // 2) ** 3
+    _, _, lc, _ = t.order()
+    assert np.all(lc == 8)
+
+
+def test_single_leaf_and_empty(oracle):
+    pos, _ = datagen.uniform(50, 61, 0.1)
+    st = oracle.Tree(pos, 64).stats()
+    assert st["depth"] == 0 and st["leaves"] == 1 and st["nodes"] == 0
+    st = oracle.Tree(np.zeros((0, 3)), 64).stats()
+    assert st["leaves"] == 0
+
+
+def test_coincident_points_depth_cap(oracle):
+    s = 8
+    pos = np.tile(np.array([[0.25, 0.5, 0.75]]), (s + 1, 1))
+    pos = np.concatenate([pos, [[0.0, 0.0, 0.0], [1.0, 1.0, 1.0]]])
+    h = np.full(len(pos), 0.01)
+    t = oracle.Tree(pos, s, depth_cap=64)
+    st = t.stats()
+    assert st["overfull"] == 1 and st["max_leaf"] == s + 1 and st["depth"] == 64
+    c = t.count(h)
+    assert list(c[: s + 1]) == [s] * (s + 1) and list(c[s + 1:]) == [0, 0]
+
+
+def test_halving_hand_derived(oracle):
+    """1000 points in [0,0.1)^3 plus one at (1,1,1), s=8, beta=0.5:
+    Eq. 1 gives b=6 (5^3 < 126 <= 6^3); r = 215/216 >= 0.5 -> b=3;
+    r = 26/27 -> b = max(2, 1) = 2; at b=2 the loop stops (octree limit)."""
+    rng = np.random.default_rng(3)
+    pos = np.concatenate([rng.random((1000, 3)) * 0.1, [[1.0, 1.0, 1.0]]])
+    t = oracle.Tree(pos, 8, 0.5)
+    st = t.stats()
+    assert st["root_b"] == 2
+    # with beta = 1.0 the ratio never reaches beta (r < 1): b stays 6
+    assert oracle.Tree(pos, 8, 1.0).stats()["root_b"] == 6
+
+
+def test_uniform_root_needs_no_halving(oracle):
+    pos, _ = datagen.uniform(20000, 71, 0.01)
+    st = oracle.Tree(pos, 64).stats()
+    assert st["root_b"] == oracle.branching_factor(20000, 64) == 7
