@@ -1,0 +1,180 @@
+/*
+ * btree.h -- C ABI of the B200-native b-tree exact close-neighbor search.
+ *
+ * The method is the b-tree of Cavelan, Cabezon, Korndorfer, Ciorba,
+ * "Finding Neighbors in a Forest: A b-tree for Smoothed Particle Hydrodynamics
+ * Simulations" (arXiv 1910.02639).  P:n below is line n of that paper's text
+ * with the section / equation / algorithm it falls in.
+ *
+ * Result computed (the plain definition, BASELINE.json north_star):
+ *   N(i) = { j in [0,n), j != i :
+ *            ((dx*dx + dy*dy) + dz*dz) < (2 h_i) * (2 h_i) }
+ *   dx = x_i - x_j (likewise y, z), IEEE-754 binary64, round-to-nearest-even,
+ *   each operation rounded separately (no FMA), left to right.  This is the
+ *   paper's "all particles that are within the 2h radius" (Sec. III-B,
+ *   P:266-280) with the gather radius of the query (Alg. 2 uses h_p),
+ *   strict inequality (reading R1 in DESIGN.md) and self excluded (R12).
+ *   The set is a function of the inputs alone: it does not depend on the tree,
+ *   bucket_size, max_empty or alpha.
+ *
+ * Conventions for every entry point
+ *   - Device pointers are CUDA global-memory pointers of the current device
+ *     (e.g. torch CUDA tensors' data_ptr()); host pointers are plain memory.
+ *   - All work is enqueued on the calling thread's stream (bt_set_stream;
+ *     default: the per-thread default stream) and the call returns after the
+ *     work has completed (it synchronises that stream).
+ *   - Inputs and outputs are in CALLER order: particle i is row i of pos/h.
+ *   - Return codes: BT_OK or one of bt_status; constructors return NULL on
+ *     failure.  The message of the last failure on this thread is in
+ *     bt_last_error(), its code in bt_last_status().  No C++ exception crosses
+ *     this boundary.
+ *   - A bt_tree may be used by one thread at a time (it owns scratch memory).
+ */
+#ifndef BTREE_H
+#define BTREE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bt_tree bt_tree; /* opaque, library-owned */
+
+typedef enum bt_status {
+    BT_OK = 0,
+    BT_ERR_ARG = 1,      /* invalid argument (NULL pointer, range, size)        */
+    BT_ERR_INPUT = 2,    /* invalid data (non-finite or |coordinate| > 1e150,
+                            h not finite or h <= 0)                              */
+    BT_ERR_CAPACITY = 3, /* neighbor output does not fit the given capacity      */
+    BT_ERR_CUDA = 4,     /* CUDA runtime / launch failure                        */
+    BT_ERR_OOM = 5       /* device memory exhausted                              */
+} bt_status;
+
+/*
+ * bt_build -- BuildTree (Alg. 1; Eq. 1-4) on the device.
+ *
+ *   pos          DEVICE, n*3 fp64, AoS x,y,z per particle, caller-owned,
+ *                read-only; finite with |coordinate| <= 1e150.  The tree keeps
+ *                its own copy (records in depth-first leaf order, Sec. IV-E
+ *                P:491), so pos may be freed after the call.
+ *   n            0 <= n <= 2^31 - 1.  n == 0 gives a valid empty tree.
+ *   bucket_size  s >= 1: maximum particles per leaf (Table I).
+ *   max_empty    beta in (0, 1]: a node's branching factor b is halved while
+ *                the ratio r of sub-cells holding <= alpha*s particles is
+ *                >= beta and b > 2 (Eq. 4 + Step 3; readings R3, R4,
+ *                R7).  alpha = 0.5 (Table IV; reading R10).
+ *
+ * The root box is the data's bounding box, each side expanded by
+ * max(1e-9 * extent, 1e-12) (reading R9).  Nodes at depth 64 become leaves
+ * even when they hold more than s particles (coincident points, R14).
+ * Returns NULL on failure (BT_ERR_ARG / BT_ERR_INPUT / BT_ERR_CUDA / BT_ERR_OOM).
+ */
+bt_tree *bt_build(const double *pos, int64_t n, int32_t bucket_size, double max_empty);
+
+/* bt_build with alpha in [0, 1] (Table I) and the depth cap (>= 0). */
+bt_tree *bt_build_ex(const double *pos, int64_t n, int32_t bucket_size, double max_empty,
+                     double alpha, int32_t depth_cap);
+
+/*
+ * bt_find_neighbors -- FindNeighbors (Alg. 2; Eq. 5)
+ * for every particle of the tree, count-then-fill CSR output.
+ *
+ *   t        tree from bt_build (the particles whose neighbors are searched
+ *            and the candidate set are the same n particles).
+ *   h        DEVICE, n fp64 smoothing lengths in caller order, finite, > 0.
+ *   ngmax    >= 1; nbr_idx has capacity n * ngmax entries.  A capacity, not a
+ *            truncation: counts are exact and never clamped (reading R17).
+ *   counts   DEVICE out, n int32: counts[i] = |N(i)|.
+ *   offsets  DEVICE out, n+1 int64: exclusive scan of counts, offsets[n] = total.
+ *   nbr_idx  DEVICE out, int32, capacity n*ngmax, or NULL for a count-only call.
+ *            Row i = nbr_idx[offsets[i] .. offsets[i+1]) holds the caller
+ *            indices j of N(i) in unspecified order.
+ *
+ * Returns BT_OK; BT_ERR_ARG (NULL t/h/counts/offsets with n > 0, ngmax < 1);
+ * BT_ERR_INPUT (bad h; outputs undefined); BT_ERR_CAPACITY when
+ * offsets[n] > n*ngmax: counts and offsets are valid, nbr_idx is untouched,
+ * and the caller may retry with bt_fill_neighbors and a larger buffer.
+ */
+int bt_find_neighbors(const bt_tree *t, const double *h, int32_t ngmax, int32_t *counts,
+                      int64_t *offsets, int32_t *nbr_idx);
+
+/*
+ * bt_fill_neighbors -- the fill pass alone, using offsets from a previous
+ * bt_find_neighbors call on the same tree and the same h (e.g. count-only,
+ * then an exactly sized buffer).  capacity = number of int32 slots of nbr_idx;
+ * BT_ERR_CAPACITY if offsets[n] > capacity (nothing written).
+ */
+int bt_fill_neighbors(const bt_tree *t, const double *h, const int64_t *offsets,
+                      int32_t *nbr_idx, int64_t capacity);
+
+/* Frees all tree-owned device memory.  NULL-safe. */
+void bt_free(bt_tree *t);
+
+/*
+ * bt_search_host -- end-to-end convenience call on HOST buffers: copies pos
+ * and h to the device, builds, counts, scans and fills, and copies counts,
+ * offsets and the neighbor lists back.  Host buffers should be pinned
+ * (cudaHostAlloc / torch pin_memory) for full PCIe bandwidth.
+ *   pos_h [n*3] fp64, h_h [n] fp64, counts_h [n] int32, offsets_h [n+1] int64,
+ *   nbr_h [capacity] int32.  BT_ERR_CAPACITY if the total exceeds capacity
+ *   (counts_h and offsets_h are then valid, nbr_h untouched).
+ */
+int bt_search_host(const double *pos_h, const double *h_h, int64_t n, int32_t bucket_size,
+                   double max_empty, int32_t *counts_h, int64_t *offsets_h, int32_t *nbr_h,
+                   int64_t capacity);
+
+/* Stream for this thread's subsequent calls (a cudaStream_t; NULL = default). */
+int bt_set_stream(void *cuda_stream);
+
+const char *bt_last_error(void);
+int bt_last_status(void);
+
+typedef struct bt_stats {
+    int64_t n;
+    int64_t nodes;        /* internal nodes                                   */
+    int64_t leaves;
+    int64_t halvings;     /* total b-halving rounds over all nodes (Eq. 4)    */
+    int64_t overfull;     /* leaves with more than s particles (depth cap)    */
+    int64_t max_leaf;
+    int32_t depth;        /* leaf depth maximum; a root leaf has depth 0      */
+    int32_t root_b;       /* accepted branching factor of the root (0: leaf)  */
+    int64_t units;        /* walk work units (<= 64 queries of one leaf)      */
+    double box_lo[3], box_hi[3];
+    /* last bt_find_neighbors on this tree */
+    int64_t total_pairs;
+    int64_t max_count;
+    int64_t staged;       /* candidate records staged by the count pass       */
+    int64_t tests;        /* pair tests issued by the count pass              */
+    int64_t exact_tests;  /* pairs decided by the fp64 predicate itself       */
+} bt_stats;
+
+int bt_tree_stats(const bt_tree *t, bt_stats *out);
+
+/*
+ * bt_tree_order -- export the tree (DEVICE outputs, any may be NULL):
+ *   perm[n]         caller index of the particle at each tree-order position
+ *                   (depth-first leaf order, children in ascending sub-cell id j,
+ *                   ascending caller index inside a leaf: Sec. IV-E);
+ *   leaf_begin[L]   first tree-order position of each leaf (depth-first order);
+ *   leaf_count[L]   particles in the leaf;
+ *   leaf_depth[L]   depth of the leaf.
+ * L = bt_stats.leaves.
+ */
+int bt_tree_order(const bt_tree *t, int32_t *perm, int64_t *leaf_begin, int32_t *leaf_count,
+                  int32_t *leaf_depth);
+
+/*
+ * Profiling: when enabled, every kernel phase is bracketed with CUDA events on
+ * the library's stream and its time accumulated (ms).  bt_profile_get fills
+ * names/values; returns the number of entries.  Launch counts are always kept.
+ */
+int bt_profile_enable(int on);
+int bt_profile_reset(void);
+int bt_profile_get(int max_entries, const char **names, double *ms, int64_t *launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BTREE_H */

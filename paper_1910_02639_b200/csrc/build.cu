@@ -1,0 +1,623 @@
+// build.cu -- BuildTree (Alg. 1) as level-synchronous device kernels.
+//
+// All nodes of one depth are processed together ("level").  For a level:
+//   A2  Eq. 1 per node: b0 = smallest b >= 2 with b^3 s >= n_i   (level_b)
+//   A3  Eq. 2 + Eq. 3 key per active particle, A4 histogram       (key_hist)
+//   A5  Eq. 4 ratio, halve b while r >= beta and b > 2; redo A3/A4 for the
+//       halved nodes only                                         (under_count, ratio_decide)
+//   A6  one scan over the level's cells -> in-node offsets, child node ids,
+//       next-level positions, leaf ids                            (device_scan)
+//   A8  emit child nodes (equal 1/b slices of the parent box), leaves and the
+//       cell table                                                (emit)
+//   A7  counting-sort scatter of the particle records: leaf cells go to their
+//       final tree-order position, child-node cells to the next level's
+//       active array                                              (scatter)
+// After the last level: A9 per leaf, sort by caller index (canonical order,
+// SPEC S:180), tight bounding box; work units of <= 64 queries.
+//
+// The tree order is the paper's depth-first walk order (Sec. IV-E):
+// a node's particles occupy one contiguous range, its sub-cells follow in
+// ascending j, recursively.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace bt {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+struct LevelNode {
+    int32_t act_begin;   // first active particle of this node (level array)
+    int32_t count;       // n_i
+    int32_t final_begin; // first tree-order position of the node's range
+    int32_t gid;         // global node id (NodeRec index)
+    int32_t b0;          // Eq. 1
+    int32_t b;           // current / accepted branching factor
+    int32_t flag;        // (re)distribute in this round
+    int32_t halvings;
+    int64_t cell_base;   // level-local first cell
+    int64_t under;       // #{j < b^3 : n_j <= alpha s}   (Eq. 4 numerator)
+};
+
+struct CellScan {  // per-cell values scanned in one pass (A6)
+    long long pre;     // particles before this cell (level-wide)
+    long long actoff;  // particles of child-node cells before this cell
+    int nnode;         // child-node cells before this cell
+    int nleaf;         // leaf cells before this cell
+    __host__ __device__ CellScan operator+(const CellScan &o) const {
+        return CellScan{pre + o.pre, actoff + o.actoff, nnode + o.nnode, nleaf + o.nleaf};
+    }
+};
+
+// ---- A1: records + bounding box -------------------------------------------
+__global__ void __launch_bounds__(kThreads) pack_bbox_kernel(const double *__restrict__ pos, int64_t n,
+                                                             double4 *__restrict__ rec, double *partials,
+                                                             int *bad) {
+    double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    int badv = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+        // finite and |x| <= 1e150 (keeps squared distances finite)
+        if (!(fabs(x) <= 1e150) || !(fabs(y) <= 1e150) || !(fabs(z) <= 1e150)) badv = 1;
+        rec[i] = make_double4(x, y, z, __longlong_as_double((long long)i));
+        mn[0] = fmin(mn[0], x); mn[1] = fmin(mn[1], y); mn[2] = fmin(mn[2], z);
+        mx[0] = fmax(mx[0], x); mx[1] = fmax(mx[1], y); mx[2] = fmax(mx[2], z);
+    }
+    if (badv) atomicOr(bad, 1);
+    __shared__ double sh[6][kThreads / 32];
+    int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int l = 0; l < 3; l++) {
+        double a = mn[l], b = mx[l];
+        for (int d = 16; d; d >>= 1) {
+            a = fmin(a, __shfl_xor_sync(0xffffffffu, a, d));
+            b = fmax(b, __shfl_xor_sync(0xffffffffu, b, d));
+        }
+        if (lane == 0) { sh[l][wid] = a; sh[3 + l][wid] = b; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        int l = threadIdx.x;
+        double a = INFINITY, b = -INFINITY;
+        for (int w = 0; w < kThreads / 32; w++) { a = fmin(a, sh[l][w]); b = fmax(b, sh[3 + l][w]); }
+        partials[6 * blockIdx.x + l] = a;
+        partials[6 * blockIdx.x + 3 + l] = b;
+    }
+}
+
+// Root box: exact min/max, each side expanded by max(1e-9 * extent, 1e-12)
+// (reading R9).  Writes the root NodeRec lo/ext and box[0..6], M.
+__global__ void root_box_kernel(const double *partials, int nblocks, NodeRec *root, double *box) {
+    if (threadIdx.x != 0) return;
+    double M = 0.0;
+    for (int l = 0; l < 3; l++) {
+        double a = INFINITY, b = -INFINITY;
+        for (int k = 0; k < nblocks; k++) { a = fmin(a, partials[6 * k + l]); b = fmax(b, partials[6 * k + 3 + l]); }
+        double pad = __dmul_rn(1e-9, __dsub_rn(b, a));
+        if (pad < 1e-12) pad = 1e-12;
+        double lo = __dsub_rn(a, pad), hi = __dadd_rn(b, pad);
+        box[l] = lo;
+        box[3 + l] = hi;
+        root->lo[l] = lo;
+        root->ext[l] = __dsub_rn(hi, lo);
+        M = fmax(M, fmax(fabs(lo), fabs(hi)));
+    }
+    box[6] = M;
+    root->depth = 0;
+    root->b = 0;
+    root->cell_base = 0;
+}
+
+__global__ void copy_rec_kernel(const double4 *__restrict__ src, double4 *__restrict__ dst, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// ---- A2: Eq. 1 --------------------------------------------------------------
+__device__ __forceinline__ int eq1_branching(int64_t n, int64_t s) {
+    int64_t m = (n + s - 1) / s;  // b^3 s >= n  <=>  b^3 >= ceil(n/s)   (R6)
+    int64_t b = (int64_t)cbrt((double)m);
+    if (b < 2) b = 2;
+    while (b > 2 && (b - 1) * (b - 1) * (b - 1) >= m) b--;
+    while (b * b * b < m) b++;
+    return (int)b;
+}
+
+__global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+    int b = eq1_branching(ln[i].count, s);
+    ln[i].b0 = b;
+    ln[i].b = b;
+    ln[i].flag = 1;
+    ln[i].halvings = 0;
+    ln[i].under = 0;
+}
+
+__device__ __forceinline__ int64_t find_node(const LevelNode *ln, int64_t nn, int64_t g) {
+    int64_t a = 0, z = nn - 1;  // largest i with cell_base <= g
+    while (a < z) {
+        int64_t m = (a + z + 1) >> 1;
+        if (ln[m].cell_base <= g) a = m; else z = m - 1;
+    }
+    return a;
+}
+
+// ---- A3 + A4: Eq. 2, Eq. 3, histogram ---------------------------------------
+__global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__restrict__ act, const int32_t *__restrict__ act_node,
+                                                            int64_t n_act, const LevelNode *__restrict__ ln,
+                                                            const NodeRec *__restrict__ nodes, uint32_t *__restrict__ keys,
+                                                            int32_t *__restrict__ hist, int round) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_act; p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t node = act_node[p];
+        const LevelNode &L = ln[node];
+        if (round > 0 && !L.flag) continue;
+        const NodeRec &nr = nodes[L.gid];
+        double4 r = act[p];
+        int b = L.b;
+        int c1 = cell_coord(r.x, nr.lo[0], nr.ext[0], b);
+        int c2 = cell_coord(r.y, nr.lo[1], nr.ext[1], b);
+        int c3 = cell_coord(r.z, nr.lo[2], nr.ext[2], b);
+        uint32_t j = (uint32_t)c1 + (uint32_t)c2 * (uint32_t)b + (uint32_t)c3 * (uint32_t)b * (uint32_t)b;
+        keys[p] = j;
+        atomicAdd(&hist[L.cell_base + j], 1);
+    }
+}
+
+// zero the histogram of nodes that redistribute in this round
+__global__ void zero_flagged_kernel(const LevelNode *__restrict__ ln, int64_t nn, int32_t *hist, int64_t ncells) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ncells; g += (int64_t)gridDim.x * blockDim.x) {
+        int64_t node = find_node(ln, nn, g);
+        if (ln[node].flag) hist[g] = 0;
+    }
+}
+
+// ---- A5: Eq. 4 numerator -----------------------------------------------------
+// Warp-uniform loop: every lane runs the same iterations (full-mask ballots).
+__global__ void __launch_bounds__(kThreads) under_count_kernel(LevelNode *ln, int64_t nn, const int32_t *__restrict__ hist,
+                                                               int64_t ncells, double alpha_s) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ncells; base += stride) {
+        int64_t g = base + threadIdx.x;
+        bool under = false;
+        int64_t node = 0;
+        if (g < ncells) {
+            node = find_node(ln, nn, g);
+            const LevelNode &L = ln[node];
+            int64_t B = (int64_t)L.b * L.b * L.b;
+            under = L.flag && (g - L.cell_base) < B && (double)hist[g] <= alpha_s;
+        }
+        unsigned m = __ballot_sync(0xffffffffu, under);
+        if (under) {  // aggregate per node within the warp (warp-aggregated atomics)
+            unsigned same = __match_any_sync(m, (unsigned long long)node);
+            int leader = __ffs(same) - 1;
+            if ((int)(threadIdx.x & 31) == leader)
+                atomicAdd((unsigned long long *)&ln[node].under, (unsigned long long)__popc(same));
+        }
+    }
+}
+
+// r = u / b^3 (Eq. 4); halve iff r >= beta and b > 2 (readings R3, R7)
+__global__ void ratio_decide_kernel(LevelNode *ln, int64_t nn, double beta, int *any) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+    LevelNode &L = ln[i];
+    if (!L.flag) return;
+    double B = (double)((int64_t)L.b * L.b * L.b);
+    double r = __ddiv_rn((double)L.under, B);
+    if (r >= beta && L.b > 2) {
+        L.b = max(2, L.b / 2);
+        L.halvings++;
+        L.under = 0;
+        L.flag = 1;
+        atomicOr(any, 1);
+    } else {
+        L.flag = 0;
+    }
+}
+
+// ---- A6 scan functors ------------------------------------------------------
+struct CellIn {
+    const int32_t *hist;
+    int32_t s;
+    bool child_ok;  // depth + 1 < depth_cap
+    __device__ CellScan operator()(int64_t g) const {
+        long long c = hist[g];
+        bool is_node = child_ok && c > s;
+        bool is_leaf = c > 0 && !is_node;
+        return CellScan{c, is_node ? c : 0, is_node ? 1 : 0, is_leaf ? 1 : 0};
+    }
+};
+struct CellOut {
+    int64_t *cpre;
+    int32_t *cid;
+    int32_t *cact;
+    __device__ void operator()(int64_t g, const CellScan &exc, const CellScan &v) const {
+        cpre[g] = exc.pre;
+        cid[g] = v.nnode ? exc.nnode : (v.nleaf ? exc.nleaf : -1);
+        cact[g] = (int32_t)exc.actoff;
+    }
+};
+struct CellsOfNode {
+    const LevelNode *ln;
+    __device__ long long operator()(int64_t i) const { return (long long)ln[i].b0 * ln[i].b0 * ln[i].b0; }
+};
+struct CellBaseOut {
+    LevelNode *ln;
+    __device__ void operator()(int64_t i, long long exc, long long) const { ln[i].cell_base = exc; }
+};
+
+// ---- A8: children, leaves, cell table --------------------------------------
+__global__ void __launch_bounds__(kThreads) emit_kernel(const LevelNode *__restrict__ ln, int64_t nn, const int32_t *__restrict__ hist,
+                                                        int64_t ncells, const int64_t *__restrict__ cpre,
+                                                        const int32_t *__restrict__ cid, const int32_t *__restrict__ cact,
+                                                        NodeRec *nodes, int32_t *cells, int64_t cells_base,
+                                                        LevelNode *ln_next, int32_t next_gid_base, int32_t *leaf_begin,
+                                                        int32_t *leaf_count, int32_t *leaf_depth, int64_t leaf_base,
+                                                        int32_t child_depth, int32_t *cdst, int32_t s) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ncells; g += (int64_t)gridDim.x * blockDim.x) {
+        int64_t node = find_node(ln, nn, g);
+        const LevelNode &L = ln[node];
+        int32_t c = hist[g];
+        int32_t id = cid[g];
+        int64_t j = g - L.cell_base;
+        int32_t final_pos = L.final_begin + (int32_t)(cpre[g] - cpre[L.cell_base]);
+        int32_t code = -1;
+        if (id >= 0 && c > 0) {
+            // re-derived exactly as in CellIn: ln_next is null at the depth cap
+            bool is_node = (c > s) && (ln_next != nullptr);
+            if (is_node) {
+                int32_t gid = next_gid_base + id;
+                LevelNode &C = ln_next[id];
+                C.act_begin = cact[g];
+                C.count = c;
+                C.final_begin = final_pos;
+                C.gid = gid;
+                const NodeRec &P = nodes[L.gid];
+                NodeRec &R = nodes[gid];
+                int b = L.b;
+                int cc[3] = {(int)(j % b), (int)((j / b) % b), (int)(j / ((int64_t)b * b))};
+                for (int l = 0; l < 3; l++) {
+                    // child box = equal 1/b slice of the parent (Sec. III-A Step 1)
+                    double lo = __dadd_rn(P.lo[l], __ddiv_rn(__dmul_rn((double)cc[l], P.ext[l]), (double)b));
+                    double hi = __dadd_rn(P.lo[l], __ddiv_rn(__dmul_rn((double)(cc[l] + 1), P.ext[l]), (double)b));
+                    R.lo[l] = lo;
+                    R.ext[l] = __dsub_rn(hi, lo);
+                }
+                R.depth = child_depth;
+                R.b = 0;
+                R.cell_base = 0;
+                code = node_code(gid);
+                cdst[g] = cact[g];
+            } else {
+                int64_t leaf = leaf_base + id;
+                leaf_begin[leaf] = final_pos;
+                leaf_count[leaf] = c;
+                leaf_depth[leaf] = child_depth;
+                code = (int32_t)leaf;
+                cdst[g] = final_pos;
+            }
+        }
+        cells[cells_base + g] = code;
+    }
+}
+
+// accepted b and global cell base of this level's nodes
+__global__ void finalize_level_nodes_kernel(const LevelNode *ln, int64_t nn, NodeRec *nodes, int64_t cells_base,
+                                            unsigned long long *halvings) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nn) return;
+    NodeRec &R = nodes[ln[i].gid];
+    R.b = ln[i].b;
+    R.cell_base = cells_base + ln[i].cell_base;
+    if (ln[i].halvings) atomicAdd(halvings, (unsigned long long)ln[i].halvings);
+}
+
+// ---- A7: counting-sort scatter ------------------------------------------------
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__restrict__ act, const int32_t *__restrict__ act_node,
+                                                           int64_t n_act, const LevelNode *__restrict__ ln,
+                                                           const uint32_t *__restrict__ keys, int32_t *__restrict__ cursor,
+                                                           const int32_t *__restrict__ cells, int64_t cells_base,
+                                                           const int32_t *__restrict__ cdst, const int32_t *__restrict__ cid,
+                                                           double4 *__restrict__ out_final, double4 *__restrict__ act_next,
+                                                           int32_t *__restrict__ act_node_next) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_act; p += (int64_t)gridDim.x * blockDim.x) {
+        int32_t node = act_node[p];
+        int64_t g = ln[node].cell_base + keys[p];
+        int32_t r = atomicAdd(&cursor[g], 1);
+        int32_t code = cells[cells_base + g];
+        double4 v = act[p];
+        int32_t dst = cdst[g] + r;
+        if (code >= 0) {
+            out_final[dst] = v;
+        } else {
+            act_next[dst] = v;
+            act_node_next[dst] = cid[g];
+        }
+    }
+}
+
+// ---- A9: per-leaf canonical order (ascending caller index) + tight box -------
+// One warp per leaf.  rank(e) = #{k in leaf : idx_k < idx_e} (caller indices
+// are distinct), O(m^2 / 32) per leaf: m <= s = 64 in the configurations.
+__global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *__restrict__ src, double4 *__restrict__ dst,
+                                                                 const int32_t *__restrict__ leaf_begin,
+                                                                 const int32_t *__restrict__ leaf_count, int64_t n_leaves,
+                                                                 double *__restrict__ leaf_box,
+                                                                 unsigned long long *max_leaf, int32_t s) {
+    int lane = threadIdx.x & 31;
+    int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t L = warp; L < n_leaves; L += nwarps) {
+        int32_t b0 = leaf_begin[L], m = leaf_count[L];
+        double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int32_t e0 = 0; e0 < m; e0 += 32) {
+            int32_t e = e0 + lane;
+            double4 v = make_double4(0, 0, 0, 0);
+            long long my = 0x7fffffffffffffffLL;
+            if (e < m) {
+                v = src[b0 + e];
+                my = __double_as_longlong(v.w);
+                mn[0] = fmin(mn[0], v.x); mn[1] = fmin(mn[1], v.y); mn[2] = fmin(mn[2], v.z);
+                mx[0] = fmax(mx[0], v.x); mx[1] = fmax(mx[1], v.y); mx[2] = fmax(mx[2], v.z);
+            }
+            int32_t rank = 0;
+            for (int32_t k0 = 0; k0 < m; k0 += 32) {
+                long long o = 0x7fffffffffffffffLL;
+                if (k0 + lane < m) o = __double_as_longlong(src[b0 + k0 + lane].w);
+                int lim = min(32, m - k0);
+                for (int q = 0; q < lim; q++) {
+                    long long ok = __shfl_sync(0xffffffffu, o, q);
+                    rank += (ok < my);
+                }
+            }
+            if (e < m) dst[b0 + rank] = v;
+        }
+        for (int l = 0; l < 3; l++) {
+            double a = mn[l], b = mx[l];
+            for (int d = 16; d; d >>= 1) {
+                a = fmin(a, __shfl_xor_sync(0xffffffffu, a, d));
+                b = fmax(b, __shfl_xor_sync(0xffffffffu, b, d));
+            }
+            if (lane == 0) { leaf_box[6 * L + l] = a; leaf_box[6 * L + 3 + l] = b; }
+        }
+        if (lane == 0) {
+            atomicMax(max_leaf, (unsigned long long)m);
+            if (m > s) atomicAdd(max_leaf + 1, 1ull);  // over-full leaf (depth cap, R14)
+        }
+    }
+}
+
+constexpr int kUnitQ = 64;  // queries per walk work unit
+
+struct UnitsOfLeaf {
+    const int32_t *cnt;
+    __device__ long long operator()(int64_t L) const { return (cnt[L] + kUnitQ - 1) / kUnitQ; }
+};
+struct NullOut {
+    __device__ void operator()(int64_t, long long, long long) const {}
+};
+struct UnitsOut {
+    const int32_t *begin;
+    const int32_t *cnt;
+    int4 *units;
+    __device__ void operator()(int64_t L, long long exc, long long v) const {
+        for (long long u = 0; u < v; u++) {
+            int q0 = (int)(u * kUnitQ);
+            units[exc + u] = make_int4((int)L, begin[L] + q0, min(kUnitQ, cnt[L] - q0), 0);
+        }
+    }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Host driver (K12): level loop.  Reads back a few scalars per level (total
+// cells, any-halving flag per round, next-level totals).
+// ---------------------------------------------------------------------------
+void build_tree(TreeDev &t, const double *pos) {
+    const int64_t n = t.n;
+    cudaStream_t st = stream();
+    int64_t *hs = host_scratch().p;
+    t.n_nodes = t.n_cells = t.n_leaves = t.n_units = 0;
+    t.depth = 0;
+    t.root_b = 0;
+    t.halvings = t.overfull = t.max_leaf = 0;
+    t.root_is_leaf = true;
+    if (n == 0) {
+        t.M = 0;
+        for (int l = 0; l < 3; l++) t.box_lo[l] = t.box_hi[l] = 0;
+        return;
+    }
+    const int sms = num_sms();
+    const unsigned gridN = grid_for(n, kThreads, (int64_t)sms * 16);
+
+    DBuf<double4> act[2];
+    DBuf<int32_t> act_node[2];
+    DBuf<double4> fin(n);
+    t.rec.alloc(n);
+    DBuf<int> dflags(4);
+    DBuf<unsigned long long> dstat(4);  // halvings, max_leaf
+    BT_CUDA(cudaMemsetAsync(dflags.p, 0, 4 * sizeof(int), st));
+    BT_CUDA(cudaMemsetAsync(dstat.p, 0, 4 * sizeof(unsigned long long), st));
+
+    // A1: records in caller order + root box
+    DBuf<double> partials(6 * (size_t)gridN);
+    DBuf<double> dbox(8);
+    t.nodes.reserve(1024, 0);
+    {
+        Phase ph("build.bbox");
+        act[0].alloc(n);
+        pack_bbox_kernel<<<gridN, kThreads, 0, st>>>(pos, n, act[0].p, partials.p, dflags.p);
+        BT_LAUNCH("pack_bbox");
+        root_box_kernel<<<1, 32, 0, st>>>(partials.p, (int)gridN, t.nodes.p, dbox.p);
+        BT_LAUNCH("root_box");
+        double hb[8];
+        int hbad = 0;
+        BT_CUDA(cudaMemcpyAsync(hb, dbox.p, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
+        BT_CUDA(cudaMemcpyAsync(&hbad, dflags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        BT_CUDA(cudaStreamSynchronize(st));
+        if (hbad) throw Error(BT_ERR_INPUT, "bt_build: non-finite coordinate or |coordinate| > 1e150");
+        for (int l = 0; l < 3; l++) { t.box_lo[l] = hb[l]; t.box_hi[l] = hb[3 + l]; }
+        t.M = hb[6];
+    }
+
+    // Root is a leaf when n <= s or the depth cap is 0.
+    if (n <= t.s || t.depth_cap == 0) {
+        t.leaf_begin.alloc(1);
+        t.leaf_count.alloc(1);
+        t.leaf_depth.alloc(1);
+        int32_t hl[3] = {0, (int32_t)n, 0};
+        BT_CUDA(cudaMemcpyAsync(t.leaf_begin.p, &hl[0], 4, cudaMemcpyHostToDevice, st));
+        BT_CUDA(cudaMemcpyAsync(t.leaf_count.p, &hl[1], 4, cudaMemcpyHostToDevice, st));
+        BT_CUDA(cudaMemcpyAsync(t.leaf_depth.p, &hl[2], 4, cudaMemcpyHostToDevice, st));
+        copy_rec_kernel<<<gridN, kThreads, 0, st>>>(act[0].p, fin.p, n);
+        BT_LAUNCH("copy_rec");
+        t.n_leaves = 1;
+        t.n_nodes = 0;
+        t.root_is_leaf = true;
+    } else {
+        t.root_is_leaf = false;
+        act_node[0].alloc(n);
+        BT_CUDA(cudaMemsetAsync(act_node[0].p, 0, n * sizeof(int32_t), st));
+        act[1].alloc(n);
+        act_node[1].alloc(n);
+        DBuf<uint32_t> keys(n);
+        DBuf<LevelNode> ln(1), ln_next;
+        {
+            LevelNode r{};
+            r.act_begin = 0;
+            r.count = (int32_t)n;
+            r.final_begin = 0;
+            r.gid = 0;
+            BT_CUDA(cudaMemcpyAsync(ln.p, &r, sizeof(r), cudaMemcpyHostToDevice, st));
+        }
+        t.n_nodes = 1;
+        t.leaf_begin.reserve(1024, 0);
+        t.leaf_count.reserve(1024, 0);
+        t.leaf_depth.reserve(1024, 0);
+        int64_t nn = 1, n_act = n;
+        int cur = 0;
+        int level = 0;
+        DBuf<int32_t> hist;
+        DBuf<int64_t> cpre;
+        DBuf<int32_t> cid, cact, cdst;
+        DBuf<long long> dtotal(1);
+        DBuf<CellScan> dcs(1);
+        while (nn > 0) {
+            Phase ph("build.level");
+            // A2: Eq. 1 and the level's cell layout
+            level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s);
+            BT_LAUNCH("level_b");
+            device_scan<long long>(CellsOfNode{ln.p}, CellBaseOut{ln.p}, nn, dtotal.p);
+            BT_CUDA(cudaMemcpyAsync(hs, dtotal.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+            BT_CUDA(cudaStreamSynchronize(st));
+            const int64_t ncells = hs[0];
+            hist.reserve(ncells, 0);
+            cpre.reserve(ncells, 0);
+            cid.reserve(ncells, 0);
+            cact.reserve(ncells, 0);
+            cdst.reserve(ncells, 0);
+            t.cells.reserve(t.n_cells + ncells, t.n_cells);
+            BT_CUDA(cudaMemsetAsync(hist.p, 0, ncells * sizeof(int32_t), st));
+            const unsigned gridC = grid_for(ncells, kThreads, (int64_t)sms * 16);
+            const unsigned gridA = grid_for(n_act, kThreads, (int64_t)sms * 16);
+
+            // A3-A5: distribute, ratio, halving rounds (at most log2 b0 rounds)
+            for (int round = 0;; round++) {
+                if (round > 0) {
+                    zero_flagged_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells);
+                    BT_LAUNCH("zero_flagged");
+                }
+                key_hist_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, t.nodes.p, keys.p,
+                                                            hist.p, round);
+                BT_LAUNCH("key_hist");
+                under_count_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, t.alpha * (double)t.s);
+                BT_LAUNCH("under_count");
+                BT_CUDA(cudaMemsetAsync(dflags.p + 1, 0, sizeof(int), st));
+                ratio_decide_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.beta, dflags.p + 1);
+                BT_LAUNCH("ratio_decide");
+                int any = 0;
+                BT_CUDA(cudaMemcpyAsync(&any, dflags.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+                BT_CUDA(cudaStreamSynchronize(st));
+                if (!any) break;
+            }
+            finalize_level_nodes_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.nodes.p, t.n_cells,
+                                                                                       dstat.p);
+            BT_LAUNCH("finalize_level_nodes");
+
+            // A6: one scan over the level's cells
+            const bool child_ok = (level + 1) < t.depth_cap;
+            device_scan<CellScan>(CellIn{hist.p, t.s, child_ok}, CellOut{cpre.p, cid.p, cact.p}, ncells, dcs.p);
+            CellScan tot;
+            BT_CUDA(cudaMemcpyAsync(&tot, dcs.p, sizeof(CellScan), cudaMemcpyDeviceToHost, st));
+            BT_CUDA(cudaStreamSynchronize(st));
+            const int64_t nn_next = tot.nnode, n_act_next = tot.actoff, nleaf = tot.nleaf;
+
+            // A8: emit children / leaves / cell table
+            ln_next.alloc(nn_next > 0 ? nn_next : 1);
+            t.nodes.reserve(t.n_nodes + nn_next, t.n_nodes);
+            t.leaf_begin.reserve(t.n_leaves + nleaf, t.n_leaves);
+            t.leaf_count.reserve(t.n_leaves + nleaf, t.n_leaves);
+            t.leaf_depth.reserve(t.n_leaves + nleaf, t.n_leaves);
+            emit_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, cpre.p, cid.p, cact.p, t.nodes.p, t.cells.p,
+                                                    t.n_cells, child_ok ? ln_next.p : nullptr, (int32_t)t.n_nodes,
+                                                    t.leaf_begin.p, t.leaf_count.p, t.leaf_depth.p, t.n_leaves,
+                                                    level + 1, cdst.p, t.s);
+            BT_LAUNCH("emit");
+
+            // A7: scatter (cursor = zeroed histogram)
+            BT_CUDA(cudaMemsetAsync(hist.p, 0, ncells * sizeof(int32_t), st));
+            scatter_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, keys.p, hist.p, t.cells.p,
+                                                       t.n_cells, cdst.p, cid.p, fin.p, act[cur ^ 1].p,
+                                                       act_node[cur ^ 1].p);
+            BT_LAUNCH("scatter");
+
+            if (nleaf > 0) t.depth = level + 1;
+            t.n_cells += ncells;
+            t.n_leaves += nleaf;
+            t.n_nodes += nn_next;
+            std::swap(ln, ln_next);
+            nn = nn_next;
+            n_act = n_act_next;
+            cur ^= 1;
+            level++;
+        }
+        int32_t rb = 0;
+        BT_CUDA(cudaMemcpyAsync(&rb, &t.nodes.p[0].b, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        BT_CUDA(cudaStreamSynchronize(st));
+        t.root_b = rb;
+    }
+
+    // A9: canonical leaf order + tight boxes; work units
+    {
+        Phase ph("build.leaves");
+        t.leaf_box.alloc(6 * (size_t)t.n_leaves);
+        leaf_finalize_kernel<<<grid_for(t.n_leaves * 32, kThreads, (int64_t)sms * 32), kThreads, 0, st>>>(
+            fin.p, t.rec.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
+        BT_LAUNCH("leaf_finalize");
+        DBuf<long long> dtot(1);
+        // units: count first (to size the array), then write
+        // (two scans over the leaves; cheap: L <= n / 1)
+        device_scan<long long>(UnitsOfLeaf{t.leaf_count.p}, NullOut{}, t.n_leaves, dtot.p);
+        long long nu = 0;
+        BT_CUDA(cudaMemcpyAsync(&nu, dtot.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
+        BT_CUDA(cudaStreamSynchronize(st));
+        t.units.alloc(nu);
+        t.n_units = nu;
+        device_scan<long long>(UnitsOfLeaf{t.leaf_count.p}, UnitsOut{t.leaf_begin.p, t.leaf_count.p, t.units.p},
+                               t.n_leaves, dtot.p);
+        unsigned long long hstat[4];
+        BT_CUDA(cudaMemcpyAsync(hstat, dstat.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        BT_CUDA(cudaStreamSynchronize(st));
+        t.halvings = (int64_t)hstat[0];
+        t.max_leaf = (int64_t)hstat[1];
+        t.overfull = (int64_t)hstat[2];
+    }
+}
+
+}  // namespace bt

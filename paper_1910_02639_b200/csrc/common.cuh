@@ -1,0 +1,190 @@
+// common.cuh -- shared device/host definitions of the CUDA b-tree library.
+// Citations: P:n = PAPER.md line n (arXiv 1910.02639); R-numbers = readings in
+// DESIGN.md section 3.  Nothing here is shared with oracle/ (independent code).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/btree.h"
+
+namespace bt {
+
+// ---------------------------------------------------------------------------
+// Errors: thrown inside the library, converted to bt_status at the ABI.
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+inline void cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return;
+    int code = (e == cudaErrorMemoryAllocation) ? BT_ERR_OOM : BT_ERR_CUDA;
+    cudaGetLastError();  // clear sticky-free errors
+    throw Error(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define BT_CUDA(x) ::bt::cuda_check((x), #x)
+#define BT_LAUNCH(name) ::bt::after_launch(name)
+
+cudaStream_t stream();  // this thread's stream
+void after_launch(const char *name);
+
+// Phase profiling (CUDA events on the library stream).
+struct Phase {
+    const char *name;
+    bool on;
+    cudaEvent_t a, b;
+    explicit Phase(const char *n);
+    ~Phase();
+};
+
+// Stream-ordered device allocation (cudaMallocAsync on the library stream).
+void *dmalloc(size_t bytes);
+void dfree(void *p);
+
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    DBuf() = default;
+    explicit DBuf(size_t count) { alloc(count); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+        return *this;
+    }
+    ~DBuf() { release(); }
+    void alloc(size_t count) {
+        release();
+        n = count;
+        p = count ? static_cast<T *>(dmalloc(count * sizeof(T))) : nullptr;
+    }
+    // grow (preserving the first `keep` elements) to at least `count`
+    void reserve(size_t count, size_t keep) {
+        if (count <= n) return;
+        size_t cap = count + count / 2 + 1024;
+        T *q = static_cast<T *>(dmalloc(cap * sizeof(T)));
+        if (keep && p) BT_CUDA(cudaMemcpyAsync(q, p, keep * sizeof(T), cudaMemcpyDeviceToDevice, stream()));
+        release();
+        p = q;
+        n = cap;
+    }
+    void release() {
+        if (p) dfree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+// Pinned host scratch for the few control scalars read back per level.
+struct HostScratch {
+    int64_t *p = nullptr;
+    HostScratch() { BT_CUDA(cudaMallocHost(&p, 64 * sizeof(int64_t))); }
+    ~HostScratch() { if (p) cudaFreeHost(p); }
+};
+HostScratch &host_scratch();
+
+// ---------------------------------------------------------------------------
+// Tree representation in HBM.
+// ---------------------------------------------------------------------------
+struct NodeRec {      // one internal node
+    double lo[3];     // x_{l,min}
+    double ext[3];    // x_{l,max} - x_{l,min}  (Eq. 2 denominator)
+    int32_t b;        // accepted branching factor per dimension
+    int32_t depth;
+    int64_t cell_base;  // first entry of this node's b^3 cells in the cell table
+};
+
+// cell table code: -1 empty, >= 0 leaf id, <= -2 internal node (id = -2 - code)
+__host__ __device__ inline int32_t node_code(int32_t node) { return -2 - node; }
+__host__ __device__ inline int32_t code_node(int32_t code) { return -2 - code; }
+
+struct TreeDev {
+    int64_t n = 0;
+    int32_t s = 64;
+    double beta = 0.5, alpha = 0.5;
+    int32_t depth_cap = 64;
+    // records in tree (depth-first leaf) order: x, y, z, caller index (bits)
+    DBuf<double4> rec;
+    DBuf<NodeRec> nodes;       // internal nodes, all levels
+    int64_t n_nodes = 0;
+    DBuf<int32_t> cells;       // cell table, all levels
+    int64_t n_cells = 0;
+    DBuf<int32_t> leaf_begin;  // tree-order position of each leaf (depth-first order)
+    DBuf<int32_t> leaf_count;
+    DBuf<int32_t> leaf_depth;
+    DBuf<double> leaf_box;     // [6*L]: lo x,y,z, hi x,y,z (tight, exact min/max)
+    int64_t n_leaves = 0;
+    DBuf<int32_t> leaf_id_of_level;  // scratch
+    DBuf<int4> units;          // {leaf, first query (tree pos), n queries, 0}
+    int64_t n_units = 0;
+    double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};
+    double M = 0.0;            // max |root box coordinate|
+    int32_t depth = 0, root_b = 0;
+    int64_t halvings = 0, overfull = 0, max_leaf = 0;
+    bool root_is_leaf = true;
+    // search scratch
+    DBuf<double> h_tree;       // h in tree order
+    DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
+    DBuf<int2> stack;          // walk stacks (per resident warp)
+    int64_t stack_per_warp = 0;
+    int64_t total_pairs = 0, max_count = 0, staged = 0, tests = 0, exact_tests = 0;
+};
+
+// Build (build.cu) and search (walk.cu) entry points.
+void build_tree(TreeDev &t, const double *pos);
+void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets,
+                    int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass);
+
+// Device scans (scan.cu)
+void exclusive_scan_i32_to_i64(const int32_t *in, int64_t *out, int64_t n, int64_t *total_dev);
+
+// ---------------------------------------------------------------------------
+// Eq. 2 with the clamp of reading R8, evaluated exactly as
+//   floor( ((x - lo) / ext) * b ),  ext = x_max - x_min,
+// one IEEE rounding per operation (no contraction: explicit _rn intrinsics).
+// Build and walk call this same function with the same stored (lo, ext, b)
+// of a node, which makes the walk's Eq. 5 ranges consistent with the build's
+// distribution (lemma L2).  NaN (0/0 on a zero-extent box) -> 0.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int cell_coord(double x, double lo, double ext, int b) {
+    double q = __dmul_rn(__ddiv_rn(__dsub_rn(x, lo), ext), (double)b);
+    double f = floor(q);
+    if (!(f >= 0.0)) return 0;
+    if (f > (double)(b - 1)) return b - 1;
+    return (int)f;
+}
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+inline int num_sms() {
+    static int v = 0;
+    if (!v) {
+        int dev;
+        BT_CUDA(cudaGetDevice(&dev));
+        BT_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return v;
+}
+
+inline unsigned grid_for(int64_t n, int threads, int64_t max_blocks = 1 << 20) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > max_blocks) b = max_blocks;
+    return (unsigned)b;
+}
+
+}  // namespace bt

@@ -1,0 +1,249 @@
+"""GPU parity: the CUDA path (through the C ABI, libbtree.so) against the CPU
+oracle, element by element, on seeded inputs.  Bit-exact: counts, offsets,
+per-row-sorted neighbor lists, and the tree itself (leaf partition in
+depth-first order, statistics) -- all integer results.
+
+Run with ``pytest -m gpu`` on a B200.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_1910_02639_b200 import datagen  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1910_02639_b200 as P
+    P.lib()
+    return P
+
+
+def sort_rows(counts, offsets, nbr):
+    """Sort each CSR row ascending (on the device; harness plumbing only)."""
+    n = counts.numel()
+    total = int(offsets[-1].item())
+    if total == 0:
+        return np.zeros(0, dtype=np.int32)
+    rows = torch.repeat_interleave(torch.arange(n, device=counts.device, dtype=torch.int64),
+                                   counts.to(torch.int64), output_size=total)
+    key = rows * (1 << 32) + nbr[:total].to(torch.int64)
+    key, _ = torch.sort(key)
+    return (key & 0xFFFFFFFF).to(torch.int32).cpu().numpy()
+
+
+def gpu_run(P, pos, h, s=64, beta=0.5, alpha=None, depth_cap=None, ngmax=None):
+    t = P.build(torch.from_numpy(pos).to(DEV), s, beta, alpha=alpha, depth_cap=depth_cap)
+    hd = torch.from_numpy(h).to(DEV)
+    counts, offsets, nbr = t.find_neighbors(hd, ngmax)
+    torch.cuda.synchronize()
+    res = (counts.cpu().numpy(), offsets.cpu().numpy(), sort_rows(counts, offsets, nbr))
+    return t, res
+
+
+def assert_same(gpu, ref):
+    gc, go, gi = gpu
+    rc, ro, ri = ref
+    assert gc.shape == rc.shape
+    bad = np.nonzero(gc != rc)[0]
+    assert bad.size == 0, f"{bad.size} counts differ, first rows {bad[:10]} gpu {gc[bad[:10]]} oracle {rc[bad[:10]]}"
+    assert np.array_equal(go, ro)
+    assert np.array_equal(gi, ri)
+
+
+def assert_same_tree(t, otree):
+    gs = t.stats()
+    os_ = otree.stats()
+    for k in ("nodes", "leaves", "halvings", "overfull", "max_leaf", "depth", "root_b"):
+        assert gs[k] == os_[k], (k, gs[k], os_[k])
+    perm, lb, lc, ld = t.order()
+    operm, olb, olc, old = otree.order()
+    assert np.array_equal(perm.cpu().numpy(), operm)
+    assert np.array_equal(lb.cpu().numpy(), olb)
+    assert np.array_equal(lc.cpu().numpy(), olc)
+    assert np.array_equal(ld.cpu().numpy(), old)
+
+
+# ---- the five configurations --------------------------------------------------
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, 200_003), (3, 216_000), (4, 300_001), (5, 400_000)])
+def test_parity_scaled_configs(P, oracle, cfg, n):
+    pos, h = datagen.make_config(cfg, n=n)
+    t, gpu = gpu_run(P, pos, h, ngmax=datagen.NGMAX)
+    ot = oracle.Tree(pos, 64, 0.5)
+    assert_same(gpu, ot.neighbors(h))
+    assert_same_tree(t, ot)
+    st = t.stats()
+    assert st["total_pairs"] == int(gpu[1][-1]) == int(gpu[0].sum())
+
+
+@pytest.mark.parametrize("cfg", [2, 3, 4])
+def test_parity_full_size_configs(P, oracle, cfg):
+    pos, h = datagen.make_config(cfg)
+    t, gpu = gpu_run(P, pos, h, ngmax=datagen.NGMAX)
+    ot = oracle.Tree(pos, 64, 0.5)
+    assert_same(gpu, ot.neighbors(h))
+    assert_same_tree(t, ot)
+
+
+def test_parity_cfg5_full_size_sampled(P, oracle):
+    """cfg 5 at full size (2^25 particles) in the bench's launch configuration:
+    counts of 40k sampled rows and their sorted rows against the oracle's own
+    tree walk, 2k rows against brute force; invariants at every row."""
+    pos, h = datagen.make_config(5)
+    n = pos.shape[0]
+    t = P.build(torch.from_numpy(pos).to(DEV), 64, 0.5)
+    hd = torch.from_numpy(h).to(DEV)
+    counts, offsets = t.count(hd)
+    nbr = t.fill(hd, offsets)
+    torch.cuda.synchronize()
+    c = counts.cpu().numpy()
+    off = offsets.cpu().numpy()
+    assert off[0] == 0 and np.all(np.diff(off) == c) and off[-1] == c.sum()
+    rng = np.random.default_rng(99)
+    q = np.sort(rng.choice(n, 40_000, replace=False)).astype(np.int64)
+    ot = oracle.Tree(pos, 64, 0.5)
+    oc, ooff, oidx = ot.neighbors(h, queries=q)
+    assert np.array_equal(c[q], oc)
+    qd = torch.from_numpy(q).to(DEV)
+    starts = offsets[qd]
+    for k in range(0, q.size, 97):
+        row = nbr[int(starts[k]):int(starts[k]) + int(oc[k])].cpu().numpy()
+        assert np.array_equal(np.sort(row), oidx[ooff[k]:ooff[k + 1]])
+    bc, _, _ = oracle.brute_force(pos, h, queries=q[:2000])
+    assert np.array_equal(c[q[:2000]], bc)
+    # the tree statistics of the full-size build equal the oracle's
+    assert_same_tree(t, ot)
+
+
+# ---- invariance, edge cases ------------------------------------------------------
+def test_independent_of_bucket_size_and_beta(P, oracle):
+    pos, h = datagen.clustered(30_000, 5, h=0.008)
+    ref = oracle.Tree(pos, 64).neighbors(h)
+    for s in (1, 2, 8, 64, 4096):
+        for beta in (0.1, 0.5, 1.0):
+            t, gpu = gpu_run(P, pos, h, s=s, beta=beta)
+            assert_same(gpu, ref)
+            assert_same_tree(t, oracle.Tree(pos, s, beta))
+    t, gpu = gpu_run(P, pos, h, s=16, beta=0.5, alpha=0.0)
+    assert_same(gpu, ref)
+    assert_same_tree(t, oracle.Tree(pos, 16, 0.5, 0.0))
+
+
+def test_near_boundary_adversarial(P, oracle):
+    pos, h = datagen.near_boundary(1024, 64, 17)
+    ref = oracle.brute_force(pos, h)
+    for s in (8, 64):
+        _, gpu = gpu_run(P, pos, h, s=s)
+        assert_same(gpu, ref)
+
+
+@pytest.mark.parametrize("two_h,interior", [(2.5, 80), (1.01, 6)])
+def test_lattice_closed_form_gpu(P, oracle, two_h, interior):
+    m = 20
+    pos = datagen.lattice(m, 1.0)
+    h = np.full(len(pos), two_h / 2)
+    _, gpu = gpu_run(P, pos, h, s=8)
+    assert_same(gpu, oracle.brute_force(pos, h))
+    centre = (m // 2) * (m * m + m + 1)
+    assert gpu[0][centre] == interior
+
+
+def test_edge_cases(P, oracle):
+    cases = []
+    cases.append((np.zeros((1, 3)), np.array([0.1])))                      # n = 1
+    p, hh = datagen.uniform(50, 3, 0.2)
+    cases.append((p, hh))                                                  # n <= s: root leaf
+    cases.append((np.tile([[0.3, 0.3, 0.3]], (300, 1)), np.full(300, 1e-3)))  # coincident, depth cap
+    p, hh = datagen.uniform(5000, 4, 0.03)
+    p[:, 2] = 0.5
+    cases.append((p, hh))                                                  # plane: zero z extent
+    p, hh = datagen.uniform(3000, 5, 2.0)
+    cases.append((p, hh))                                                  # 2h > domain: n - 1 each
+    p, _ = datagen.uniform(4000, 6, 0.01)
+    hh = np.where(np.arange(4000) % 2 == 0, 0.2, 0.001)
+    cases.append((p, np.ascontiguousarray(hh)))                            # strongly asymmetric h
+    p, hh = datagen.uniform(1_000_003 // 10, 7, 0.02, 0.03)
+    cases.append((p, hh))                                                  # ragged n
+    for k, (p, hh) in enumerate(cases):
+        for s in (8, 64):
+            t, gpu = gpu_run(P, np.ascontiguousarray(p), np.ascontiguousarray(hh), s=s)
+            ref = oracle.Tree(p, s).neighbors(hh)
+            assert_same(gpu, ref)
+            assert_same_tree(t, oracle.Tree(p, s))
+    # 2h > domain -> every particle sees all others
+    _, gpu = gpu_run(P, *datagen.uniform(3000, 5, 2.0))
+    assert np.all(gpu[0] == 2999)
+
+
+def test_empty_input(P):
+    t = P.build(torch.zeros((0, 3), dtype=torch.float64, device=DEV))
+    counts, offsets = t.count(torch.zeros(0, dtype=torch.float64, device=DEV))
+    assert counts.numel() == 0 and int(offsets[0]) == 0
+    assert t.stats()["leaves"] == 0
+
+
+def test_count_then_fill_and_determinism(P):
+    pos, h = datagen.make_config(2, n=100_000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd = torch.from_numpy(h).to(DEV)
+    c1, o1, n1 = t.find_neighbors(hd)             # count-only + exact fill
+    c2, o2, n2 = t.find_neighbors(hd, ngmax=512)  # single call
+    total = int(o1[-1])
+    assert torch.equal(c1, c2) and torch.equal(o1, o2)
+    assert torch.equal(n1[:total], n2[:total])    # same row order run to run
+    t2 = P.build(torch.from_numpy(pos).to(DEV))
+    _, _, n3 = t2.find_neighbors(hd, ngmax=512)
+    assert torch.equal(n2[:total], n3[:total])
+
+
+def test_errors(P):
+    pos, h = datagen.uniform(2000, 8, 0.05)
+    bad = pos.copy()
+    bad[5, 1] = np.nan
+    with pytest.raises(P.BtreeError) as e:
+        P.build(torch.from_numpy(bad).to(DEV))
+    assert e.value.code == 2
+    with pytest.raises(P.BtreeError) as e:
+        P.build(torch.from_numpy(pos).to(DEV), 0)
+    assert e.value.code == 1
+    with pytest.raises(P.BtreeError) as e:
+        P.build(torch.from_numpy(pos).to(DEV), 8, 0.0)
+    assert e.value.code == 1
+    t = P.build(torch.from_numpy(pos).to(DEV), 8)
+    hb = h.copy()
+    hb[3] = 0.0
+    with pytest.raises(P.BtreeError) as e:
+        t.count(torch.from_numpy(hb).to(DEV))
+    assert e.value.code == 2
+    # capacity: counts/offsets valid, nbr untouched
+    hd = torch.from_numpy(h).to(DEV)
+    counts = torch.empty(2000, dtype=torch.int32, device=DEV)
+    offsets = torch.empty(2001, dtype=torch.int64, device=DEV)
+    nbr = torch.full((2000,), -7, dtype=torch.int32, device=DEV)
+    with pytest.raises(P.BtreeError) as e:
+        t.find_neighbors(hd, ngmax=1, counts=counts, offsets=offsets, nbr_idx=nbr)
+    assert e.value.code == 3
+    c_ref, o_ref = t.count(hd)
+    assert torch.equal(counts, c_ref) and torch.equal(offsets, o_ref)
+    assert bool((nbr == -7).all())
+
+
+def test_search_host_end_to_end(P, oracle):
+    pos, h = datagen.make_config(2, n=50_000)
+    oc, ooff, oidx = oracle.Tree(pos, 64).neighbors(h)
+    cap = int(ooff[-1])
+    c, off, nbr = P.search_host(torch.from_numpy(pos), torch.from_numpy(h), capacity=cap)
+    assert np.array_equal(c.numpy(), oc) and np.array_equal(off.numpy(), ooff)
+    nb = nbr.numpy()
+    for i in range(0, 50_000, 37):
+        assert np.array_equal(np.sort(nb[off[i]:off[i + 1]]), oidx[ooff[i]:ooff[i + 1]])
+    with pytest.raises(P.BtreeError) as e:
+        P.search_host(torch.from_numpy(pos), torch.from_numpy(h), capacity=cap - 1)
+    assert e.value.code == 3
