@@ -1,0 +1,339 @@
+"""bench.py -- b-tree exact close-neighbor search on B200 (arXiv 1910.02639).
+
+One step = one pass of the whole hot path over one particle set resident in
+HBM: bt_build (root box, levels of Eq. 1-4 + scatter, leaves) +
+bt_find_neighbors (count pass, offsets scan, capacity check, fill pass into
+the CSR) + bt_free.  Workload: BASELINE.json configs[4] ("cfg 5",
+N = 2^25, ngmax = 512, count-then-fill CSR), seeded synthetic data.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl b200|reference]
+
+Multi-GPU (torchrun): every rank searches its own independently drawn
+sub-domain of the same recipe (the paper's per-node sub-domain);
+no data-path collective; weak scaling; time = max over ranks.
+--impl reference runs the CPU oracle (oracle/, the paper's Alg. 1 + Alg. 2 in
+plain C) on a bounded sample, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+from paper_1910_02639_b200 import datagen  # noqa: E402
+
+WORKLOADS = {
+    1: "N=10,000 uniform [0,1)^3, h=0.0668, s=64",
+    2: "N=1,000,000 uniform [0,1)^3, h_i=0.0144*U(0.8,1.2), s=64",
+    3: "100^3 jittered lattice, h=0.015, s=64",
+    4: "N=4,000,000 Evrard-like sphere, h from n(r), s=64",
+    5: "N=33,554,432: 50% uniform + 50% in 64 Gaussian clumps (sigma 0.01), h from a 64^3 histogram, "
+       "s=64, max_empty=0.5, ngmax=512, count-then-fill CSR",
+}
+METRIC = "neighbor-search particles/s (build + count + fill, all particles)"
+UNIT = "particles/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--n", type=int, default=None, help="override particle count (not a bench line)")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000, help="oracle queries timed for cpu_baseline")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def config_block(cfg, n, ws):
+    return {"workload": (f"BASELINE.json configs[{cfg - 1}] (cfg {cfg}): {WORKLOADS[cfg]}"
+                         + ("" if n is None else f" [n overridden to {n}: not a bench line]")),
+            "N_per_gpu": n if n is not None else datagen.FULL_N[cfg], "bucket_size": datagen.BUCKET_SIZE,
+            "max_empty": datagen.MAX_EMPTY, "alpha": 0.5, "ngmax": datagen.NGMAX, "parallelism": f"sub-domain x{ws}",
+            "l2": "inputs larger than L2 (pos 805 MB + h 268 MB at cfg 5); no flush"}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for k, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(k)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle: cpu_baseline / --impl reference
+# ---------------------------------------------------------------------------
+def oracle_sample(pos, h, sample_queries: int):
+    """Time the oracle as it stands on this host: full BuildTree + the
+    FindNeighbors count and row passes for a random sample of queries, all
+    host cores (OpenMP over queries).  Returns (est. seconds per full step,
+    description, cores)."""
+    import oracle
+    n = pos.shape[0]
+    cores = oracle.default_threads()
+    t0 = time.perf_counter()
+    tree = oracle.Tree(pos, datagen.BUCKET_SIZE, datagen.MAX_EMPTY)
+    t1 = time.perf_counter()
+    rng = np.random.default_rng(7)
+    k = min(sample_queries, n)
+    q = np.sort(rng.choice(n, k, replace=False)).astype(np.int64)
+    tree.neighbors(h, queries=q, threads=cores)
+    t2 = time.perf_counter()
+    build_s = t1 - t0
+    search_s = (t2 - t1) * n / k
+    desc = (f"oracle BuildTree on all {n} particles ({build_s:.2f} s, 1 thread) + count and row passes for "
+            f"{k} random queries ({t2 - t1:.2f} s, {cores} threads), search scaled x{n / k:.1f} to all queries")
+    return build_s + search_s, desc, cores, build_s, search_s
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    pos, h = datagen.make_config(args.config, n=args.n)
+    n = pos.shape[0]
+    steps = []
+    desc = cores = None
+    for s in range(args.warmup + args.steps):
+        step_s, desc, cores, b, srch = oracle_sample(pos, h, min(args.cpu_sample, 200_000))
+        if s >= args.warmup:
+            steps.append(step_s)
+    t = float(np.mean(steps))
+    v = n / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy PCG64, SURVEY 8(d) recipe)",
+            "config": config_block(args.config, args.n, 1),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def run_b200(args):
+    import torch
+
+    import paper_1910_02639_b200 as P
+
+    ws, rank, local = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    P.lib()
+
+    pos_np, h_np = datagen.make_config(args.config, n=args.n, seed_offset=rank)
+    n = pos_np.shape[0]
+    ngmax = datagen.NGMAX
+    pos = torch.from_numpy(pos_np).to(dev)
+    h = torch.from_numpy(h_np).to(dev)
+    counts = torch.empty(n, dtype=torch.int32, device=dev)
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    nbr = torch.empty(n * ngmax, dtype=torch.int32, device=dev)  # capacity n * ngmax (BJ)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        t = P.Tree(pos, datagen.BUCKET_SIZE, datagen.MAX_EMPTY)
+        t.find_neighbors(h, ngmax, counts=counts, offsets=offsets, nbr_idx=nbr)
+        st = t.stats()
+        t.free()
+        return st
+
+    for _ in range(args.warmup):
+        st = step()
+    torch.cuda.synchronize()
+
+    P.profile_reset()
+    P.profile_enable(True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        st = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    P.profile_enable(False)
+    prof = P.profile()
+    if ws > 1:
+        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        ms = float(tt.item())
+    total_pairs = int(st["total_pairs"])
+
+    def ph(name):
+        return prof.get(name, (0.0, 0))[0] / args.steps
+
+    launches = sum(v[1] for k, v in prof.items() if k.startswith("kernel.")) // args.steps
+    kern = {"build": ph("build.total"), "walk_count": ph("search.count"), "scan": ph("search.scan"),
+            "walk_fill": ph("search.fill"), "gather_h": ph("search.gather_h")}
+
+    # ---- roofline of the dominant kernel -----------------
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    dom = max(("walk_count", "walk_fill"), key=lambda k: kern[k])
+    if dom == "walk_fill":
+        # algorithmic HBM bytes of one fill launch: per particle its 32-B record,
+        # 8-B h and 8-B offset, plus the 4-B output index per neighbor pair
+        alg_bytes = n * (32 + 8 + 8) + 4 * total_pairs
+    else:
+        # count launch: per particle 32-B record + 8-B h + 4-B count
+        alg_bytes = n * (32 + 8 + 4)
+    achieved = alg_bytes / (kern[dom] * 1e-3) / 1e9
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": None, "peak_source": hbm_src,
+                "algorithmic_bytes": alg_bytes}
+    # BJ's own definition: bytes of candidate positions actually read (staged
+    # records x 32 B per walk pass, both passes) over peak HBM bandwidth
+    bcand = 2 * int(st["staged"]) * 32
+    walk_ms = kern["walk_count"] + kern["walk_fill"]
+    bj_roof = {"B_cand_bytes": bcand, "walk_ms": walk_ms,
+               "frac": (bcand / (walk_ms * 1e-3) / 1e9) / hbm_peak if walk_ms > 0 else None}
+
+    # ---- end to end through the public API on host buffers --------------------
+    e2e = None
+    if not args.no_e2e and args.e2e_steps > 0:
+        pos_h = torch.from_numpy(pos_np).pin_memory()
+        h_h = torch.from_numpy(h_np).pin_memory()
+        c_h = torch.empty(n, dtype=torch.int32).pin_memory()
+        o_h = torch.empty(n + 1, dtype=torch.int64).pin_memory()
+        nb_h = torch.empty(max(total_pairs, 1), dtype=torch.int32).pin_memory()
+        del nbr
+        torch.cuda.empty_cache()
+        P.search_host(pos_h, h_h, capacity=total_pairs, counts=c_h, offsets=o_h, nbr=nb_h)  # warm-up
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            P.search_host(pos_h, h_h, capacity=total_pairs, counts=c_h, offsets=o_h, nbr=nb_h)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1) / args.e2e_steps
+        if ws > 1:
+            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
+            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+            ems = float(tt.item())
+        e2e = {"value": n * ws / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": n * 4 + (n + 1) * 8 + 4 * total_pairs,
+               "api": "bt_search_host (pinned host buffers; H2D pos+h, build, count, fill, D2H counts+offsets+CSR)"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        step_s, desc, cores, _, _ = oracle_sample(pos_np, h_np, args.cpu_sample)
+        cpu = {"value": n / step_s, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": n * ws / (ms * 1e-3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy PCG64, SURVEY 8(d) recipe)",
+                "config": config_block(args.config, args.n, ws),
+                "pairs_per_s": total_pairs * ws / (ms * 1e-3), "total_pairs_per_gpu": total_pairs,
+                "build_ms": kern["build"], "kernel_ms": kern, "gpu_launches": launches,
+                "roofline": roofline, "bj_hbm_roofline": bj_roof,
+                "tree": {k: st[k] for k in ("depth", "root_b", "nodes", "leaves", "halvings", "units")},
+                "walk_counters": {"staged": st["staged"], "tests": st["tests"], "exact_tests": st["exact_tests"]},
+                "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

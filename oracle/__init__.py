@@ -153,8 +153,11 @@ class Tree:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            lib().orc_free(h)
+        if h and _lib is not None:
+            try:
+                _lib.orc_free(h)
+            except Exception:
+                pass
             self._h = None
 
     def stats(self) -> dict:

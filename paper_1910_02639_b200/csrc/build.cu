@@ -392,6 +392,36 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
     }
 }
 
+// ---- leaves renumbered in depth-first order (ascending tree position) -------
+__global__ void mark_leaf_begin_kernel(const int32_t *begin, int64_t n_leaves, int32_t *flag) {
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n_leaves; L += (int64_t)gridDim.x * blockDim.x)
+        flag[begin[L]] = 1;
+}
+struct FlagIn {
+    const int32_t *f;
+    __device__ int operator()(int64_t i) const { return f[i]; }
+};
+struct FlagOut {
+    int32_t *excl;
+    __device__ void operator()(int64_t i, int exc, int) const { excl[i] = exc; }
+};
+__global__ void permute_leaves_kernel(const int32_t *excl, int64_t n_leaves, const int32_t *b0, const int32_t *c0,
+                                      const int32_t *d0, int32_t *b1, int32_t *c1, int32_t *d1, int32_t *map) {
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n_leaves; L += (int64_t)gridDim.x * blockDim.x) {
+        int32_t nid = excl[b0[L]];
+        b1[nid] = b0[L];
+        c1[nid] = c0[L];
+        d1[nid] = d0[L];
+        map[L] = nid;
+    }
+}
+__global__ void remap_cells_kernel(int32_t *cells, int64_t n_cells, const int32_t *map) {
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n_cells; g += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c = cells[g];
+        if (c >= 0) cells[g] = map[c];
+    }
+}
+
 constexpr int kUnitQ = 64;  // queries per walk work unit
 
 struct UnitsOfLeaf {
@@ -591,6 +621,28 @@ void build_tree(TreeDev &t, const double *pos) {
         BT_CUDA(cudaMemcpyAsync(&rb, &t.nodes.p[0].b, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         BT_CUDA(cudaStreamSynchronize(st));
         t.root_b = rb;
+    }
+
+    // Leaves were numbered level by level; renumber them in depth-first order
+    // (ascending first tree position), which is the paper's walk order.
+    if (!t.root_is_leaf) {
+        Phase ph("build.leaf_order");
+        DBuf<int32_t> flag(n), excl(n), map(t.n_leaves);
+        DBuf<int32_t> b1(t.n_leaves), c1(t.n_leaves), d1(t.n_leaves);
+        BT_CUDA(cudaMemsetAsync(flag.p, 0, n * sizeof(int32_t), st));
+        mark_leaf_begin_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 16), kThreads, 0, st>>>(
+            t.leaf_begin.p, t.n_leaves, flag.p);
+        BT_LAUNCH("mark_leaf_begin");
+        device_scan<int>(FlagIn{flag.p}, FlagOut{excl.p}, n, (int *)nullptr);
+        permute_leaves_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 16), kThreads, 0, st>>>(
+            excl.p, t.n_leaves, t.leaf_begin.p, t.leaf_count.p, t.leaf_depth.p, b1.p, c1.p, d1.p, map.p);
+        BT_LAUNCH("permute_leaves");
+        remap_cells_kernel<<<grid_for(t.n_cells, kThreads, (int64_t)sms * 16), kThreads, 0, st>>>(t.cells.p, t.n_cells,
+                                                                                                  map.p);
+        BT_LAUNCH("remap_cells");
+        t.leaf_begin = std::move(b1);
+        t.leaf_count = std::move(c1);
+        t.leaf_depth = std::move(d1);
     }
 
     // A9: canonical leaf order + tight boxes; work units
