@@ -127,6 +127,14 @@ int bt_search_host(const double *pos_h, const double *h_h, int64_t n, int32_t bu
 /* Stream for this thread's subsequent calls (a cudaStream_t; NULL = default). */
 int bt_set_stream(void *cuda_stream);
 
+/*
+ * Validation knob (thread-local): on != 0 sends every candidate pair to the
+ * fp64 predicate itself instead of deciding the certain cases with the fp32
+ * pre-test of lemma L4.  Results are identical by
+ * construction; tests use it to check that, bench-style runs to measure it.
+ */
+int bt_set_exact_only(int on);
+
 const char *bt_last_error(void);
 int bt_last_status(void);
 

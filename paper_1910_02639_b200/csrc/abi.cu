@@ -267,6 +267,12 @@ int bt_set_stream(void *s) {
     return BT_OK;
 }
 
+int bt_set_exact_only(int on) {
+    set_exact_only(on != 0);
+    g_status = BT_OK;
+    return BT_OK;
+}
+
 const char *bt_last_error(void) { return g_err.c_str(); }
 int bt_last_status(void) { return g_status; }
 

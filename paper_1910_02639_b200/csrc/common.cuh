@@ -106,6 +106,13 @@ struct NodeRec {      // one internal node
 __host__ __device__ inline int32_t node_code(int32_t node) { return -2 - node; }
 __host__ __device__ inline int32_t code_node(int32_t code) { return -2 - code; }
 
+struct WalkBatch {          // one staged candidate batch of a walk unit
+    long long mask_base;    // mask word (chunk k, query q) at mask_base + k * nq + q
+    long long cand_base;    // first candidate slot (64 per chunk)
+    int ncand;
+    int next;               // next batch of the same unit, -1 = last
+};
+
 struct TreeDev {
     int64_t n = 0;
     int32_t s = 64;
@@ -132,6 +139,14 @@ struct TreeDev {
     bool root_is_leaf = true;
     // search scratch
     DBuf<double> h_tree;       // h in tree order
+    DBuf<int32_t> head;        // first recorded batch of each unit
+    DBuf<unsigned long long> arena_masks;  // neighbor masks per (query, 64-candidate chunk)
+    DBuf<int32_t> arena_cands;             // candidate caller indices per chunk slot
+    DBuf<WalkBatch> arena_batches;
+    bool rec_valid = false;    // arena holds the test pass of (rec_h, rec_hsum, rec_exact)
+    const double *rec_h = nullptr;
+    long long rec_hsum = 0;
+    int rec_exact = 0;
     DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
     DBuf<int2> stack;          // walk stacks (per resident warp)
     int64_t stack_per_warp = 0;
@@ -143,8 +158,7 @@ void build_tree(TreeDev &t, const double *pos);
 void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets,
                     int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass);
 
-// Device scans (scan.cu)
-void exclusive_scan_i32_to_i64(const int32_t *in, int64_t *out, int64_t n, int64_t *total_dev);
+void set_exact_only(int on);
 
 // ---------------------------------------------------------------------------
 // Eq. 2 with the clamp of reading R8, evaluated exactly as

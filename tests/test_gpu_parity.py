@@ -247,3 +247,48 @@ def test_search_host_end_to_end(P, oracle):
     with pytest.raises(P.BtreeError) as e:
         P.search_host(torch.from_numpy(pos), torch.from_numpy(h), capacity=cap - 1)
     assert e.value.code == 3
+
+
+# ---- the fp32 pre-test (lemma L4) decides nothing the fp64 predicate would not --
+@pytest.mark.parametrize("case", ["boundary", "cfg2", "cfg5", "far_origin", "tiny_h"])
+def test_exact_only_mode_identical(P, oracle, case):
+    if case == "boundary":
+        pos, h = datagen.near_boundary(2048, 64, 23)
+    elif case == "cfg2":
+        pos, h = datagen.make_config(2, n=150_000)
+    elif case == "cfg5":
+        pos, h = datagen.make_config(5, n=300_000)
+    elif case == "far_origin":   # large |x| relative to h: wide fp32 error band
+        pos, h = datagen.uniform(40_000, 29, 0.01, 0.02)
+        pos = np.ascontiguousarray(pos + 1.0e4)
+    else:                        # h so small that the fp32 squares underflow
+        pos, h = datagen.uniform(20_000, 31, 1e-5)
+        pos = np.ascontiguousarray(pos * 1e-3)
+    ref = oracle.brute_force(pos, h) if pos.shape[0] <= 50_000 else oracle.Tree(pos, 64).neighbors(h)
+    try:
+        P.set_exact_only(True)
+        _, g_exact = gpu_run(P, pos, h)
+    finally:
+        P.set_exact_only(False)
+    t, g_fast = gpu_run(P, pos, h)
+    assert_same(g_exact, ref)
+    assert_same(g_fast, ref)
+    st = t.stats()
+    assert st["exact_tests"] <= st["tests"]
+
+
+def test_fill_reuses_or_recomputes_record(P, oracle):
+    pos, h = datagen.make_config(2, n=60_000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd = torch.from_numpy(h).to(DEV)
+    c, off = t.count(hd)
+    nb = t.fill(hd, off)                      # reuses the recorded test pass
+    ref = oracle.Tree(pos, 64).neighbors(h)
+    assert_same((c.cpu().numpy(), off.cpu().numpy(), sort_rows(c, off, nb)), ref)
+    h2 = h * 1.05
+    hd2 = torch.from_numpy(h2).to(DEV)
+    c2, off2 = t.count(hd2)
+    hd.copy_(hd2)                             # same pointer, new values: must recompute
+    nb2 = t.fill(hd, off2)
+    ref2 = oracle.Tree(pos, 64).neighbors(h2)
+    assert_same((c2.cpu().numpy(), off2.cpu().numpy(), sort_rows(c2, off2, nb2)), ref2)
