@@ -148,7 +148,7 @@ struct TreeDev {
     long long rec_hsum = 0;
     int rec_exact = 0;
     DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
-    DBuf<int2> stack;          // walk stacks (per resident warp)
+    DBuf<int32_t> front;       // walk frontier scratch (per resident warp)
     int64_t stack_per_warp = 0;
     int64_t total_pairs = 0, max_count = 0, staged = 0, tests = 0, exact_tests = 0;
 };

@@ -6,25 +6,24 @@
 // from an atomic counter.
 //
 // Test pass (count), per unit:
-//   A10  descend from the root with Eq. 5 index ranges of the unit's query box
-//        widened by R'_u = max_i R'_i (lemma L1/L2): empty cells
-//        skipped, internal cells pushed on a per-warp stack (depth first),
-//        leaf cells culled by their tight bounding box (L3);
-//        stage the surviving leaves' particles into shared memory, culled per
-//        particle against the query box in fp64 (Minkowski test, L3), as fp32
-//        coordinates relative to the unit centre;
+//   A10  breadth-first descent from the root with Eq. 5 index ranges of the
+//        unit's query box widened by R'_u = max_i R'_i (lemma L1/L2,
+//        DESIGN.md): all cells of all frontier nodes of a level are flattened
+//        over the 32 lanes; empty cells skipped, internal cells form the next
+//        frontier, leaf cells are culled by their tight box (L3) and queued;
+//        queued leaves' particles are staged (flattened, two loads in flight
+//        per lane), culled per particle against the query box in fp64 (L3),
+//        as fp32 coordinates relative to the unit centre;
 //   A11  lanes = candidates (two per lane, packed f32x2), loop over queries:
-//        s32 = fp32 squared distance; s32 < A_i -> certainly a neighbor,
-//        s32 >= B_i -> certainly not, else the exact fp64 predicate
-//        ((dx*dx + dy*dy) + dz*dz) < (2h)^2 decides (lemma L4 gives A_i, B_i
-//        from the error bound of the fp32 evaluation):
-//        the recorded neighbor set is exactly the fp64 one.
-//        __ballot_sync gives the per-(query, 64-candidate chunk) neighbor
-//        masks; their __popc sums are the counts.  The masks and the chunk's
-//        candidate indices are recorded in an arena.
+//        s32 < A_i -> certainly a neighbor, s32 >= B_i -> certainly not, else
+//        the exact fp64 predicate ((dx*dx + dy*dy) + dz*dz) < (2h)^2 decides
+//        (lemma L4).  __ballot_sync gives a 64-bit
+//        neighbor mask per (64-candidate chunk, query), kept in shared memory;
+//        __popc of the masks are the counts; masks and the chunk's candidate
+//        indices are recorded in an arena for the fill pass.
 // Scan (A12): offsets = exclusive scan of counts.
-// Fill pass (A13): replay the recorded masks: __popc(mask & lanemask_lt)
-//        gives each neighbor's slot in its CSR row; coalesced row writes.
+// Fill pass (A13): replay the recorded masks: __popc(mask & lanemask_lt) is
+//        each neighbor's slot in its CSR row; coalesced row writes.
 #include <algorithm>
 #include <cfloat>
 
@@ -36,9 +35,12 @@ namespace bt {
 namespace {
 
 constexpr int kQ = 64;          // queries per unit (== build.cu kUnitQ)
-constexpr int kCand = 256;      // staged candidates per warp and batch
+constexpr int kCand = 256;      // staged candidates per batch
+constexpr int kChunks = kCand / 64;
+constexpr int kLeafCap = 128;   // queued candidate leaves
 constexpr int kWarpsPerBlock = 4;
 constexpr int kWalkThreads = kWarpsPerBlock * 32;
+constexpr int kFillThreads = 256;
 
 // device counters (int64 slots of TreeDev::counters)
 enum {
@@ -58,16 +60,15 @@ enum {
 using Batch = WalkBatch;
 
 struct WarpSmem {
-    float4 q0[kQ];              // ax, ax, ay, ay   (fp32, relative to the unit centre)
-    float4 q1[kQ];              // az, az, A, B     (certain-accept / certain-reject thresholds)
-    double qx[kQ], qy[kQ], qz[kQ], qT[kQ];  // fp64 query data for the exact band
-    int32_t qpos[kQ];
-    int32_t qorig[kQ];
-    int32_t qself[kQ];          // batch-local slot of the query itself, -1 if not in this batch
+    float4 q0[kQ];                         // ax, ax, ay, ay  (fp32, relative to the unit centre)
+    float4 q1[kQ];                         // az, az, A, B    (certain-accept / certain-reject)
+    int32_t qself[kQ];                     // batch slot of the query itself, -1 if not staged in this batch
     float2 px[kCand / 2], py[kCand / 2], pz[kCand / 2];  // chunk k, lane l: (c[64k+l], c[64k+32+l])
-    int32_t cpos[kCand];
-    int32_t corig[kCand];
-    int32_t leafq[32];
+    int32_t cpos[kCand];                   // tree position of each staged candidate
+    int32_t corig[kCand];                  // caller index of each staged candidate
+    unsigned long long mask[kChunks][kQ];  // neighbor masks of the batch
+    int32_t lbeg[kLeafCap + 1];              // queued leaves: first tree position
+    int32_t lpre[kLeafCap + 1];            // queued leaves: exclusive prefix of counts
 };
 
 struct WalkArgs {
@@ -83,8 +84,8 @@ struct WalkArgs {
     double M;
     int root_is_leaf;
     int exact_only;
-    int2 *stack;
-    int64_t stack_per_warp;
+    int32_t *front;           // per-warp frontier scratch: 2 x front_cap node ids
+    int64_t front_cap;
     int32_t *counts;
     const int64_t *offsets;
     int32_t *nbr;
@@ -109,8 +110,8 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 // packed fp32 pair arithmetic (sm_100a FADD2 / FMUL2 / FFMA2)
-__device__ __forceinline__ unsigned long long f2(float2 v) {
-    return ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x);
+__device__ __forceinline__ unsigned long long pk(float lo, float hi) {
+    return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
 }
 __device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
     unsigned long long r;
@@ -148,7 +149,7 @@ __device__ __forceinline__ void l4_thresholds(double T, double E, bool exact_onl
         return;
     }
     const double eps = u * E + w * (1.0 + u) * E + 0x1p-149;  // |a - (x - c)| per coordinate
-    const double a0 = 2.0 * eps * (1.0 + w) + 0x1p-150;        // |d - D| = a0 + w |D|
+    const double a0 = 2.0 * eps * (1.0 + w) + 0x1p-150;        // |d - D| <= a0 + w |D|
     const double g3 = 3.0 * w / (1.0 - 3.0 * w);
     auto err = [&](double S) {
         double D = 3.0 * a0 * a0 + 2.0 * 1.7320508075688775 * a0 * (1.0 + w) * sqrt(S) + (2.0 * w + w * w) * S;
@@ -165,74 +166,55 @@ __device__ __forceinline__ void l4_thresholds(double T, double E, bool exact_onl
     B = (hb < 3.0e38) ? __double2float_ru(hb) : __int_as_float(0x7f800000);
 }
 
-// squared distance from point to box [lo, hi], fp64 rounded ops
-__device__ __forceinline__ double box_gap2(double x, double y, double z, const double *lo, const double *hi) {
-    double gx = fmax(0.0, fmax(__dsub_rn(lo[0], x), __dsub_rn(x, hi[0])));
-    double gy = fmax(0.0, fmax(__dsub_rn(lo[1], y), __dsub_rn(y, hi[1])));
-    double gz = fmax(0.0, fmax(__dsub_rn(lo[2], z), __dsub_rn(z, hi[2])));
+// squared distance from a point to the box [lo, hi], fp64 rounded ops
+__device__ __forceinline__ double box_gap2(double x, double y, double z, double lx, double ly, double lz, double hx,
+                                           double hy, double hz) {
+    double gx = fmax(0.0, fmax(__dsub_rn(lx, x), __dsub_rn(x, hx)));
+    double gy = fmax(0.0, fmax(__dsub_rn(ly, y), __dsub_rn(y, hy)));
+    double gz = fmax(0.0, fmax(__dsub_rn(lz, z), __dsub_rn(z, hz)));
     return __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
 }
 
-// ---------------------------------------------------------------------------
-// Test pass
-// ---------------------------------------------------------------------------
-struct CountState {
-    int nq;
-    int c0, c1;           // counts of queries lane, lane + 32
+// per-unit state, held in registers (every field warp-uniform unless noted)
+struct Unit {
+    int64_t id;
+    int q0, nq;
+    double lo[3], hi[3], c[3];
+    double Ru, Ru2;
+    int ncand;        // staged candidates in the current batch
+    int nleaf;        // queued leaves
     int prev_batch;
-    long long tests, exact;
+    int cnt0, cnt1;   // per lane: counts of queries lane, lane + 32
+    long long staged, tests, exact;
 };
 
-// Test all queries of the unit against the staged batch [0, ncand), record
-// masks and candidates, accumulate counts.
-__device__ __noinline__ void test_batch(WarpSmem &S, int ncand, CountState &st, int lane, const WalkArgs &a,
-                                        int64_t unit) {
+// ---------------------------------------------------------------------------
+// A11: test the staged batch against all queries, record it, count.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
+    const int ncand = U.ncand;
+    const int nq = U.nq;
     const int nch = (ncand + 63) >> 6;
     const float inf = __int_as_float(0x7f800000);
-    // pad the last chunk with +inf coordinates (s32 = +inf: never a neighbor)
+    // pad the last chunk: +inf coordinates never pass (s32 = +inf)
     for (int c = ncand + lane; c < nch * 64; c += 32) {
-        int k = c >> 6, l = c & 31, hi = (c >> 5) & 1;
-        float *px = reinterpret_cast<float *>(&S.px[32 * k + l]);
-        float *py = reinterpret_cast<float *>(&S.py[32 * k + l]);
-        float *pz = reinterpret_cast<float *>(&S.pz[32 * k + l]);
-        px[hi] = inf;
-        py[hi] = inf;
-        pz[hi] = inf;
+        const int k = c >> 6, l = c & 31, hi = (c >> 5) & 1;
+        reinterpret_cast<float *>(&S.px[32 * k + l])[hi] = inf;
+        reinterpret_cast<float *>(&S.py[32 * k + l])[hi] = inf;
+        reinterpret_cast<float *>(&S.pz[32 * k + l])[hi] = inf;
         S.corig[c] = -1;
         S.cpos[c] = -1;
     }
-    // arena allocation for this batch
-    long long mb = 0, cb = 0, bi = 0;
-    if (lane == 0) {
-        mb = atomicAdd((unsigned long long *)&a.ctr[C_MASK], (unsigned long long)(nch * st.nq));
-        cb = atomicAdd((unsigned long long *)&a.ctr[C_CAND], (unsigned long long)(nch * 64));
-        bi = atomicAdd((unsigned long long *)&a.ctr[C_BATCH], 1ull);
-    }
-    mb = __shfl_sync(0xffffffffu, mb, 0);
-    cb = __shfl_sync(0xffffffffu, cb, 0);
-    bi = __shfl_sync(0xffffffffu, bi, 0);
-    const bool record = (mb + (long long)nch * st.nq <= a.mask_cap) && (cb + (long long)nch * 64 <= a.cand_cap) &&
-                        (bi < a.batch_cap);
     __syncwarp();
-    if (record) {
-        for (int c = lane; c < nch * 64; c += 32) a.cands[cb + c] = S.corig[c];
-        if (lane == 0) {
-            a.batches[bi] = Batch{mb, cb, ncand, -1};
-            if (st.prev_batch >= 0) a.batches[st.prev_batch].next = (int)bi;
-            else a.head[unit] = (int)bi;
-        }
-        st.prev_batch = (int)bi;
-    }
     for (int k = 0; k < nch; k++) {
-        const unsigned long long cx = f2(S.px[32 * k + lane]);
-        const unsigned long long cy = f2(S.py[32 * k + lane]);
-        const unsigned long long cz = f2(S.pz[32 * k + lane]);
-        const int cp0 = S.cpos[64 * k + lane], cp1 = S.cpos[64 * k + 32 + lane];
-        for (int q = 0; q < st.nq; q++) {
+        const float2 vx = S.px[32 * k + lane], vy = S.py[32 * k + lane], vz = S.pz[32 * k + lane];
+        const unsigned long long cx = pk(vx.x, vx.y), cy = pk(vy.x, vy.y), cz = pk(vz.x, vz.y);
+#pragma unroll 2
+        for (int q = 0; q < nq; q++) {
             const float4 Q0 = S.q0[q], Q1 = S.q1[q];
-            unsigned long long dx = f2_sub(cx, f2(make_float2(Q0.x, Q0.y)));
-            unsigned long long dy = f2_sub(cy, f2(make_float2(Q0.z, Q0.w)));
-            unsigned long long dz = f2_sub(cz, f2(make_float2(Q1.x, Q1.y)));
+            const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
+            const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
+            const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
             unsigned long long s = f2_mul(dx, dx);
             s = f2_fma(dy, dy, s);
             s = f2_fma(dz, dz, s);
@@ -243,191 +225,317 @@ __device__ __noinline__ void test_batch(WarpSmem &S, int ncand, CountState &st, 
             unsigned m1 = __ballot_sync(0xffffffffu, a1);
             if (__any_sync(0xffffffffu, u0 || u1)) {
                 // exact band: the fp64 predicate decides (rare)
-                const double qx = S.qx[q], qy = S.qy[q], qz = S.qz[q], T = S.qT[q];
-                const int qp = S.qpos[q];
+                const int qp = U.q0 + q;
+                const double4 Qr = a.rec[qp];
+                const double t = __dmul_rn(2.0, a.h_tree[qp]);
+                const double T = __dmul_rn(t, t);
                 bool e0 = false, e1 = false;
-                if (u0) e0 = cp0 != qp && exact_pair(qx, qy, qz, T, a.rec[cp0]);
-                if (u1) e1 = cp1 != qp && exact_pair(qx, qy, qz, T, a.rec[cp1]);
+                const int cp0 = S.cpos[64 * k + lane], cp1 = S.cpos[64 * k + 32 + lane];
+                if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
+                if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
                 m0 |= __ballot_sync(0xffffffffu, e0);
                 m1 |= __ballot_sync(0xffffffffu, e1);
-                st.exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
+                U.exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
             }
-            // self is never its own neighbor (R12)
-            const int sl = S.qself[q] - 64 * k;
-            if ((unsigned)sl < 64u) {
-                if (sl < 32) m0 &= ~(1u << sl);
-                else m1 &= ~(1u << (sl - 32));
-            }
-            const int pc = __popc(m0) + __popc(m1);
-            if (q < 32) st.c0 += (lane == q) ? pc : 0;
-            else st.c1 += (lane == q - 32) ? pc : 0;
-            if (record && lane == 0) a.masks[mb + (long long)k * st.nq + q] = ((unsigned long long)m1 << 32) | m0;
+            if (lane == 0) S.mask[k][q] = ((unsigned long long)m1 << 32) | m0;
         }
     }
-    st.tests += (long long)ncand * st.nq;
+    __syncwarp();
+    // self is never its own neighbor (R12); counts; record the batch
+    for (int q = lane; q < nq; q += 32) {
+        const int sl = S.qself[q];
+        if (sl >= 0) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
+        int c = 0;
+        for (int k = 0; k < nch; k++) c += __popcll(S.mask[k][q]);
+        if (q < 32) U.cnt0 += c;
+        else U.cnt1 += c;
+        S.qself[q] = -1;
+    }
+    long long mb = 0, cb = 0, bi = 0;
+    if (lane == 0) {
+        mb = atomicAdd((unsigned long long *)&a.ctr[C_MASK], (unsigned long long)(nch * nq));
+        cb = atomicAdd((unsigned long long *)&a.ctr[C_CAND], (unsigned long long)(nch * 64));
+        bi = atomicAdd((unsigned long long *)&a.ctr[C_BATCH], 1ull);
+    }
+    mb = __shfl_sync(0xffffffffu, mb, 0);
+    cb = __shfl_sync(0xffffffffu, cb, 0);
+    bi = __shfl_sync(0xffffffffu, bi, 0);
+    const bool record = (mb + (long long)nch * nq <= a.mask_cap) && (cb + (long long)nch * 64 <= a.cand_cap) &&
+                        (bi < a.batch_cap);
+    __syncwarp();
+    if (record) {
+        for (int c = lane; c < nch * 64; c += 32) a.cands[cb + c] = S.corig[c];
+        for (int w = lane; w < nch * nq; w += 32) a.masks[mb + w] = S.mask[w / nq][w % nq];
+        if (lane == 0) {
+            a.batches[bi] = Batch{mb, cb, ncand, -1};
+            if (U.prev_batch >= 0) a.batches[U.prev_batch].next = (int)bi;
+            else a.head[U.id] = (int)bi;
+        }
+        U.prev_batch = (int)bi;
+    }
+    U.tests += (long long)ncand * nq;
+    U.ncand = 0;
+    __syncwarp();
 }
 
-__global__ void __launch_bounds__(kWalkThreads) test_kernel(WalkArgs a) {
+// ---------------------------------------------------------------------------
+// Stage the queued leaves' particles (flattened over the lanes, two loads in
+// flight per lane), per-particle cull (L3), fp32 relative coordinates.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
+    const unsigned lt = lanemask_lt();
+    const int nl = U.nleaf;
+    // exclusive prefix of the queued leaf counts (lpre was filled with counts)
+    int carry = 0;
+    for (int i0 = 0; i0 < nl; i0 += 32) {
+        const int i = i0 + lane;
+        const int v = (i < nl) ? S.lpre[i] : 0;
+        int inc = v;
+        for (int d = 1; d < 32; d <<= 1) {
+            int o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += o;
+        }
+        if (i < nl) S.lpre[i] = carry + inc - v;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) S.lpre[nl] = carry;
+    __syncwarp();
+    const int total = carry;
+    int owner = 0;  // queued leaf that holds flattened position p0
+    for (int p0 = 0; p0 < total; p0 += 64) {
+        if (U.ncand + 64 > kCand) test_batch(S, U, lane, a);
+        double4 r[2];
+        int pos[2];
+        bool valid[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int w0 = p0 + 32 * h;
+            // owners of the 32 positions [w0, w0 + 32): leaf starts inside the window
+            const int nxt = owner + 1 + lane;
+            const int st = (nxt <= nl) ? S.lpre[nxt] : 0x7fffffff;
+            const int off = st - w0;  // >= 1 for leaves after `owner` (until it crosses)
+            const unsigned bits = __reduce_or_sync(0xffffffffu, (off >= 1 && off < 32) ? (1u << off) : 0u);
+            const int mine = owner + __popc(bits & ((2u << lane) - 1u));
+            const unsigned past = __ballot_sync(0xffffffffu, off <= 32);  // starts at or before w0 + 32
+            const int p = w0 + lane;
+            valid[h] = p < total;
+            pos[h] = valid[h] ? S.lbeg[mine] + (p - S.lpre[mine]) : 0;
+            owner += __popc(past);
+            if (valid[h]) r[h] = a.rec[pos[h]];
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const bool keep = valid[h] && box_gap2(r[h].x, r[h].y, r[h].z, U.lo[0], U.lo[1], U.lo[2], U.hi[0], U.hi[1],
+                                                U.hi[2]) < U.Ru2;
+            const unsigned km = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int slot = U.ncand + __popc(km & lt);
+                const int ck = slot >> 6, cl = slot & 31, ch = (slot >> 5) & 1;
+                reinterpret_cast<float *>(&S.px[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r[h].x, U.c[0]));
+                reinterpret_cast<float *>(&S.py[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r[h].y, U.c[1]));
+                reinterpret_cast<float *>(&S.pz[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r[h].z, U.c[2]));
+                S.cpos[slot] = pos[h];
+                S.corig[slot] = (int32_t)__double_as_longlong(r[h].w);
+                const int qi = pos[h] - U.q0;
+                if (qi >= 0 && qi < U.nq) S.qself[qi] = slot;
+            }
+            U.ncand += __popc(km);
+            U.staged += __popc(km);
+        }
+        __syncwarp();
+    }
+    U.nleaf = 0;
+    __syncwarp();
+}
+
+// queue a leaf (if its tight box is within R'_u of the query box: L3)
+__device__ __forceinline__ void queue_leaves(WarpSmem &S, Unit &U, int lane, const WalkArgs &a, bool is_leaf,
+                                             int32_t leaf) {
+    const unsigned lt = lanemask_lt();
+    bool keep = false;
+    if (is_leaf) {
+        const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
+        const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
+        double gx = fmax(0.0, fmax(__dsub_rn(b0.x, U.hi[0]), __dsub_rn(U.lo[0], b1.y)));
+        double gy = fmax(0.0, fmax(__dsub_rn(b0.y, U.hi[1]), __dsub_rn(U.lo[1], b2.x)));
+        double gz = fmax(0.0, fmax(__dsub_rn(b1.x, U.hi[2]), __dsub_rn(U.lo[2], b2.y)));
+        double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
+        keep = g2 < U.Ru2;
+    }
+    const unsigned km = __ballot_sync(0xffffffffu, keep);
+    if (!km) return;
+    if (U.nleaf + __popc(km) > kLeafCap) stage_leaves(S, U, lane, a);
+    if (keep) {
+        const int slot = U.nleaf + __popc(km & lt);
+        S.lbeg[slot] = a.leaf_begin[leaf];
+        S.lpre[slot] = a.leaf_count[leaf];  // counts; stage_leaves turns them into a prefix
+    }
+    U.nleaf += __popc(km);
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
     __shared__ WarpSmem smem[kWarpsPerBlock];
     const int lane = threadIdx.x & 31;
     WarpSmem &S = smem[threadIdx.x >> 5];
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int2 *stk = a.stack + gwarp * a.stack_per_warp;
+    int32_t *const front_base = a.front + gwarp * 2 * a.front_cap;
     const unsigned lt = lanemask_lt();
     long long staged = 0, tests = 0, exact = 0;
 
     for (;;) {
-        unsigned long long u = 0;
-        if (lane == 0) u = atomicAdd((unsigned long long *)&a.ctr[C_WORK], 1ull);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= (unsigned long long)a.n_units) break;
-        const int4 U = a.units[u];
-        const int q0 = U.y;
-        CountState st;
-        st.nq = U.z;
-        st.c0 = st.c1 = 0;
-        st.prev_batch = -1;
-        st.tests = st.exact = 0;
-        if (lane == 0) a.head[u] = -1;
+        unsigned long long uid = 0;
+        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK], 1ull);
+        uid = __shfl_sync(0xffffffffu, uid, 0);
+        if (uid >= (unsigned long long)a.n_units) break;
+        const int4 UU = a.units[uid];
+        Unit U;
+        U.id = (int64_t)uid;
+        U.q0 = UU.y;
+        U.nq = UU.z;
+        U.ncand = U.nleaf = 0;
+        U.prev_batch = -1;
+        U.cnt0 = U.cnt1 = 0;
+        U.staged = U.tests = U.exact = 0;
+        if (lane == 0) a.head[uid] = -1;
 
-        // ---- query box, R'_u
+        // ---- queries: coordinates, (2h)^2, R', box
+        double qx[2], qy[2], qz[2], qT[2];
+        int32_t qo[2] = {0, 0};
         double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
         double Ru = 0.0;
-        for (int k = lane; k < st.nq; k += 32) {
-            int32_t p = q0 + k;
-            double4 r = a.rec[p];
-            double t = __dmul_rn(2.0, a.h_tree[p]);  // 2h (exact)
-            S.qx[k] = r.x;
-            S.qy[k] = r.y;
-            S.qz[k] = r.z;
-            S.qT[k] = __dmul_rn(t, t);
-            S.qpos[k] = p;
-            S.qorig[k] = (int32_t)__double_as_longlong(r.w);
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int k = lane + 32 * h;
+            qx[h] = qy[h] = qz[h] = qT[h] = 0.0;
+            if (k < U.nq) {
+                const double4 r = a.rec[U.q0 + k];
+                const double t = __dmul_rn(2.0, a.h_tree[U.q0 + k]);  // 2h (exact)
+                qx[h] = r.x;
+                qy[h] = r.y;
+                qz[h] = r.z;
+                qT[h] = __dmul_rn(t, t);
+                qo[h] = (int32_t)__double_as_longlong(r.w);
+                // R' = 2h (1 + 2^-40) + 2^-50 M   (lemma L1/L2)
+                Ru = fmax(Ru, __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M)));
+                lo[0] = fmin(lo[0], r.x); lo[1] = fmin(lo[1], r.y); lo[2] = fmin(lo[2], r.z);
+                hi[0] = fmax(hi[0], r.x); hi[1] = fmax(hi[1], r.y); hi[2] = fmax(hi[2], r.z);
+            }
             S.qself[k] = -1;
-            // R' = 2h (1 + 2^-40) + 2^-50 M   (lemma L1/L2)
-            double Rp = __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M));
-            Ru = fmax(Ru, Rp);
-            lo[0] = fmin(lo[0], r.x); lo[1] = fmin(lo[1], r.y); lo[2] = fmin(lo[2], r.z);
-            hi[0] = fmax(hi[0], r.x); hi[1] = fmax(hi[1], r.y); hi[2] = fmax(hi[2], r.z);
         }
-        for (int l = 0; l < 3; l++) { lo[l] = warp_min(lo[l]); hi[l] = warp_max(hi[l]); }
-        Ru = warp_max(Ru);
-        const double Ru2 = __dmul_rn(Ru, Ru);
-        // unit centre c and the a-priori coordinate bound E (|x - c| <= E per
-        // axis for every query and every staged candidate)
-        double c[3], E = 0.0, Mu = 0.0;
+        double E = 0.0, Mu = 0.0;
         for (int l = 0; l < 3; l++) {
-            c[l] = 0.5 * (lo[l] + hi[l]);
-            E = fmax(E, 0.5 * (hi[l] - lo[l]));
-            Mu = fmax(Mu, fmax(fabs(lo[l]), fabs(hi[l])));
+            U.lo[l] = warp_min(lo[l]);
+            U.hi[l] = warp_max(hi[l]);
+            U.c[l] = 0.5 * (U.lo[l] + U.hi[l]);
+            E = fmax(E, 0.5 * (U.hi[l] - U.lo[l]));
+            Mu = fmax(Mu, fmax(fabs(U.lo[l]), fabs(U.hi[l])));
         }
-        E = (E + Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
-        for (int k = lane; k < st.nq; k += 32) {
-            float ax = __double2float_rn(__dsub_rn(S.qx[k], c[0]));
-            float ay = __double2float_rn(__dsub_rn(S.qy[k], c[1]));
-            float az = __double2float_rn(__dsub_rn(S.qz[k], c[2]));
-            float A, B;
-            l4_thresholds(S.qT[k], E, a.exact_only != 0, A, B);
-            S.q0[k] = make_float4(ax, ax, ay, ay);
-            S.q1[k] = make_float4(az, az, A, B);
+        U.Ru = warp_max(Ru);
+        U.Ru2 = __dmul_rn(U.Ru, U.Ru);
+        // a-priori bound |x - c| <= E per axis for queries and staged candidates (L4)
+        E = (E + U.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int k = lane + 32 * h;
+            if (k < U.nq) {
+                const float ax = __double2float_rn(__dsub_rn(qx[h], U.c[0]));
+                const float ay = __double2float_rn(__dsub_rn(qy[h], U.c[1]));
+                const float az = __double2float_rn(__dsub_rn(qz[h], U.c[2]));
+                float A, B;
+                l4_thresholds(qT[h], E, a.exact_only != 0, A, B);
+                S.q0[k] = make_float4(ax, ax, ay, ay);
+                S.q1[k] = make_float4(az, az, A, B);
+            }
         }
         __syncwarp();
 
-        int ncand = 0;
-        auto stage_leaf = [&](int32_t L) {
-            const int32_t b0 = a.leaf_begin[L], m = a.leaf_count[L];
-            for (int k0 = 0; k0 < m; k0 += 32) {
-                if (ncand + 32 > kCand) {
-                    __syncwarp();
-                    test_batch(S, ncand, st, lane, a, (int64_t)u);
-                    for (int k = lane; k < st.nq; k += 32) S.qself[k] = -1;
-                    ncand = 0;
-                    __syncwarp();
-                }
-                int k = k0 + lane;
-                bool keep = false;
-                double4 r;
-                if (k < m) {
-                    r = a.rec[b0 + k];
-                    keep = box_gap2(r.x, r.y, r.z, lo, hi) < Ru2;
-                }
-                unsigned km = __ballot_sync(0xffffffffu, keep);
-                if (keep) {
-                    int slot = ncand + __popc(km & lt);
-                    int ck = slot >> 6, cl = slot & 31, ch = (slot >> 5) & 1;
-                    reinterpret_cast<float *>(&S.px[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r.x, c[0]));
-                    reinterpret_cast<float *>(&S.py[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r.y, c[1]));
-                    reinterpret_cast<float *>(&S.pz[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r.z, c[2]));
-                    S.cpos[slot] = b0 + k;
-                    S.corig[slot] = (int32_t)__double_as_longlong(r.w);
-                    const int qi = b0 + k - q0;
-                    if (qi >= 0 && qi < st.nq) S.qself[qi] = slot;
-                }
-                ncand += __popc(km);
-                staged += (lane == 0) ? __popc(km) : 0;
-            }
-        };
-
+        // ---- A10: breadth-first descent, all cells of a level flattened over the lanes
         if (a.root_is_leaf) {
-            stage_leaf(0);
+            queue_leaves(S, U, lane, a, lane == 0, 0);
         } else {
-            // ---- A10: depth-first descent with Eq. 5 ranges
-            int top = 1;
-            if (lane == 0) stk[0] = make_int2(0, 0);
+            int32_t *fcur = front_base, *fnext = front_base + a.front_cap;
+            int nf = 1;
+            if (lane == 0) fcur[0] = 0;
             __syncwarp();
-            while (top > 0) {
-                const int2 e = stk[top - 1];
-                const NodeRec &nd = a.nodes[e.x];
-                const int b = nd.b;
-                int r0[3], r1[3];
-                for (int l = 0; l < 3; l++) {
-                    r0[l] = cell_coord(__dsub_rn(lo[l], Ru), nd.lo[l], nd.ext[l], b);
-                    r1[l] = cell_coord(__dadd_rn(hi[l], Ru), nd.lo[l], nd.ext[l], b);
-                }
-                const long long nx = r1[0] - r0[0] + 1, ny = r1[1] - r0[1] + 1, nz = r1[2] - r0[2] + 1;
-                const long long total = nx * ny * nz;
-                const long long idx = (long long)e.y + lane;
-                bool is_leaf = false, is_node = false;
-                int32_t code = -1;
-                if (idx < total) {
-                    long long cx = r0[0] + idx % nx;
-                    long long cy = r0[1] + (idx / nx) % ny;
-                    long long cz = r0[2] + idx / (nx * ny);
-                    long long j = cx + cy * b + cz * (long long)b * b;  // Eq. 3
-                    code = a.cells[nd.cell_base + j];
-                    if (code >= 0) {
-                        // L3: cull the leaf if its tight box is farther than R'_u from the query box
-                        const double *lb = a.leaf_box + 6 * (int64_t)code;
-                        double gx = fmax(0.0, fmax(__dsub_rn(lb[0], hi[0]), __dsub_rn(lo[0], lb[3])));
-                        double gy = fmax(0.0, fmax(__dsub_rn(lb[1], hi[1]), __dsub_rn(lo[1], lb[4])));
-                        double gz = fmax(0.0, fmax(__dsub_rn(lb[2], hi[2]), __dsub_rn(lo[2], lb[5])));
-                        double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
-                        is_leaf = g2 < Ru2;
-                    } else if (code <= -2) {
-                        is_node = true;
+            while (nf > 0) {
+                int nnext = 0;
+                for (int f0 = 0; f0 < nf; f0 += 32) {
+                    const int fi = f0 + lane;
+                    int b = 0, r0x = 0, r0y = 0, r0z = 0, nx = 1, ny = 1;
+                    long long cb = 0, tot = 0;
+                    if (fi < nf) {
+                        const NodeRec &nd = a.nodes[fcur[fi]];
+                        b = nd.b;
+                        cb = nd.cell_base;
+                        int r0[3], r1[3];
+                        for (int l = 0; l < 3; l++) {
+                            r0[l] = cell_coord(__dsub_rn(U.lo[l], U.Ru), nd.lo[l], nd.ext[l], b);
+                            r1[l] = cell_coord(__dadd_rn(U.hi[l], U.Ru), nd.lo[l], nd.ext[l], b);
+                        }
+                        r0x = r0[0];
+                        r0y = r0[1];
+                        r0z = r0[2];
+                        nx = r1[0] - r0[0] + 1;
+                        ny = r1[1] - r0[1] + 1;
+                        tot = (long long)nx * ny * (r1[2] - r0[2] + 1);
+                    }
+                    // inclusive scan of the cell counts over the lanes
+                    long long inc = tot;
+                    for (int d = 1; d < 32; d <<= 1) {
+                        long long o = __shfl_up_sync(0xffffffffu, inc, d);
+                        if (lane >= d) inc += o;
+                    }
+                    const long long start = inc - tot;
+                    const long long T = __shfl_sync(0xffffffffu, inc, 31);
+                    int owner = 0;
+                    for (long long c0 = 0; c0 < T; c0 += 32) {
+                        // owner lane of cell g = c0 + lane (node starts inside the window)
+                        const long long off = start - c0;
+                        const unsigned bits =
+                            __reduce_or_sync(0xffffffffu, (lane > owner && off >= 1 && off < 32) ? (1u << off) : 0u);
+                        const int o = owner + __popc(bits & ((2u << lane) - 1u));
+                        const unsigned past = __ballot_sync(0xffffffffu, lane > owner && off <= 32);
+                        const int ob = __shfl_sync(0xffffffffu, b, o);
+                        const long long ocb = __shfl_sync(0xffffffffu, cb, o);
+                        const int ox = __shfl_sync(0xffffffffu, r0x, o), oy = __shfl_sync(0xffffffffu, r0y, o),
+                                  oz = __shfl_sync(0xffffffffu, r0z, o);
+                        const int onx = __shfl_sync(0xffffffffu, nx, o), ony = __shfl_sync(0xffffffffu, ny, o);
+                        const long long ostart = __shfl_sync(0xffffffffu, start, o);
+                        owner += __popc(past);
+                        const long long g = c0 + lane;
+                        bool is_leaf = false, is_node = false;
+                        int32_t code = -1;
+                        if (g < T) {
+                            const int local = (int)(g - ostart);
+                            const int cx = ox + local % onx;
+                            const int cy = oy + (local / onx) % ony;
+                            const int cz = oz + local / (onx * ony);
+                            const long long j = cx + (long long)cy * ob + (long long)cz * ob * ob;  // Eq. 3
+                            code = a.cells[ocb + j];
+                            is_leaf = code >= 0;
+                            is_node = code <= -2;
+                        }
+                        const unsigned nm = __ballot_sync(0xffffffffu, is_node);
+                        if (is_node) fnext[nnext + __popc(nm & lt)] = code_node(code);
+                        nnext += __popc(nm);
+                        queue_leaves(S, U, lane, a, is_leaf, code);
                     }
                 }
                 __syncwarp();
-                const long long next = (long long)e.y + 32;
-                if (next >= total) top--;
-                else if (lane == 0) stk[top - 1].y = (int)next;
-                unsigned nm = __ballot_sync(0xffffffffu, is_node);
-                if (is_node) stk[top + __popc(nm & lt)] = make_int2(code_node(code), 0);
-                top += __popc(nm);
-                unsigned lm = __ballot_sync(0xffffffffu, is_leaf);
-                if (is_leaf) S.leafq[__popc(lm & lt)] = code;
-                __syncwarp();
-                const int nl = __popc(lm);
-                for (int i = 0; i < nl; i++) stage_leaf(S.leafq[i]);
-                __syncwarp();
+                int32_t *tmp = fcur;
+                fcur = fnext;
+                fnext = tmp;
+                nf = nnext;
             }
         }
-        __syncwarp();
-        if (ncand > 0 || st.prev_batch < 0) test_batch(S, ncand, st, lane, a, (int64_t)u);
-        if (lane < st.nq) a.counts[S.qorig[lane]] = st.c0;
-        if (lane + 32 < st.nq) a.counts[S.qorig[lane + 32]] = st.c1;
-        tests += st.tests;
-        exact += st.exact;
+        if (U.nleaf > 0) stage_leaves(S, U, lane, a);
+        if (U.ncand > 0 || U.prev_batch < 0) test_batch(S, U, lane, a);
+        if (lane < U.nq) a.counts[qo[0]] = U.cnt0;
+        if (lane + 32 < U.nq) a.counts[qo[1]] = U.cnt1;
+        staged += U.staged;
+        tests += U.tests;
+        exact += U.exact;
         __syncwarp();
     }
     if (lane == 0) {
@@ -440,7 +548,7 @@ __global__ void __launch_bounds__(kWalkThreads) test_kernel(WalkArgs a) {
 // ---------------------------------------------------------------------------
 // Fill pass: replay the recorded masks into the CSR rows
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kWalkThreads) fill_kernel(WalkArgs a) {
+__global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     for (;;) {
@@ -548,14 +656,18 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     BT_CUDA(cudaStreamSynchronize(st));
     if (hbad) throw Error(BT_ERR_INPUT, "bt_find_neighbors: h must be finite, > 0 and <= 1e150");
 
-    // persistent grid: all resident warps
-    int per_sm = 0;
+    // persistent grids: all resident warps
+    int per_sm = 0, per_sm_fill = 0;
     BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, test_kernel, kWalkThreads, 0));
-    if (per_sm < 1) per_sm = 1;
+    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fill, fill_kernel, kFillThreads, 0));
+    per_sm = std::max(per_sm, 1);
+    per_sm_fill = std::max(per_sm_fill, 1);
     const unsigned grid = (unsigned)(sms * per_sm);
+    const unsigned grid_fill = (unsigned)(sms * per_sm_fill);
     const int64_t nwarps = (int64_t)grid * kWarpsPerBlock;
-    t.stack_per_warp = 33 * (int64_t)(t.depth + 2);
-    t.stack.reserve(nwarps * t.stack_per_warp, 0);
+    // frontier scratch: a unit's frontier holds each internal node at most once
+    const int64_t front_cap = std::max<int64_t>(t.n_nodes, 1);
+    t.front.reserve(nwarps * 2 * front_cap, 0);
     t.head.reserve(t.n_units, 0);
 
     // the recorded masks of a previous test pass are reused by a fill-only
@@ -576,8 +688,8 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     a.M = t.M;
     a.root_is_leaf = t.root_is_leaf ? 1 : 0;
     a.exact_only = g_exact_only;
-    a.stack = t.stack.p;
-    a.stack_per_warp = t.stack_per_warp;
+    a.front = t.front.p;
+    a.front_cap = front_cap;
     a.offsets = offsets;
     a.nbr = nbr_idx;
     a.ctr = (long long *)t.counters.p;
@@ -592,7 +704,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         }
         a.counts = cnt;
         // arena sized from the previous run on this thread (grown on overflow)
-        static thread_local double mask_per_q = 12.0, cand_per_q = 24.0, batch_per_unit = 1.5;
+        static thread_local double mask_per_q = 12.0, cand_per_q = 24.0, batch_per_unit = 3.0;
         for (int attempt = 0;; attempt++) {
             long long mcap = (long long)(mask_per_q * n) + 4096, ccap = (long long)(cand_per_q * n) + 4096;
             long long bcap = (long long)(batch_per_unit * t.n_units) + 1024;
@@ -620,7 +732,8 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             const bool fits = hc[C_MASK] <= a.mask_cap && hc[C_CAND] <= a.cand_cap && hc[C_BATCH] <= a.batch_cap;
             mask_per_q = std::max(mask_per_q, 1.1 * (double)hc[C_MASK] / (double)n);
             cand_per_q = std::max(cand_per_q, 1.1 * (double)hc[C_CAND] / (double)n);
-            batch_per_unit = std::max(batch_per_unit, 1.1 * (double)hc[C_BATCH] / (double)std::max<int64_t>(1, t.n_units));
+            batch_per_unit =
+                std::max(batch_per_unit, 1.1 * (double)hc[C_BATCH] / (double)std::max<int64_t>(1, t.n_units));
             if (fits || !fill_pass || nbr_idx == nullptr) {
                 t.rec_valid = fits;
                 t.rec_h = h;
@@ -660,7 +773,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     BT_CUDA(cudaMemsetAsync(t.counters.p + C_WORK2, 0, sizeof(int64_t), st));
     {
         Phase ph("search.fill");
-        fill_kernel<<<grid, kWalkThreads, 0, st>>>(a);
+        fill_kernel<<<grid_fill, kFillThreads, 0, st>>>(a);
         BT_LAUNCH("walk_fill");
     }
     BT_CUDA(cudaStreamSynchronize(st));
