@@ -320,7 +320,7 @@ def run_b200(args):
                 "build_ms": kern["build"], "kernel_ms": kern, "gpu_launches": launches,
                 "roofline": roofline, "bj_hbm_roofline": bj_roof,
                 "tree": {k: st[k] for k in ("depth", "root_b", "nodes", "leaves", "halvings", "units")},
-                "walk_counters": {"staged": st["staged"], "tests": st["tests"], "exact_tests": st["exact_tests"]},
+                "walk_counters": {"loaded": st["loaded"], "staged": st["staged"], "tests": st["tests"], "exact_tests": st["exact_tests"]},
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if ws > 1:

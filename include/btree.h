@@ -155,6 +155,7 @@ typedef struct bt_stats {
     int64_t staged;       /* candidate records staged by the count pass       */
     int64_t tests;        /* pair tests issued by the count pass              */
     int64_t exact_tests;  /* pairs decided by the fp64 predicate itself       */
+    int64_t loaded;       /* particle records read by staging (before the cull) */
 } bt_stats;
 
 int bt_tree_stats(const bt_tree *t, bt_stats *out);

@@ -301,6 +301,7 @@ int bt_tree_stats(const bt_tree *t, bt_stats *out) {
     out->staged = d.staged;
     out->tests = d.tests;
     out->exact_tests = d.exact_tests;
+    out->loaded = d.loaded;
     return BT_OK;
 }
 

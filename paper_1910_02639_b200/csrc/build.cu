@@ -91,12 +91,29 @@ __global__ void __launch_bounds__(kThreads) pack_bbox_kernel(const double *__res
 
 // Root box: exact min/max, each side expanded by max(1e-9 * extent, 1e-12)
 // (reading R9).  Writes the root NodeRec lo/ext and box[0..6], M.
-__global__ void root_box_kernel(const double *partials, int nblocks, NodeRec *root, double *box) {
+__global__ void __launch_bounds__(256) root_box_kernel(const double *partials, int nblocks, NodeRec *root,
+                                                       double *box) {
+    __shared__ double sh[6][8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double v[6] = {INFINITY, INFINITY, INFINITY, -INFINITY, -INFINITY, -INFINITY};
+    for (int k = threadIdx.x; k < nblocks; k += blockDim.x)
+        for (int l = 0; l < 3; l++) {
+            v[l] = fmin(v[l], partials[6 * k + l]);
+            v[3 + l] = fmax(v[3 + l], partials[6 * k + 3 + l]);
+        }
+    for (int l = 0; l < 6; l++) {
+        for (int d = 16; d; d >>= 1) {
+            double o = __shfl_xor_sync(0xffffffffu, v[l], d);
+            v[l] = l < 3 ? fmin(v[l], o) : fmax(v[l], o);
+        }
+        if (lane == 0) sh[l][wid] = v[l];
+    }
+    __syncthreads();
     if (threadIdx.x != 0) return;
     double M = 0.0;
     for (int l = 0; l < 3; l++) {
         double a = INFINITY, b = -INFINITY;
-        for (int k = 0; k < nblocks; k++) { a = fmin(a, partials[6 * k + l]); b = fmax(b, partials[6 * k + 3 + l]); }
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) { a = fmin(a, sh[l][w]); b = fmax(b, sh[3 + l][w]); }
         double pad = __dmul_rn(1e-9, __dsub_rn(b, a));
         if (pad < 1e-12) pad = 1e-12;
         double lo = __dsub_rn(a, pad), hi = __dadd_rn(b, pad);
@@ -468,23 +485,30 @@ void build_tree(TreeDev &t, const double *pos) {
 
     DBuf<double4> act[2];
     DBuf<int32_t> act_node[2];
-    DBuf<double4> fin(n);
-    t.rec.alloc(n);
-    DBuf<int> dflags(4);
-    DBuf<unsigned long long> dstat(4);  // halvings, max_leaf
-    BT_CUDA(cudaMemsetAsync(dflags.p, 0, 4 * sizeof(int), st));
-    BT_CUDA(cudaMemsetAsync(dstat.p, 0, 4 * sizeof(unsigned long long), st));
+    DBuf<double4> fin;
+    DBuf<int> dflags;
+    DBuf<unsigned long long> dstat;  // halvings, max_leaf, overfull
+    DBuf<double> partials, dbox;
+    {
+        Phase ph("build.setup");
+        fin.alloc(n);
+        t.rec.alloc(n);
+        dflags.alloc(4);
+        dstat.alloc(4);
+        BT_CUDA(cudaMemsetAsync(dflags.p, 0, 4 * sizeof(int), st));
+        BT_CUDA(cudaMemsetAsync(dstat.p, 0, 4 * sizeof(unsigned long long), st));
+        partials.alloc(6 * (size_t)gridN);
+        dbox.alloc(8);
+        t.nodes.reserve(1024, 0);
+    }
 
     // A1: records in caller order + root box
-    DBuf<double> partials(6 * (size_t)gridN);
-    DBuf<double> dbox(8);
-    t.nodes.reserve(1024, 0);
     {
         Phase ph("build.bbox");
         act[0].alloc(n);
         pack_bbox_kernel<<<gridN, kThreads, 0, st>>>(pos, n, act[0].p, partials.p, dflags.p);
         BT_LAUNCH("pack_bbox");
-        root_box_kernel<<<1, 32, 0, st>>>(partials.p, (int)gridN, t.nodes.p, dbox.p);
+        root_box_kernel<<<1, 256, 0, st>>>(partials.p, (int)gridN, t.nodes.p, dbox.p);
         BT_LAUNCH("root_box");
         double hb[8];
         int hbad = 0;

@@ -54,6 +54,7 @@ enum {
     C_MAXC = 7,
     C_WORK2 = 8,     // unit counter (fill pass)
     C_HSUM = 9,      // checksum of h (bit patterns)
+    C_LOADED = 10,   // particle records loaded by staging (before the cull)
     C_N = 16
 };
 
@@ -181,17 +182,35 @@ struct Unit {
     int q0, nq;
     double lo[3], hi[3], c[3];
     double Ru, Ru2;
+    float blo[3], bhi[3];   // query box in fp32 relative coordinates
+    float cull2;            // fp32 Minkowski cull threshold (conservative)
     int ncand;        // staged candidates in the current batch
     int nleaf;        // queued leaves
     int prev_batch;
     int cnt0, cnt1;   // per lane: counts of queries lane, lane + 32
-    long long staged, tests, exact;
+    long long staged, loaded, tests, exact;
 };
+
+// The exact band of lemma L4: the fp64 predicate itself decides (rare path).
+__device__ __noinline__ void resolve_band(const WarpSmem &S, Unit &U, int lane, const WalkArgs &a, int k, int q,
+                                         bool u0, bool u1, unsigned &m0, unsigned &m1) {
+    const int qp = U.q0 + q;
+    const double4 Qr = a.rec[qp];
+    const double t = __dmul_rn(2.0, a.h_tree[qp]);
+    const double T = __dmul_rn(t, t);
+    bool e0 = false, e1 = false;
+    const int cp0 = S.cpos[64 * k + lane], cp1 = S.cpos[64 * k + 32 + lane];
+    if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
+    if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
+    m0 |= __ballot_sync(0xffffffffu, e0);
+    m1 |= __ballot_sync(0xffffffffu, e1);
+    U.exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
+}
 
 // ---------------------------------------------------------------------------
 // A11: test the staged batch against all queries, record it, count.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
+__device__ __noinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
     const int ncand = U.ncand;
     const int nq = U.nq;
     const int nch = (ncand + 63) >> 6;
@@ -223,20 +242,7 @@ __device__ __forceinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const
             const bool u0 = !a0 && s0 < Q1.w, u1 = !a1 && s1 < Q1.w;
             unsigned m0 = __ballot_sync(0xffffffffu, a0);
             unsigned m1 = __ballot_sync(0xffffffffu, a1);
-            if (__any_sync(0xffffffffu, u0 || u1)) {
-                // exact band: the fp64 predicate decides (rare)
-                const int qp = U.q0 + q;
-                const double4 Qr = a.rec[qp];
-                const double t = __dmul_rn(2.0, a.h_tree[qp]);
-                const double T = __dmul_rn(t, t);
-                bool e0 = false, e1 = false;
-                const int cp0 = S.cpos[64 * k + lane], cp1 = S.cpos[64 * k + 32 + lane];
-                if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
-                if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
-                m0 |= __ballot_sync(0xffffffffu, e0);
-                m1 |= __ballot_sync(0xffffffffu, e1);
-                U.exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
-            }
+            if (__any_sync(0xffffffffu, u0 || u1)) resolve_band(S, U, lane, a, k, q, u0, u1, m0, m1);
             if (lane == 0) S.mask[k][q] = ((unsigned long long)m1 << 32) | m0;
         }
     }
@@ -282,7 +288,7 @@ __device__ __forceinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const
 // Stage the queued leaves' particles (flattened over the lanes, two loads in
 // flight per lane), per-particle cull (L3), fp32 relative coordinates.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
+__device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
     const unsigned lt = lanemask_lt();
     const int nl = U.nleaf;
     // exclusive prefix of the queued leaf counts (lpre was filled with counts)
@@ -325,15 +331,23 @@ __device__ __forceinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, con
         }
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            const bool keep = valid[h] && box_gap2(r[h].x, r[h].y, r[h].z, U.lo[0], U.lo[1], U.lo[2], U.hi[0], U.hi[1],
-                                                U.hi[2]) < U.Ru2;
+            // fp32 relative coordinates a = fl32(fl64(x - c)) and the conservative
+            // fp32 Minkowski cull against the query box (L3 / L4)
+            const float ax = __double2float_rn(__dsub_rn(r[h].x, U.c[0]));
+            const float ay = __double2float_rn(__dsub_rn(r[h].y, U.c[1]));
+            const float az = __double2float_rn(__dsub_rn(r[h].z, U.c[2]));
+            const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[0], ax), __fsub_rn(ax, U.bhi[0])));
+            const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[1], ay), __fsub_rn(ay, U.bhi[1])));
+            const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[2], az), __fsub_rn(az, U.bhi[2])));
+            const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
+            const bool keep = valid[h] && g2 < U.cull2;
             const unsigned km = __ballot_sync(0xffffffffu, keep);
             if (keep) {
                 const int slot = U.ncand + __popc(km & lt);
                 const int ck = slot >> 6, cl = slot & 31, ch = (slot >> 5) & 1;
-                reinterpret_cast<float *>(&S.px[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r[h].x, U.c[0]));
-                reinterpret_cast<float *>(&S.py[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r[h].y, U.c[1]));
-                reinterpret_cast<float *>(&S.pz[32 * ck + cl])[ch] = __double2float_rn(__dsub_rn(r[h].z, U.c[2]));
+                reinterpret_cast<float *>(&S.px[32 * ck + cl])[ch] = ax;
+                reinterpret_cast<float *>(&S.py[32 * ck + cl])[ch] = ay;
+                reinterpret_cast<float *>(&S.pz[32 * ck + cl])[ch] = az;
                 S.cpos[slot] = pos[h];
                 S.corig[slot] = (int32_t)__double_as_longlong(r[h].w);
                 const int qi = pos[h] - U.q0;
@@ -341,6 +355,7 @@ __device__ __forceinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, con
             }
             U.ncand += __popc(km);
             U.staged += __popc(km);
+            U.loaded += __popc(__ballot_sync(0xffffffffu, valid[h]));
         }
         __syncwarp();
     }
@@ -381,7 +396,7 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int32_t *const front_base = a.front + gwarp * 2 * a.front_cap;
     const unsigned lt = lanemask_lt();
-    long long staged = 0, tests = 0, exact = 0;
+    long long staged = 0, loaded = 0, tests = 0, exact = 0;
 
     for (;;) {
         unsigned long long uid = 0;
@@ -396,7 +411,7 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
         U.ncand = U.nleaf = 0;
         U.prev_batch = -1;
         U.cnt0 = U.cnt1 = 0;
-        U.staged = U.tests = U.exact = 0;
+        U.staged = U.loaded = U.tests = U.exact = 0;
         if (lane == 0) a.head[uid] = -1;
 
         // ---- queries: coordinates, (2h)^2, R', box
@@ -435,6 +450,18 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
         U.Ru2 = __dmul_rn(U.Ru, U.Ru);
         // a-priori bound |x - c| <= E per axis for queries and staged candidates (L4)
         E = (E + U.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
+        {
+            // fp32 images of the query box and the conservative cull radius
+            // (R'_u + 4 eps)(1 + 2^-20), eps = the fp32 coordinate error bound of L4
+            const double eps = 0x1p-53 * E + 0x1p-24 * (1.0 + 0x1p-53) * E + 0x1p-149;
+            for (int l = 0; l < 3; l++) {
+                U.blo[l] = __double2float_rn(__dsub_rn(U.lo[l], U.c[l]));
+                U.bhi[l] = __double2float_rn(__dsub_rn(U.hi[l], U.c[l]));
+            }
+            const double rc = (U.Ru + 4.0 * eps) * (1.0 + 0x1p-20);
+            const double rc2 = rc * rc * (1.0 + 0x1p-40);
+            U.cull2 = (rc2 < 3.0e38) ? __double2float_ru(rc2) : __int_as_float(0x7f800000);
+        }
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int k = lane + 32 * h;
@@ -534,12 +561,14 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
         if (lane < U.nq) a.counts[qo[0]] = U.cnt0;
         if (lane + 32 < U.nq) a.counts[qo[1]] = U.cnt1;
         staged += U.staged;
+        loaded += U.loaded;
         tests += U.tests;
         exact += U.exact;
         __syncwarp();
     }
     if (lane == 0) {
         atomicAdd((unsigned long long *)&a.ctr[C_STAGED], (unsigned long long)staged);
+        atomicAdd((unsigned long long *)&a.ctr[C_LOADED], (unsigned long long)loaded);
         atomicAdd((unsigned long long *)&a.ctr[C_TESTS], (unsigned long long)tests);
         atomicAdd((unsigned long long *)&a.ctr[C_EXACT], (unsigned long long)exact);
     }
@@ -718,6 +747,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             a.batches = t.arena_batches.p;
             a.batch_cap = (long long)t.arena_batches.n;
             BT_CUDA(cudaMemsetAsync(t.counters.p, 0, C_HSUM * sizeof(int64_t), st));
+            BT_CUDA(cudaMemsetAsync(t.counters.p + C_HSUM + 1, 0, (C_N - C_HSUM - 1) * sizeof(int64_t), st));
             {
                 Phase ph("search.count");
                 test_kernel<<<grid, kWalkThreads, 0, st>>>(a);
@@ -727,6 +757,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             BT_CUDA(cudaMemcpyAsync(hc, t.counters.p, C_N * sizeof(long long), cudaMemcpyDeviceToHost, st));
             BT_CUDA(cudaStreamSynchronize(st));
             t.staged = hc[C_STAGED];
+            t.loaded = hc[C_LOADED];
             t.tests = hc[C_TESTS];
             t.exact_tests = hc[C_EXACT];
             const bool fits = hc[C_MASK] <= a.mask_cap && hc[C_CAND] <= a.cand_cap && hc[C_BATCH] <= a.batch_cap;
