@@ -66,6 +66,27 @@ def dist_env():
     return ws, rank, local
 
 
+def max_over_ranks(x: float, device=None) -> float:
+    """Max of a per-rank time over all ranks (identity without a process group)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def subdomain(cfg: int, n, rank: int):
+    """Rank r's own sub-domain: the cfg recipe drawn with seed offset r (weak scaling)."""
+    return datagen.make_config(cfg, n=n, seed_offset=rank)
+
+
+def weak_value(n_per_rank: int, ws: int, ms: float) -> float:
+    """Whole-job throughput: all ranks' particles over the max-over-ranks step time."""
+    return n_per_rank * ws / (ms * 1e-3)
+
+
 def config_block(cfg, n, ws):
     return {"workload": (f"BASELINE.json configs[{cfg - 1}] (cfg {cfg}): {WORKLOADS[cfg]}"
                          + ("" if n is None else f" [n overridden to {n}: not a bench line]")),
@@ -195,7 +216,7 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=dev)
     P.lib()
 
-    pos_np, h_np = datagen.make_config(args.config, n=args.n, seed_offset=rank)
+    pos_np, h_np = subdomain(args.config, args.n, rank)
     n = pos_np.shape[0]
     ngmax = datagen.NGMAX
     pos = torch.from_numpy(pos_np).to(dev)
@@ -236,10 +257,7 @@ def run_b200(args):
     clk = clocks.stop()
     P.profile_enable(False)
     prof = P.profile()
-    if ws > 1:
-        tt = torch.tensor([ms], device=dev, dtype=torch.float64)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        ms = float(tt.item())
+    ms = max_over_ranks(ms, dev)
     total_pairs = int(st["total_pairs"])
 
     def ph(name):
@@ -298,11 +316,8 @@ def run_b200(args):
         f1.record(stream)
         torch.cuda.synchronize()
         ems = f0.elapsed_time(f1) / args.e2e_steps
-        if ws > 1:
-            tt = torch.tensor([ems], device=dev, dtype=torch.float64)
-            torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-            ems = float(tt.item())
-        e2e = {"value": n * ws / (ems * 1e-3), "unit": UNIT, "ms_per_step": ems,
+        ems = max_over_ranks(ems, dev)
+        e2e = {"value": weak_value(n, ws, ems), "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": n * 32, "d2h_bytes_per_step": n * 4 + (n + 1) * 8 + 4 * total_pairs,
                "api": "bt_search_host (pinned host buffers; H2D pos+h, build, count, fill, D2H counts+offsets+CSR)"}
 
@@ -312,7 +327,7 @@ def run_b200(args):
         cpu = {"value": n / step_s, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": n * ws / (ms * 1e-3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        line = {"metric": METRIC, "value": weak_value(n, ws, ms), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy PCG64, SURVEY 8(d) recipe)",
                 "config": config_block(args.config, args.n, ws),

@@ -191,20 +191,47 @@ struct Unit {
     long long staged, loaded, tests, exact;
 };
 
-// The exact band of lemma L4: the fp64 predicate itself decides (rare path).
-__device__ __noinline__ void resolve_band(const WarpSmem &S, Unit &U, int lane, const WalkArgs &a, int k, int q,
-                                         bool u0, bool u1, unsigned &m0, unsigned &m1) {
-    const int qp = U.q0 + q;
-    const double4 Qr = a.rec[qp];
-    const double t = __dmul_rn(2.0, a.h_tree[qp]);
-    const double T = __dmul_rn(t, t);
-    bool e0 = false, e1 = false;
-    const int cp0 = S.cpos[64 * k + lane], cp1 = S.cpos[64 * k + 32 + lane];
-    if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
-    if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
-    m0 |= __ballot_sync(0xffffffffu, e0);
-    m1 |= __ballot_sync(0xffffffffu, e1);
-    U.exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
+// s32 of candidate pair (lane, lane + 32) of chunk k against query q
+struct Pair32 {
+    float s0, s1;
+};
+__device__ __forceinline__ Pair32 s32_pair(unsigned long long cx, unsigned long long cy, unsigned long long cz,
+                                           const float4 &Q0, const float4 &Q1) {
+    const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
+    const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
+    const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
+    unsigned long long s = f2_mul(dx, dx);
+    s = f2_fma(dy, dy, s);
+    s = f2_fma(dz, dz, s);
+    return Pair32{__uint_as_float((unsigned)s), __uint_as_float((unsigned)(s >> 32))};
+}
+
+// The exact band of lemma L4 (rare): redo the batch's pairs, and let the fp64
+// predicate itself decide every pair with A <= s32 < B.
+__device__ __noinline__ void resolve_band(WarpSmem &S, Unit &U, int lane, const WalkArgs &a, int nch) {
+    for (int k = 0; k < nch; k++) {
+        const float2 vx = S.px[32 * k + lane], vy = S.py[32 * k + lane], vz = S.pz[32 * k + lane];
+        const unsigned long long cx = pk(vx.x, vx.y), cy = pk(vy.x, vy.y), cz = pk(vz.x, vz.y);
+        const int cp0 = S.cpos[64 * k + lane], cp1 = S.cpos[64 * k + 32 + lane];
+        for (int q = 0; q < U.nq; q++) {
+            const float4 Q0 = S.q0[q], Q1 = S.q1[q];
+            const Pair32 p = s32_pair(cx, cy, cz, Q0, Q1);
+            const bool u0 = !(p.s0 < Q1.z) && p.s0 < Q1.w, u1 = !(p.s1 < Q1.z) && p.s1 < Q1.w;
+            if (!__any_sync(0xffffffffu, u0 || u1)) continue;
+            const int qp = U.q0 + q;
+            const double4 Qr = a.rec[qp];
+            const double t = __dmul_rn(2.0, a.h_tree[qp]);
+            const double T = __dmul_rn(t, t);
+            bool e0 = false, e1 = false;
+            if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
+            if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
+            const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
+            if (lane == 0) S.mask[k][q] |= ((unsigned long long)m1 << 32) | m0;
+            U.exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
+            __syncwarp();
+        }
+    }
+    __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -225,27 +252,31 @@ __device__ __noinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const Wa
         S.cpos[c] = -1;
     }
     __syncwarp();
+    // Hot loop, branch free: certain accepts (s32 < A) go into the masks; the
+    // ballots of s32 < B are compared with them, and any difference (a pair in
+    // the band [A, B) of lemma L4) is resolved afterwards by the fp64
+    // predicate.  Queries are padded to a multiple of 4 with A = B = 0.
+    unsigned diff = 0;
     for (int k = 0; k < nch; k++) {
         const float2 vx = S.px[32 * k + lane], vy = S.py[32 * k + lane], vz = S.pz[32 * k + lane];
         const unsigned long long cx = pk(vx.x, vx.y), cy = pk(vy.x, vy.y), cz = pk(vz.x, vz.y);
-#pragma unroll 2
-        for (int q = 0; q < nq; q++) {
-            const float4 Q0 = S.q0[q], Q1 = S.q1[q];
-            const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
-            const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
-            const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
-            unsigned long long s = f2_mul(dx, dx);
-            s = f2_fma(dy, dy, s);
-            s = f2_fma(dz, dz, s);
-            const float s0 = __uint_as_float((unsigned)s), s1 = __uint_as_float((unsigned)(s >> 32));
-            const bool a0 = s0 < Q1.z, a1 = s1 < Q1.z;
-            const bool u0 = !a0 && s0 < Q1.w, u1 = !a1 && s1 < Q1.w;
-            unsigned m0 = __ballot_sync(0xffffffffu, a0);
-            unsigned m1 = __ballot_sync(0xffffffffu, a1);
-            if (__any_sync(0xffffffffu, u0 || u1)) resolve_band(S, U, lane, a, k, q, u0, u1, m0, m1);
-            if (lane == 0) S.mask[k][q] = ((unsigned long long)m1 << 32) | m0;
+        unsigned long long *mrow = &S.mask[k][0];
+        for (int q = 0; q < nq; q += 4) {
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                const float4 Q0 = S.q0[q + i], Q1 = S.q1[q + i];
+                const Pair32 p = s32_pair(cx, cy, cz, Q0, Q1);
+                const unsigned m0 = __ballot_sync(0xffffffffu, p.s0 < Q1.z);
+                const unsigned m1 = __ballot_sync(0xffffffffu, p.s1 < Q1.z);
+                const unsigned n0 = __ballot_sync(0xffffffffu, p.s0 < Q1.w);
+                const unsigned n1 = __ballot_sync(0xffffffffu, p.s1 < Q1.w);
+                diff |= (n0 ^ m0) | (n1 ^ m1);
+                if (lane == 0) mrow[q + i] = ((unsigned long long)m1 << 32) | m0;
+            }
         }
     }
+    __syncwarp();
+    if (diff) resolve_band(S, U, lane, a, nch);
     __syncwarp();
     // self is never its own neighbor (R12); counts; record the batch
     for (int q = lane; q < nq; q += 32) {
@@ -473,6 +504,9 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
                 l4_thresholds(qT[h], E, a.exact_only != 0, A, B);
                 S.q0[k] = make_float4(ax, ax, ay, ay);
                 S.q1[k] = make_float4(az, az, A, B);
+            } else {
+                S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                S.q1[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // A = B = 0: never a neighbor
             }
         }
         __syncwarp();
