@@ -1,7 +1,9 @@
 // abi.cu -- the extern "C" boundary declared in include/btree.h: argument
 // validation, error codes, the per-thread stream, stream-ordered allocation,
 // phase profiling with CUDA events, and the host-buffer end-to-end call.
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -117,7 +119,13 @@ void *dmalloc(size_t bytes) {
         g_pool_configured = true;
     }
     void *p = nullptr;
+    static const bool trace = getenv("BT_TRACE") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
     cudaError_t e = cudaMallocAsync(&p, bytes, g_stream);
+    if (trace) {
+        double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+        if (us > 50.0) fprintf(stderr, "[bt] cudaMallocAsync %zu bytes: %.1f us\n", bytes, us);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         throw Error(e == cudaErrorMemoryAllocation ? BT_ERR_OOM : BT_ERR_CUDA,

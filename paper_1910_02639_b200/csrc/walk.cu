@@ -40,7 +40,7 @@ constexpr int kChunks = kCand / 64;
 constexpr int kLeafCap = 128;   // queued candidate leaves
 constexpr int kWarpsPerBlock = 4;
 constexpr int kWalkThreads = kWarpsPerBlock * 32;
-constexpr int kFillThreads = 256;
+constexpr int kFillThreads = 128;
 
 // device counters (int64 slots of TreeDev::counters)
 enum {
@@ -609,11 +609,24 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Fill pass: replay the recorded masks into the CSR rows
+// Fill pass: replay the recorded masks into the CSR rows.  Lanes = queries
+// (32 at a time): each lane expands its own masks bit by bit into its row,
+// assembled in shared memory, then every row is copied out with coalesced
+// stores (row order inside a CSR row is unspecified, R15).  A query whose row
+// does not fit the buffer is expanded straight into global memory.
 // ---------------------------------------------------------------------------
+constexpr int kRowBuf = 2048;  // ints of row staging per warp
+constexpr int kFillWarps = kFillThreads / 32;
+
+struct FillSmem {
+    int32_t rows[kRowBuf];
+    int32_t cand[kCand];
+};
+
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
+    __shared__ FillSmem fsm[kFillWarps];
     const int lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
+    FillSmem &F = fsm[threadIdx.x >> 5];
     for (;;) {
         unsigned long long u = 0;
         if (lane == 0) u = atomicAdd((unsigned long long *)&a.ctr[C_WORK2], 1ull);
@@ -621,32 +634,66 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
         if (u >= (unsigned long long)a.n_units) break;
         const int4 U = a.units[u];
         const int nq = U.z;
-        long long wr0 = 0, wr1 = 0;
-        if (lane < nq) wr0 = a.offsets[(int32_t)__double_as_longlong(a.rec[U.y + lane].w)];
-        if (lane + 32 < nq) wr1 = a.offsets[(int32_t)__double_as_longlong(a.rec[U.y + lane + 32].w)];
-        for (int b = a.head[u]; b >= 0;) {
-            const Batch B = a.batches[b];
-            const int nch = (B.ncand + 63) >> 6;
-            for (int k = 0; k < nch; k++) {
-                const int32_t c0 = a.cands[B.cand_base + 64 * k + lane];
-                const int32_t c1 = a.cands[B.cand_base + 64 * k + 32 + lane];
-                const unsigned long long *mk = a.masks + B.mask_base + (long long)k * nq;
-                const unsigned long long mA = (lane < nq) ? mk[lane] : 0ull;
-                const unsigned long long mB = (lane + 32 < nq) ? mk[lane + 32] : 0ull;
-                for (int q = 0; q < nq; q++) {
-                    const unsigned long long m = __shfl_sync(0xffffffffu, q < 32 ? mA : mB, q & 31);
-                    if (m == 0ull) continue;
-                    const long long base = __shfl_sync(0xffffffffu, q < 32 ? wr0 : wr1, q & 31);
-                    const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
-                    const int plo = __popc(lo);
-                    if ((lo >> lane) & 1u) a.nbr[base + __popc(lo & lt)] = c0;
-                    if ((hi >> lane) & 1u) a.nbr[base + plo + __popc(hi & lt)] = c1;
-                    const int pc = plo + __popc(hi);
-                    if (q < 32) wr0 += (lane == q) ? pc : 0;
-                    else wr1 += (lane == q - 32) ? pc : 0;
-                }
+        for (int g0 = 0; g0 < nq; g0 += 32) {
+            // this lane's query: row start and length
+            const int q = g0 + lane;
+            long long wr = 0;
+            int len = 0;
+            if (q < nq) {
+                const int32_t o = (int32_t)__double_as_longlong(a.rec[U.y + q].w);
+                wr = a.offsets[o];
+                len = (int)(a.offsets[o + 1] - wr);
             }
-            b = B.next;
+            // groups of consecutive lanes whose rows fit the staging buffer together
+            int inc = len;
+            for (int d = 1; d < 32; d <<= 1) {
+                int v = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += v;
+            }
+            int first = 0;  // first lane of the current group
+            while (first < 32) {
+                const int base = first ? __shfl_sync(0xffffffffu, inc, first - 1) : 0;
+                // lanes >= first whose rows end within base + kRowBuf; at least `first` itself
+                const unsigned fit = __ballot_sync(0xffffffffu, lane >= first && inc - base <= kRowBuf);
+                const int last = fit ? 31 - __clz(fit) : first;  // fit is a contiguous run from `first`
+                const bool direct = !fit;                        // row of lane `first` exceeds the buffer
+                const bool mine = lane >= first && lane <= last;
+                int ws = mine ? inc - len - base : 0;  // row start in the staging buffer
+                int cnt = 0;
+                for (int b = a.head[u]; b >= 0;) {
+                    const Batch B = a.batches[b];
+                    const int nch = (B.ncand + 63) >> 6;
+                    __syncwarp();
+                    for (int c = lane; c < nch * 64; c += 32) F.cand[c] = a.cands[B.cand_base + c];
+                    __syncwarp();
+                    for (int k = 0; k < nch; k++) {
+                        unsigned long long m = (mine && q < nq) ? a.masks[B.mask_base + (long long)k * nq + q] : 0ull;
+                        while (__any_sync(0xffffffffu, m != 0ull)) {
+                            if (m) {
+                                const int bit = __ffsll((long long)m) - 1;
+                                const int32_t v = F.cand[64 * k + bit];
+                                if (direct) a.nbr[wr + cnt] = v;
+                                else F.rows[ws + cnt] = v;
+                                cnt++;
+                                m &= m - 1ull;
+                            }
+                        }
+                    }
+                    b = B.next;
+                }
+                __syncwarp();
+                if (!direct) {
+                    // coalesced copy of the group's rows
+                    for (int l = first; l <= last; l++) {
+                        const long long dst = __shfl_sync(0xffffffffu, wr, l);
+                        const int n = __shfl_sync(0xffffffffu, len, l);
+                        const int src = __shfl_sync(0xffffffffu, ws, l);
+                        for (int i = lane; i < n; i += 32) a.nbr[dst + i] = F.rows[src + i];
+                    }
+                }
+                __syncwarp();
+                first = last + 1;
+            }
         }
     }
 }
