@@ -108,8 +108,16 @@ int bt_find_neighbors(const bt_tree *t, const double *h, int32_t ngmax, int32_t 
 int bt_fill_neighbors(const bt_tree *t, const double *h, const int64_t *offsets,
                       int32_t *nbr_idx, int64_t capacity);
 
-/* Frees all tree-owned device memory.  NULL-safe. */
+/* Frees all tree-owned device memory (into this thread's block cache).  NULL-safe. */
 void bt_free(bt_tree *t);
+
+/*
+ * Device memory comes from a per-thread block cache over cudaMalloc: blocks
+ * freed by bt_free or by internal scratch are reused by later calls of the
+ * same thread (repeated builds cost no driver allocation).  This returns the
+ * cached blocks of the calling thread to the driver.
+ */
+int bt_release_cache(void);
 
 /*
  * bt_search_host -- end-to-end convenience call on HOST buffers: copies pos

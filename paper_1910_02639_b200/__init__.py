@@ -4,4 +4,4 @@ The compute path is the CUDA library ``libbtree.so`` (C ABI in
 ``include/btree.h``); ``btree`` is its thin ctypes binding.  ``datagen`` draws
 the seeded synthetic inputs.  Nothing here imports ``oracle/``.
 """
-from .btree import BtreeError, Tree, build, lib, profile, profile_enable, profile_reset, search_host, set_exact_only  # noqa: F401
+from .btree import BtreeError, Tree, build, lib, profile, profile_enable, profile_reset, release_cache, search_host, set_exact_only  # noqa: F401

@@ -21,7 +21,7 @@ _NAMES = {0: "BT_OK", 1: "BT_ERR_ARG", 2: "BT_ERR_INPUT", 3: "BT_ERR_CAPACITY", 
 
 # every symbol include/btree.h declares
 EXPORTS = ["bt_build", "bt_build_ex", "bt_find_neighbors", "bt_fill_neighbors", "bt_free",
-           "bt_search_host", "bt_set_stream", "bt_set_exact_only", "bt_last_error", "bt_last_status", "bt_tree_stats",
+           "bt_search_host", "bt_set_stream", "bt_set_exact_only", "bt_release_cache", "bt_last_error", "bt_last_status", "bt_tree_stats",
            "bt_tree_order", "bt_profile_enable", "bt_profile_reset", "bt_profile_get"]
 
 
@@ -73,6 +73,8 @@ def lib():
         L.bt_search_host.restype = C.c_int
         L.bt_set_stream.argtypes = [_P]
         L.bt_set_stream.restype = C.c_int
+        L.bt_release_cache.argtypes = []
+        L.bt_release_cache.restype = C.c_int
         L.bt_set_exact_only.argtypes = [C.c_int]
         L.bt_set_exact_only.restype = C.c_int
         L.bt_last_error.argtypes = []
@@ -228,6 +230,11 @@ def search_host(pos, h, bucket_size: int = 64, max_empty: float = 0.5, capacity:
     _check(lib().bt_search_host(_ptr(pos), _ptr(h), n, int(bucket_size), float(max_empty), _ptr(counts),
                                 _ptr(offsets), _ptr(nbr), cap))
     return counts, offsets, nbr[:int(offsets[n])]
+
+
+def release_cache():
+    """Return this thread's cached device blocks to the driver."""
+    _check(lib().bt_release_cache())
 
 
 def set_exact_only(on: bool = True):

@@ -6,6 +6,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <unordered_map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -36,7 +37,6 @@ struct Pending {
 };
 thread_local std::vector<Pending> g_pending;
 thread_local std::vector<cudaEvent_t> g_event_pool;
-bool g_pool_configured = false;
 
 cudaEvent_t get_event() {
     if (!g_event_pool.empty()) {
@@ -108,33 +108,88 @@ Phase::~Phase() {
     if (cudaEventRecord(b, g_stream) == cudaSuccess) g_pending.push_back(Pending{name, a, b});
 }
 
-void *dmalloc(size_t bytes) {
-    if (!g_pool_configured) {
-        int dev;
-        BT_CUDA(cudaGetDevice(&dev));
-        cudaMemPool_t pool;
-        BT_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
-        uint64_t thr = UINT64_MAX;  // keep freed blocks reserved for the next build
-        BT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-        g_pool_configured = true;
+// Device memory: a per-thread caching allocator over cudaMalloc.  Freed blocks
+// are kept and handed out again (best fit, at most 2x the request) to later
+// calls of the same thread, whose work is ordered on the same stream -- the
+// stream-ordered pool (cudaMallocAsync) re-mapped physical memory on every
+// build here (~5 ms per GB), which dominated small steps.  On OOM the cache
+// is released and the allocation retried once.
+namespace {
+struct BlockCache {
+    std::multimap<size_t, void *> free_blocks;
+    std::unordered_map<void *, size_t> size_of;
+    size_t cached = 0;
+    void release_all() {
+        cudaStreamSynchronize(g_stream);
+        for (auto &kv : free_blocks) {
+            cudaFree(kv.second);
+            size_of.erase(kv.second);
+        }
+        free_blocks.clear();
+        cached = 0;
     }
-    void *p = nullptr;
+    ~BlockCache() {
+        for (auto &kv : free_blocks) cudaFree(kv.second);
+    }
+};
+BlockCache &block_cache() {
+    thread_local BlockCache c;
+    return c;
+}
+size_t round_block(size_t bytes) {
+    if (bytes < 512) return 512;
+    if (bytes < (1u << 20)) return (bytes + 511) & ~size_t(511);
+    return (bytes + (2u << 20) - 1) & ~size_t((2u << 20) - 1);
+}
+}  // namespace
+
+void *dmalloc(size_t bytes) {
+    BlockCache &C = block_cache();
+    const size_t want = round_block(bytes);
+    auto it = C.free_blocks.lower_bound(want);
+    if (it != C.free_blocks.end() && it->first <= 2 * want) {
+        void *p = it->second;
+        C.cached -= it->first;
+        C.free_blocks.erase(it);
+        return p;
+    }
     static const bool trace = getenv("BT_TRACE") != nullptr;
     auto t0 = std::chrono::steady_clock::now();
-    cudaError_t e = cudaMallocAsync(&p, bytes, g_stream);
+    void *p = nullptr;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        C.release_all();
+        e = cudaMalloc(&p, want);
+    }
     if (trace) {
         double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-        if (us > 50.0) fprintf(stderr, "[bt] cudaMallocAsync %zu bytes: %.1f us\n", bytes, us);
+        fprintf(stderr, "[bt] cudaMalloc %zu bytes: %.1f us\n", want, us);
     }
     if (e != cudaSuccess) {
         cudaGetLastError();
         throw Error(e == cudaErrorMemoryAllocation ? BT_ERR_OOM : BT_ERR_CUDA,
                     "device allocation of " + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e));
     }
+    C.size_of[p] = want;
     return p;
 }
 void dfree(void *p) {
-    if (p) cudaFreeAsync(p, g_stream);
+    if (!p) return;
+    BlockCache &C = block_cache();
+    auto it = C.size_of.find(p);
+    if (it == C.size_of.end()) {  // allocated by another thread: return it to the driver
+        cudaStreamSynchronize(g_stream);
+        cudaFree(p);
+        return;
+    }
+    C.free_blocks.emplace(it->second, p);
+    C.cached += it->second;
+}
+
+int release_cache() {
+    block_cache().release_all();
+    return 0;
 }
 
 HostScratch &host_scratch() {
@@ -215,7 +270,7 @@ int bt_fill_neighbors(const bt_tree *tc, const double *h, const int64_t *offsets
 
 void bt_free(bt_tree *t) {
     if (!t) return;
-    delete t;  // DBuf destructors enqueue cudaFreeAsync on this thread's stream
+    delete t;  // DBuf destructors return the blocks to this thread's cache
     cudaStreamSynchronize(stream());
 }
 
@@ -273,6 +328,10 @@ int bt_set_stream(void *s) {
     g_stream = s ? (cudaStream_t)s : cudaStreamPerThread;
     g_status = BT_OK;
     return BT_OK;
+}
+
+int bt_release_cache(void) {
+    return guarded([&] { release_cache(); });
 }
 
 int bt_set_exact_only(int on) {

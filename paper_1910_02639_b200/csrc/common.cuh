@@ -43,7 +43,7 @@ struct Phase {
     ~Phase();
 };
 
-// Stream-ordered device allocation (cudaMallocAsync on the library stream).
+// Device allocation through the per-thread block cache (abi.cu).
 void *dmalloc(size_t bytes);
 void dfree(void *p);
 
@@ -159,6 +159,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
                     int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass);
 
 void set_exact_only(int on);
+int release_cache();
 
 // ---------------------------------------------------------------------------
 // Eq. 2 with the clamp of reading R8, evaluated exactly as

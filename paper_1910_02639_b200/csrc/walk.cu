@@ -40,7 +40,7 @@ constexpr int kChunks = kCand / 64;
 constexpr int kLeafCap = 128;   // queued candidate leaves
 constexpr int kWarpsPerBlock = 4;
 constexpr int kWalkThreads = kWarpsPerBlock * 32;
-constexpr int kFillThreads = 128;
+constexpr int kFillThreads = 256;
 
 // device counters (int64 slots of TreeDev::counters)
 enum {
@@ -609,23 +609,25 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// Fill pass: replay the recorded masks into the CSR rows.  Lanes = queries
-// (32 at a time): each lane expands its own masks bit by bit into its row,
-// assembled in shared memory, then every row is copied out with coalesced
-// stores (row order inside a CSR row is unspecified, R15).  A query whose row
-// does not fit the buffer is expanded straight into global memory.
+// Fill pass: replay the recorded masks into the CSR rows.  Per unit and batch
+// the candidate indices and masks are staged in shared memory; for each
+// (chunk, query) mask word, lane l owns candidates 64k + l and 64k + 32 + l,
+// and __popc(mask & lanemask_lt) gives its slot in the query's row (row order
+// unspecified, R15).  The next write position of each query lives in shared
+// memory.
 // ---------------------------------------------------------------------------
-constexpr int kRowBuf = 2048;  // ints of row staging per warp
 constexpr int kFillWarps = kFillThreads / 32;
 
 struct FillSmem {
-    int32_t rows[kRowBuf];
-    int32_t cand[kCand];
+    unsigned long long wr[kQ];                 // next write position of each query's row
+    unsigned long long mask[kChunks * kQ];     // the batch's masks, [k][q]
+    int32_t cand[kCand];                       // the batch's candidate caller indices
 };
 
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     __shared__ FillSmem fsm[kFillWarps];
     const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
     FillSmem &F = fsm[threadIdx.x >> 5];
     for (;;) {
         unsigned long long u = 0;
@@ -634,66 +636,31 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
         if (u >= (unsigned long long)a.n_units) break;
         const int4 U = a.units[u];
         const int nq = U.z;
-        for (int g0 = 0; g0 < nq; g0 += 32) {
-            // this lane's query: row start and length
-            const int q = g0 + lane;
-            long long wr = 0;
-            int len = 0;
-            if (q < nq) {
-                const int32_t o = (int32_t)__double_as_longlong(a.rec[U.y + q].w);
-                wr = a.offsets[o];
-                len = (int)(a.offsets[o + 1] - wr);
-            }
-            // groups of consecutive lanes whose rows fit the staging buffer together
-            int inc = len;
-            for (int d = 1; d < 32; d <<= 1) {
-                int v = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= d) inc += v;
-            }
-            int first = 0;  // first lane of the current group
-            while (first < 32) {
-                const int base = first ? __shfl_sync(0xffffffffu, inc, first - 1) : 0;
-                // lanes >= first whose rows end within base + kRowBuf; at least `first` itself
-                const unsigned fit = __ballot_sync(0xffffffffu, lane >= first && inc - base <= kRowBuf);
-                const int last = fit ? 31 - __clz(fit) : first;  // fit is a contiguous run from `first`
-                const bool direct = !fit;                        // row of lane `first` exceeds the buffer
-                const bool mine = lane >= first && lane <= last;
-                int ws = mine ? inc - len - base : 0;  // row start in the staging buffer
-                int cnt = 0;
-                for (int b = a.head[u]; b >= 0;) {
-                    const Batch B = a.batches[b];
-                    const int nch = (B.ncand + 63) >> 6;
-                    __syncwarp();
-                    for (int c = lane; c < nch * 64; c += 32) F.cand[c] = a.cands[B.cand_base + c];
-                    __syncwarp();
-                    for (int k = 0; k < nch; k++) {
-                        unsigned long long m = (mine && q < nq) ? a.masks[B.mask_base + (long long)k * nq + q] : 0ull;
-                        while (__any_sync(0xffffffffu, m != 0ull)) {
-                            if (m) {
-                                const int bit = __ffsll((long long)m) - 1;
-                                const int32_t v = F.cand[64 * k + bit];
-                                if (direct) a.nbr[wr + cnt] = v;
-                                else F.rows[ws + cnt] = v;
-                                cnt++;
-                                m &= m - 1ull;
-                            }
-                        }
-                    }
-                    b = B.next;
+        for (int q = lane; q < nq; q += 32)
+            F.wr[q] = (unsigned long long)a.offsets[(int32_t)__double_as_longlong(a.rec[U.y + q].w)];
+        for (int b = a.head[u]; b >= 0;) {
+            const Batch B = a.batches[b];
+            const int nch = (B.ncand + 63) >> 6;
+            __syncwarp();
+            for (int c = lane; c < nch * 64; c += 32) F.cand[c] = a.cands[B.cand_base + c];
+            for (int w = lane; w < nch * nq; w += 32) F.mask[w] = a.masks[B.mask_base + w];
+            __syncwarp();
+            for (int k = 0; k < nch; k++) {
+                const int32_t c0 = F.cand[64 * k + lane], c1 = F.cand[64 * k + 32 + lane];
+                const unsigned long long *mk = F.mask + k * nq;
+                for (int q = 0; q < nq; q++) {
+                    const unsigned long long m = mk[q];
+                    if (m == 0ull) continue;
+                    const unsigned long long base = F.wr[q];
+                    const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+                    const int plo = __popc(lo);
+                    if ((lo >> lane) & 1u) a.nbr[base + __popc(lo & lt)] = c0;
+                    if ((hi >> lane) & 1u) a.nbr[base + plo + __popc(hi & lt)] = c1;
+                    if (lane == 0) F.wr[q] = base + plo + __popc(hi);
                 }
                 __syncwarp();
-                if (!direct) {
-                    // coalesced copy of the group's rows
-                    for (int l = first; l <= last; l++) {
-                        const long long dst = __shfl_sync(0xffffffffu, wr, l);
-                        const int n = __shfl_sync(0xffffffffu, len, l);
-                        const int src = __shfl_sync(0xffffffffu, ws, l);
-                        for (int i = lane; i < n; i += 32) a.nbr[dst + i] = F.rows[src + i];
-                    }
-                }
-                __syncwarp();
-                first = last + 1;
             }
+            b = B.next;
         }
     }
 }
