@@ -362,6 +362,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__rest
 // One warp per leaf.  rank(e) = #{k in leaf : idx_k < idx_e} (caller indices
 // are distinct), O(m^2 / 32) per leaf: m <= s = 64 in the configurations.
 __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *__restrict__ src, double4 *__restrict__ dst,
+                                                                 float4 *__restrict__ dst32,
                                                                  const int32_t *__restrict__ leaf_begin,
                                                                  const int32_t *__restrict__ leaf_count, int64_t n_leaves,
                                                                  double *__restrict__ leaf_box,
@@ -371,7 +372,24 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t L = warp; L < n_leaves; L += nwarps) {
         int32_t b0 = leaf_begin[L], m = leaf_count[L];
+        // tight box (exact fp64 min / max)
         double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+        for (int32_t e = lane; e < m; e += 32) {
+            const double4 v = src[b0 + e];
+            mn[0] = fmin(mn[0], v.x); mn[1] = fmin(mn[1], v.y); mn[2] = fmin(mn[2], v.z);
+            mx[0] = fmax(mx[0], v.x); mx[1] = fmax(mx[1], v.y); mx[2] = fmax(mx[2], v.z);
+        }
+        double c[3];
+        for (int l = 0; l < 3; l++) {
+            double a = mn[l], b = mx[l];
+            for (int d = 16; d; d >>= 1) {
+                a = fmin(a, __shfl_xor_sync(0xffffffffu, a, d));
+                b = fmax(b, __shfl_xor_sync(0xffffffffu, b, d));
+            }
+            if (lane == 0) { leaf_box[6 * L + l] = a; leaf_box[6 * L + 3 + l] = b; }
+            c[l] = 0.5 * (a + b);  // leaf centre for the compact fp32 records
+        }
+        // canonical order: rank(e) = #{k : idx_k < idx_e}
         for (int32_t e0 = 0; e0 < m; e0 += 32) {
             int32_t e = e0 + lane;
             double4 v = make_double4(0, 0, 0, 0);
@@ -379,8 +397,6 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
             if (e < m) {
                 v = src[b0 + e];
                 my = __double_as_longlong(v.w);
-                mn[0] = fmin(mn[0], v.x); mn[1] = fmin(mn[1], v.y); mn[2] = fmin(mn[2], v.z);
-                mx[0] = fmax(mx[0], v.x); mx[1] = fmax(mx[1], v.y); mx[2] = fmax(mx[2], v.z);
             }
             int32_t rank = 0;
             for (int32_t k0 = 0; k0 < m; k0 += 32) {
@@ -392,15 +408,13 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
                     rank += (ok < my);
                 }
             }
-            if (e < m) dst[b0 + rank] = v;
-        }
-        for (int l = 0; l < 3; l++) {
-            double a = mn[l], b = mx[l];
-            for (int d = 16; d; d >>= 1) {
-                a = fmin(a, __shfl_xor_sync(0xffffffffu, a, d));
-                b = fmax(b, __shfl_xor_sync(0xffffffffu, b, d));
+            if (e < m) {
+                dst[b0 + rank] = v;
+                // compact record: fl32(fl64(x - c_L)), caller index (walk staging, lemma L4)
+                dst32[b0 + rank] = make_float4(__double2float_rn(__dsub_rn(v.x, c[0])),
+                                               __double2float_rn(__dsub_rn(v.y, c[1])),
+                                               __double2float_rn(__dsub_rn(v.z, c[2])), __int_as_float((int)my));
             }
-            if (lane == 0) { leaf_box[6 * L + l] = a; leaf_box[6 * L + 3 + l] = b; }
         }
         if (lane == 0) {
             atomicMax(max_leaf, (unsigned long long)m);
@@ -673,8 +687,9 @@ void build_tree(TreeDev &t, const double *pos) {
     {
         Phase ph("build.leaves");
         t.leaf_box.alloc(6 * (size_t)t.n_leaves);
+        t.rec32.alloc(n);
         leaf_finalize_kernel<<<grid_for(t.n_leaves * 32, kThreads, (int64_t)sms * 32), kThreads, 0, st>>>(
-            fin.p, t.rec.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
+            fin.p, t.rec.p, t.rec32.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
         BT_LAUNCH("leaf_finalize");
         DBuf<long long> dtot(1);
         // units: count first (to size the array), then write

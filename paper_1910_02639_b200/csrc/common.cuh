@@ -120,6 +120,8 @@ struct TreeDev {
     int32_t depth_cap = 64;
     // records in tree (depth-first leaf) order: x, y, z, caller index (bits)
     DBuf<double4> rec;
+    // compact records in tree order: fl32(fl64(x - c_leaf)) per axis, caller index (int bits)
+    DBuf<float4> rec32;
     DBuf<NodeRec> nodes;       // internal nodes, all levels
     int64_t n_nodes = 0;
     DBuf<int32_t> cells;       // cell table, all levels

@@ -37,7 +37,7 @@ namespace {
 constexpr int kQ = 64;          // queries per unit (== build.cu kUnitQ)
 constexpr int kCand = 256;      // staged candidates per batch
 constexpr int kChunks = kCand / 64;
-constexpr int kLeafCap = 128;   // queued candidate leaves
+constexpr int kLeafCap = 64;    // queued candidate leaves
 constexpr int kWarpsPerBlock = 4;
 constexpr int kWalkThreads = kWarpsPerBlock * 32;
 constexpr int kFillThreads = 256;
@@ -70,10 +70,12 @@ struct WarpSmem {
     unsigned long long mask[kChunks][kQ];  // neighbor masks of the batch
     int32_t lbeg[kLeafCap + 1];              // queued leaves: first tree position
     int32_t lpre[kLeafCap + 1];            // queued leaves: exclusive prefix of counts
+    float4 loff[kLeafCap + 1];             // queued leaves: fl32(c_leaf - c_unit), w = 1 if staged from rec32
 };
 
 struct WalkArgs {
     const double4 *rec;
+    const float4 *rec32;
     const double *h_tree;
     const NodeRec *nodes;
     const int32_t *cells;
@@ -137,19 +139,27 @@ __device__ __forceinline__ bool exact_pair(double qx, double qy, double qz, doub
     return d2 < T;
 }
 
+// Bound on |a - (x - c)| for the fp32 relative coordinates a of every query
+// and staged candidate of a unit (lemma L4): queries use a = fl32(fl64(x - c))
+// (error <= u E + w (1+u) E + 2^-149); candidates staged from the compact
+// records use a = fl32(r32 + fl32(fl64(c_leaf - c))) with r32 =
+// fl32(fl64(x - c_leaf)), only for leaves of half-extent H <= 0.999 E, whose
+// error is <= (u + w(1+u))(H + D) + w(|x - c| + ...) + 3 2^-149 <= 4.0001 w E +
+// 3 2^-149 (D = |c_leaf - c| <= H + E).  One bound covers both.
+__device__ __forceinline__ double l4_eps(double E) { return 4.01 * 0x1p-24 * E + 0x1p-147; }
+
 // Lemma L4: thresholds A <= B (fp32) such that for the
 // fp32 squared distance s32 of a pair whose coordinates relative to the unit
 // centre are bounded by E (per axis),
 //   s32 <  A  =>  fp64 predicate true,     s32 >= B  =>  fp64 predicate false.
 // All slack factors round the bounds outward.
-__device__ __forceinline__ void l4_thresholds(double T, double E, bool exact_only, float &A, float &B) {
+__device__ __forceinline__ void l4_thresholds(double T, double E, double eps, bool exact_only, float &A, float &B) {
     const double u = 0x1p-53, w = 0x1p-24;
     if (exact_only || !(E < 1e15)) {
         A = 0.0f;
         B = __int_as_float(0x7f800000);  // +inf: every pair goes to the fp64 predicate
         return;
     }
-    const double eps = u * E + w * (1.0 + u) * E + 0x1p-149;  // |a - (x - c)| per coordinate
     const double a0 = 2.0 * eps * (1.0 + w) + 0x1p-150;        // |d - D| <= a0 + w |D|
     const double g3 = 3.0 * w / (1.0 - 3.0 * w);
     auto err = [&](double S) {
@@ -184,6 +194,7 @@ struct Unit {
     double Ru, Ru2;
     float blo[3], bhi[3];   // query box in fp32 relative coordinates
     float cull2;            // fp32 Minkowski cull threshold (conservative)
+    double E;               // a-priori bound |x - c| per axis (L4)
     int ncand;        // staged candidates in the current batch
     int nleaf;        // queued leaves
     int prev_batch;
@@ -341,7 +352,8 @@ __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const 
     int owner = 0;  // queued leaf that holds flattened position p0
     for (int p0 = 0; p0 < total; p0 += 64) {
         if (U.ncand + 64 > kCand) test_batch(S, U, lane, a);
-        double4 r[2];
+        float4 r[2];
+        float4 of[2];
         int pos[2];
         bool valid[2];
 #pragma unroll
@@ -357,16 +369,27 @@ __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const 
             const int p = w0 + lane;
             valid[h] = p < total;
             pos[h] = valid[h] ? S.lbeg[mine] + (p - S.lpre[mine]) : 0;
+            of[h] = S.loff[mine];
             owner += __popc(past);
-            if (valid[h]) r[h] = a.rec[pos[h]];
+            if (valid[h]) {
+                if (of[h].w != 0.0f) {
+                    r[h] = a.rec32[pos[h]];
+                } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
+                    const double4 d = a.rec[pos[h]];
+                    r[h] = make_float4(__double2float_rn(__dsub_rn(d.x, U.c[0])), __double2float_rn(__dsub_rn(d.y, U.c[1])),
+                                       __double2float_rn(__dsub_rn(d.z, U.c[2])),
+                                       __int_as_float((int)__double_as_longlong(d.w)));
+                }
+            }
         }
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            // fp32 relative coordinates a = fl32(fl64(x - c)) and the conservative
-            // fp32 Minkowski cull against the query box (L3 / L4)
-            const float ax = __double2float_rn(__dsub_rn(r[h].x, U.c[0]));
-            const float ay = __double2float_rn(__dsub_rn(r[h].y, U.c[1]));
-            const float az = __double2float_rn(__dsub_rn(r[h].z, U.c[2]));
+            // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
+            // conservative fp32 Minkowski cull against the query box (L3 / L4)
+            const bool cmp = of[h].w != 0.0f;
+            const float ax = cmp ? __fadd_rn(r[h].x, of[h].x) : r[h].x;
+            const float ay = cmp ? __fadd_rn(r[h].y, of[h].y) : r[h].y;
+            const float az = cmp ? __fadd_rn(r[h].z, of[h].z) : r[h].z;
             const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[0], ax), __fsub_rn(ax, U.bhi[0])));
             const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[1], ay), __fsub_rn(ay, U.bhi[1])));
             const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[2], az), __fsub_rn(az, U.bhi[2])));
@@ -380,7 +403,7 @@ __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const 
                 reinterpret_cast<float *>(&S.py[32 * ck + cl])[ch] = ay;
                 reinterpret_cast<float *>(&S.pz[32 * ck + cl])[ch] = az;
                 S.cpos[slot] = pos[h];
-                S.corig[slot] = (int32_t)__double_as_longlong(r[h].w);
+                S.corig[slot] = __float_as_int(r[h].w);
                 const int qi = pos[h] - U.q0;
                 if (qi >= 0 && qi < U.nq) S.qself[qi] = slot;
             }
@@ -399,6 +422,7 @@ __device__ __forceinline__ void queue_leaves(WarpSmem &S, Unit &U, int lane, con
                                              int32_t leaf) {
     const unsigned lt = lanemask_lt();
     bool keep = false;
+    float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
     if (is_leaf) {
         const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
         const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
@@ -407,6 +431,12 @@ __device__ __forceinline__ void queue_leaves(WarpSmem &S, Unit &U, int lane, con
         double gz = fmax(0.0, fmax(__dsub_rn(b1.x, U.hi[2]), __dsub_rn(U.lo[2], b2.y)));
         double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
         keep = g2 < U.Ru2;
+        // leaf centre (as build.cu computed it) relative to the unit centre; the
+        // compact records are usable when the leaf half-extent H <= 0.999 E (l4_eps)
+        const double cx = 0.5 * (b0.x + b1.y), cy = 0.5 * (b0.y + b2.x), cz = 0.5 * (b1.x + b2.y);
+        const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
+        off = make_float4(__double2float_rn(__dsub_rn(cx, U.c[0])), __double2float_rn(__dsub_rn(cy, U.c[1])),
+                          __double2float_rn(__dsub_rn(cz, U.c[2])), (H <= 0.999 * U.E) ? 1.0f : 0.0f);
     }
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     if (!km) return;
@@ -415,12 +445,13 @@ __device__ __forceinline__ void queue_leaves(WarpSmem &S, Unit &U, int lane, con
         const int slot = U.nleaf + __popc(km & lt);
         S.lbeg[slot] = a.leaf_begin[leaf];
         S.lpre[slot] = a.leaf_count[leaf];  // counts; stage_leaves turns them into a prefix
+        S.loff[slot] = off;
     }
     U.nleaf += __popc(km);
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
+__global__ void __launch_bounds__(kWalkThreads, 5) test_kernel(WalkArgs a) {
     __shared__ WarpSmem smem[kWarpsPerBlock];
     const int lane = threadIdx.x & 31;
     WarpSmem &S = smem[threadIdx.x >> 5];
@@ -470,9 +501,12 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
             S.qself[k] = -1;
         }
         double E = 0.0, Mu = 0.0;
+        // a unit holding its whole leaf has the leaf's tight box as its query box
+        const bool whole = U.nq == a.leaf_count[UU.x];
+        const double *lb = a.leaf_box + 6 * (int64_t)UU.x;
         for (int l = 0; l < 3; l++) {
-            U.lo[l] = warp_min(lo[l]);
-            U.hi[l] = warp_max(hi[l]);
+            U.lo[l] = whole ? lb[l] : warp_min(lo[l]);
+            U.hi[l] = whole ? lb[3 + l] : warp_max(hi[l]);
             U.c[l] = 0.5 * (U.lo[l] + U.hi[l]);
             E = fmax(E, 0.5 * (U.hi[l] - U.lo[l]));
             Mu = fmax(Mu, fmax(fabs(U.lo[l]), fabs(U.hi[l])));
@@ -481,10 +515,11 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
         U.Ru2 = __dmul_rn(U.Ru, U.Ru);
         // a-priori bound |x - c| <= E per axis for queries and staged candidates (L4)
         E = (E + U.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
+        U.E = E;
         {
             // fp32 images of the query box and the conservative cull radius
             // (R'_u + 4 eps)(1 + 2^-20), eps = the fp32 coordinate error bound of L4
-            const double eps = 0x1p-53 * E + 0x1p-24 * (1.0 + 0x1p-53) * E + 0x1p-149;
+            const double eps = l4_eps(E);
             for (int l = 0; l < 3; l++) {
                 U.blo[l] = __double2float_rn(__dsub_rn(U.lo[l], U.c[l]));
                 U.bhi[l] = __double2float_rn(__dsub_rn(U.hi[l], U.c[l]));
@@ -501,7 +536,7 @@ __global__ void __launch_bounds__(kWalkThreads, 4) test_kernel(WalkArgs a) {
                 const float ay = __double2float_rn(__dsub_rn(qy[h], U.c[1]));
                 const float az = __double2float_rn(__dsub_rn(qz[h], U.c[2]));
                 float A, B;
-                l4_thresholds(qT[h], E, a.exact_only != 0, A, B);
+                l4_thresholds(qT[h], E, l4_eps(E), a.exact_only != 0, A, B);
                 S.q0[k] = make_float4(ax, ax, ay, ay);
                 S.q1[k] = make_float4(az, az, A, B);
             } else {
@@ -754,6 +789,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
 
     WalkArgs a{};
     a.rec = t.rec.p;
+    a.rec32 = t.rec32.p;
     a.h_tree = t.h_tree.p;
     a.nodes = t.nodes.p;
     a.cells = t.cells.p;
