@@ -13,7 +13,7 @@ import os
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libbtree.so")
+LIB_PATH = os.environ.get("BT_LIB") or os.path.join(_PKG, "libbtree.so")  # BT_LIB: A/B experiments
 
 BT_OK, BT_ERR_ARG, BT_ERR_INPUT, BT_ERR_CAPACITY, BT_ERR_CUDA, BT_ERR_OOM = range(6)
 _NAMES = {0: "BT_OK", 1: "BT_ERR_ARG", 2: "BT_ERR_INPUT", 3: "BT_ERR_CAPACITY", 4: "BT_ERR_CUDA",

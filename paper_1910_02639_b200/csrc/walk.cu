@@ -263,26 +263,49 @@ __device__ __noinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const Wa
         S.cpos[c] = -1;
     }
     __syncwarp();
-    // Hot loop, branch free: certain accepts (s32 < A) go into the masks; the
-    // ballots of s32 < B are compared with them, and any difference (a pair in
-    // the band [A, B) of lemma L4) is resolved afterwards by the fp64
-    // predicate.  Queries are padded to a multiple of 4 with A = B = 0.
+    // Hot loop, branch free, register blocked: 4 queries held in registers,
+    // candidate pairs of each chunk streamed from shared memory.  Certain
+    // accepts (s32 < A) go into the masks; the ballots of s32 < B are compared
+    // with them, and any difference (a pair in the band [A, B) of lemma L4) is
+    // resolved afterwards by the fp64 predicate.  Queries are padded to a
+    // multiple of 4 with A = B = 0.
     unsigned diff = 0;
-    for (int k = 0; k < nch; k++) {
-        const float2 vx = S.px[32 * k + lane], vy = S.py[32 * k + lane], vz = S.pz[32 * k + lane];
-        const unsigned long long cx = pk(vx.x, vx.y), cy = pk(vy.x, vy.y), cz = pk(vz.x, vz.y);
-        unsigned long long *mrow = &S.mask[k][0];
-        for (int q = 0; q < nq; q += 4) {
+    for (int q = 0; q < nq; q += 4) {
+        unsigned long long qx[4], qy[4], qz[4];
+        float A[4], B[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const float4 Q0 = S.q0[q + i], Q1 = S.q1[q + i];
+            qx[i] = pk(Q0.x, Q0.y);
+            qy[i] = pk(Q0.z, Q0.w);
+            qz[i] = pk(Q1.x, Q1.y);
+            A[i] = Q1.z;
+            B[i] = Q1.w;
+        }
+        for (int k = 0; k < nch; k++) {
+            const float2 vx = S.px[32 * k + lane], vy = S.py[32 * k + lane], vz = S.pz[32 * k + lane];
+            const unsigned long long cx = pk(vx.x, vx.y), cy = pk(vy.x, vy.y), cz = pk(vz.x, vz.y);
+            unsigned long long m[4];
 #pragma unroll
             for (int i = 0; i < 4; i++) {
-                const float4 Q0 = S.q0[q + i], Q1 = S.q1[q + i];
-                const Pair32 p = s32_pair(cx, cy, cz, Q0, Q1);
-                const unsigned m0 = __ballot_sync(0xffffffffu, p.s0 < Q1.z);
-                const unsigned m1 = __ballot_sync(0xffffffffu, p.s1 < Q1.z);
-                const unsigned n0 = __ballot_sync(0xffffffffu, p.s0 < Q1.w);
-                const unsigned n1 = __ballot_sync(0xffffffffu, p.s1 < Q1.w);
+                const unsigned long long dx = f2_sub(cx, qx[i]);
+                const unsigned long long dy = f2_sub(cy, qy[i]);
+                const unsigned long long dz = f2_sub(cz, qz[i]);
+                unsigned long long s = f2_mul(dx, dx);
+                s = f2_fma(dy, dy, s);
+                s = f2_fma(dz, dz, s);
+                const float s0 = __uint_as_float((unsigned)s), s1 = __uint_as_float((unsigned)(s >> 32));
+                const unsigned m0 = __ballot_sync(0xffffffffu, s0 < A[i]);
+                const unsigned m1 = __ballot_sync(0xffffffffu, s1 < A[i]);
+                const unsigned n0 = __ballot_sync(0xffffffffu, s0 < B[i]);
+                const unsigned n1 = __ballot_sync(0xffffffffu, s1 < B[i]);
                 diff |= (n0 ^ m0) | (n1 ^ m1);
-                if (lane == 0) mrow[q + i] = ((unsigned long long)m1 << 32) | m0;
+                m[i] = ((unsigned long long)m1 << 32) | m0;
+            }
+            if (lane == 0) {
+                ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(&S.mask[k][q]);
+                dst[0] = make_ulonglong2(m[0], m[1]);
+                dst[1] = make_ulonglong2(m[2], m[3]);
             }
         }
     }
@@ -333,6 +356,14 @@ __device__ __noinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const Wa
 __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
     const unsigned lt = lanemask_lt();
     const int nl = U.nleaf;
+    // unit constants in registers (U lives in local memory across calls)
+    const float blo0 = U.blo[0], blo1 = U.blo[1], blo2 = U.blo[2];
+    const float bhi0 = U.bhi[0], bhi1 = U.bhi[1], bhi2 = U.bhi[2];
+    const float cull2 = U.cull2;
+    const double c0 = U.c[0], c1 = U.c[1], c2 = U.c[2];
+    const int q0 = U.q0, nq = U.nq;
+    int ncand = U.ncand;
+    int staged = 0, loaded = 0;
     // exclusive prefix of the queued leaf counts (lpre was filled with counts)
     int carry = 0;
     for (int i0 = 0; i0 < nl; i0 += 32) {
@@ -349,13 +380,9 @@ __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const 
     if (lane == 0) S.lpre[nl] = carry;
     __syncwarp();
     const int total = carry;
-    int owner = 0;  // queued leaf that holds flattened position p0
-    for (int p0 = 0; p0 < total; p0 += 64) {
-        if (U.ncand + 64 > kCand) test_batch(S, U, lane, a);
-        float4 r[2];
-        float4 of[2];
-        int pos[2];
-        bool valid[2];
+    int owner = 0;  // queued leaf that holds the next flattened position
+    // gather one group of 64 flattened positions: record, leaf offset, position
+    auto gather = [&](int p0, float4 (&r)[2], float4 (&of)[2], int (&pos)[2], bool (&valid)[2]) {
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int w0 = p0 + 32 * h;
@@ -371,48 +398,76 @@ __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const 
             pos[h] = valid[h] ? S.lbeg[mine] + (p - S.lpre[mine]) : 0;
             of[h] = S.loff[mine];
             owner += __popc(past);
+            r[h] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (valid[h]) {
                 if (of[h].w != 0.0f) {
                     r[h] = a.rec32[pos[h]];
                 } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
                     const double4 d = a.rec[pos[h]];
-                    r[h] = make_float4(__double2float_rn(__dsub_rn(d.x, U.c[0])), __double2float_rn(__dsub_rn(d.y, U.c[1])),
-                                       __double2float_rn(__dsub_rn(d.z, U.c[2])),
+                    r[h] = make_float4(__double2float_rn(__dsub_rn(d.x, c0)), __double2float_rn(__dsub_rn(d.y, c1)),
+                                       __double2float_rn(__dsub_rn(d.z, c2)),
                                        __int_as_float((int)__double_as_longlong(d.w)));
+                    of[h].x = of[h].y = of[h].z = 0.0f;
                 }
             }
         }
+    };
+    float4 r[2], of[2];
+    int pos[2];
+    bool valid[2];
+    if (total > 0) gather(0, r, of, pos, valid);
+    for (int p0 = 0; p0 < total; p0 += 64) {
+        // prefetch the next group before culling this one (loads in flight)
+        float4 rn[2], ofn[2];
+        int posn[2];
+        bool validn[2] = {false, false};
+        if (p0 + 64 < total) gather(p0 + 64, rn, ofn, posn, validn);
+        if (ncand + 64 > kCand) {
+            U.ncand = ncand;
+            test_batch(S, U, lane, a);
+            ncand = 0;
+        }
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
-            // conservative fp32 Minkowski cull against the query box (L3 / L4, DESIGN.md 8)
-            const bool cmp = of[h].w != 0.0f;
-            const float ax = cmp ? __fadd_rn(r[h].x, of[h].x) : r[h].x;
-            const float ay = cmp ? __fadd_rn(r[h].y, of[h].y) : r[h].y;
-            const float az = cmp ? __fadd_rn(r[h].z, of[h].z) : r[h].z;
-            const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[0], ax), __fsub_rn(ax, U.bhi[0])));
-            const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[1], ay), __fsub_rn(ay, U.bhi[1])));
-            const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(U.blo[2], az), __fsub_rn(az, U.bhi[2])));
+            // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c)); the
+            // fp64 path already holds fl32(fl64(x - c)) with a zero offset) and the
+            // conservative fp32 Minkowski cull against the query box (L3 / L4)
+            const float ax = __fadd_rn(r[h].x, of[h].x);
+            const float ay = __fadd_rn(r[h].y, of[h].y);
+            const float az = __fadd_rn(r[h].z, of[h].z);
+            const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(blo0, ax), __fsub_rn(ax, bhi0)));
+            const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(blo1, ay), __fsub_rn(ay, bhi1)));
+            const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(blo2, az), __fsub_rn(az, bhi2)));
             const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
-            const bool keep = valid[h] && g2 < U.cull2;
+            const bool keep = valid[h] && g2 < cull2;
             const unsigned km = __ballot_sync(0xffffffffu, keep);
             if (keep) {
-                const int slot = U.ncand + __popc(km & lt);
+                const int slot = ncand + __popc(km & lt);
                 const int ck = slot >> 6, cl = slot & 31, ch = (slot >> 5) & 1;
                 reinterpret_cast<float *>(&S.px[32 * ck + cl])[ch] = ax;
                 reinterpret_cast<float *>(&S.py[32 * ck + cl])[ch] = ay;
                 reinterpret_cast<float *>(&S.pz[32 * ck + cl])[ch] = az;
                 S.cpos[slot] = pos[h];
                 S.corig[slot] = __float_as_int(r[h].w);
-                const int qi = pos[h] - U.q0;
-                if (qi >= 0 && qi < U.nq) S.qself[qi] = slot;
+                const int qi = pos[h] - q0;
+                if (qi >= 0 && qi < nq) S.qself[qi] = slot;
             }
-            U.ncand += __popc(km);
-            U.staged += __popc(km);
-            U.loaded += __popc(__ballot_sync(0xffffffffu, valid[h]));
+            ncand += __popc(km);
+            staged += __popc(km);
+            loaded += __popc(__ballot_sync(0xffffffffu, valid[h]));
+        }
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            r[h] = rn[h];
+            of[h] = ofn[h];
+            pos[h] = posn[h];
+            valid[h] = validn[h];
         }
         __syncwarp();
     }
+    U.ncand = ncand;
+    U.staged += staged;
+    U.loaded += loaded;
     U.nleaf = 0;
     __syncwarp();
 }
@@ -451,7 +506,10 @@ __device__ __forceinline__ void queue_leaves(WarpSmem &S, Unit &U, int lane, con
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kWalkThreads, 5) test_kernel(WalkArgs a) {
+#ifndef BT_WALK_MIN_BLOCKS
+#define BT_WALK_MIN_BLOCKS 5
+#endif
+__global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) test_kernel(WalkArgs a) {
     __shared__ WarpSmem smem[kWarpsPerBlock];
     const int lane = threadIdx.x & 31;
     WarpSmem &S = smem[threadIdx.x >> 5];
