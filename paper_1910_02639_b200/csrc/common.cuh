@@ -107,8 +107,8 @@ __host__ __device__ inline int32_t node_code(int32_t node) { return -2 - node; }
 __host__ __device__ inline int32_t code_node(int32_t code) { return -2 - code; }
 
 struct WalkBatch {          // one staged candidate batch of a walk unit
-    long long mask_base;    // mask word (chunk k, query q) at mask_base + k * nq + q
-    long long cand_base;    // first candidate slot (64 per chunk)
+    long long mask_base;    // mask word (chunk k, query q) at mask_base + k * nq + q (-1: none yet)
+    long long cand_base;    // first candidate slot of the block
     int ncand;
     int next;               // next batch of the same unit, -1 = last
 };
@@ -143,7 +143,9 @@ struct TreeDev {
     DBuf<double> h_tree;       // h in tree order
     DBuf<int32_t> head;        // first recorded batch of each unit
     DBuf<unsigned long long> arena_masks;  // neighbor masks per (query, 64-candidate chunk)
-    DBuf<int32_t> arena_cands;             // candidate caller indices per chunk slot
+    DBuf<float4> arena_cand4;              // candidate slots: fp32 relative coordinates, tree position
+    DBuf<int32_t> arena_cands;             // candidate caller indices per slot
+    DBuf<int64_t> self_slot;               // per tree position: arena slot of the query itself
     DBuf<WalkBatch> arena_batches;
     bool rec_valid = false;    // arena holds the test pass of (rec_h, rec_hsum, rec_exact)
     const double *rec_h = nullptr;

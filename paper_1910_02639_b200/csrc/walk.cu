@@ -3,27 +3,25 @@
 // Work unit = up to 64 queries of one leaf bucket (the paper's "blocked
 // approach", Sec. IV-E: particles are in tree order, so a unit's queries
 // are spatial neighbours).  One warp per unit; persistent warps pull units
-// from an atomic counter.
+// from an atomic counter.  Three kernels:
 //
-// Test pass (count), per unit:
-//   A10  breadth-first descent from the root with Eq. 5 index ranges of the
-//        unit's query box widened by R'_u = max_i R'_i (lemma L1/L2,
-//        DESIGN.md): all cells of all frontier nodes of a level are flattened
-//        over the 32 lanes; empty cells skipped, internal cells form the next
-//        frontier, leaf cells are culled by their tight box (L3) and queued;
-//        queued leaves' particles are staged (flattened, two loads in flight
-//        per lane), culled per particle against the query box in fp64 (L3),
-//        as fp32 coordinates relative to the unit centre;
-//   A11  lanes = candidates (two per lane, packed f32x2), loop over queries:
-//        s32 < A_i -> certainly a neighbor, s32 >= B_i -> certainly not, else
-//        the exact fp64 predicate ((dx*dx + dy*dy) + dz*dz) < (2h)^2 decides
-//        (lemma L4).  __ballot_sync gives a 64-bit
-//        neighbor mask per (64-candidate chunk, query), kept in shared memory;
-//        __popc of the masks are the counts; masks and the chunk's candidate
-//        indices are recorded in an arena for the fill pass.
+// gather_kernel (A10): per unit, breadth-first descent from the root with
+//   Eq. 5 index ranges of the unit's query box widened by R'_u = max_i R'_i
+//   (lemma L1/L2): all cells of all frontier nodes of a level are
+//   flattened over the 32 lanes; empty cells skipped, internal cells form the
+//   next frontier, leaf cells are culled by their tight box (L3) and queued;
+//   queued leaves' particles are loaded (flattened over the lanes), culled
+//   per particle against the query box (L3) and written as fp32 coordinates
+//   relative to the unit centre into candidate blocks of <= 256 in an arena.
+// test_kernel (A11): per unit and candidate block, lanes = candidates (two
+//   per lane, packed f32x2), loop over queries: s32 < A_i -> certainly a
+//   neighbor, s32 >= B_i -> certainly not, else the exact fp64 predicate
+//   ((dx*dx + dy*dy) + dz*dz) < (2h)^2 decides (lemma L4).
+//   __ballot_sync gives a 64-bit neighbor mask per (64-candidate chunk,
+//   query); __popc of the masks are the counts; the masks are recorded.
 // Scan (A12): offsets = exclusive scan of counts.
-// Fill pass (A13): replay the recorded masks: __popc(mask & lanemask_lt) is
-//        each neighbor's slot in its CSR row; coalesced row writes.
+// fill_kernel (A13): replay the recorded masks: __popc(mask & lanemask_lt) is
+//   each neighbor's slot in its CSR row.
 #include <algorithm>
 #include <cfloat>
 
@@ -35,43 +33,31 @@ namespace bt {
 namespace {
 
 constexpr int kQ = 64;          // queries per unit (== build.cu kUnitQ)
-constexpr int kCand = 256;      // staged candidates per batch
-constexpr int kChunks = kCand / 64;
-constexpr int kLeafCap = 64;    // queued candidate leaves
-constexpr int kWarpsPerBlock = 4;
-constexpr int kWalkThreads = kWarpsPerBlock * 32;
+constexpr int kBlock = 256;     // candidates per arena block
+constexpr int kChunks = kBlock / 64;
+constexpr int kLeafCap = 64;    // queued candidate leaves (gather)
+constexpr int kGatherThreads = 128;
+constexpr int kTestThreads = 128;
 constexpr int kFillThreads = 256;
 
 // device counters (int64 slots of TreeDev::counters)
 enum {
-    C_WORK = 0,      // unit counter (test pass)
+    C_WORK = 0,      // unit counter (gather)
     C_MASK = 1,      // mask words requested
     C_CAND = 2,      // candidate slots requested
-    C_BATCH = 3,     // batches requested
+    C_BATCH = 3,     // candidate blocks requested
     C_STAGED = 4,
     C_TESTS = 5,
     C_EXACT = 6,
     C_MAXC = 7,
-    C_WORK2 = 8,     // unit counter (fill pass)
+    C_WORK2 = 8,     // unit counter (fill)
     C_HSUM = 9,      // checksum of h (bit patterns)
-    C_LOADED = 10,   // particle records loaded by staging (before the cull)
+    C_LOADED = 10,   // particle records loaded by the gather (before the cull)
+    C_WORK3 = 11,    // unit counter (test)
     C_N = 16
 };
 
 using Batch = WalkBatch;
-
-struct WarpSmem {
-    float4 q0[kQ];                         // ax, ax, ay, ay  (fp32, relative to the unit centre)
-    float4 q1[kQ];                         // az, az, A, B    (certain-accept / certain-reject)
-    int32_t qself[kQ];                     // batch slot of the query itself, -1 if not staged in this batch
-    float2 px[kCand / 2], py[kCand / 2], pz[kCand / 2];  // chunk k, lane l: (c[64k+l], c[64k+32+l])
-    int32_t cpos[kCand];                   // tree position of each staged candidate
-    int32_t corig[kCand];                  // caller index of each staged candidate
-    unsigned long long mask[kChunks][kQ];  // neighbor masks of the batch
-    int32_t lbeg[kLeafCap + 1];              // queued leaves: first tree position
-    int32_t lpre[kLeafCap + 1];            // queued leaves: exclusive prefix of counts
-    float4 loff[kLeafCap + 1];             // queued leaves: fl32(c_leaf - c_unit), w = 1 if staged from rec32
-};
 
 struct WalkArgs {
     const double4 *rec;
@@ -94,13 +80,15 @@ struct WalkArgs {
     int32_t *nbr;
     long long *ctr;
     // arena
-    unsigned long long *masks;
-    long long mask_cap;
-    int32_t *cands;
+    float4 *cand4;            // candidate block slots: ax, ay, az (fp32 rel.), tree position (int bits)
+    int32_t *cands;           // caller index of each candidate slot (-1 = padding)
     long long cand_cap;
+    long long *self_slot;     // per tree position: the arena slot of the query itself in its own unit
     Batch *batches;
     long long batch_cap;
-    int32_t *head;  // first batch of each unit
+    int32_t *head;            // first block of each unit
+    unsigned long long *masks;
+    long long mask_cap;
 };
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -140,17 +128,17 @@ __device__ __forceinline__ bool exact_pair(double qx, double qy, double qz, doub
 }
 
 // Bound on |a - (x - c)| for the fp32 relative coordinates a of every query
-// and staged candidate of a unit (lemma L4): queries use a = fl32(fl64(x - c))
-// (error <= u E + w (1+u) E + 2^-149); candidates staged from the compact
-// records use a = fl32(r32 + fl32(fl64(c_leaf - c))) with r32 =
-// fl32(fl64(x - c_leaf)), only for leaves of half-extent H <= 0.999 E, whose
-// error is <= (u + w(1+u))(H + D) + w(|x - c| + ...) + 3 2^-149 <= 4.0001 w E +
-// 3 2^-149 (D = |c_leaf - c| <= H + E).  One bound covers both.
+// and candidate of a unit (lemma L4): queries use a = fl32(fl64(x - c))
+// (error <= u E + w (1+u) E + 2^-149); candidates from the compact records
+// use a = fl32(r32 + fl32(fl64(c_leaf - c))) with r32 = fl32(fl64(x - c_leaf)),
+// only for leaves of half-extent H <= 0.999 E, whose error is
+// <= (u + w(1+u))(H + D) + w(|x - c| + ...) + 3 2^-149 <= 4.0001 w E + 3 2^-149
+// (D = |c_leaf - c| <= H + E).  One bound covers both.
 __device__ __forceinline__ double l4_eps(double E) { return 4.01 * 0x1p-24 * E + 0x1p-147; }
 
 // Lemma L4: thresholds A <= B (fp32) such that for the
 // fp32 squared distance s32 of a pair whose coordinates relative to the unit
-// centre are bounded by E (per axis),
+// centre carry error <= eps (E: coordinate bound),
 //   s32 <  A  =>  fp64 predicate true,     s32 >= B  =>  fp64 predicate false.
 // All slack factors round the bounds outward.
 __device__ __forceinline__ void l4_thresholds(double T, double E, double eps, bool exact_only, float &A, float &B) {
@@ -160,7 +148,7 @@ __device__ __forceinline__ void l4_thresholds(double T, double E, double eps, bo
         B = __int_as_float(0x7f800000);  // +inf: every pair goes to the fp64 predicate
         return;
     }
-    const double a0 = 2.0 * eps * (1.0 + w) + 0x1p-150;        // |d - D| <= a0 + w |D|
+    const double a0 = 2.0 * eps * (1.0 + w) + 0x1p-150;  // |d - D| <= a0 + w |D|
     const double g3 = 3.0 * w / (1.0 - 3.0 * w);
     auto err = [&](double S) {
         double D = 3.0 * a0 * a0 + 2.0 * 1.7320508075688775 * a0 * (1.0 + w) * sqrt(S) + (2.0 * w + w * w) * S;
@@ -177,194 +165,115 @@ __device__ __forceinline__ void l4_thresholds(double T, double E, double eps, bo
     B = (hb < 3.0e38) ? __double2float_ru(hb) : __int_as_float(0x7f800000);
 }
 
-// squared distance from a point to the box [lo, hi], fp64 rounded ops
-__device__ __forceinline__ double box_gap2(double x, double y, double z, double lx, double ly, double lz, double hx,
-                                           double hy, double hz) {
-    double gx = fmax(0.0, fmax(__dsub_rn(lx, x), __dsub_rn(x, hx)));
-    double gy = fmax(0.0, fmax(__dsub_rn(ly, y), __dsub_rn(y, hy)));
-    double gz = fmax(0.0, fmax(__dsub_rn(lz, z), __dsub_rn(z, hz)));
-    return __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
-}
-
-// per-unit state, held in registers (every field warp-uniform unless noted)
-struct Unit {
-    int64_t id;
-    int q0, nq;
+// ---------------------------------------------------------------------------
+// Unit geometry: identical code in the gather and the test kernels, so both
+// derive bit-identical c, E and R'_u.
+// ---------------------------------------------------------------------------
+struct UnitGeom {
+    int q0, nq, leaf;
     double lo[3], hi[3], c[3];
-    double Ru, Ru2;
-    float blo[3], bhi[3];   // query box in fp32 relative coordinates
-    float cull2;            // fp32 Minkowski cull threshold (conservative)
-    double E;               // a-priori bound |x - c| per axis (L4)
-    int ncand;        // staged candidates in the current batch
-    int nleaf;        // queued leaves
-    int prev_batch;
-    int cnt0, cnt1;   // per lane: counts of queries lane, lane + 32
-    long long staged, loaded, tests, exact;
+    double Ru, Ru2, E;
+    // this lane's queries (lane, lane + 32): fp64 coordinates, (2h)^2, caller index
+    double qx[2], qy[2], qz[2], qT[2];
+    int32_t qo[2];
 };
 
-// s32 of candidate pair (lane, lane + 32) of chunk k against query q
-struct Pair32 {
-    float s0, s1;
-};
-__device__ __forceinline__ Pair32 s32_pair(unsigned long long cx, unsigned long long cy, unsigned long long cz,
-                                           const float4 &Q0, const float4 &Q1) {
-    const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
-    const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
-    const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
-    unsigned long long s = f2_mul(dx, dx);
-    s = f2_fma(dy, dy, s);
-    s = f2_fma(dz, dz, s);
-    return Pair32{__uint_as_float((unsigned)s), __uint_as_float((unsigned)(s >> 32))};
-}
-
-// The exact band of lemma L4 (rare): redo the batch's pairs, and let the fp64
-// predicate itself decide every pair with A <= s32 < B.
-__device__ __noinline__ void resolve_band(WarpSmem &S, Unit &U, int lane, const WalkArgs &a, int nch) {
-    for (int k = 0; k < nch; k++) {
-        const float2 vx = S.px[32 * k + lane], vy = S.py[32 * k + lane], vz = S.pz[32 * k + lane];
-        const unsigned long long cx = pk(vx.x, vx.y), cy = pk(vy.x, vy.y), cz = pk(vz.x, vz.y);
-        const int cp0 = S.cpos[64 * k + lane], cp1 = S.cpos[64 * k + 32 + lane];
-        for (int q = 0; q < U.nq; q++) {
-            const float4 Q0 = S.q0[q], Q1 = S.q1[q];
-            const Pair32 p = s32_pair(cx, cy, cz, Q0, Q1);
-            const bool u0 = !(p.s0 < Q1.z) && p.s0 < Q1.w, u1 = !(p.s1 < Q1.z) && p.s1 < Q1.w;
-            if (!__any_sync(0xffffffffu, u0 || u1)) continue;
-            const int qp = U.q0 + q;
-            const double4 Qr = a.rec[qp];
-            const double t = __dmul_rn(2.0, a.h_tree[qp]);
-            const double T = __dmul_rn(t, t);
-            bool e0 = false, e1 = false;
-            if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
-            if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
-            const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
-            if (lane == 0) S.mask[k][q] |= ((unsigned long long)m1 << 32) | m0;
-            U.exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
-            __syncwarp();
+__device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, int lane, UnitGeom &G) {
+    G.leaf = UU.x;
+    G.q0 = UU.y;
+    G.nq = UU.z;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    double Ru = 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int k = lane + 32 * h;
+        G.qx[h] = G.qy[h] = G.qz[h] = G.qT[h] = 0.0;
+        G.qo[h] = 0;
+        if (k < G.nq) {
+            const double4 r = a.rec[G.q0 + k];
+            const double t = __dmul_rn(2.0, a.h_tree[G.q0 + k]);  // 2h (exact)
+            G.qx[h] = r.x;
+            G.qy[h] = r.y;
+            G.qz[h] = r.z;
+            G.qT[h] = __dmul_rn(t, t);
+            G.qo[h] = (int32_t)__double_as_longlong(r.w);
+            // R' = 2h (1 + 2^-40) + 2^-50 M   (lemma L1/L2)
+            Ru = fmax(Ru, __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M)));
+            lo[0] = fmin(lo[0], r.x); lo[1] = fmin(lo[1], r.y); lo[2] = fmin(lo[2], r.z);
+            hi[0] = fmax(hi[0], r.x); hi[1] = fmax(hi[1], r.y); hi[2] = fmax(hi[2], r.z);
         }
     }
-    __syncwarp();
+    // a unit holding its whole leaf has the leaf's tight box as its query box
+    const bool whole = G.nq == a.leaf_count[G.leaf];
+    const double *lb = a.leaf_box + 6 * (int64_t)G.leaf;
+    double E = 0.0, Mu = 0.0;
+    for (int l = 0; l < 3; l++) {
+        G.lo[l] = whole ? lb[l] : warp_min(lo[l]);
+        G.hi[l] = whole ? lb[3 + l] : warp_max(hi[l]);
+        G.c[l] = 0.5 * (G.lo[l] + G.hi[l]);
+        E = fmax(E, 0.5 * (G.hi[l] - G.lo[l]));
+        Mu = fmax(Mu, fmax(fabs(G.lo[l]), fabs(G.hi[l])));
+    }
+    G.Ru = warp_max(Ru);
+    G.Ru2 = __dmul_rn(G.Ru, G.Ru);
+    // a-priori bound |x - c| <= E per axis for queries and kept candidates (L4)
+    G.E = (E + G.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
 }
 
 // ---------------------------------------------------------------------------
-// A11: test the staged batch against all queries, record it, count.
+// gather_kernel
 // ---------------------------------------------------------------------------
-__device__ __noinline__ void test_batch(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
-    const int ncand = U.ncand;
-    const int nq = U.nq;
-    const int nch = (ncand + 63) >> 6;
-    const float inf = __int_as_float(0x7f800000);
-    // pad the last chunk: +inf coordinates never pass (s32 = +inf)
-    for (int c = ncand + lane; c < nch * 64; c += 32) {
-        const int k = c >> 6, l = c & 31, hi = (c >> 5) & 1;
-        reinterpret_cast<float *>(&S.px[32 * k + l])[hi] = inf;
-        reinterpret_cast<float *>(&S.py[32 * k + l])[hi] = inf;
-        reinterpret_cast<float *>(&S.pz[32 * k + l])[hi] = inf;
-        S.corig[c] = -1;
-        S.cpos[c] = -1;
-    }
-    __syncwarp();
-    // Hot loop, branch free, register blocked: 4 queries held in registers,
-    // candidate pairs of each chunk streamed from shared memory.  Certain
-    // accepts (s32 < A) go into the masks; the ballots of s32 < B are compared
-    // with them, and any difference (a pair in the band [A, B) of lemma L4) is
-    // resolved afterwards by the fp64 predicate.  Queries are padded to a
-    // multiple of 4 with A = B = 0.
-    unsigned diff = 0;
-    for (int q = 0; q < nq; q += 4) {
-        unsigned long long qx[4], qy[4], qz[4];
-        float A[4], B[4];
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            const float4 Q0 = S.q0[q + i], Q1 = S.q1[q + i];
-            qx[i] = pk(Q0.x, Q0.y);
-            qy[i] = pk(Q0.z, Q0.w);
-            qz[i] = pk(Q1.x, Q1.y);
-            A[i] = Q1.z;
-            B[i] = Q1.w;
-        }
-        for (int k = 0; k < nch; k++) {
-            const float2 vx = S.px[32 * k + lane], vy = S.py[32 * k + lane], vz = S.pz[32 * k + lane];
-            const unsigned long long cx = pk(vx.x, vx.y), cy = pk(vy.x, vy.y), cz = pk(vz.x, vz.y);
-            unsigned long long m[4];
-#pragma unroll
-            for (int i = 0; i < 4; i++) {
-                const unsigned long long dx = f2_sub(cx, qx[i]);
-                const unsigned long long dy = f2_sub(cy, qy[i]);
-                const unsigned long long dz = f2_sub(cz, qz[i]);
-                unsigned long long s = f2_mul(dx, dx);
-                s = f2_fma(dy, dy, s);
-                s = f2_fma(dz, dz, s);
-                const float s0 = __uint_as_float((unsigned)s), s1 = __uint_as_float((unsigned)(s >> 32));
-                const unsigned m0 = __ballot_sync(0xffffffffu, s0 < A[i]);
-                const unsigned m1 = __ballot_sync(0xffffffffu, s1 < A[i]);
-                const unsigned n0 = __ballot_sync(0xffffffffu, s0 < B[i]);
-                const unsigned n1 = __ballot_sync(0xffffffffu, s1 < B[i]);
-                diff |= (n0 ^ m0) | (n1 ^ m1);
-                m[i] = ((unsigned long long)m1 << 32) | m0;
-            }
-            if (lane == 0) {
-                ulonglong2 *dst = reinterpret_cast<ulonglong2 *>(&S.mask[k][q]);
-                dst[0] = make_ulonglong2(m[0], m[1]);
-                dst[1] = make_ulonglong2(m[2], m[3]);
-            }
-        }
-    }
-    __syncwarp();
-    if (diff) resolve_band(S, U, lane, a, nch);
-    __syncwarp();
-    // self is never its own neighbor (R12); counts; record the batch
-    for (int q = lane; q < nq; q += 32) {
-        const int sl = S.qself[q];
-        if (sl >= 0) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
-        int c = 0;
-        for (int k = 0; k < nch; k++) c += __popcll(S.mask[k][q]);
-        if (q < 32) U.cnt0 += c;
-        else U.cnt1 += c;
-        S.qself[q] = -1;
-    }
-    long long mb = 0, cb = 0, bi = 0;
+struct GatherSmem {
+    int32_t lbeg[kLeafCap + 1];  // queued leaves: first tree position
+    int32_t lpre[kLeafCap + 1];  // queued leaves: counts, then exclusive prefix
+    float4 loff[kLeafCap + 1];   // queued leaves: fl32(c_leaf - c_unit), w = 1 if staged from rec32
+};
+
+struct GatherState {
+    int64_t uid;
+    int nleaf;
+    // current candidate block
+    int blk;           // block index, -1 = none
+    long long base;    // first arena slot of the block
+    int fill;          // candidates in the block
+    bool rec_ok;       // arena space was available for every block
+    // cull constants
+    float blo[3], bhi[3], cull2;
+    long long staged, loaded;
+};
+
+__device__ __forceinline__ void close_block(GatherState &st, int lane, const WalkArgs &a) {
+    if (st.blk >= 0 && st.rec_ok && lane == 0) a.batches[st.blk].ncand = st.fill;
+}
+
+__device__ __noinline__ void open_block(GatherState &st, int lane, const WalkArgs &a) {
+    close_block(st, lane, a);
+    long long base = 0, bi = 0;
     if (lane == 0) {
-        mb = atomicAdd((unsigned long long *)&a.ctr[C_MASK], (unsigned long long)(nch * nq));
-        cb = atomicAdd((unsigned long long *)&a.ctr[C_CAND], (unsigned long long)(nch * 64));
+        base = atomicAdd((unsigned long long *)&a.ctr[C_CAND], (unsigned long long)kBlock);
         bi = atomicAdd((unsigned long long *)&a.ctr[C_BATCH], 1ull);
     }
-    mb = __shfl_sync(0xffffffffu, mb, 0);
-    cb = __shfl_sync(0xffffffffu, cb, 0);
+    base = __shfl_sync(0xffffffffu, base, 0);
     bi = __shfl_sync(0xffffffffu, bi, 0);
-    const bool record = (mb + (long long)nch * nq <= a.mask_cap) && (cb + (long long)nch * 64 <= a.cand_cap) &&
-                        (bi < a.batch_cap);
-    __syncwarp();
-    if (record) {
-        for (int c = lane; c < nch * 64; c += 32) a.cands[cb + c] = S.corig[c];
-        for (int w = lane; w < nch * nq; w += 32) a.masks[mb + w] = S.mask[w / nq][w % nq];
-        if (lane == 0) {
-            a.batches[bi] = Batch{mb, cb, ncand, -1};
-            if (U.prev_batch >= 0) a.batches[U.prev_batch].next = (int)bi;
-            else a.head[U.id] = (int)bi;
-        }
-        U.prev_batch = (int)bi;
+    const bool ok = st.rec_ok && base + kBlock <= a.cand_cap && bi < a.batch_cap;
+    if (ok && lane == 0) {
+        a.batches[bi] = Batch{-1, base, 0, -1};
+        if (st.blk >= 0) a.batches[st.blk].next = (int)bi;
+        else a.head[st.uid] = (int)bi;
     }
-    U.tests += (long long)ncand * nq;
-    U.ncand = 0;
+    st.rec_ok = ok;
+    st.blk = (int)bi;
+    st.base = base;
+    st.fill = 0;
     __syncwarp();
 }
 
-// ---------------------------------------------------------------------------
-// Stage the queued leaves' particles (flattened over the lanes, two loads in
-// flight per lane), per-particle cull (L3), fp32 relative coordinates.
-// ---------------------------------------------------------------------------
-__device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const WalkArgs &a) {
+// Load the queued leaves' particles (flattened over the lanes), cull them per
+// particle (L3, fp32 conservative) and append the kept ones to the arena.
+__device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &st, const UnitGeom &G, int lane,
+                                          const WalkArgs &a) {
     const unsigned lt = lanemask_lt();
-    const int nl = U.nleaf;
-    // unit constants in registers (U lives in local memory across calls)
-    const float blo0 = U.blo[0], blo1 = U.blo[1], blo2 = U.blo[2];
-    const float bhi0 = U.bhi[0], bhi1 = U.bhi[1], bhi2 = U.bhi[2];
-    const float cull2 = U.cull2;
-    const double c0 = U.c[0], c1 = U.c[1], c2 = U.c[2];
-    const int q0 = U.q0, nq = U.nq;
-    int ncand = U.ncand;
-    int staged = 0, loaded = 0;
-    // exclusive prefix of the queued leaf counts (lpre was filled with counts)
+    const int nl = st.nleaf;
     int carry = 0;
     for (int i0 = 0; i0 < nl; i0 += 32) {
         const int i = i0 + lane;
@@ -380,19 +289,24 @@ __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const 
     if (lane == 0) S.lpre[nl] = carry;
     __syncwarp();
     const int total = carry;
-    int owner = 0;  // queued leaf that holds the next flattened position
-    // gather one group of 64 flattened positions: record, leaf offset, position
-    auto gather = [&](int p0, float4 (&r)[2], float4 (&of)[2], int (&pos)[2], bool (&valid)[2]) {
+    const int q0 = G.q0, nq = G.nq;
+    const double c0 = G.c[0], c1 = G.c[1], c2 = G.c[2];
+    int owner = 0;  // queued leaf holding the next flattened position
+    for (int p0 = 0; p0 < total; p0 += 64) {
+        if (st.blk < 0 || st.fill + 64 > kBlock) open_block(st, lane, a);
+        float4 r[2], of[2];
+        int pos[2];
+        bool valid[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int w0 = p0 + 32 * h;
             // owners of the 32 positions [w0, w0 + 32): leaf starts inside the window
             const int nxt = owner + 1 + lane;
-            const int st = (nxt <= nl) ? S.lpre[nxt] : 0x7fffffff;
-            const int off = st - w0;  // >= 1 for leaves after `owner` (until it crosses)
+            const int stt = (nxt <= nl) ? S.lpre[nxt] : 0x7fffffff;
+            const int off = stt - w0;  // >= 1 for leaves after `owner`
             const unsigned bits = __reduce_or_sync(0xffffffffu, (off >= 1 && off < 32) ? (1u << off) : 0u);
             const int mine = owner + __popc(bits & ((2u << lane) - 1u));
-            const unsigned past = __ballot_sync(0xffffffffu, off <= 32);  // starts at or before w0 + 32
+            const unsigned past = __ballot_sync(0xffffffffu, off <= 32);
             const int p = w0 + lane;
             valid[h] = p < total;
             pos[h] = valid[h] ? S.lbeg[mine] + (p - S.lpre[mine]) : 0;
@@ -411,203 +325,110 @@ __device__ __noinline__ void stage_leaves(WarpSmem &S, Unit &U, int lane, const 
                 }
             }
         }
-    };
-    float4 r[2], of[2];
-    int pos[2];
-    bool valid[2];
-    if (total > 0) gather(0, r, of, pos, valid);
-    for (int p0 = 0; p0 < total; p0 += 64) {
-        // prefetch the next group before culling this one (loads in flight)
-        float4 rn[2], ofn[2];
-        int posn[2];
-        bool validn[2] = {false, false};
-        if (p0 + 64 < total) gather(p0 + 64, rn, ofn, posn, validn);
-        if (ncand + 64 > kCand) {
-            U.ncand = ncand;
-            test_batch(S, U, lane, a);
-            ncand = 0;
-        }
 #pragma unroll
         for (int h = 0; h < 2; h++) {
-            // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c)); the
-            // fp64 path already holds fl32(fl64(x - c)) with a zero offset) and the
+            // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
             // conservative fp32 Minkowski cull against the query box (L3 / L4)
             const float ax = __fadd_rn(r[h].x, of[h].x);
             const float ay = __fadd_rn(r[h].y, of[h].y);
             const float az = __fadd_rn(r[h].z, of[h].z);
-            const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(blo0, ax), __fsub_rn(ax, bhi0)));
-            const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(blo1, ay), __fsub_rn(ay, bhi1)));
-            const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(blo2, az), __fsub_rn(az, bhi2)));
+            const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(st.blo[0], ax), __fsub_rn(ax, st.bhi[0])));
+            const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(st.blo[1], ay), __fsub_rn(ay, st.bhi[1])));
+            const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(st.blo[2], az), __fsub_rn(az, st.bhi[2])));
             const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
-            const bool keep = valid[h] && g2 < cull2;
+            const bool keep = valid[h] && g2 < st.cull2;
             const unsigned km = __ballot_sync(0xffffffffu, keep);
-            if (keep) {
-                const int slot = ncand + __popc(km & lt);
-                const int ck = slot >> 6, cl = slot & 31, ch = (slot >> 5) & 1;
-                reinterpret_cast<float *>(&S.px[32 * ck + cl])[ch] = ax;
-                reinterpret_cast<float *>(&S.py[32 * ck + cl])[ch] = ay;
-                reinterpret_cast<float *>(&S.pz[32 * ck + cl])[ch] = az;
-                S.cpos[slot] = pos[h];
-                S.corig[slot] = __float_as_int(r[h].w);
+            if (keep && st.rec_ok) {
+                const long long slot = st.base + st.fill + __popc(km & lt);
+                a.cand4[slot] = make_float4(ax, ay, az, __int_as_float(pos[h]));
+                a.cands[slot] = __float_as_int(r[h].w);
                 const int qi = pos[h] - q0;
-                if (qi >= 0 && qi < nq) S.qself[qi] = slot;
+                if (qi >= 0 && qi < nq) a.self_slot[pos[h]] = slot;
             }
-            ncand += __popc(km);
-            staged += __popc(km);
-            loaded += __popc(__ballot_sync(0xffffffffu, valid[h]));
+            st.fill += __popc(km);
+            st.staged += __popc(km);
+            st.loaded += __popc(__ballot_sync(0xffffffffu, valid[h]));
         }
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            r[h] = rn[h];
-            of[h] = ofn[h];
-            pos[h] = posn[h];
-            valid[h] = validn[h];
-        }
-        __syncwarp();
     }
-    U.ncand = ncand;
-    U.staged += staged;
-    U.loaded += loaded;
-    U.nleaf = 0;
+    st.nleaf = 0;
     __syncwarp();
 }
 
-// queue a leaf (if its tight box is within R'_u of the query box: L3)
-__device__ __forceinline__ void queue_leaves(WarpSmem &S, Unit &U, int lane, const WalkArgs &a, bool is_leaf,
-                                             int32_t leaf) {
+// queue the leaf cells found by the lanes (if the tight box is within R'_u of
+// the query box: L3)
+__device__ __forceinline__ void queue_leaves(GatherSmem &S, GatherState &st, const UnitGeom &G, int lane,
+                                             const WalkArgs &a, bool is_leaf, int32_t leaf) {
     const unsigned lt = lanemask_lt();
     bool keep = false;
     float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
     if (is_leaf) {
         const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
         const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
-        double gx = fmax(0.0, fmax(__dsub_rn(b0.x, U.hi[0]), __dsub_rn(U.lo[0], b1.y)));
-        double gy = fmax(0.0, fmax(__dsub_rn(b0.y, U.hi[1]), __dsub_rn(U.lo[1], b2.x)));
-        double gz = fmax(0.0, fmax(__dsub_rn(b1.x, U.hi[2]), __dsub_rn(U.lo[2], b2.y)));
+        double gx = fmax(0.0, fmax(__dsub_rn(b0.x, G.hi[0]), __dsub_rn(G.lo[0], b1.y)));
+        double gy = fmax(0.0, fmax(__dsub_rn(b0.y, G.hi[1]), __dsub_rn(G.lo[1], b2.x)));
+        double gz = fmax(0.0, fmax(__dsub_rn(b1.x, G.hi[2]), __dsub_rn(G.lo[2], b2.y)));
         double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
-        keep = g2 < U.Ru2;
+        keep = g2 < G.Ru2;
         // leaf centre (as build.cu computed it) relative to the unit centre; the
         // compact records are usable when the leaf half-extent H <= 0.999 E (l4_eps)
         const double cx = 0.5 * (b0.x + b1.y), cy = 0.5 * (b0.y + b2.x), cz = 0.5 * (b1.x + b2.y);
         const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
-        off = make_float4(__double2float_rn(__dsub_rn(cx, U.c[0])), __double2float_rn(__dsub_rn(cy, U.c[1])),
-                          __double2float_rn(__dsub_rn(cz, U.c[2])), (H <= 0.999 * U.E) ? 1.0f : 0.0f);
+        off = make_float4(__double2float_rn(__dsub_rn(cx, G.c[0])), __double2float_rn(__dsub_rn(cy, G.c[1])),
+                          __double2float_rn(__dsub_rn(cz, G.c[2])), (H <= 0.999 * G.E) ? 1.0f : 0.0f);
     }
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     if (!km) return;
-    if (U.nleaf + __popc(km) > kLeafCap) stage_leaves(S, U, lane, a);
+    if (st.nleaf + __popc(km) > kLeafCap) stage_leaves(S, st, G, lane, a);
     if (keep) {
-        const int slot = U.nleaf + __popc(km & lt);
+        const int slot = st.nleaf + __popc(km & lt);
         S.lbeg[slot] = a.leaf_begin[leaf];
         S.lpre[slot] = a.leaf_count[leaf];  // counts; stage_leaves turns them into a prefix
         S.loff[slot] = off;
     }
-    U.nleaf += __popc(km);
+    st.nleaf += __popc(km);
     __syncwarp();
 }
 
-#ifndef BT_WALK_MIN_BLOCKS
-#define BT_WALK_MIN_BLOCKS 5
-#endif
-__global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) test_kernel(WalkArgs a) {
-    __shared__ WarpSmem smem[kWarpsPerBlock];
+__global__ void __launch_bounds__(kGatherThreads, 6) gather_kernel(WalkArgs a) {
+    __shared__ GatherSmem smem[kGatherThreads / 32];
     const int lane = threadIdx.x & 31;
-    WarpSmem &S = smem[threadIdx.x >> 5];
+    GatherSmem &S = smem[threadIdx.x >> 5];
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int32_t *const front_base = a.front + gwarp * 2 * a.front_cap;
     const unsigned lt = lanemask_lt();
-    long long staged = 0, loaded = 0, tests = 0, exact = 0;
-
+    long long staged = 0, loaded = 0;
     for (;;) {
         unsigned long long uid = 0;
         if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK], 1ull);
         uid = __shfl_sync(0xffffffffu, uid, 0);
         if (uid >= (unsigned long long)a.n_units) break;
-        const int4 UU = a.units[uid];
-        Unit U;
-        U.id = (int64_t)uid;
-        U.q0 = UU.y;
-        U.nq = UU.z;
-        U.ncand = U.nleaf = 0;
-        U.prev_batch = -1;
-        U.cnt0 = U.cnt1 = 0;
-        U.staged = U.loaded = U.tests = U.exact = 0;
+        UnitGeom G;
+        unit_setup(a, a.units[uid], lane, G);
+        GatherState st;
+        st.uid = (int64_t)uid;
+        st.nleaf = 0;
+        st.blk = -1;
+        st.base = 0;
+        st.fill = 0;
+        st.rec_ok = true;
+        st.staged = st.loaded = 0;
         if (lane == 0) a.head[uid] = -1;
-
-        // ---- queries: coordinates, (2h)^2, R', box
-        double qx[2], qy[2], qz[2], qT[2];
-        int32_t qo[2] = {0, 0};
-        double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-        double Ru = 0.0;
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int k = lane + 32 * h;
-            qx[h] = qy[h] = qz[h] = qT[h] = 0.0;
-            if (k < U.nq) {
-                const double4 r = a.rec[U.q0 + k];
-                const double t = __dmul_rn(2.0, a.h_tree[U.q0 + k]);  // 2h (exact)
-                qx[h] = r.x;
-                qy[h] = r.y;
-                qz[h] = r.z;
-                qT[h] = __dmul_rn(t, t);
-                qo[h] = (int32_t)__double_as_longlong(r.w);
-                // R' = 2h (1 + 2^-40) + 2^-50 M   (lemma L1/L2)
-                Ru = fmax(Ru, __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M)));
-                lo[0] = fmin(lo[0], r.x); lo[1] = fmin(lo[1], r.y); lo[2] = fmin(lo[2], r.z);
-                hi[0] = fmax(hi[0], r.x); hi[1] = fmax(hi[1], r.y); hi[2] = fmax(hi[2], r.z);
-            }
-            S.qself[k] = -1;
-        }
-        double E = 0.0, Mu = 0.0;
-        // a unit holding its whole leaf has the leaf's tight box as its query box
-        const bool whole = U.nq == a.leaf_count[UU.x];
-        const double *lb = a.leaf_box + 6 * (int64_t)UU.x;
-        for (int l = 0; l < 3; l++) {
-            U.lo[l] = whole ? lb[l] : warp_min(lo[l]);
-            U.hi[l] = whole ? lb[3 + l] : warp_max(hi[l]);
-            U.c[l] = 0.5 * (U.lo[l] + U.hi[l]);
-            E = fmax(E, 0.5 * (U.hi[l] - U.lo[l]));
-            Mu = fmax(Mu, fmax(fabs(U.lo[l]), fabs(U.hi[l])));
-        }
-        U.Ru = warp_max(Ru);
-        U.Ru2 = __dmul_rn(U.Ru, U.Ru);
-        // a-priori bound |x - c| <= E per axis for queries and staged candidates (L4)
-        E = (E + U.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
-        U.E = E;
         {
             // fp32 images of the query box and the conservative cull radius
-            // (R'_u + 4 eps)(1 + 2^-20), eps = the fp32 coordinate error bound of L4
-            const double eps = l4_eps(E);
+            // (R'_u + 4 eps)(1 + 2^-20) (L3 / L4)
+            const double eps = l4_eps(G.E);
             for (int l = 0; l < 3; l++) {
-                U.blo[l] = __double2float_rn(__dsub_rn(U.lo[l], U.c[l]));
-                U.bhi[l] = __double2float_rn(__dsub_rn(U.hi[l], U.c[l]));
+                st.blo[l] = __double2float_rn(__dsub_rn(G.lo[l], G.c[l]));
+                st.bhi[l] = __double2float_rn(__dsub_rn(G.hi[l], G.c[l]));
             }
-            const double rc = (U.Ru + 4.0 * eps) * (1.0 + 0x1p-20);
+            const double rc = (G.Ru + 4.0 * eps) * (1.0 + 0x1p-20);
             const double rc2 = rc * rc * (1.0 + 0x1p-40);
-            U.cull2 = (rc2 < 3.0e38) ? __double2float_ru(rc2) : __int_as_float(0x7f800000);
+            st.cull2 = (rc2 < 3.0e38) ? __double2float_ru(rc2) : __int_as_float(0x7f800000);
         }
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int k = lane + 32 * h;
-            if (k < U.nq) {
-                const float ax = __double2float_rn(__dsub_rn(qx[h], U.c[0]));
-                const float ay = __double2float_rn(__dsub_rn(qy[h], U.c[1]));
-                const float az = __double2float_rn(__dsub_rn(qz[h], U.c[2]));
-                float A, B;
-                l4_thresholds(qT[h], E, l4_eps(E), a.exact_only != 0, A, B);
-                S.q0[k] = make_float4(ax, ax, ay, ay);
-                S.q1[k] = make_float4(az, az, A, B);
-            } else {
-                S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                S.q1[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // A = B = 0: never a neighbor
-            }
-        }
-        __syncwarp();
-
-        // ---- A10: breadth-first descent, all cells of a level flattened over the lanes
         if (a.root_is_leaf) {
-            queue_leaves(S, U, lane, a, lane == 0, 0);
+            queue_leaves(S, st, G, lane, a, lane == 0, 0);
         } else {
+            // ---- A10: breadth-first descent, all cells of a level flattened over the lanes
             int32_t *fcur = front_base, *fnext = front_base + a.front_cap;
             int nf = 1;
             if (lane == 0) fcur[0] = 0;
@@ -624,8 +445,8 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) test_kernel(
                         cb = nd.cell_base;
                         int r0[3], r1[3];
                         for (int l = 0; l < 3; l++) {
-                            r0[l] = cell_coord(__dsub_rn(U.lo[l], U.Ru), nd.lo[l], nd.ext[l], b);
-                            r1[l] = cell_coord(__dadd_rn(U.hi[l], U.Ru), nd.lo[l], nd.ext[l], b);
+                            r0[l] = cell_coord(__dsub_rn(G.lo[l], G.Ru), nd.lo[l], nd.ext[l], b);
+                            r1[l] = cell_coord(__dadd_rn(G.hi[l], G.Ru), nd.lo[l], nd.ext[l], b);
                         }
                         r0x = r0[0];
                         r0y = r0[1];
@@ -673,7 +494,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) test_kernel(
                         const unsigned nm = __ballot_sync(0xffffffffu, is_node);
                         if (is_node) fnext[nnext + __popc(nm & lt)] = code_node(code);
                         nnext += __popc(nm);
-                        queue_leaves(S, U, lane, a, is_leaf, code);
+                        queue_leaves(S, st, G, lane, a, is_leaf, code);
                     }
                 }
                 __syncwarp();
@@ -683,19 +504,167 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) test_kernel(
                 nf = nnext;
             }
         }
-        if (U.nleaf > 0) stage_leaves(S, U, lane, a);
-        if (U.ncand > 0 || U.prev_batch < 0) test_batch(S, U, lane, a);
-        if (lane < U.nq) a.counts[qo[0]] = U.cnt0;
-        if (lane + 32 < U.nq) a.counts[qo[1]] = U.cnt1;
-        staged += U.staged;
-        loaded += U.loaded;
-        tests += U.tests;
-        exact += U.exact;
+        if (st.nleaf > 0) stage_leaves(S, st, G, lane, a);
+        close_block(st, lane, a);
+        staged += st.staged;
+        loaded += st.loaded;
         __syncwarp();
     }
     if (lane == 0) {
         atomicAdd((unsigned long long *)&a.ctr[C_STAGED], (unsigned long long)staged);
         atomicAdd((unsigned long long *)&a.ctr[C_LOADED], (unsigned long long)loaded);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// test_kernel
+// ---------------------------------------------------------------------------
+struct TestSmem {
+    float4 q0[kQ];                         // ax, ax, ay, ay  (fp32, relative to the unit centre)
+    float4 q1[kQ];                         // az, az, A, B    (certain-accept / certain-reject)
+    unsigned long long mask[kChunks][kQ];  // neighbor masks of the block
+};
+
+// The exact band of lemma L4 (rare): redo the block's pairs and let the fp64
+// predicate itself decide every pair with A <= s32 < B.
+__device__ __noinline__ void resolve_band(TestSmem &S, const UnitGeom &G, int lane, const WalkArgs &a,
+                                          const Batch &B, int nch, long long &exact) {
+    for (int k = 0; k < nch; k++) {
+        const int s0 = 64 * k + lane, s1 = s0 + 32;
+        const float inf = __int_as_float(0x7f800000);
+        float4 c0 = make_float4(inf, inf, inf, __int_as_float(-1)), c1 = c0;
+        if (s0 < B.ncand) c0 = a.cand4[B.cand_base + s0];
+        if (s1 < B.ncand) c1 = a.cand4[B.cand_base + s1];
+        const unsigned long long cx = pk(c0.x, c1.x), cy = pk(c0.y, c1.y), cz = pk(c0.z, c1.z);
+        const int cp0 = __float_as_int(c0.w), cp1 = __float_as_int(c1.w);
+        for (int q = 0; q < G.nq; q++) {
+            const float4 Q0 = S.q0[q], Q1 = S.q1[q];
+            const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
+            const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
+            const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
+            unsigned long long s = f2_mul(dx, dx);
+            s = f2_fma(dy, dy, s);
+            s = f2_fma(dz, dz, s);
+            const float v0 = __uint_as_float((unsigned)s), v1 = __uint_as_float((unsigned)(s >> 32));
+            const bool u0 = !(v0 < Q1.z) && v0 < Q1.w, u1 = !(v1 < Q1.z) && v1 < Q1.w;
+            if (!__any_sync(0xffffffffu, u0 || u1)) continue;
+            const int qp = G.q0 + q;
+            const double4 Qr = a.rec[qp];
+            const double t = __dmul_rn(2.0, a.h_tree[qp]);
+            const double T = __dmul_rn(t, t);
+            bool e0 = false, e1 = false;
+            if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
+            if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
+            const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
+            if (lane == 0) S.mask[k][q] |= ((unsigned long long)m1 << 32) | m0;
+            exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+}
+
+__global__ void __launch_bounds__(kTestThreads, 6) test_kernel(WalkArgs a) {
+    __shared__ TestSmem smem[kTestThreads / 32];
+    const int lane = threadIdx.x & 31;
+    TestSmem &S = smem[threadIdx.x >> 5];
+    long long tests = 0, exact = 0;
+    const float inf = __int_as_float(0x7f800000);
+    for (;;) {
+        unsigned long long uid = 0;
+        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK3], 1ull);
+        uid = __shfl_sync(0xffffffffu, uid, 0);
+        if (uid >= (unsigned long long)a.n_units) break;
+        UnitGeom G;
+        unit_setup(a, a.units[uid], lane, G);
+        const int nq = G.nq;
+        long long self[2] = {-1, -1};
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int k = lane + 32 * h;
+            if (k < nq) {
+                const float ax = __double2float_rn(__dsub_rn(G.qx[h], G.c[0]));
+                const float ay = __double2float_rn(__dsub_rn(G.qy[h], G.c[1]));
+                const float az = __double2float_rn(__dsub_rn(G.qz[h], G.c[2]));
+                float A, B;
+                l4_thresholds(G.qT[h], G.E, l4_eps(G.E), a.exact_only != 0, A, B);
+                S.q0[k] = make_float4(ax, ax, ay, ay);
+                S.q1[k] = make_float4(az, az, A, B);
+                self[h] = a.self_slot[G.q0 + k];
+            } else {
+                S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                S.q1[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // A = B = 0: never a neighbor
+            }
+        }
+        int cnt[2] = {0, 0};
+        __syncwarp();
+        for (int b = a.head[uid]; b >= 0;) {
+            const Batch B = a.batches[b];
+            const int nch = (B.ncand + 63) >> 6;
+            // Hot loop, branch free: certain accepts (s32 < A) go into the masks;
+            // the ballots of s32 < B are compared with them, and any difference
+            // (a pair in the band [A, B) of lemma L4) is resolved afterwards by
+            // the fp64 predicate.  Queries are padded to a multiple of 4.
+            unsigned diff = 0;
+            for (int k = 0; k < nch; k++) {
+                const int s0 = 64 * k + lane, s1 = s0 + 32;
+                float4 c0 = make_float4(inf, inf, inf, 0.f), c1 = c0;  // padding: s32 = +inf
+                if (s0 < B.ncand) c0 = a.cand4[B.cand_base + s0];
+                if (s1 < B.ncand) c1 = a.cand4[B.cand_base + s1];
+                const unsigned long long cx = pk(c0.x, c1.x), cy = pk(c0.y, c1.y), cz = pk(c0.z, c1.z);
+                unsigned long long *mrow = &S.mask[k][0];
+                for (int q = 0; q < nq; q += 4) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) {
+                        const float4 Q0 = S.q0[q + i], Q1 = S.q1[q + i];
+                        const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
+                        const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
+                        const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
+                        unsigned long long s = f2_mul(dx, dx);
+                        s = f2_fma(dy, dy, s);
+                        s = f2_fma(dz, dz, s);
+                        const float v0 = __uint_as_float((unsigned)s), v1 = __uint_as_float((unsigned)(s >> 32));
+                        const unsigned m0 = __ballot_sync(0xffffffffu, v0 < Q1.z);
+                        const unsigned m1 = __ballot_sync(0xffffffffu, v1 < Q1.z);
+                        const unsigned n0 = __ballot_sync(0xffffffffu, v0 < Q1.w);
+                        const unsigned n1 = __ballot_sync(0xffffffffu, v1 < Q1.w);
+                        diff |= (n0 ^ m0) | (n1 ^ m1);
+                        if (lane == 0) mrow[q + i] = ((unsigned long long)m1 << 32) | m0;
+                    }
+                }
+            }
+            __syncwarp();
+            if (diff) resolve_band(S, G, lane, a, B, nch, exact);
+            // self is never its own neighbor (R12); counts
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int q = lane + 32 * h;
+                if (q < nq) {
+                    const long long sl = self[h] - B.cand_base;
+                    if (sl >= 0 && sl < 64 * nch) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
+                    int c = 0;
+                    for (int k = 0; k < nch; k++) c += __popcll(S.mask[k][q]);
+                    cnt[h] += c;
+                }
+            }
+            // record the masks for the fill pass
+            long long mb = 0;
+            if (lane == 0) mb = atomicAdd((unsigned long long *)&a.ctr[C_MASK], (unsigned long long)(nch * nq));
+            mb = __shfl_sync(0xffffffffu, mb, 0);
+            __syncwarp();
+            if (mb + (long long)nch * nq <= a.mask_cap) {
+                for (int w = lane; w < nch * nq; w += 32) a.masks[mb + w] = S.mask[w / nq][w % nq];
+                if (lane == 0) a.batches[b].mask_base = mb;
+            }
+            tests += (long long)B.ncand * nq;
+            __syncwarp();
+            b = B.next;
+        }
+        if (lane < nq) a.counts[G.qo[0]] = cnt[0];
+        if (lane + 32 < nq) a.counts[G.qo[1]] = cnt[1];
+        __syncwarp();
+    }
+    if (lane == 0) {
         atomicAdd((unsigned long long *)&a.ctr[C_TESTS], (unsigned long long)tests);
         atomicAdd((unsigned long long *)&a.ctr[C_EXACT], (unsigned long long)exact);
     }
@@ -714,7 +683,7 @@ constexpr int kFillWarps = kFillThreads / 32;
 struct FillSmem {
     unsigned long long wr[kQ];                 // next write position of each query's row
     unsigned long long mask[kChunks * kQ];     // the batch's masks, [k][q]
-    int32_t cand[kCand];                       // the batch's candidate caller indices
+    int32_t cand[kBlock];                      // the block's candidate caller indices
 };
 
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
@@ -803,7 +772,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     const int64_t n = t.n;
     if (n == 0) {
         if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
-        t.total_pairs = t.max_count = t.staged = t.tests = t.exact_tests = 0;
+        t.total_pairs = t.max_count = t.staged = t.loaded = t.tests = t.exact_tests = 0;
         BT_CUDA(cudaStreamSynchronize(st));
         return;
     }
@@ -826,19 +795,20 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     BT_CUDA(cudaStreamSynchronize(st));
     if (hbad) throw Error(BT_ERR_INPUT, "bt_find_neighbors: h must be finite, > 0 and <= 1e150");
 
-    // persistent grids: all resident warps
-    int per_sm = 0, per_sm_fill = 0;
-    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, test_kernel, kWalkThreads, 0));
-    BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_fill, fill_kernel, kFillThreads, 0));
-    per_sm = std::max(per_sm, 1);
-    per_sm_fill = std::max(per_sm_fill, 1);
-    const unsigned grid = (unsigned)(sms * per_sm);
-    const unsigned grid_fill = (unsigned)(sms * per_sm_fill);
-    const int64_t nwarps = (int64_t)grid * kWarpsPerBlock;
+    // persistent grids: all resident warps of each kernel
+    auto grid_of = [&](const void *fn, int threads) {
+        int per_sm = 0;
+        BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
+        return (unsigned)(sms * std::max(per_sm, 1));
+    };
+    const unsigned grid_g = grid_of((const void *)gather_kernel, kGatherThreads);
+    const unsigned grid_t = grid_of((const void *)test_kernel, kTestThreads);
+    const unsigned grid_f = grid_of((const void *)fill_kernel, kFillThreads);
     // frontier scratch: a unit's frontier holds each internal node at most once
     const int64_t front_cap = std::max<int64_t>(t.n_nodes, 1);
-    t.front.reserve(nwarps * 2 * front_cap, 0);
+    t.front.reserve((int64_t)grid_g * (kGatherThreads / 32) * 2 * front_cap, 0);
     t.head.reserve(t.n_units, 0);
+    t.self_slot.reserve(n, 0);
 
     // the recorded masks of a previous test pass are reused by a fill-only
     // call when the tree, h pointer, exactness mode and h checksum all match
@@ -865,6 +835,13 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     a.nbr = nbr_idx;
     a.ctr = (long long *)t.counters.p;
     a.head = t.head.p;
+    a.self_slot = (long long *)t.self_slot.p;
+
+    auto read_counters = [&](long long *hc) {
+        BT_CUDA(cudaMemcpyAsync(hc, t.counters.p, C_N * sizeof(long long), cudaMemcpyDeviceToHost, st));
+        BT_CUDA(cudaStreamSynchronize(st));
+    };
+    auto zero = [&](int c) { BT_CUDA(cudaMemsetAsync(t.counters.p + c, 0, sizeof(int64_t), st)); };
 
     DBuf<int32_t> tmp_counts;
     if (run_test) {
@@ -875,38 +852,46 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         }
         a.counts = cnt;
         // arena sized from the previous run on this thread (grown on overflow)
-        static thread_local double mask_per_q = 12.0, cand_per_q = 24.0, batch_per_unit = 3.0;
-        for (int attempt = 0;; attempt++) {
-            long long mcap = (long long)(mask_per_q * n) + 4096, ccap = (long long)(cand_per_q * n) + 4096;
-            long long bcap = (long long)(batch_per_unit * t.n_units) + 1024;
-            t.arena_masks.reserve(mcap, 0);
-            t.arena_cands.reserve(ccap, 0);
-            t.arena_batches.reserve(bcap, 0);
-            a.masks = t.arena_masks.p;
-            a.mask_cap = (long long)t.arena_masks.n;
+        static thread_local double cand_per_q = 32.0, batch_per_unit = 3.0, mask_per_q = 12.0;
+        long long hc[C_N];
+        t.rec_valid = false;
+        for (int attempt = 0;; attempt++) {  // A10: gather
+            t.arena_cand4.reserve((long long)(cand_per_q * n) + 4096, 0);
+            t.arena_cands.reserve(t.arena_cand4.n, 0);
+            t.arena_batches.reserve((long long)(batch_per_unit * t.n_units) + 1024, 0);
+            a.cand4 = t.arena_cand4.p;
             a.cands = t.arena_cands.p;
-            a.cand_cap = (long long)t.arena_cands.n;
+            a.cand_cap = (long long)std::min(t.arena_cand4.n, t.arena_cands.n);
             a.batches = t.arena_batches.p;
             a.batch_cap = (long long)t.arena_batches.n;
-            BT_CUDA(cudaMemsetAsync(t.counters.p, 0, C_HSUM * sizeof(int64_t), st));
-            BT_CUDA(cudaMemsetAsync(t.counters.p + C_HSUM + 1, 0, (C_N - C_HSUM - 1) * sizeof(int64_t), st));
+            for (int c : {C_WORK, C_CAND, C_BATCH, C_STAGED, C_LOADED}) zero(c);
             {
-                Phase ph("search.count");
-                test_kernel<<<grid, kWalkThreads, 0, st>>>(a);
-                BT_LAUNCH("walk_test");
+                Phase ph("search.gather");
+                gather_kernel<<<grid_g, kGatherThreads, 0, st>>>(a);
+                BT_LAUNCH("walk_gather");
             }
-            long long hc[C_N];
-            BT_CUDA(cudaMemcpyAsync(hc, t.counters.p, C_N * sizeof(long long), cudaMemcpyDeviceToHost, st));
-            BT_CUDA(cudaStreamSynchronize(st));
-            t.staged = hc[C_STAGED];
-            t.loaded = hc[C_LOADED];
-            t.tests = hc[C_TESTS];
-            t.exact_tests = hc[C_EXACT];
-            const bool fits = hc[C_MASK] <= a.mask_cap && hc[C_CAND] <= a.cand_cap && hc[C_BATCH] <= a.batch_cap;
-            mask_per_q = std::max(mask_per_q, 1.1 * (double)hc[C_MASK] / (double)n);
+            read_counters(hc);
             cand_per_q = std::max(cand_per_q, 1.1 * (double)hc[C_CAND] / (double)n);
             batch_per_unit =
                 std::max(batch_per_unit, 1.1 * (double)hc[C_BATCH] / (double)std::max<int64_t>(1, t.n_units));
+            if (hc[C_CAND] <= a.cand_cap && hc[C_BATCH] <= a.batch_cap) break;
+            if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: candidate arena does not converge");
+        }
+        t.staged = hc[C_STAGED];
+        t.loaded = hc[C_LOADED];
+        for (int attempt = 0;; attempt++) {  // A11: pair tests, counts, masks
+            t.arena_masks.reserve((long long)(mask_per_q * n) + 4096, 0);
+            a.masks = t.arena_masks.p;
+            a.mask_cap = (long long)t.arena_masks.n;
+            for (int c : {C_WORK3, C_MASK, C_TESTS, C_EXACT}) zero(c);
+            {
+                Phase ph("search.count");
+                test_kernel<<<grid_t, kTestThreads, 0, st>>>(a);
+                BT_LAUNCH("walk_test");
+            }
+            read_counters(hc);
+            mask_per_q = std::max(mask_per_q, 1.1 * (double)hc[C_MASK] / (double)n);
+            const bool fits = hc[C_MASK] <= a.mask_cap;
             if (fits || !fill_pass || nbr_idx == nullptr) {
                 t.rec_valid = fits;
                 t.rec_h = h;
@@ -914,16 +899,17 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
                 t.rec_exact = g_exact_only;
                 break;
             }
-            // arena overflow with a fill to do: grow and repeat the test pass
-            if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: candidate arena does not converge");
+            if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: mask arena does not converge");
         }
+        t.tests = hc[C_TESTS];
+        t.exact_tests = hc[C_EXACT];
         if (count_pass) {
             DBuf<long long> dtot(1);
             Phase ph("search.scan");
             device_scan<long long>(CountIn{cnt}, OffsetOut{offsets}, n, dtot.p);
             write_total_kernel<<<1, 1, 0, st>>>(offsets, n, dtot.p);
             BT_LAUNCH("write_total");
-            BT_CUDA(cudaMemsetAsync(t.counters.p + C_MAXC, 0, sizeof(int64_t), st));
+            zero(C_MAXC);
             max_count_kernel<<<grid_for(n, 256, (int64_t)sms * 8), 256, 0, st>>>(cnt, n,
                                                                                   (long long *)t.counters.p + C_MAXC);
             BT_LAUNCH("max_count");
@@ -943,10 +929,10 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     a.masks = t.arena_masks.p;
     a.cands = t.arena_cands.p;
     a.batches = t.arena_batches.p;
-    BT_CUDA(cudaMemsetAsync(t.counters.p + C_WORK2, 0, sizeof(int64_t), st));
+    zero(C_WORK2);
     {
         Phase ph("search.fill");
-        fill_kernel<<<grid_fill, kFillThreads, 0, st>>>(a);
+        fill_kernel<<<grid_f, kFillThreads, 0, st>>>(a);
         BT_LAUNCH("walk_fill");
     }
     BT_CUDA(cudaStreamSynchronize(st));
