@@ -598,19 +598,35 @@ __global__ void __launch_bounds__(kTestThreads, 6) test_kernel(WalkArgs a) {
         }
         int cnt[2] = {0, 0};
         __syncwarp();
-        for (int b = a.head[uid]; b >= 0;) {
-            const Batch B = a.batches[b];
+        // candidate chunk k of block B (padding slots: +inf, s32 = +inf)
+        auto load_chunk = [&](const Batch &Bk, int k, float4 &c0, float4 &c1) {
+            const int s0 = 64 * k + lane, s1 = s0 + 32;
+            c0 = make_float4(inf, inf, inf, 0.f);
+            c1 = c0;
+            if (s0 < Bk.ncand) c0 = a.cand4[Bk.cand_base + s0];
+            if (s1 < Bk.ncand) c1 = a.cand4[Bk.cand_base + s1];
+        };
+        int b = a.head[uid];
+        Batch B{-1, 0, 0, -1};
+        float4 p0, p1;  // prefetched next chunk
+        if (b >= 0) {
+            B = a.batches[b];
+            load_chunk(B, 0, p0, p1);
+        }
+        while (b >= 0) {
             const int nch = (B.ncand + 63) >> 6;
+            Batch Bn{-1, 0, 0, -1};
+            if (B.next >= 0) Bn = a.batches[B.next];
             // Hot loop, branch free: certain accepts (s32 < A) go into the masks;
             // the ballots of s32 < B are compared with them, and any difference
             // (a pair in the band [A, B) of lemma L4) is resolved afterwards by
             // the fp64 predicate.  Queries are padded to a multiple of 4.
             unsigned diff = 0;
             for (int k = 0; k < nch; k++) {
-                const int s0 = 64 * k + lane, s1 = s0 + 32;
-                float4 c0 = make_float4(inf, inf, inf, 0.f), c1 = c0;  // padding: s32 = +inf
-                if (s0 < B.ncand) c0 = a.cand4[B.cand_base + s0];
-                if (s1 < B.ncand) c1 = a.cand4[B.cand_base + s1];
+                const float4 c0 = p0, c1 = p1;
+                // prefetch the following chunk (this block's next, or the next block's first)
+                if (k + 1 < nch) load_chunk(B, k + 1, p0, p1);
+                else if (B.next >= 0) load_chunk(Bn, 0, p0, p1);
                 const unsigned long long cx = pk(c0.x, c1.x), cy = pk(c0.y, c1.y), cz = pk(c0.z, c1.z);
                 unsigned long long *mrow = &S.mask[k][0];
                 for (int q = 0; q < nq; q += 4) {
@@ -659,6 +675,7 @@ __global__ void __launch_bounds__(kTestThreads, 6) test_kernel(WalkArgs a) {
             tests += (long long)B.ncand * nq;
             __syncwarp();
             b = B.next;
+            B = Bn;
         }
         if (lane < nq) a.counts[G.qo[0]] = cnt[0];
         if (lane + 32 < nq) a.counts[G.qo[1]] = cnt[1];
