@@ -131,10 +131,10 @@ __device__ __forceinline__ bool exact_pair(double qx, double qy, double qz, doub
 // and candidate of a unit (lemma L4): queries use a = fl32(fl64(x - c))
 // (error <= u E + w (1+u) E + 2^-149); candidates from the compact records
 // use a = fl32(r32 + fl32(fl64(c_leaf - c))) with r32 = fl32(fl64(x - c_leaf)),
-// only for leaves of half-extent H <= 0.999 E, whose error is
-// <= (u + w(1+u))(H + D) + w(|x - c| + ...) + 3 2^-149 <= 4.0001 w E + 3 2^-149
-// (D = |c_leaf - c| <= H + E).  One bound covers both.
-__device__ __forceinline__ double l4_eps(double E) { return 4.01 * 0x1p-24 * E + 0x1p-147; }
+// only for leaves of half-extent H <= 7 E, whose error is
+// <= (u + w(1+u))(H + D) + w(|x - c| + ...) + 3 2^-149 <= 16.01 w E + 3 2^-149
+// (D = |c_leaf - c| <= H + E, so H + D <= 15 E).  One bound covers both.
+__device__ __forceinline__ double l4_eps(double E) { return 16.02 * 0x1p-24 * E + 0x1p-146; }
 
 // Lemma L4: thresholds A <= B (fp32) such that for the
 // fp32 squared distance s32 of a pair whose coordinates relative to the unit
@@ -246,7 +246,7 @@ __device__ __forceinline__ void close_block(GatherState &st, int lane, const Wal
     if (st.blk >= 0 && st.rec_ok && lane == 0) a.batches[st.blk].ncand = st.fill;
 }
 
-__device__ __noinline__ void open_block(GatherState &st, int lane, const WalkArgs &a) {
+__device__ __forceinline__ void open_block(GatherState &st, int lane, const WalkArgs &a) {
     close_block(st, lane, a);
     long long base = 0, bi = 0;
     if (lane == 0) {
@@ -270,8 +270,9 @@ __device__ __noinline__ void open_block(GatherState &st, int lane, const WalkArg
 
 // Load the queued leaves' particles (flattened over the lanes), cull them per
 // particle (L3, fp32 conservative) and append the kept ones to the arena.
-__device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &st, const UnitGeom &G, int lane,
+__device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const UnitGeom &G, int lane,
                                           const WalkArgs &a) {
+    GatherState st = stm;  // registers (the caller's copy lives in local memory)
     const unsigned lt = lanemask_lt();
     const int nl = st.nleaf;
     int carry = 0;
@@ -351,6 +352,7 @@ __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &st, const 
         }
     }
     st.nleaf = 0;
+    stm = st;
     __syncwarp();
 }
 
@@ -370,11 +372,11 @@ __device__ __forceinline__ void queue_leaves(GatherSmem &S, GatherState &st, con
         double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
         keep = g2 < G.Ru2;
         // leaf centre (as build.cu computed it) relative to the unit centre; the
-        // compact records are usable when the leaf half-extent H <= 0.999 E (l4_eps)
+        // compact records are usable when the leaf half-extent H <= 7 E (l4_eps)
         const double cx = 0.5 * (b0.x + b1.y), cy = 0.5 * (b0.y + b2.x), cz = 0.5 * (b1.x + b2.y);
         const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
         off = make_float4(__double2float_rn(__dsub_rn(cx, G.c[0])), __double2float_rn(__dsub_rn(cy, G.c[1])),
-                          __double2float_rn(__dsub_rn(cz, G.c[2])), (H <= 0.999 * G.E) ? 1.0f : 0.0f);
+                          __double2float_rn(__dsub_rn(cz, G.c[2])), (H <= 7.0 * G.E) ? 1.0f : 0.0f);
     }
     const unsigned km = __ballot_sync(0xffffffffu, keep);
     if (!km) return;
@@ -389,7 +391,10 @@ __device__ __forceinline__ void queue_leaves(GatherSmem &S, GatherState &st, con
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kGatherThreads, 6) gather_kernel(WalkArgs a) {
+#ifndef BT_GATHER_MIN_BLOCKS
+#define BT_GATHER_MIN_BLOCKS 6
+#endif
+__global__ void __launch_bounds__(kGatherThreads, BT_GATHER_MIN_BLOCKS) gather_kernel(WalkArgs a) {
     __shared__ GatherSmem smem[kGatherThreads / 32];
     const int lane = threadIdx.x & 31;
     GatherSmem &S = smem[threadIdx.x >> 5];
