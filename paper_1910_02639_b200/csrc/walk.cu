@@ -273,6 +273,12 @@ __device__ __forceinline__ void open_block(GatherState &st, int lane, const Walk
 __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const UnitGeom &G, int lane,
                                           const WalkArgs &a) {
     GatherState st = stm;  // registers (the caller's copy lives in local memory)
+    // pointers in registers (the args struct lives in local memory here)
+    const float4 *__restrict__ rec32 = a.rec32;
+    const double4 *__restrict__ rec = a.rec;
+    float4 *__restrict__ cand4 = a.cand4;
+    int32_t *__restrict__ cands = a.cands;
+    long long *__restrict__ self_slot = a.self_slot;
     const unsigned lt = lanemask_lt();
     const int nl = st.nleaf;
     int carry = 0;
@@ -316,9 +322,9 @@ __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const
             r[h] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (valid[h]) {
                 if (of[h].w != 0.0f) {
-                    r[h] = a.rec32[pos[h]];
+                    r[h] = rec32[pos[h]];
                 } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
-                    const double4 d = a.rec[pos[h]];
+                    const double4 d = rec[pos[h]];
                     r[h] = make_float4(__double2float_rn(__dsub_rn(d.x, c0)), __double2float_rn(__dsub_rn(d.y, c1)),
                                        __double2float_rn(__dsub_rn(d.z, c2)),
                                        __int_as_float((int)__double_as_longlong(d.w)));
@@ -341,10 +347,10 @@ __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const
             const unsigned km = __ballot_sync(0xffffffffu, keep);
             if (keep && st.rec_ok) {
                 const long long slot = st.base + st.fill + __popc(km & lt);
-                a.cand4[slot] = make_float4(ax, ay, az, __int_as_float(pos[h]));
-                a.cands[slot] = __float_as_int(r[h].w);
+                cand4[slot] = make_float4(ax, ay, az, __int_as_float(pos[h]));
+                cands[slot] = __float_as_int(r[h].w);
                 const int qi = pos[h] - q0;
-                if (qi >= 0 && qi < nq) a.self_slot[pos[h]] = slot;
+                if (qi >= 0 && qi < nq) self_slot[pos[h]] = slot;
             }
             st.fill += __popc(km);
             st.staged += __popc(km);
