@@ -298,9 +298,20 @@ __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const
     const int total = carry;
     const int q0 = G.q0, nq = G.nq;
     const double c0 = G.c[0], c1 = G.c[1], c2 = G.c[2];
+    // any large leaf (staged from the fp64 records) among the queued ones?
+    bool mixed = false;
+    for (int i = lane; i < nl; i += 32) mixed |= S.loff[i].w == 0.0f;
+    mixed = __any_sync(0xffffffffu, mixed);
+    st.loaded += total;
+    float4 *blk4 = cand4 + st.base;
+    int32_t *blki = cands + st.base;
     int owner = 0;  // queued leaf holding the next flattened position
     for (int p0 = 0; p0 < total; p0 += 64) {
-        if (st.blk < 0 || st.fill + 64 > kBlock) open_block(st, lane, a);
+        if (st.blk < 0 || st.fill + 64 > kBlock) {
+            open_block(st, lane, a);
+            blk4 = cand4 + st.base;
+            blki = cands + st.base;
+        }
         float4 r[2], of[2];
         int pos[2];
         bool valid[2];
@@ -320,7 +331,9 @@ __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const
             of[h] = S.loff[mine];
             owner += __popc(past);
             r[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (valid[h]) {
+            if (!mixed) {
+                if (valid[h]) r[h] = rec32[pos[h]];
+            } else if (valid[h]) {
                 if (of[h].w != 0.0f) {
                     r[h] = rec32[pos[h]];
                 } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
@@ -346,15 +359,14 @@ __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const
             const bool keep = valid[h] && g2 < st.cull2;
             const unsigned km = __ballot_sync(0xffffffffu, keep);
             if (keep && st.rec_ok) {
-                const long long slot = st.base + st.fill + __popc(km & lt);
-                cand4[slot] = make_float4(ax, ay, az, __int_as_float(pos[h]));
-                cands[slot] = __float_as_int(r[h].w);
-                const int qi = pos[h] - q0;
-                if (qi >= 0 && qi < nq) self_slot[pos[h]] = slot;
+                const int slot = st.fill + __popc(km & lt);
+                blk4[slot] = make_float4(ax, ay, az, __int_as_float(pos[h]));
+                blki[slot] = __float_as_int(r[h].w);
+                if ((unsigned)(pos[h] - q0) < (unsigned)nq) self_slot[pos[h]] = st.base + slot;
             }
-            st.fill += __popc(km);
-            st.staged += __popc(km);
-            st.loaded += __popc(__ballot_sync(0xffffffffu, valid[h]));
+            const int nk = __popc(km);
+            st.fill += nk;
+            st.staged += nk;
         }
     }
     st.nleaf = 0;
@@ -709,16 +721,17 @@ __global__ void __launch_bounds__(kTestThreads, 6) test_kernel(WalkArgs a) {
 constexpr int kFillWarps = kFillThreads / 32;
 
 struct FillSmem {
-    unsigned long long wr[kQ];                 // next write position of each query's row
-    unsigned long long mask[kChunks * kQ];     // the batch's masks, [k][q]
-    int32_t cand[kBlock];                      // the block's candidate caller indices
+    int32_t *row[kQ];                          // next write address of each query's row
+    unsigned long long mask[kChunks * kQ];     // the block's masks, [k][q]
 };
 
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     __shared__ FillSmem fsm[kFillWarps];
     const int lane = threadIdx.x & 31;
-    const unsigned lt = lanemask_lt();
+    const unsigned lt = lanemask_lt(), lanebit = 1u << lane;
     FillSmem &F = fsm[threadIdx.x >> 5];
+    const int32_t *__restrict__ cands = a.cands;
+    const unsigned long long *__restrict__ masks = a.masks;
     for (;;) {
         unsigned long long u = 0;
         if (lane == 0) u = atomicAdd((unsigned long long *)&a.ctr[C_WORK2], 1ull);
@@ -727,29 +740,39 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
         const int4 U = a.units[u];
         const int nq = U.z;
         for (int q = lane; q < nq; q += 32)
-            F.wr[q] = (unsigned long long)a.offsets[(int32_t)__double_as_longlong(a.rec[U.y + q].w)];
+            F.row[q] = a.nbr + a.offsets[(int32_t)__double_as_longlong(a.rec[U.y + q].w)];
         for (int b = a.head[u]; b >= 0;) {
             const Batch B = a.batches[b];
             const int nch = (B.ncand + 63) >> 6;
+            // the block's candidates in registers: chunk k, lane l -> slots 64k + l, 64k + 32 + l
+            int32_t c0[kChunks], c1[kChunks];
+#pragma unroll
+            for (int k = 0; k < kChunks; k++) {
+                c0[k] = (k < nch) ? cands[B.cand_base + 64 * k + lane] : -1;
+                c1[k] = (k < nch) ? cands[B.cand_base + 64 * k + 32 + lane] : -1;
+            }
             __syncwarp();
-            for (int c = lane; c < nch * 64; c += 32) F.cand[c] = a.cands[B.cand_base + c];
-            for (int w = lane; w < nch * nq; w += 32) F.mask[w] = a.masks[B.mask_base + w];
+            for (int w = lane; w < nch * nq; w += 32) F.mask[w] = masks[B.mask_base + w];
             __syncwarp();
-            for (int k = 0; k < nch; k++) {
-                const int32_t c0 = F.cand[64 * k + lane], c1 = F.cand[64 * k + 32 + lane];
-                const unsigned long long *mk = F.mask + k * nq;
-                for (int q = 0; q < nq; q++) {
-                    const unsigned long long m = mk[q];
+            for (int q = 0; q < nq; q++) {
+                int32_t *dst = F.row[q];
+                int wrote = 0;
+#pragma unroll
+                for (int k = 0; k < kChunks; k++) {
+                    if (k >= nch) break;
+                    const unsigned long long m = F.mask[k * nq + q];
                     if (m == 0ull) continue;
-                    const unsigned long long base = F.wr[q];
                     const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
                     const int plo = __popc(lo);
-                    if ((lo >> lane) & 1u) a.nbr[base + __popc(lo & lt)] = c0;
-                    if ((hi >> lane) & 1u) a.nbr[base + plo + __popc(hi & lt)] = c1;
-                    if (lane == 0) F.wr[q] = base + plo + __popc(hi);
+                    if (lo & lanebit) dst[__popc(lo & lt)] = c0[k];
+                    if (hi & lanebit) dst[plo + __popc(hi & lt)] = c1[k];
+                    const int n = plo + __popc(hi);
+                    dst += n;
+                    wrote += n;
                 }
-                __syncwarp();
+                if (lane == 0 && wrote) F.row[q] = dst;
             }
+            __syncwarp();
             b = B.next;
         }
     }
