@@ -197,6 +197,22 @@ HostScratch &host_scratch() {
     return hs;
 }
 
+void read_back(std::initializer_list<ReadBack> items) {
+    char *buf = reinterpret_cast<char *>(host_scratch().p);
+    size_t off = 0;
+    for (const auto &it : items) {
+        if (off + it.bytes > 64 * sizeof(int64_t)) throw Error(BT_ERR_CUDA, "read_back: scratch too small");
+        BT_CUDA(cudaMemcpyAsync(buf + off, it.src, it.bytes, cudaMemcpyDeviceToHost, g_stream));
+        off += (it.bytes + 15) & ~size_t(15);
+    }
+    BT_CUDA(cudaStreamSynchronize(g_stream));
+    off = 0;
+    for (const auto &it : items) {
+        memcpy(it.dst, buf + off, it.bytes);
+        off += (it.bytes + 15) & ~size_t(15);
+    }
+}
+
 }  // namespace bt
 
 using namespace bt;

@@ -483,7 +483,6 @@ struct UnitsOut {
 void build_tree(TreeDev &t, const double *pos) {
     const int64_t n = t.n;
     cudaStream_t st = stream();
-    int64_t *hs = host_scratch().p;
     t.n_nodes = t.n_cells = t.n_leaves = t.n_units = 0;
     t.depth = 0;
     t.root_b = 0;
@@ -526,9 +525,7 @@ void build_tree(TreeDev &t, const double *pos) {
         BT_LAUNCH("root_box");
         double hb[8];
         int hbad = 0;
-        BT_CUDA(cudaMemcpyAsync(hb, dbox.p, 7 * sizeof(double), cudaMemcpyDeviceToHost, st));
-        BT_CUDA(cudaMemcpyAsync(&hbad, dflags.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-        BT_CUDA(cudaStreamSynchronize(st));
+        read_back({{dbox.p, hb, 7 * sizeof(double)}, {dflags.p, &hbad, sizeof(int)}});
         if (hbad) throw Error(BT_ERR_INPUT, "bt_build: non-finite coordinate or |coordinate| > 1e150");
         for (int l = 0; l < 3; l++) { t.box_lo[l] = hb[l]; t.box_hi[l] = hb[3 + l]; }
         t.M = hb[6];
@@ -582,9 +579,9 @@ void build_tree(TreeDev &t, const double *pos) {
             level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s);
             BT_LAUNCH("level_b");
             device_scan<long long>(CellsOfNode{ln.p}, CellBaseOut{ln.p}, nn, dtotal.p);
-            BT_CUDA(cudaMemcpyAsync(hs, dtotal.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
-            BT_CUDA(cudaStreamSynchronize(st));
-            const int64_t ncells = hs[0];
+            long long ncells_h = 0;
+            read_back({{dtotal.p, &ncells_h, sizeof(long long)}});
+            const int64_t ncells = ncells_h;
             hist.reserve(ncells, 0);
             cpre.reserve(ncells, 0);
             cid.reserve(ncells, 0);
@@ -610,8 +607,7 @@ void build_tree(TreeDev &t, const double *pos) {
                 ratio_decide_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.beta, dflags.p + 1);
                 BT_LAUNCH("ratio_decide");
                 int any = 0;
-                BT_CUDA(cudaMemcpyAsync(&any, dflags.p + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
-                BT_CUDA(cudaStreamSynchronize(st));
+                read_back({{dflags.p + 1, &any, sizeof(int)}});
                 if (!any) break;
             }
             finalize_level_nodes_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.nodes.p, t.n_cells,
@@ -622,8 +618,7 @@ void build_tree(TreeDev &t, const double *pos) {
             const bool child_ok = (level + 1) < t.depth_cap;
             device_scan<CellScan>(CellIn{hist.p, t.s, child_ok}, CellOut{cpre.p, cid.p, cact.p}, ncells, dcs.p);
             CellScan tot;
-            BT_CUDA(cudaMemcpyAsync(&tot, dcs.p, sizeof(CellScan), cudaMemcpyDeviceToHost, st));
-            BT_CUDA(cudaStreamSynchronize(st));
+            read_back({{dcs.p, &tot, sizeof(CellScan)}});
             const int64_t nn_next = tot.nnode, n_act_next = tot.actoff, nleaf = tot.nleaf;
 
             // A8: emit children / leaves / cell table
@@ -656,8 +651,7 @@ void build_tree(TreeDev &t, const double *pos) {
             level++;
         }
         int32_t rb = 0;
-        BT_CUDA(cudaMemcpyAsync(&rb, &t.nodes.p[0].b, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        BT_CUDA(cudaStreamSynchronize(st));
+        read_back({{&t.nodes.p[0].b, &rb, sizeof(int32_t)}});
         t.root_b = rb;
     }
 
@@ -696,15 +690,13 @@ void build_tree(TreeDev &t, const double *pos) {
         // (two scans over the leaves; cheap: L <= n / 1)
         device_scan<long long>(UnitsOfLeaf{t.leaf_count.p}, NullOut{}, t.n_leaves, dtot.p);
         long long nu = 0;
-        BT_CUDA(cudaMemcpyAsync(&nu, dtot.p, sizeof(long long), cudaMemcpyDeviceToHost, st));
-        BT_CUDA(cudaStreamSynchronize(st));
+        read_back({{dtot.p, &nu, sizeof(long long)}});
         t.units.alloc(nu);
         t.n_units = nu;
         device_scan<long long>(UnitsOfLeaf{t.leaf_count.p}, UnitsOut{t.leaf_begin.p, t.leaf_count.p, t.units.p},
                                t.n_leaves, dtot.p);
         unsigned long long hstat[4];
-        BT_CUDA(cudaMemcpyAsync(hstat, dstat.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
-        BT_CUDA(cudaStreamSynchronize(st));
+        read_back({{dstat.p, hstat, 4 * sizeof(unsigned long long)}});
         t.halvings = (int64_t)hstat[0];
         t.max_leaf = (int64_t)hstat[1];
         t.overfull = (int64_t)hstat[2];

@@ -8,6 +8,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <initializer_list>
 #include <vector>
 
 #include "../../include/btree.h"
@@ -90,6 +91,15 @@ struct HostScratch {
     ~HostScratch() { if (p) cudaFreeHost(p); }
 };
 HostScratch &host_scratch();
+
+// Device -> host control reads through pinned scratch (pageable destinations
+// would make every small copy a staged, synchronous transfer); syncs the stream.
+struct ReadBack {
+    const void *src;
+    void *dst;
+    size_t bytes;
+};
+void read_back(std::initializer_list<ReadBack> items);
 
 // ---------------------------------------------------------------------------
 // Tree representation in HBM.

@@ -841,9 +841,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     }
     int hbad = 0;
     long long hsum = 0;
-    BT_CUDA(cudaMemcpyAsync(&hbad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaMemcpyAsync(&hsum, t.counters.p + C_HSUM, sizeof(long long), cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaStreamSynchronize(st));
+    read_back({{dbad.p, &hbad, sizeof(int)}, {t.counters.p + C_HSUM, &hsum, sizeof(long long)}});
     if (hbad) throw Error(BT_ERR_INPUT, "bt_find_neighbors: h must be finite, > 0 and <= 1e150");
 
     // persistent grids: all resident warps of each kernel
@@ -889,8 +887,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     a.self_slot = (long long *)t.self_slot.p;
 
     auto read_counters = [&](long long *hc) {
-        BT_CUDA(cudaMemcpyAsync(hc, t.counters.p, C_N * sizeof(long long), cudaMemcpyDeviceToHost, st));
-        BT_CUDA(cudaStreamSynchronize(st));
+        read_back({{t.counters.p, hc, C_N * sizeof(long long)}});
     };
     auto zero = [&](int c) { BT_CUDA(cudaMemsetAsync(t.counters.p + c, 0, sizeof(int64_t), st)); };
 
@@ -967,9 +964,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         }
     }
     int64_t total = 0, maxc = 0;
-    BT_CUDA(cudaMemcpyAsync(&total, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    if (count_pass) BT_CUDA(cudaMemcpyAsync(&maxc, t.counters.p + C_MAXC, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    BT_CUDA(cudaStreamSynchronize(st));
+    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)}});
     if (count_pass) t.max_count = maxc;
     t.total_pairs = total;
     if (!fill_pass || nbr_idx == nullptr) return;
