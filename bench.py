@@ -264,8 +264,8 @@ def run_b200(args):
         return prof.get(name, (0.0, 0))[0] / args.steps
 
     launches = sum(v[1] for k, v in prof.items() if k.startswith("kernel.")) // args.steps
-    kern = {"build": ph("build.total"), "walk_count": ph("search.count"), "scan": ph("search.scan"),
-            "walk_fill": ph("search.fill"), "gather_h": ph("search.gather_h")}
+    kern = {"build": ph("build.total"), "walk_gather": ph("search.gather"), "walk_test": ph("search.count"),
+            "scan": ph("search.scan"), "walk_fill": ph("search.fill"), "gather_h": ph("search.gather_h")}
 
     # ---- roofline of the dominant kernel -----------------
     peaks = {}
@@ -274,23 +274,48 @@ def run_b200(args):
     except Exception:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    hbm_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    dom = max(("walk_count", "walk_fill"), key=lambda k: kern[k])
-    if dom == "walk_fill":
-        # algorithmic HBM bytes of one fill launch: per particle its 32-B record,
-        # 8-B h and 8-B offset, plus the 4-B output index per neighbor pair
-        alg_bytes = n * (32 + 8 + 8) + 4 * total_pairs
+    hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
+    loaded, staged, tests = int(st["loaded"]), int(st["staged"]), int(st["tests"])
+    dom = max(("walk_gather", "walk_test", "walk_fill", "build"), key=lambda k: kern[k])
+    if dom == "walk_test":
+        # pair tests are fp32 ALU work: 3 sub + 1 mul + 2 fma + 1 compare = 7
+        # lane-ops per pair test; peak = 148 SMs x 128 fp32 lanes x max SM clock
+        sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+        alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+        achieved = tests * 7 / (kern[dom] * 1e-3) / 1e12
+        roofline = {"kernel": dom, "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
+                    "frac": achieved / alu_peak, "traffic": None,
+                    "peak_source": "derived: 148 SM x 128 fp32 lanes x sm_max_mhz (B200_PROFILING.md / MEASURED_PEAKS)",
+                    "algorithmic_ops": tests * 7}
     else:
-        # count launch: per particle 32-B record + 8-B h + 4-B count
-        alg_bytes = n * (32 + 8 + 4)
-    achieved = alg_bytes / (kern[dom] * 1e-3) / 1e9
-    roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                "frac": achieved / hbm_peak, "traffic": None, "peak_source": hbm_src,
-                "algorithmic_bytes": alg_bytes}
-    # BJ's own definition: bytes of candidate positions actually read (staged
-    # records x 32 B per walk pass, both passes) over peak HBM bandwidth
-    bcand = 2 * int(st["staged"]) * 32
-    walk_ms = kern["walk_count"] + kern["walk_fill"]
+        if dom == "walk_gather":
+            # candidate records read (16-B compact record per loaded particle) +
+            # candidate slots written (16-B coordinates + 4-B caller index)
+            alg_bytes = loaded * 16 + staged * 20
+        elif dom == "walk_fill":
+            # recorded masks (8 B/word) + candidate indices (4 B/slot) read, per
+            # particle record + offset read, 4-B output index per neighbor pair
+            alg_bytes = int(st["mask_words"]) * 8 + int(st["cand_slots"]) * 4 + n * (32 + 8) + 4 * total_pairs
+        else:
+            # build: per particle pos read (24 B) + records written / re-read over
+            # the levels and the final sort (~4 x 32 B)
+            alg_bytes = n * (24 + 4 * 32)
+        achieved = alg_bytes / (kern[dom] * 1e-3) / 1e9
+        roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved / hbm_peak, "traffic": None, "peak_source": hbm_src,
+                    "algorithmic_bytes": alg_bytes}
+    try:  # per-launch DRAM bytes from the committed ncu capture (profiles/), if any
+        tr = json.load(open(os.path.join(ROOT, "profiles", "dram_traffic.json")))
+        if tr.get("config") == args.config and dom in tr.get("kernels", {}):
+            roofline["traffic"] = tr["kernels"][dom]
+            roofline["traffic_source"] = tr.get("source")
+    except Exception:
+        pass
+    # BASELINE.json's own definition: bytes of candidate positions actually read
+    # by the walk (16-B compact records loaded by the gather) over the whole walk
+    # time (gather + test + fill) and peak HBM bandwidth
+    bcand = loaded * 16
+    walk_ms = kern["walk_gather"] + kern["walk_test"] + kern["walk_fill"]
     bj_roof = {"B_cand_bytes": bcand, "walk_ms": walk_ms,
                "frac": (bcand / (walk_ms * 1e-3) / 1e9) / hbm_peak if walk_ms > 0 else None}
 
@@ -335,7 +360,8 @@ def run_b200(args):
                 "build_ms": kern["build"], "kernel_ms": kern, "gpu_launches": launches,
                 "roofline": roofline, "bj_hbm_roofline": bj_roof,
                 "tree": {k: st[k] for k in ("depth", "root_b", "nodes", "leaves", "halvings", "units")},
-                "walk_counters": {"loaded": st["loaded"], "staged": st["staged"], "tests": st["tests"], "exact_tests": st["exact_tests"]},
+                "walk_counters": {k: st[k] for k in ("loaded", "staged", "tests", "exact_tests", "mask_words",
+                                                     "cand_slots")},
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if ws > 1:

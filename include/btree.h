@@ -163,7 +163,9 @@ typedef struct bt_stats {
     int64_t staged;       /* candidate records staged by the count pass       */
     int64_t tests;        /* pair tests issued by the count pass              */
     int64_t exact_tests;  /* pairs decided by the fp64 predicate itself       */
-    int64_t loaded;       /* particle records read by staging (before the cull) */
+    int64_t loaded;       /* particle records read by the gather (before the cull) */
+    int64_t mask_words;   /* 64-bit neighbor masks recorded for the fill pass   */
+    int64_t cand_slots;   /* candidate arena slots allocated                     */
 } bt_stats;
 
 int bt_tree_stats(const bt_tree *t, bt_stats *out);

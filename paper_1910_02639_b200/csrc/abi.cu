@@ -385,6 +385,8 @@ int bt_tree_stats(const bt_tree *t, bt_stats *out) {
     out->tests = d.tests;
     out->exact_tests = d.exact_tests;
     out->loaded = d.loaded;
+    out->mask_words = d.mask_words;
+    out->cand_slots = d.cand_slots;
     return BT_OK;
 }
 

@@ -165,6 +165,7 @@ struct TreeDev {
     DBuf<int32_t> front;       // walk frontier scratch (per resident warp)
     int64_t stack_per_warp = 0;
     int64_t total_pairs = 0, max_count = 0, staged = 0, loaded = 0, tests = 0, exact_tests = 0;
+    int64_t mask_words = 0, cand_slots = 0;
 };
 
 // Build (build.cu) and search (walk.cu) entry points.

@@ -927,6 +927,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         }
         t.staged = hc[C_STAGED];
         t.loaded = hc[C_LOADED];
+        t.cand_slots = hc[C_CAND];
         for (int attempt = 0;; attempt++) {  // A11: pair tests, counts, masks
             t.arena_masks.reserve((long long)(mask_per_q * n) + 4096, 0);
             a.masks = t.arena_masks.p;
@@ -951,6 +952,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         }
         t.tests = hc[C_TESTS];
         t.exact_tests = hc[C_EXACT];
+        t.mask_words = hc[C_MASK];
         if (count_pass) {
             DBuf<long long> dtot(1);
             Phase ph("search.scan");

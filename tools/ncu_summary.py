@@ -1,0 +1,111 @@
+"""Summarise ncu outputs into profiles/: per-kernel launch times (launch list
+CSV) and, for a --set full report, the headline metrics + DRAM bytes per launch.
+
+  python tools/ncu_summary.py launches <launches.csv> <out.txt>
+  python tools/ncu_summary.py full <report.ncu-rep> <out.txt> [<traffic.json> <kernel-key> <config>]
+"""
+import csv
+import json
+import subprocess
+import sys
+from collections import defaultdict
+
+
+def to_ms(v, unit):
+    v = float(str(v).replace(",", ""))
+    return {"nsecond": 1e-6, "ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0,
+            "second": 1e3, "s": 1e3}.get(unit, 1e-6) * v
+
+
+def launches(path, out):
+    rows = list(csv.reader(open(path)))
+    hdr = None
+    per = defaultdict(lambda: defaultdict(float))
+    order = []
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if not hdr or len(r) != len(hdr):
+            continue
+        d = dict(zip(hdr, r))
+        key = (d["ID"], d["Kernel Name"])
+        if key not in order:
+            order.append(key)
+        m = d["Metric Name"]
+        if m == "gpu__time_duration.sum":
+            per[key]["ms"] = to_ms(d["Metric Value"], d["Metric Unit"])
+        elif m.startswith("dram__bytes"):
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(d["Metric Unit"], 1)
+            per[key][m] = float(d["Metric Value"].replace(",", "")) * scale
+    agg = defaultdict(lambda: [0, 0.0, 0.0])
+    for key in order:
+        name = key[1].split("(")[0].replace("bt::<unnamed>::", "").replace("(anonymous namespace)::", "")
+        name = name.split("::")[-1]
+        a = agg[name]
+        a[0] += 1
+        a[1] += per[key].get("ms", 0.0)
+        a[2] += per[key].get("dram__bytes_read.sum", 0.0) + per[key].get("dram__bytes_write.sum", 0.0)
+    tot = sum(a[1] for a in agg.values()) or 1.0
+    lines = [f"ncu launch list ({len(order)} launches, serialised, cold-cache): {path}",
+             f"{'kernel':40s} {'launches':>8s} {'ms':>10s} {'share':>7s} {'DRAM GB':>9s}"]
+    for name, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"{name:40s} {a[0]:8d} {a[1]:10.3f} {100 * a[1] / tot:6.1f}% {a[2] / 1e9:9.3f}")
+    lines.append(f"{'total':40s} {len(order):8d} {tot:10.3f}")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def full(rep, out, traffic=None, key=None, config=None):
+    res = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(res.splitlines()))
+    hdr = rows[0]
+    want = ["Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Hit Rate", "L2 Hit Rate",
+            "Compute (SM) Throughput", "Executed Ipc Active", "Issue Slots Busy", "Achieved Occupancy",
+            "Theoretical Occupancy", "Registers Per Thread", "Warp Cycles Per Issued Instruction"]
+    lines = [f"ncu --set full summary: {rep}"]
+    kernels = defaultdict(list)
+    for r in rows[1:]:
+        d = dict(zip(hdr, r))
+        if d.get("Metric Name") in want:
+            kernels[(d["ID"], d["Kernel Name"][:60])].append(f"{d['Metric Name']}: {d['Metric Value']} {d['Metric Unit']}")
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    h2 = rr[0]
+    dram = {}
+    for r in rr[2:]:
+        d = dict(zip(h2, r))
+        try:
+            rd = float(d.get("dram__bytes_read.sum", "0").replace(",", ""))
+            wr = float(d.get("dram__bytes_write.sum", "0").replace(",", ""))
+        except ValueError:
+            continue
+        unit_r = rr[1][h2.index("dram__bytes_read.sum")] if "dram__bytes_read.sum" in h2 else "byte"
+        unit_w = rr[1][h2.index("dram__bytes_write.sum")] if "dram__bytes_write.sum" in h2 else "byte"
+        sc = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        dram[(d["ID"], d["Kernel Name"][:60])] = rd * sc.get(unit_r, 1) + wr * sc.get(unit_w, 1)
+    for k, v in kernels.items():
+        lines.append(f"[{k[0]}] {k[1]}")
+        lines += ["    " + x for x in v]
+        if k in dram:
+            lines.append(f"    dram bytes (read + write): {dram[k]:.4g}")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if traffic and dram:
+        t = {}
+        try:
+            t = json.load(open(traffic))
+        except Exception:
+            pass
+        t.setdefault("kernels", {})
+        t["kernels"][key] = max(dram.values())
+        t["config"] = int(config)
+        t["source"] = f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum ({rep.split('/')[-1]})"
+        json.dump(t, open(traffic, "w"), indent=1)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(*sys.argv[2:])
