@@ -453,6 +453,54 @@ __global__ void remap_cells_kernel(int32_t *cells, int64_t n_cells, const int32_
     }
 }
 
+// ---- walk unit order: Morton (Z-order) of the leaf centre ------------------
+// The walk processes units in array order; depth-first leaf order puts the
+// +z neighbour of a root cell b^2 cells later, so concurrently processed units
+// would not share candidate leaves in L2.  Units are bucketed by the top 21
+// bits of the 30-bit Morton code of their leaf centre (counting sort).
+constexpr int kMortonBits = 21;
+
+__device__ __forceinline__ unsigned spread3(unsigned v) {  // 10 bits -> every third bit
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void unit_key_kernel(const int4 *__restrict__ units, int64_t nu, const double *__restrict__ leaf_box,
+                                const double *__restrict__ box, unsigned *__restrict__ key, int32_t *__restrict__ hist) {
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
+        const double *lb = leaf_box + 6 * (int64_t)units[u].x;
+        unsigned q[3];
+        for (int l = 0; l < 3; l++) {
+            const double c = 0.5 * (lb[l] + lb[3 + l]);
+            const double f = (c - box[l]) / (box[3 + l] - box[l]);
+            q[l] = (unsigned)fmin(1023.0, fmax(0.0, f * 1024.0));
+        }
+        const unsigned m = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
+        const unsigned k = m >> (30 - kMortonBits);
+        key[u] = k;
+        atomicAdd(&hist[k], 1);
+    }
+}
+
+struct HistIn {
+    const int32_t *h;
+    __device__ long long operator()(int64_t i) const { return h[i]; }
+};
+struct HistOut {
+    int32_t *start;
+    __device__ void operator()(int64_t i, long long exc, long long) const { start[i] = (int32_t)exc; }
+};
+
+__global__ void unit_scatter_kernel(const int4 *__restrict__ units, int64_t nu, const unsigned *__restrict__ key,
+                                    int32_t *__restrict__ cursor, int4 *__restrict__ out) {
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x)
+        out[atomicAdd(&cursor[key[u]], 1)] = units[u];
+}
+
 constexpr int kUnitQ = 64;  // queries per walk work unit
 
 struct UnitsOfLeaf {
@@ -695,6 +743,20 @@ void build_tree(TreeDev &t, const double *pos) {
         t.n_units = nu;
         device_scan<long long>(UnitsOfLeaf{t.leaf_count.p}, UnitsOut{t.leaf_begin.p, t.leaf_count.p, t.units.p},
                                t.n_leaves, dtot.p);
+        if (nu > 1) {  // Morton order of the units (walk locality)
+            DBuf<unsigned> key(nu);
+            DBuf<int32_t> bucket(1u << kMortonBits);
+            DBuf<int4> sorted(nu);
+            BT_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(int32_t) << kMortonBits, st));
+            unit_key_kernel<<<grid_for(nu, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(t.units.p, nu, t.leaf_box.p,
+                                                                                       dbox.p, key.p, bucket.p);
+            BT_LAUNCH("unit_key");
+            device_scan<long long>(HistIn{bucket.p}, HistOut{bucket.p}, 1 << kMortonBits, (long long *)nullptr);
+            unit_scatter_kernel<<<grid_for(nu, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(t.units.p, nu, key.p,
+                                                                                           bucket.p, sorted.p);
+            BT_LAUNCH("unit_scatter");
+            t.units = std::move(sorted);
+        }
         unsigned long long hstat[4];
         read_back({{dstat.p, hstat, 4 * sizeof(unsigned long long)}});
         t.halvings = (int64_t)hstat[0];
