@@ -77,6 +77,18 @@ bt_tree *bt_build_ex(const double *pos, int64_t n, int32_t bucket_size, double m
                      double alpha, int32_t depth_cap);
 
 /*
+ * bt_build_policy -- bt_build_ex with a subdivision policy:
+ *   BT_POLICY_BTREE   the paper's adaptive b (Eq. 1 + the Eq. 4 halving loop);
+ *   BT_POLICY_OCTREE  the classical octree the paper compares against (Sec. II,
+ *                     P:98-103; Table II): b = 2 at every node, no ratio test
+ *                     (max_empty and alpha are ignored).
+ * The neighbor sets found through either tree are identical.
+ */
+enum { BT_POLICY_BTREE = 0, BT_POLICY_OCTREE = 1 };
+bt_tree *bt_build_policy(const double *pos, int64_t n, int32_t bucket_size, double max_empty,
+                         double alpha, int32_t depth_cap, int32_t policy);
+
+/*
  * bt_find_neighbors -- FindNeighbors (Alg. 2; Eq. 5)
  * for every particle of the tree, count-then-fill CSR output.
  *

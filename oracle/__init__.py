@@ -70,6 +70,8 @@ def lib():
         L.orc_root_box.restype = None
         L.orc_build.argtypes = [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_int32]
         L.orc_build.restype = _P
+        L.orc_build_policy.argtypes = [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int]
+        L.orc_build_policy.restype = _P
         L.orc_free.argtypes = [_P]
         L.orc_free.restype = None
         L.orc_get_stats.argtypes = [_P, C.POINTER(Stats)]
@@ -144,10 +146,11 @@ class Tree:
     """b-tree built by the oracle's BuildTree (Alg. 1)."""
 
     def __init__(self, pos, bucket_size: int = 64, max_empty: float = 0.5,
-                 alpha: float = 0.5, depth_cap: int = 64):
+                 alpha: float = 0.5, depth_cap: int = 64, policy: str = "btree"):
         self.pos = _f64(pos, (-1, 3))
         self.n = self.pos.shape[0]
-        self._h = lib().orc_build(_ptr(self.pos), self.n, bucket_size, max_empty, alpha, depth_cap)
+        self._h = lib().orc_build_policy(_ptr(self.pos), self.n, bucket_size, max_empty, alpha, depth_cap,
+                                         1 if policy == "octree" else 0)
         if not self._h:
             raise ValueError("oracle: invalid build arguments")
 

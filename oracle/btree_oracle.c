@@ -144,6 +144,7 @@ typedef struct {
     int32_t s;
     double beta, alpha;
     int32_t depth_cap;
+    int octree; /* FixedOctree policy: b = 2, no ratio loop (Sec. II) */
     double box_lo[3], box_hi[3];
     double M;       /* max |root box coordinate|, for the radius margin */
     orc_node *root; /* NULL iff n == 0 */
@@ -195,7 +196,8 @@ static orc_node *build_tree(orc_tree *t, const double *pos, const double *lo,
     t->nodes++;
 
     /* Step 1: branching factor, Eq. 1 (computed once, then only halved: R6). */
-    int b = orc_branching_factor(n, t->s);
+    /* The octree policy fixes b = 2 and skips Step 3.                       */
+    int b = t->octree ? 2 : orc_branching_factor(n, t->s);
     int64_t *cell = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
     int64_t *cnt = NULL;
     int64_t B = 0;
@@ -214,6 +216,8 @@ static orc_node *build_tree(orc_tree *t, const double *pos, const double *lo,
             cnt[j]++; /* "Update n_j" */
         }
         /* Step 3: distribution ratio, Eq. 4; halve while r >= beta (R3, R7). */
+        if (t->octree)
+            break;
         double r = orc_ratio(cnt, B, t->alpha, t->s);
         if (r >= t->beta && b > 2) {
             b = b / 2;
@@ -270,8 +274,17 @@ static orc_node *build_tree(orc_tree *t, const double *pos, const double *lo,
     return nd;
 }
 
+orc_tree *orc_build_policy(const double *pos, int64_t n, int32_t s, double beta,
+                           double alpha, int32_t depth_cap, int octree);
+
 orc_tree *orc_build(const double *pos, int64_t n, int32_t s, double beta,
                     double alpha, int32_t depth_cap)
+{
+    return orc_build_policy(pos, n, s, beta, alpha, depth_cap, 0);
+}
+
+orc_tree *orc_build_policy(const double *pos, int64_t n, int32_t s, double beta,
+                           double alpha, int32_t depth_cap, int octree)
 {
     if (n < 0 || s < 1 || !(beta > 0.0 && beta <= 1.0) || depth_cap < 0)
         return NULL;
@@ -281,6 +294,7 @@ orc_tree *orc_build(const double *pos, int64_t n, int32_t s, double beta,
     t->beta = beta;
     t->alpha = alpha;
     t->depth_cap = depth_cap;
+    t->octree = octree != 0;
     if (n == 0)
         return t;
     orc_root_box(pos, n, t->box_lo, t->box_hi);

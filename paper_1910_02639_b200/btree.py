@@ -20,7 +20,7 @@ _NAMES = {0: "BT_OK", 1: "BT_ERR_ARG", 2: "BT_ERR_INPUT", 3: "BT_ERR_CAPACITY", 
           5: "BT_ERR_OOM"}
 
 # every symbol include/btree.h declares
-EXPORTS = ["bt_build", "bt_build_ex", "bt_find_neighbors", "bt_fill_neighbors", "bt_free",
+EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "bt_fill_neighbors", "bt_free",
            "bt_search_host", "bt_set_stream", "bt_set_exact_only", "bt_release_cache", "bt_last_error", "bt_last_status", "bt_tree_stats",
            "bt_tree_order", "bt_profile_enable", "bt_profile_reset", "bt_profile_get"]
 
@@ -64,6 +64,8 @@ def lib():
         L.bt_build.restype = _P
         L.bt_build_ex.argtypes = [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_int32]
         L.bt_build_ex.restype = _P
+        L.bt_build_policy.argtypes = [_P, C.c_int64, C.c_int32, C.c_double, C.c_double, C.c_int32, C.c_int32]
+        L.bt_build_policy.restype = _P
         L.bt_find_neighbors.argtypes = [_P, _P, C.c_int32, _P, _P, _P]
         L.bt_find_neighbors.restype = C.c_int
         L.bt_fill_neighbors.argtypes = [_P, _P, _P, _P, C.c_int64]
@@ -122,12 +124,18 @@ class Tree:
     """b-tree over n particles (bt_build).  pos: CUDA float64 [n, 3]."""
 
     def __init__(self, pos: torch.Tensor, bucket_size: int = 64, max_empty: float = 0.5,
-                 alpha: float | None = None, depth_cap: int | None = None):
+                 alpha: float | None = None, depth_cap: int | None = None, policy: str = "btree"):
         pos = _dev_f64(pos, 3)
         self.n = pos.shape[0]
         self.device = pos.device
         _use_current_stream()
-        if alpha is None and depth_cap is None:
+        if policy not in ("btree", "octree"):
+            raise ValueError("policy must be 'btree' or 'octree'")
+        if policy == "octree":
+            h = lib().bt_build_policy(_ptr(pos), self.n, int(bucket_size), float(max_empty),
+                                      0.5 if alpha is None else float(alpha),
+                                      64 if depth_cap is None else int(depth_cap), 1)
+        elif alpha is None and depth_cap is None:
             h = lib().bt_build(_ptr(pos), self.n, int(bucket_size), float(max_empty))
         else:
             h = lib().bt_build_ex(_ptr(pos), self.n, int(bucket_size), float(max_empty),

@@ -219,8 +219,12 @@ using namespace bt;
 
 extern "C" {
 
-bt_tree *bt_build_ex(const double *pos, int64_t n, int32_t bucket_size, double max_empty, double alpha,
-                     int32_t depth_cap) {
+bt_tree *bt_build_policy(const double *pos, int64_t n, int32_t bucket_size, double max_empty, double alpha,
+                         int32_t depth_cap, int32_t policy) {
+    if (policy != BT_POLICY_BTREE && policy != BT_POLICY_OCTREE) {
+        set_error(BT_ERR_ARG, "bt_build_policy: policy must be BT_POLICY_BTREE or BT_POLICY_OCTREE");
+        return nullptr;
+    }
     if (n < 0 || n > 2147483647LL || (pos == nullptr && n > 0) || bucket_size < 1 || !(max_empty > 0.0 && max_empty <= 1.0) ||
         !(alpha >= 0.0 && alpha <= 1.0) || depth_cap < 0 || depth_cap > 1000) {
         set_error(BT_ERR_ARG,
@@ -236,6 +240,7 @@ bt_tree *bt_build_ex(const double *pos, int64_t n, int32_t bucket_size, double m
         t->t.beta = max_empty;
         t->t.alpha = alpha;
         t->t.depth_cap = depth_cap;
+        t->t.octree = policy == BT_POLICY_OCTREE;
         Phase ph("build.total");
         build_tree(t->t, pos);
         BT_CUDA(cudaStreamSynchronize(stream()));
@@ -251,6 +256,11 @@ bt_tree *bt_build_ex(const double *pos, int64_t n, int32_t bucket_size, double m
         return nullptr;
     }
     return t;
+}
+
+bt_tree *bt_build_ex(const double *pos, int64_t n, int32_t bucket_size, double max_empty, double alpha,
+                     int32_t depth_cap) {
+    return bt_build_policy(pos, n, bucket_size, max_empty, alpha, depth_cap, BT_POLICY_BTREE);
 }
 
 bt_tree *bt_build(const double *pos, int64_t n, int32_t bucket_size, double max_empty) {

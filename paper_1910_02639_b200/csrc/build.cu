@@ -144,10 +144,11 @@ __device__ __forceinline__ int eq1_branching(int64_t n, int64_t s) {
     return (int)b;
 }
 
-__global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s) {
+__global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s, int octree) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nn) return;
-    int b = eq1_branching(ln[i].count, s);
+    // FixedOctree policy (the paper's comparison baseline): b = 2
+    int b = octree ? 2 : eq1_branching(ln[i].count, s);
     ln[i].b0 = b;
     ln[i].b = b;
     ln[i].flag = 1;
@@ -624,7 +625,7 @@ void build_tree(TreeDev &t, const double *pos) {
         while (nn > 0) {
             Phase ph("build.level");
             // A2: Eq. 1 and the level's cell layout
-            level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s);
+            level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s, t.octree ? 1 : 0);
             BT_LAUNCH("level_b");
             device_scan<long long>(CellsOfNode{ln.p}, CellBaseOut{ln.p}, nn, dtotal.p);
             long long ncells_h = 0;
@@ -649,6 +650,7 @@ void build_tree(TreeDev &t, const double *pos) {
                 key_hist_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, t.nodes.p, keys.p,
                                                             hist.p, round);
                 BT_LAUNCH("key_hist");
+                if (t.octree) break;  // no ratio test for the octree policy
                 under_count_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, t.alpha * (double)t.s);
                 BT_LAUNCH("under_count");
                 BT_CUDA(cudaMemsetAsync(dflags.p + 1, 0, sizeof(int), st));

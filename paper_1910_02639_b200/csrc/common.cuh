@@ -128,6 +128,7 @@ struct TreeDev {
     int32_t s = 64;
     double beta = 0.5, alpha = 0.5;
     int32_t depth_cap = 64;
+    bool octree = false;       // FixedOctree policy: b = 2 at every node, no ratio test
     // records in tree (depth-first leaf) order: x, y, z, caller index (bits)
     DBuf<double4> rec;
     // compact records in tree order: fl32(fl64(x - c_leaf)) per axis, caller index (int bits)

@@ -360,8 +360,9 @@ __device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const
             const unsigned km = __ballot_sync(0xffffffffu, keep);
             if (keep && st.rec_ok) {
                 const int slot = st.fill + __popc(km & lt);
-                blk4[slot] = make_float4(ax, ay, az, __int_as_float(pos[h]));
-                blki[slot] = __float_as_int(r[h].w);
+                // streaming stores (read once, by the test / fill kernels): keep L2 for the records
+                __stcs(&blk4[slot], make_float4(ax, ay, az, __int_as_float(pos[h])));
+                __stcs(&blki[slot], __float_as_int(r[h].w));
                 if ((unsigned)(pos[h] - q0) < (unsigned)nq) self_slot[pos[h]] = st.base + slot;
             }
             const int nk = __popc(km);
@@ -626,8 +627,8 @@ __global__ void __launch_bounds__(kTestThreads, 6) test_kernel(WalkArgs a) {
             const int s0 = 64 * k + lane, s1 = s0 + 32;
             c0 = make_float4(inf, inf, inf, 0.f);
             c1 = c0;
-            if (s0 < Bk.ncand) c0 = a.cand4[Bk.cand_base + s0];
-            if (s1 < Bk.ncand) c1 = a.cand4[Bk.cand_base + s1];
+            if (s0 < Bk.ncand) c0 = __ldcs(&a.cand4[Bk.cand_base + s0]);
+            if (s1 < Bk.ncand) c1 = __ldcs(&a.cand4[Bk.cand_base + s1]);
         };
         int b = a.head[uid];
         Batch B{-1, 0, 0, -1};
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(kTestThreads, 6) test_kernel(WalkArgs a) {
             mb = __shfl_sync(0xffffffffu, mb, 0);
             __syncwarp();
             if (mb + (long long)nch * nq <= a.mask_cap) {
-                for (int w = lane; w < nch * nq; w += 32) a.masks[mb + w] = S.mask[w / nq][w % nq];
+                for (int w = lane; w < nch * nq; w += 32) __stcs(&a.masks[mb + w], S.mask[w / nq][w % nq]);
                 if (lane == 0) a.batches[b].mask_base = mb;
             }
             tests += (long long)B.ncand * nq;
@@ -748,11 +749,11 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
             int32_t c0[kChunks], c1[kChunks];
 #pragma unroll
             for (int k = 0; k < kChunks; k++) {
-                c0[k] = (k < nch) ? cands[B.cand_base + 64 * k + lane] : -1;
-                c1[k] = (k < nch) ? cands[B.cand_base + 64 * k + 32 + lane] : -1;
+                c0[k] = (k < nch) ? __ldcs(&cands[B.cand_base + 64 * k + lane]) : -1;
+                c1[k] = (k < nch) ? __ldcs(&cands[B.cand_base + 64 * k + 32 + lane]) : -1;
             }
             __syncwarp();
-            for (int w = lane; w < nch * nq; w += 32) F.mask[w] = masks[B.mask_base + w];
+            for (int w = lane; w < nch * nq; w += 32) F.mask[w] = __ldcs(&masks[B.mask_base + w]);
             __syncwarp();
             for (int q = 0; q < nq; q++) {
                 int32_t *dst = F.row[q];
@@ -764,8 +765,8 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
                     if (m == 0ull) continue;
                     const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
                     const int plo = __popc(lo);
-                    if (lo & lanebit) dst[__popc(lo & lt)] = c0[k];
-                    if (hi & lanebit) dst[plo + __popc(hi & lt)] = c1[k];
+                    if (lo & lanebit) __stcs(&dst[__popc(lo & lt)], c0[k]);
+                    if (hi & lanebit) __stcs(&dst[plo + __popc(hi & lt)], c1[k]);
                     const int n = plo + __popc(hi);
                     dst += n;
                     wrote += n;

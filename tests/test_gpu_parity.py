@@ -292,3 +292,15 @@ def test_fill_reuses_or_recomputes_record(P, oracle):
     nb2 = t.fill(hd, off2)
     ref2 = oracle.Tree(pos, 64).neighbors(h2)
     assert_same((c2.cpu().numpy(), off2.cpu().numpy(), sort_rows(c2, off2, nb2)), ref2)
+
+
+@pytest.mark.parametrize("cfg,n", [(2, 100_000), (4, 200_000), (5, 300_000)])
+def test_octree_policy_parity(P, oracle, cfg, n):
+    pos, h = datagen.make_config(cfg, n=n)
+    t = P.build(torch.from_numpy(pos).to(DEV), 64, 0.5, policy="octree")
+    hd = torch.from_numpy(h).to(DEV)
+    counts, offsets, nbr = t.find_neighbors(hd)
+    gpu = (counts.cpu().numpy(), offsets.cpu().numpy(), sort_rows(counts, offsets, nbr))
+    ot = oracle.Tree(pos, 64, 0.5, policy="octree")
+    assert_same(gpu, ot.neighbors(h))
+    assert_same_tree(t, ot)

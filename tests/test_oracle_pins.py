@@ -278,3 +278,25 @@ def test_uniform_root_needs_no_halving(oracle):
     pos, _ = datagen.uniform(20000, 71, 0.01)
     st = oracle.Tree(pos, 64).stats()
     assert st["root_b"] == oracle.branching_factor(20000, 64) == 7
+
+
+# ---- FixedOctree policy (the paper's comparison baseline, Sec. II) ----
+def test_octree_policy_lattice_depth(oracle):
+    # 8^3 lattice, s = 8: the b-tree takes b = 4 at the root (depth 1, Table II
+    # best case); the octree halves twice (8 -> 64 -> 8 particles): depth 2.
+    pos = datagen.lattice(8, 1.0)
+    bt = oracle.Tree(pos, 8).stats()
+    oc = oracle.Tree(pos, 8, policy="octree").stats()
+    assert bt["depth"] == 1 and bt["root_b"] == 4 and bt["leaves"] == 64
+    assert oc["depth"] == 2 and oc["root_b"] == 2 and oc["leaves"] == 64 and oc["nodes"] == 9
+    assert oc["halvings"] == 0
+
+
+def test_octree_same_neighbors_deeper_tree(oracle):
+    pos, h = datagen.clustered(8000, 91, h=0.01)
+    bt = oracle.Tree(pos, 16)
+    oc = oracle.Tree(pos, 16, policy="octree")
+    _assert_same(bt.neighbors(h), oc.neighbors(h))
+    assert oc.stats()["depth"] >= bt.stats()["depth"]
+    perm, lb, lc, _ = oc.order()
+    assert np.array_equal(np.sort(perm), np.arange(len(pos))) and np.all(lc <= 16)
