@@ -116,11 +116,14 @@ struct NodeRec {      // one internal node
 __host__ __device__ inline int32_t node_code(int32_t node) { return -2 - node; }
 __host__ __device__ inline int32_t code_node(int32_t code) { return -2 - code; }
 
-struct WalkBatch {          // one staged candidate batch of a walk unit
-    long long mask_base;    // mask word (chunk k, query q) at mask_base + k * nq + q (-1: none yet)
-    long long cand_base;    // first candidate slot of the block
-    int ncand;
-    int next;               // next batch of the same unit, -1 = last
+struct UnitRun {             // per walk unit, written by the walk kernels
+    long long list_off;     // first candidate leaf of the unit in the leaf-list arena
+    long long cand_base;    // first candidate slot of the unit (caller indices, for the fill)
+    long long mask_base;    // mask word (chunk kk, query q) at mask_base + kk * nq + q
+    int nleaf;              // candidate leaves (-1: descent overflowed, redo in the big pass)
+    int loaded;             // particle records of the candidate leaves (arena bound)
+    int nstaged;            // candidates kept by the per-particle cull
+    int ok;                 // the unit's masks and candidate indices were recorded
 };
 
 struct TreeDev {
@@ -152,21 +155,18 @@ struct TreeDev {
     bool root_is_leaf = true;
     // search scratch
     DBuf<double> h_tree;       // h in tree order
-    DBuf<int32_t> head;        // first recorded batch of each unit
-    DBuf<unsigned long long> arena_masks;  // neighbor masks per (query, 64-candidate chunk)
-    DBuf<float4> arena_cand4;              // candidate slots: fp32 relative coordinates, tree position
+    DBuf<UnitRun> urun;                    // per-unit walk record
+    DBuf<int32_t> ulist;                   // candidate leaf lists of all units
+    DBuf<unsigned long long> arena_masks;  // neighbor masks per (64-candidate chunk, query)
     DBuf<int32_t> arena_cands;             // candidate caller indices per slot
-    DBuf<int64_t> self_slot;               // per tree position: arena slot of the query itself
-    DBuf<WalkBatch> arena_batches;
     bool rec_valid = false;    // arena holds the test pass of (rec_h, rec_hsum, rec_exact)
     const double *rec_h = nullptr;
     long long rec_hsum = 0;
     int rec_exact = 0;
     DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
-    DBuf<int32_t> front;       // walk frontier scratch (per resident warp)
-    int64_t stack_per_warp = 0;
+    DBuf<int32_t> front;       // descent frontier scratch of the big-unit pass (per warp)
     int64_t total_pairs = 0, max_count = 0, staged = 0, loaded = 0, tests = 0, exact_tests = 0;
-    int64_t mask_words = 0, cand_slots = 0;
+    int64_t mask_words = 0, cand_slots = 0, list_entries = 0, big_units = 0;
 };
 
 // Build (build.cu) and search (walk.cu) entry points.

@@ -3,22 +3,24 @@
 // Work unit = up to 64 queries of one leaf bucket (the paper's "blocked
 // approach", Sec. IV-E: particles are in tree order, so a unit's queries
 // are spatial neighbours).  One warp per unit; persistent warps pull units
-// from an atomic counter.  Three kernels:
+// (in Morton order of their leaf, build.cu) from an atomic counter.
 //
-// gather_kernel (A10): per unit, breadth-first descent from the root with
-//   Eq. 5 index ranges of the unit's query box widened by R'_u = max_i R'_i
-//   (lemma L1/L2): all cells of all frontier nodes of a level are
+// desc_kernel (A10): per unit, breadth-first descent from the root with Eq. 5
+//   index ranges of the unit's query box widened by R'_u = max_i R'_i (lemma
+//   L1/L2): all cells of all frontier nodes of a level are
 //   flattened over the 32 lanes; empty cells skipped, internal cells form the
-//   next frontier, leaf cells are culled by their tight box (L3) and queued;
-//   queued leaves' particles are loaded (flattened over the lanes), culled
-//   per particle against the query box (L3) and written as fp32 coordinates
-//   relative to the unit centre into candidate blocks of <= 256 in an arena.
-// test_kernel (A11): per unit and candidate block, lanes = candidates (two
-//   per lane, packed f32x2), loop over queries: s32 < A_i -> certainly a
-//   neighbor, s32 >= B_i -> certainly not, else the exact fp64 predicate
-//   ((dx*dx + dy*dy) + dz*dz) < (2h)^2 decides (lemma L4).
-//   __ballot_sync gives a 64-bit neighbor mask per (64-candidate chunk,
-//   query); __popc of the masks are the counts; the masks are recorded.
+//   next frontier, leaf cells whose tight box is within R'_u of the query box
+//   (L3) are appended to the unit's candidate-leaf list.
+// walk_kernel (A10 staging + A11): per unit, the listed leaves' particles are
+//   loaded (flattened over the lanes), culled per particle against the query
+//   box (L3) and staged in shared memory as fp32 coordinates relative to the
+//   unit centre, in blocks of 128.  Each block is tested against the unit's
+//   queries: lanes = 4 candidates (two packed f32x2 pairs), loop over
+//   queries; d = fl32(s32 - Mid_i) decides the certain cases (lemma L4),
+//   pairs with |d| <= HW_i are decided by the exact fp64 predicate
+//   ((dx*dx + dy*dy) + dz*dz) < (2h)^2.  __ballot_sync gives a 64-bit
+//   neighbor mask per (64-candidate chunk, query); __popc of the masks are
+//   the counts; masks and candidate caller indices are recorded per unit.
 // Scan (A12): offsets = exclusive scan of counts.
 // fill_kernel (A13): replay the recorded masks: __popc(mask & lanemask_lt) is
 //   each neighbor's slot in its CSR row.
@@ -32,32 +34,40 @@ namespace bt {
 
 namespace {
 
-constexpr int kQ = 64;          // queries per unit (== build.cu kUnitQ)
-constexpr int kBlock = 256;     // candidates per arena block
-constexpr int kChunks = kBlock / 64;
-constexpr int kLeafCap = 64;    // queued candidate leaves (gather)
-constexpr int kGatherThreads = 128;
-constexpr int kTestThreads = 128;
+constexpr int kQ = 64;           // queries per unit (== build.cu kUnitQ)
+constexpr int kBlk = 128;        // staged candidates per test block
+constexpr int kBuf = kBlk + 64;  // staging buffer: a block + one staging step
+constexpr int kGroup = 32;       // candidate leaves per staging group (one per lane)
+constexpr int kFrontCap = 128;   // shared-memory descent frontier per level
+constexpr int kDescThreads = 128;
+constexpr int kWalkThreads = 128;
 constexpr int kFillThreads = 256;
+constexpr int kFillChunks = 4;   // 64-candidate chunks per fill round
+constexpr long long kListSlab = 8192;     // leaf-list entries per warp allocation
+constexpr long long kListReserve = 2048;  // more candidate leaves -> big-unit pass
+constexpr long long kCandSlab = 16384;    // candidate slots per warp allocation
+constexpr long long kMaskSlab = 8192;     // mask words per warp allocation
 
 // device counters (int64 slots of TreeDev::counters)
 enum {
-    C_WORK = 0,      // unit counter (gather)
-    C_MASK = 1,      // mask words requested
-    C_CAND = 2,      // candidate slots requested
-    C_BATCH = 3,     // candidate blocks requested
+    C_WORK = 0,      // unit counter (descent)
+    C_MASK = 1,      // mask words allocated
+    C_CAND = 2,      // candidate slots allocated
+    C_LIST = 3,      // leaf-list entries allocated
     C_STAGED = 4,
     C_TESTS = 5,
     C_EXACT = 6,
     C_MAXC = 7,
     C_WORK2 = 8,     // unit counter (fill)
     C_HSUM = 9,      // checksum of h (bit patterns)
-    C_LOADED = 10,   // particle records loaded by the gather (before the cull)
-    C_WORK3 = 11,    // unit counter (test)
+    C_LOADED = 10,   // particle records loaded by the staging (before the cull)
+    C_WORK3 = 11,    // unit counter (walk)
+    C_BIG = 12,      // units whose descent overflowed the shared-memory limits
+    C_WORK4 = 13,    // unit counter (big-unit descent)
+    C_NEEDC = 14,    // sum over units of `loaded` (bound on candidate slots)
+    C_NEEDM = 15,    // sum over units of ceil(loaded / 64) * nq (bound on mask words)
     C_N = 16
 };
-
-using Batch = WalkBatch;
 
 struct WalkArgs {
     const double4 *rec;
@@ -73,20 +83,17 @@ struct WalkArgs {
     double M;
     int root_is_leaf;
     int exact_only;
-    int32_t *front;           // per-warp frontier scratch: 2 x front_cap node ids
+    int32_t *front;           // big-unit pass: per-warp frontier scratch, 2 x front_cap node ids
     int64_t front_cap;
+    UnitRun *urun;
+    int32_t *ulist;
+    long long list_cap;
     int32_t *counts;
     const int64_t *offsets;
     int32_t *nbr;
     long long *ctr;
-    // arena
-    float4 *cand4;            // candidate block slots: ax, ay, az (fp32 rel.), tree position (int bits)
-    int32_t *cands;           // caller index of each candidate slot (-1 = padding)
+    int32_t *cands;           // caller index of each candidate slot
     long long cand_cap;
-    long long *self_slot;     // per tree position: the arena slot of the query itself in its own unit
-    Batch *batches;
-    long long batch_cap;
-    int32_t *head;            // first block of each unit
     unsigned long long *masks;
     long long mask_cap;
 };
@@ -100,13 +107,22 @@ __device__ __forceinline__ double warp_max(double v) {
     return v;
 }
 
-// packed fp32 pair arithmetic (sm_100a FADD2 / FMUL2 / FFMA2)
+// packed fp32 pair arithmetic (sm_100a FADD2 / FMUL2 / FFMA2): lo = first, hi = second
 __device__ __forceinline__ unsigned long long pk(float lo, float hi) {
-    return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+    unsigned long long r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
 }
+__device__ __forceinline__ float lo_f(unsigned long long v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi_f(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
 __device__ __forceinline__ unsigned long long f2_sub(unsigned long long a, unsigned long long b) {
     unsigned long long r;
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long f2_add(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
 __device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
@@ -118,6 +134,14 @@ __device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsig
     unsigned long long r;
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
+}
+// 16-byte shared-memory load (one LDS.128)
+__device__ __forceinline__ float4 lds4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
 }
 
 // Exact predicate (the definition): ((dx*dx + dy*dy) + dz*dz) < T, fp64, no FMA.
@@ -165,8 +189,33 @@ __device__ __forceinline__ void l4_thresholds(double T, double E, double eps, bo
     B = (hb < 3.0e38) ? __double2float_ru(hb) : __int_as_float(0x7f800000);
 }
 
+// The band [A, B) as one fused multiply-add: fp32
+// A <= Mid <= B, HW >= max(Mid - A, B - Mid), k = the largest power of two
+// <= 1/HW and c = -Mid k (exact: a power-of-two scaling), so the hot loop's
+// d' = fl32(s k + c) = k fl32(s - Mid).  Then
+//   s in [A, B)  =>  |s - Mid| <= HW <= 1/k  =>  |d'| <= 1
+// (round-to-nearest is monotone and 1/k is representable), so a pair with
+// |d'| > 1 is certain, and for it d' < 0 <=> s < Mid <=> s < A (a neighbor).
+// k = c = 0 (B = +inf: exact-only) bands every pair ("force": the fp64
+// predicate decides everything, also pairs whose fp32 arithmetic overflowed).
+__device__ __forceinline__ void band_params(float A, float B, float &k, float &c) {
+    k = 0.0f;
+    c = 0.0f;
+    if (!(B < __int_as_float(0x7f800000))) return;
+    float Mid = __double2float_rn(0.5 * ((double)A + (double)B));
+    Mid = fmaxf(A, fminf(B, Mid));
+    // half-width: exact difference of fp32 values rounded up, widened to
+    // >= 2^-23 Mid and >= 1e-30 (keeps Mid k <= 2^23 and k <= 2^100)
+    float HW = __double2float_ru(fmax((double)Mid - (double)A, (double)B - (double)Mid));
+    HW = fmaxf(HW, fmaxf(Mid * 0x1p-23f, 1e-30f));
+    int e;
+    frexp(1.0 / (double)HW, &e);  // 1/HW = f 2^e, f in [0.5, 1)
+    k = ldexpf(1.0f, e - 1);      // largest power of two <= 1/HW
+    c = -Mid * k;                 // exact
+}
+
 // ---------------------------------------------------------------------------
-// Unit geometry: identical code in the gather and the test kernels, so both
+// Unit geometry: identical code in the descent and the walk kernels, so both
 // derive bit-identical c, E and R'_u.
 // ---------------------------------------------------------------------------
 struct UnitGeom {
@@ -220,510 +269,626 @@ __device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, in
     G.E = (E + G.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
 }
 
-// ---------------------------------------------------------------------------
-// gather_kernel
-// ---------------------------------------------------------------------------
-struct GatherSmem {
-    int32_t lbeg[kLeafCap + 1];  // queued leaves: first tree position
-    int32_t lpre[kLeafCap + 1];  // queued leaves: counts, then exclusive prefix
-    float4 loff[kLeafCap + 1];   // queued leaves: fl32(c_leaf - c_unit), w = 1 if staged from rec32
+// Warp-uniform allocation from a per-warp slab [cur, end) refilled from a
+// global counter; returns false when the arena capacity was exceeded.
+struct Slab {
+    long long cur = 0, end = 0;
 };
+__device__ __forceinline__ bool slab_reserve(Slab &s, long long need, long long chunk, long long cap, long long *ctr,
+                                             int lane) {
+    if (s.end - s.cur < need) {
+        const long long size = need > chunk ? need : chunk;
+        long long base = 0;
+        if (lane == 0) base = (long long)atomicAdd((unsigned long long *)ctr, (unsigned long long)size);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        s.cur = base;
+        s.end = base + size;
+    }
+    return s.cur + need <= cap;
+}
 
-struct GatherState {
-    int64_t uid;
+// ---------------------------------------------------------------------------
+// desc_kernel: candidate-leaf lists (A10)
+// ---------------------------------------------------------------------------
+struct DescOut {
     int nleaf;
-    // current candidate block
-    int blk;           // block index, -1 = none
-    long long base;    // first arena slot of the block
-    int fill;          // candidates in the block
-    bool rec_ok;       // arena space was available for every block
-    // cull constants
-    float blo[3], bhi[3], cull2;
-    long long staged, loaded;
+    long long loaded;
+    bool overflow;  // a level frontier exceeded the frontier capacity
 };
 
-__device__ __forceinline__ void close_block(GatherState &st, int lane, const WalkArgs &a) {
-    if (st.blk >= 0 && st.rec_ok && lane == 0) a.batches[st.blk].ncand = st.fill;
-}
-
-__device__ __forceinline__ void open_block(GatherState &st, int lane, const WalkArgs &a) {
-    close_block(st, lane, a);
-    long long base = 0, bi = 0;
-    if (lane == 0) {
-        base = atomicAdd((unsigned long long *)&a.ctr[C_CAND], (unsigned long long)kBlock);
-        bi = atomicAdd((unsigned long long *)&a.ctr[C_BATCH], 1ull);
-    }
-    base = __shfl_sync(0xffffffffu, base, 0);
-    bi = __shfl_sync(0xffffffffu, bi, 0);
-    const bool ok = st.rec_ok && base + kBlock <= a.cand_cap && bi < a.batch_cap;
-    if (ok && lane == 0) {
-        a.batches[bi] = Batch{-1, base, 0, -1};
-        if (st.blk >= 0) a.batches[st.blk].next = (int)bi;
-        else a.head[st.uid] = (int)bi;
-    }
-    st.rec_ok = ok;
-    st.blk = (int)bi;
-    st.base = base;
-    st.fill = 0;
-    __syncwarp();
-}
-
-// Load the queued leaves' particles (flattened over the lanes), cull them per
-// particle (L3, fp32 conservative) and append the kept ones to the arena.
-__device__ __noinline__ void stage_leaves(GatherSmem &S, GatherState &stm, const UnitGeom &G, int lane,
-                                          const WalkArgs &a) {
-    GatherState st = stm;  // registers (the caller's copy lives in local memory)
-    // pointers in registers (the args struct lives in local memory here)
-    const float4 *__restrict__ rec32 = a.rec32;
-    const double4 *__restrict__ rec = a.rec;
-    float4 *__restrict__ cand4 = a.cand4;
-    int32_t *__restrict__ cands = a.cands;
-    long long *__restrict__ self_slot = a.self_slot;
+// Breadth-first descent of one unit; appends the kept leaves to out[0, lim)
+// (when out != nullptr) and returns how many there are.
+__device__ __forceinline__ DescOut descend(const WalkArgs &a, const UnitGeom &G, int lane, int32_t *fcur,
+                                           int32_t *fnext, long long fcap, int32_t *out, long long lim) {
     const unsigned lt = lanemask_lt();
-    const int nl = st.nleaf;
-    int carry = 0;
-    for (int i0 = 0; i0 < nl; i0 += 32) {
-        const int i = i0 + lane;
-        const int v = (i < nl) ? S.lpre[i] : 0;
-        int inc = v;
-        for (int d = 1; d < 32; d <<= 1) {
-            int o = __shfl_up_sync(0xffffffffu, inc, d);
-            if (lane >= d) inc += o;
+    DescOut r{0, 0, false};
+    long long loaded = 0;
+    // leaf cell found by this lane: keep it if its tight box is within R'_u of
+    // the query box (L3, exact fp64 box distance)
+    auto emit = [&](bool is_leaf, int32_t leaf) {
+        bool keep = false;
+        if (is_leaf) {
+            const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
+            const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
+            double gx = fmax(0.0, fmax(__dsub_rn(b0.x, G.hi[0]), __dsub_rn(G.lo[0], b1.y)));
+            double gy = fmax(0.0, fmax(__dsub_rn(b0.y, G.hi[1]), __dsub_rn(G.lo[1], b2.x)));
+            double gz = fmax(0.0, fmax(__dsub_rn(b1.x, G.hi[2]), __dsub_rn(G.lo[2], b2.y)));
+            double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
+            keep = g2 < G.Ru2;
         }
-        if (i < nl) S.lpre[i] = carry + inc - v;
-        carry += __shfl_sync(0xffffffffu, inc, 31);
-    }
-    if (lane == 0) S.lpre[nl] = carry;
-    __syncwarp();
-    const int total = carry;
-    const int q0 = G.q0, nq = G.nq;
-    const double c0 = G.c[0], c1 = G.c[1], c2 = G.c[2];
-    // any large leaf (staged from the fp64 records) among the queued ones?
-    bool mixed = false;
-    for (int i = lane; i < nl; i += 32) mixed |= S.loff[i].w == 0.0f;
-    mixed = __any_sync(0xffffffffu, mixed);
-    st.loaded += total;
-    float4 *blk4 = cand4 + st.base;
-    int32_t *blki = cands + st.base;
-    int owner = 0;  // queued leaf holding the next flattened position
-    for (int p0 = 0; p0 < total; p0 += 64) {
-        if (st.blk < 0 || st.fill + 64 > kBlock) {
-            open_block(st, lane, a);
-            blk4 = cand4 + st.base;
-            blki = cands + st.base;
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const long long slot = r.nleaf + __popc(km & lt);
+            if (out && slot < lim) out[slot] = leaf;
+            loaded += a.leaf_count[leaf];
         }
-        float4 r[2], of[2];
-        int pos[2];
-        bool valid[2];
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int w0 = p0 + 32 * h;
-            // owners of the 32 positions [w0, w0 + 32): leaf starts inside the window
-            const int nxt = owner + 1 + lane;
-            const int stt = (nxt <= nl) ? S.lpre[nxt] : 0x7fffffff;
-            const int off = stt - w0;  // >= 1 for leaves after `owner`
-            const unsigned bits = __reduce_or_sync(0xffffffffu, (off >= 1 && off < 32) ? (1u << off) : 0u);
-            const int mine = owner + __popc(bits & ((2u << lane) - 1u));
-            const unsigned past = __ballot_sync(0xffffffffu, off <= 32);
-            const int p = w0 + lane;
-            valid[h] = p < total;
-            pos[h] = valid[h] ? S.lbeg[mine] + (p - S.lpre[mine]) : 0;
-            of[h] = S.loff[mine];
-            owner += __popc(past);
-            r[h] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (!mixed) {
-                if (valid[h]) r[h] = rec32[pos[h]];
-            } else if (valid[h]) {
-                if (of[h].w != 0.0f) {
-                    r[h] = rec32[pos[h]];
-                } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
-                    const double4 d = rec[pos[h]];
-                    r[h] = make_float4(__double2float_rn(__dsub_rn(d.x, c0)), __double2float_rn(__dsub_rn(d.y, c1)),
-                                       __double2float_rn(__dsub_rn(d.z, c2)),
-                                       __int_as_float((int)__double_as_longlong(d.w)));
-                    of[h].x = of[h].y = of[h].z = 0.0f;
+        r.nleaf += __popc(km);
+    };
+    if (a.root_is_leaf) {
+        emit(lane == 0, 0);
+    } else {
+        int nf = 1;
+        if (lane == 0) fcur[0] = 0;
+        __syncwarp();
+        while (nf > 0) {
+            int nnext = 0;
+            for (int f0 = 0; f0 < nf; f0 += 32) {
+                const int fi = f0 + lane;
+                int b = 0, r0x = 0, r0y = 0, r0z = 0, nx = 1, ny = 1;
+                long long cb = 0, tot = 0;
+                if (fi < nf) {
+                    const NodeRec &nd = a.nodes[fcur[fi]];
+                    b = nd.b;
+                    cb = nd.cell_base;
+                    int r0[3], r1[3];
+                    for (int l = 0; l < 3; l++) {  // Eq. 5 with R'_u (lemma L2)
+                        r0[l] = cell_coord(__dsub_rn(G.lo[l], G.Ru), nd.lo[l], nd.ext[l], b);
+                        r1[l] = cell_coord(__dadd_rn(G.hi[l], G.Ru), nd.lo[l], nd.ext[l], b);
+                    }
+                    r0x = r0[0];
+                    r0y = r0[1];
+                    r0z = r0[2];
+                    nx = r1[0] - r0[0] + 1;
+                    ny = r1[1] - r0[1] + 1;
+                    tot = (long long)nx * ny * (r1[2] - r0[2] + 1);
+                }
+                // inclusive scan of the cell counts over the lanes
+                long long inc = tot;
+                for (int d = 1; d < 32; d <<= 1) {
+                    long long o = __shfl_up_sync(0xffffffffu, inc, d);
+                    if (lane >= d) inc += o;
+                }
+                const long long start = inc - tot;
+                const long long T = __shfl_sync(0xffffffffu, inc, 31);
+                int owner = 0;
+                for (long long c0 = 0; c0 < T; c0 += 32) {
+                    // owner lane of cell g = c0 + lane (node starts inside the window)
+                    const long long off = start - c0;
+                    const unsigned bits =
+                        __reduce_or_sync(0xffffffffu, (lane > owner && off >= 1 && off < 32) ? (1u << off) : 0u);
+                    const int o = owner + __popc(bits & ((2u << lane) - 1u));
+                    const unsigned past = __ballot_sync(0xffffffffu, lane > owner && off <= 32);
+                    const int ob = __shfl_sync(0xffffffffu, b, o);
+                    const long long ocb = __shfl_sync(0xffffffffu, cb, o);
+                    const int ox = __shfl_sync(0xffffffffu, r0x, o), oy = __shfl_sync(0xffffffffu, r0y, o),
+                              oz = __shfl_sync(0xffffffffu, r0z, o);
+                    const int onx = __shfl_sync(0xffffffffu, nx, o), ony = __shfl_sync(0xffffffffu, ny, o);
+                    const long long ostart = __shfl_sync(0xffffffffu, start, o);
+                    owner += __popc(past);
+                    const long long g = c0 + lane;
+                    bool is_leaf = false, is_node = false;
+                    int32_t code = -1;
+                    if (g < T) {
+                        const int local = (int)(g - ostart);
+                        const int cx = ox + local % onx;
+                        const int cy = oy + (local / onx) % ony;
+                        const int cz = oz + local / (onx * ony);
+                        const long long j = cx + (long long)cy * ob + (long long)cz * ob * ob;  // Eq. 3
+                        code = a.cells[ocb + j];
+                        is_leaf = code >= 0;
+                        is_node = code <= -2;
+                    }
+                    const unsigned nm = __ballot_sync(0xffffffffu, is_node);
+                    const int slot = nnext + __popc(nm & lt);
+                    if (is_node && slot < fcap) fnext[slot] = code_node(code);
+                    nnext += __popc(nm);
+                    emit(is_leaf, code);
                 }
             }
-        }
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
-            // conservative fp32 Minkowski cull against the query box (L3 / L4)
-            const float ax = __fadd_rn(r[h].x, of[h].x);
-            const float ay = __fadd_rn(r[h].y, of[h].y);
-            const float az = __fadd_rn(r[h].z, of[h].z);
-            const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(st.blo[0], ax), __fsub_rn(ax, st.bhi[0])));
-            const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(st.blo[1], ay), __fsub_rn(ay, st.bhi[1])));
-            const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(st.blo[2], az), __fsub_rn(az, st.bhi[2])));
-            const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
-            const bool keep = valid[h] && g2 < st.cull2;
-            const unsigned km = __ballot_sync(0xffffffffu, keep);
-            if (keep && st.rec_ok) {
-                const int slot = st.fill + __popc(km & lt);
-                // streaming stores (read once, by the test / fill kernels): keep L2 for the records
-                __stcs(&blk4[slot], make_float4(ax, ay, az, __int_as_float(pos[h])));
-                __stcs(&blki[slot], __float_as_int(r[h].w));
-                if ((unsigned)(pos[h] - q0) < (unsigned)nq) self_slot[pos[h]] = st.base + slot;
+            __syncwarp();
+            if (nnext > fcap) {
+                r.overflow = true;
+                break;
             }
-            const int nk = __popc(km);
-            st.fill += nk;
-            st.staged += nk;
+            int32_t *tmp = fcur;
+            fcur = fnext;
+            fnext = tmp;
+            nf = nnext;
         }
     }
-    st.nleaf = 0;
-    stm = st;
-    __syncwarp();
+    for (int d = 16; d; d >>= 1) loaded += __shfl_xor_sync(0xffffffffu, loaded, d);
+    r.loaded = loaded;
+    return r;
 }
 
-// queue the leaf cells found by the lanes (if the tight box is within R'_u of
-// the query box: L3)
-__device__ __forceinline__ void queue_leaves(GatherSmem &S, GatherState &st, const UnitGeom &G, int lane,
-                                             const WalkArgs &a, bool is_leaf, int32_t leaf) {
-    const unsigned lt = lanemask_lt();
-    bool keep = false;
-    float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (is_leaf) {
-        const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
-        const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
-        double gx = fmax(0.0, fmax(__dsub_rn(b0.x, G.hi[0]), __dsub_rn(G.lo[0], b1.y)));
-        double gy = fmax(0.0, fmax(__dsub_rn(b0.y, G.hi[1]), __dsub_rn(G.lo[1], b2.x)));
-        double gz = fmax(0.0, fmax(__dsub_rn(b1.x, G.hi[2]), __dsub_rn(G.lo[2], b2.y)));
-        double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
-        keep = g2 < G.Ru2;
-        // leaf centre (as build.cu computed it) relative to the unit centre; the
-        // compact records are usable when the leaf half-extent H <= 7 E (l4_eps)
-        const double cx = 0.5 * (b0.x + b1.y), cy = 0.5 * (b0.y + b2.x), cz = 0.5 * (b1.x + b2.y);
-        const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
-        off = make_float4(__double2float_rn(__dsub_rn(cx, G.c[0])), __double2float_rn(__dsub_rn(cy, G.c[1])),
-                          __double2float_rn(__dsub_rn(cz, G.c[2])), (H <= 7.0 * G.E) ? 1.0f : 0.0f);
-    }
-    const unsigned km = __ballot_sync(0xffffffffu, keep);
-    if (!km) return;
-    if (st.nleaf + __popc(km) > kLeafCap) stage_leaves(S, st, G, lane, a);
-    if (keep) {
-        const int slot = st.nleaf + __popc(km & lt);
-        S.lbeg[slot] = a.leaf_begin[leaf];
-        S.lpre[slot] = a.leaf_count[leaf];  // counts; stage_leaves turns them into a prefix
-        S.loff[slot] = off;
-    }
-    st.nleaf += __popc(km);
-    __syncwarp();
+// exact arena bounds of the walk (a unit stages at most `loaded` candidates)
+__device__ __forceinline__ void add_need(const WalkArgs &a, long long loaded, int nq) {
+    atomicAdd((unsigned long long *)&a.ctr[C_NEEDC], (unsigned long long)loaded);
+    atomicAdd((unsigned long long *)&a.ctr[C_NEEDM], (unsigned long long)(((loaded + 63) >> 6) * nq));
 }
 
-#ifndef BT_GATHER_MIN_BLOCKS
-#define BT_GATHER_MIN_BLOCKS 6
-#endif
-__global__ void __launch_bounds__(kGatherThreads, BT_GATHER_MIN_BLOCKS) gather_kernel(WalkArgs a) {
-    __shared__ GatherSmem smem[kGatherThreads / 32];
+// kBig = false: frontier in shared memory, list from per-warp slabs with at
+//   most kListReserve leaves per unit; a unit exceeding either is marked
+//   (nleaf = -1) for the big pass.
+// kBig = true: only marked units; frontier in global scratch (front_cap =
+//   all nodes), the list counted first and allocated exactly.
+template <bool kBig>
+__global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
+    __shared__ int32_t sfront[kBig ? 1 : kDescThreads / 32][2][kBig ? 1 : kFrontCap];
     const int lane = threadIdx.x & 31;
-    GatherSmem &S = smem[threadIdx.x >> 5];
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    int32_t *const front_base = a.front + gwarp * 2 * a.front_cap;
-    const unsigned lt = lanemask_lt();
-    long long staged = 0, loaded = 0;
+    int32_t *f0, *f1;
+    long long fcap;
+    if (kBig) {
+        f0 = a.front + gwarp * 2 * a.front_cap;
+        f1 = f0 + a.front_cap;
+        fcap = a.front_cap;
+    } else {
+        f0 = sfront[threadIdx.x >> 5][0];
+        f1 = sfront[threadIdx.x >> 5][1];
+        fcap = kFrontCap;
+    }
+    Slab ls;
     for (;;) {
         unsigned long long uid = 0;
-        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK], 1ull);
+        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[kBig ? C_WORK4 : C_WORK], 1ull);
         uid = __shfl_sync(0xffffffffu, uid, 0);
         if (uid >= (unsigned long long)a.n_units) break;
+        if (kBig && a.urun[uid].nleaf >= 0) continue;
         UnitGeom G;
         unit_setup(a, a.units[uid], lane, G);
-        GatherState st;
-        st.uid = (int64_t)uid;
-        st.nleaf = 0;
-        st.blk = -1;
-        st.base = 0;
-        st.fill = 0;
-        st.rec_ok = true;
-        st.staged = st.loaded = 0;
-        if (lane == 0) a.head[uid] = -1;
+        UnitRun &R = a.urun[uid];
+        if (!kBig) {
+            const bool ok = slab_reserve(ls, kListReserve, kListSlab, a.list_cap, &a.ctr[C_LIST], lane);
+            const long long lim = ls.end - ls.cur;
+            DescOut d = descend(a, G, lane, f0, f1, fcap, ok ? a.ulist + ls.cur : nullptr, lim);
+            const bool fits = ok && !d.overflow && d.nleaf <= lim;
+            if (lane == 0) {
+                R.list_off = ls.cur;
+                R.nleaf = fits ? d.nleaf : -1;
+                R.loaded = (int)d.loaded;
+                if (!fits) atomicAdd((unsigned long long *)&a.ctr[C_BIG], 1ull);
+                else add_need(a, d.loaded, G.nq);
+            }
+            if (fits) ls.cur += d.nleaf;
+        } else {
+            DescOut d = descend(a, G, lane, f0, f1, fcap, nullptr, 0);
+            long long base = 0;
+            if (lane == 0) base = (long long)atomicAdd((unsigned long long *)&a.ctr[C_LIST], (unsigned long long)d.nleaf);
+            base = __shfl_sync(0xffffffffu, base, 0);
+            const bool ok = !d.overflow && base + d.nleaf <= a.list_cap;
+            if (ok) descend(a, G, lane, f0, f1, fcap, a.ulist + base, d.nleaf);
+            if (lane == 0) {
+                R.list_off = base;
+                R.nleaf = ok ? d.nleaf : -2;  // -2: list arena too small (host grows it and redoes the pass)
+                R.loaded = (int)d.loaded;
+                add_need(a, d.loaded, G.nq);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// walk_kernel: staging + pair tests (A10, A11)
+// ---------------------------------------------------------------------------
+struct WalkSmem {
+    float4 q0[kQ];                  // ax, ax, ay, ay  (fp32, relative to the unit centre)
+    float4 q1[kQ];                  // az, az, k, k   (band map d' = s k + c)
+    float2 q2[kQ];                  // c, c
+    int self[kQ];                   // unit slot of each query's own record (-1: none)
+    float cx[kBuf], cy[kBuf], cz[kBuf];
+    int tpos[kBuf];                 // tree position of each staged candidate
+    unsigned long long mask[2][kQ]; // the block's neighbor masks [chunk][query]
+    int lbeg[kGroup];               // group leaves: first tree position
+    int lpre[kGroup + 1];           // group leaves: exclusive prefix of counts
+    float4 loff[kGroup];            // group leaves: fl32(c_leaf - c), w = 1 compact / 0 fp64 records
+};
+
+struct WalkState {
+    int q0, nq;
+    int nbuf;       // candidates in the staging buffer
+    int nblk;       // blocks tested
+    long long cand_base, mask_base;
+    bool rec_ok;
+    int cnt[2];     // counts of this lane's queries (lane, lane + 32)
+    long long tests, exact;
+    bool force;     // some query has k = 0: every pair goes to the fp64 predicate
+};
+
+// The exact band of lemma L4 (rare): recompute the block's pairs with the
+// hot loop's fp32 operations and let the fp64 predicate decide every pair
+// with |d'| <= 1 (all pairs when `force`; padding slots >= n are never
+// neighbors).
+__device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int lane, int q0, int nq, int n, bool force,
+                                          long long &exact) {
+    const int nch = (n + 63) >> 6;
+    const float inf = __int_as_float(0x7f800000);
+    for (int k = 0; k < nch; k++) {
+        float x[2], y[2], z[2];
+        int tp[2];
+        bool real[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int s = 64 * k + 32 * h + lane;
+            real[h] = s < n;
+            x[h] = real[h] ? S.cx[s] : inf;
+            y[h] = real[h] ? S.cy[s] : inf;
+            z[h] = real[h] ? S.cz[s] : inf;
+            tp[h] = real[h] ? S.tpos[s] : -1;
+        }
+        for (int q = 0; q < nq; q++) {
+            const float4 Q0 = S.q0[q], Q1 = S.q1[q];
+            const float2 Q2 = S.q2[q];
+            bool flag[2];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const float dx = __fsub_rn(x[h], Q0.x), dy = __fsub_rn(y[h], Q0.z), dz = __fsub_rn(z[h], Q1.x);
+                float s = __fmul_rn(dx, dx);
+                s = __fmaf_rn(dy, dy, s);
+                s = __fmaf_rn(dz, dz, s);
+                const float d = __fmaf_rn(s, Q1.z, Q2.x);
+                flag[h] = real[h] && (force || fabsf(d) <= 1.0f);
+            }
+            const unsigned f0 = __ballot_sync(0xffffffffu, flag[0]), f1 = __ballot_sync(0xffffffffu, flag[1]);
+            if (!(f0 | f1)) continue;
+            const int qp = q0 + q;
+            const double4 Qr = a.rec[qp];
+            const double t = __dmul_rn(2.0, a.h_tree[qp]);
+            const double T = __dmul_rn(t, t);
+            bool e0 = false, e1 = false;
+            if (flag[0]) e0 = tp[0] != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp[0]]);
+            if (flag[1]) e1 = tp[1] != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp[1]]);
+            const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
+            if (lane == 0) {
+                const unsigned long long fm = ((unsigned long long)f1 << 32) | f0;
+                const unsigned long long em = ((unsigned long long)m1 << 32) | m0;
+                S.mask[k][q] = (S.mask[k][q] & ~fm) | em;
+            }
+            exact += __popc(f0) + __popc(f1);
+            __syncwarp();
+        }
+    }
+    __syncwarp();
+}
+
+// Test the first n (<= kBlk) staged candidates against the unit's queries.
+__device__ __forceinline__ void test_block(WalkSmem &S, WalkState &st, const WalkArgs &a, int lane, int n) {
+    const float inf = __int_as_float(0x7f800000);
+    const int nch = (n + 63) >> 6;  // 1 or 2 chunks of 64
+    // this lane's candidates: chunk 0 -> slots (l, l + 32), chunk 1 -> (l + 64, l + 96)
+    float c[4][3];
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int s = 32 * j + lane;
+        const bool real = s < n;
+        c[j][0] = real ? S.cx[s] : inf;
+        c[j][1] = real ? S.cy[s] : inf;
+        c[j][2] = real ? S.cz[s] : inf;
+    }
+    const unsigned long long xa = pk(c[0][0], c[1][0]), ya = pk(c[0][1], c[1][1]), za = pk(c[0][2], c[1][2]);
+    const unsigned long long xb = pk(c[2][0], c[3][0]), yb = pk(c[2][1], c[3][1]), zb = pk(c[2][2], c[3][2]);
+    const int nqp = (st.nq + 1) & ~1;  // padded to even (the pad query never matches)
+    // shared addresses of the query records (one LDS.128 / LDS.128 / LDS.64 per query)
+    const unsigned aq0 = (unsigned)__cvta_generic_to_shared(&S.q0[0]);
+    const unsigned aq1 = (unsigned)__cvta_generic_to_shared(&S.q1[0]);
+    const unsigned aq2 = (unsigned)__cvta_generic_to_shared(&S.q2[0]);
+    float bmin = 2.0f;  // min |d'| over the block's pairs: <= 1 -> some pair is banded
+    if (nch == 2) {
+#pragma unroll 2
+        for (int q = 0; q < nqp; q++) {
+            float4 Q0, Q1;
+            float2 Q2;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(Q0.x), "=f"(Q0.y), "=f"(Q0.z), "=f"(Q0.w) : "r"(aq0 + 16 * q));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(Q1.x), "=f"(Q1.y), "=f"(Q1.z), "=f"(Q1.w) : "r"(aq1 + 16 * q));
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(Q2.x), "=f"(Q2.y) : "r"(aq2 + 8 * q));
+            const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
+                                     kk = pk(Q1.z, Q1.w), cc = pk(Q2.x, Q2.y);
+            unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
+            const unsigned long long da = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
+            dx = f2_sub(xb, qx);
+            dy = f2_sub(yb, qy);
+            dz = f2_sub(zb, qz);
+            const unsigned long long db = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
+            bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(da)), fabsf(hi_f(da))), fminf(fabsf(lo_f(db)), fabsf(hi_f(db)))));
+            const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(da) < 0.0f);
+            const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(da) < 0.0f);
+            const unsigned m2 = __ballot_sync(0xffffffffu, lo_f(db) < 0.0f);
+            const unsigned m3 = __ballot_sync(0xffffffffu, hi_f(db) < 0.0f);
+            if (lane == 0) {
+                S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
+                S.mask[1][q] = ((unsigned long long)m3 << 32) | m2;
+            }
+        }
+    } else {
+#pragma unroll 2
+        for (int q = 0; q < nqp; q++) {
+            float4 Q0, Q1;
+            float2 Q2;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(Q0.x), "=f"(Q0.y), "=f"(Q0.z), "=f"(Q0.w) : "r"(aq0 + 16 * q));
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(Q1.x), "=f"(Q1.y), "=f"(Q1.z), "=f"(Q1.w) : "r"(aq1 + 16 * q));
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(Q2.x), "=f"(Q2.y) : "r"(aq2 + 8 * q));
+            const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
+                                     kk = pk(Q1.z, Q1.w), cc = pk(Q2.x, Q2.y);
+            const unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
+            const unsigned long long da = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
+            bmin = fminf(bmin, fminf(fabsf(lo_f(da)), fabsf(hi_f(da))));
+            const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(da) < 0.0f);
+            const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(da) < 0.0f);
+            if (lane == 0) S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
+        }
+    }
+    const bool band = st.force || bmin <= 1.0f;
+    __syncwarp();
+    if (__any_sync(0xffffffffu, band)) resolve_band(S, a, lane, st.q0, st.nq, n, st.force, st.exact);
+    // self is never its own neighbor (R12); counts; record the masks
+    const int bs = st.nblk * kBlk;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int q = lane + 32 * h;
+        if (q < st.nq) {
+            const int sl = S.self[q] - bs;
+            if (sl >= 0 && sl < n) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
+            st.cnt[h] += __popcll(S.mask[0][q]) + (nch > 1 ? __popcll(S.mask[1][q]) : 0);
+        }
+    }
+    __syncwarp();
+    if (st.rec_ok) {
+        unsigned long long *dst = a.masks + st.mask_base + (long long)(2 * st.nblk) * st.nq;
+        for (int k = 0; k < nch; k++)
+            for (int q = lane; q < st.nq; q += 32) __stcs(&dst[k * st.nq + q], S.mask[k][q]);
+    }
+    st.tests += (long long)n * st.nq;
+    __syncwarp();
+}
+
+// Flattened position p of the current leaf group -> (tree position, leaf offset)
+// for the 32 positions [w0, w0 + 32); `owner` = leaf holding position w0.
+__device__ __forceinline__ void locate(const WalkSmem &S, int nl, int total, int w0, int lane, int &owner, int &pos,
+                                       float4 &of, bool &valid) {
+    const int nxt = owner + 1 + lane;
+    const int stt = (nxt <= nl) ? S.lpre[nxt] : 0x7fffffff;
+    const int off = stt - w0;  // >= 1 for leaves after `owner`
+    const unsigned bits = __reduce_or_sync(0xffffffffu, (off >= 1 && off < 32) ? (1u << off) : 0u);
+    const int mine = owner + __popc(bits & ((2u << lane) - 1u));
+    const unsigned past = __ballot_sync(0xffffffffu, off <= 32);
+    const int p = w0 + lane;
+    valid = p < total;
+    pos = valid ? S.lbeg[mine] + (p - S.lpre[mine]) : 0;
+    of = S.loff[mine];
+    owner += __popc(past);
+}
+
+#ifndef BT_WALK_MIN_BLOCKS
+#define BT_WALK_MIN_BLOCKS 7
+#endif
+__global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(WalkArgs a) {
+    __shared__ WalkSmem smem[kWalkThreads / 32];
+    const int lane = threadIdx.x & 31;
+    WalkSmem &S = smem[threadIdx.x >> 5];
+    const unsigned lt = lanemask_lt();
+    const float inf = __int_as_float(0x7f800000);
+    Slab cs, ms;
+    long long tests = 0, exact = 0, staged = 0, loaded = 0;
+    for (;;) {
+        unsigned long long uid = 0;
+        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK3], 1ull);
+        uid = __shfl_sync(0xffffffffu, uid, 0);
+        if (uid >= (unsigned long long)a.n_units) break;
+        const UnitRun R = a.urun[uid];
+        WalkState st;
+        double c0, c1, c2, E;
+        float blo[3], bhi[3], cull2;
+        int32_t qo[2];
         {
+            UnitGeom G;
+            unit_setup(a, a.units[uid], lane, G);
+            st.q0 = G.q0;
+            st.nq = G.nq;
+            c0 = G.c[0];
+            c1 = G.c[1];
+            c2 = G.c[2];
+            E = G.E;
+            qo[0] = G.qo[0];
+            qo[1] = G.qo[1];
+            const double eps = l4_eps(G.E);
+            bool force = false;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int k = lane + 32 * h;
+                if (k < G.nq) {
+                    const float ax = __double2float_rn(__dsub_rn(G.qx[h], G.c[0]));
+                    const float ay = __double2float_rn(__dsub_rn(G.qy[h], G.c[1]));
+                    const float az = __double2float_rn(__dsub_rn(G.qz[h], G.c[2]));
+                    float A, B, bk, bc;
+                    l4_thresholds(G.qT[h], G.E, eps, a.exact_only != 0, A, B);
+                    band_params(A, B, bk, bc);
+                    force |= bk == 0.0f;
+                    S.q0[k] = make_float4(ax, ax, ay, ay);
+                    S.q1[k] = make_float4(az, az, bk, bk);
+                    S.q2[k] = make_float2(bc, bc);
+                } else {  // padding query: d' = 2 (never a neighbor, never banded)
+                    S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    S.q1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    S.q2[k] = make_float2(2.f, 2.f);
+                }
+                S.self[k] = -1;
+            }
+            st.force = __any_sync(0xffffffffu, force);
             // fp32 images of the query box and the conservative cull radius
             // (R'_u + 4 eps)(1 + 2^-20) (L3 / L4)
-            const double eps = l4_eps(G.E);
             for (int l = 0; l < 3; l++) {
-                st.blo[l] = __double2float_rn(__dsub_rn(G.lo[l], G.c[l]));
-                st.bhi[l] = __double2float_rn(__dsub_rn(G.hi[l], G.c[l]));
+                blo[l] = __double2float_rn(__dsub_rn(G.lo[l], G.c[l]));
+                bhi[l] = __double2float_rn(__dsub_rn(G.hi[l], G.c[l]));
             }
             const double rc = (G.Ru + 4.0 * eps) * (1.0 + 0x1p-20);
             const double rc2 = rc * rc * (1.0 + 0x1p-40);
-            st.cull2 = (rc2 < 3.0e38) ? __double2float_ru(rc2) : __int_as_float(0x7f800000);
+            cull2 = (rc2 < 3.0e38) ? __double2float_ru(rc2) : inf;
         }
-        if (a.root_is_leaf) {
-            queue_leaves(S, st, G, lane, a, lane == 0, 0);
-        } else {
-            // ---- A10: breadth-first descent, all cells of a level flattened over the lanes
-            int32_t *fcur = front_base, *fnext = front_base + a.front_cap;
-            int nf = 1;
-            if (lane == 0) fcur[0] = 0;
+        // record space for the unit: at most `loaded` candidates
+        const long long need_c = R.loaded, need_m = (long long)((R.loaded + 63) >> 6) * st.nq;
+        const bool okc = slab_reserve(cs, need_c, kCandSlab, a.cand_cap, &a.ctr[C_CAND], lane);
+        const bool okm = slab_reserve(ms, need_m, kMaskSlab, a.mask_cap, &a.ctr[C_MASK], lane);
+        st.rec_ok = okc && okm;
+        st.cand_base = cs.cur;
+        st.mask_base = ms.cur;
+        st.nbuf = 0;
+        st.nblk = 0;
+        st.cnt[0] = st.cnt[1] = 0;
+        st.tests = st.exact = 0;
+        __syncwarp();
+        const int nleaf = R.nleaf;
+        const long long list_off = R.list_off;
+        for (int g0 = 0; g0 < nleaf; g0 += kGroup) {
+            // ---- the group's leaves: first position, count, offset of the centre
+            const int gi = g0 + lane;
+            int cnt = 0, beg = 0;
+            float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gi < nleaf) {
+                const int leaf = a.ulist[list_off + gi];
+                beg = a.leaf_begin[leaf];
+                cnt = a.leaf_count[leaf];
+                const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
+                const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
+                // leaf centre (as build.cu computed it) relative to the unit centre; the
+                // compact records are usable when the leaf half-extent H <= 7 E (l4_eps)
+                const double lx = 0.5 * (b0.x + b1.y), ly = 0.5 * (b0.y + b2.x), lz = 0.5 * (b1.x + b2.y);
+                const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
+                off = make_float4(__double2float_rn(__dsub_rn(lx, c0)), __double2float_rn(__dsub_rn(ly, c1)),
+                                  __double2float_rn(__dsub_rn(lz, c2)), (H <= 7.0 * E) ? 1.0f : 0.0f);
+            }
+            int inc = cnt;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(0xffffffffu, inc, d);
+                if (lane >= d) inc += o;
+            }
+            const int total = __shfl_sync(0xffffffffu, inc, 31);
+            const int nl = min(kGroup, nleaf - g0);
+            S.lbeg[lane] = beg;
+            S.lpre[lane] = inc - cnt;
+            S.loff[lane] = off;
+            if (lane == 0) S.lpre[kGroup] = total;
+            const bool mixed = __any_sync(0xffffffffu, gi < nleaf && off.w == 0.0f);
             __syncwarp();
-            while (nf > 0) {
-                int nnext = 0;
-                for (int f0 = 0; f0 < nf; f0 += 32) {
-                    const int fi = f0 + lane;
-                    int b = 0, r0x = 0, r0y = 0, r0z = 0, nx = 1, ny = 1;
-                    long long cb = 0, tot = 0;
-                    if (fi < nf) {
-                        const NodeRec &nd = a.nodes[fcur[fi]];
-                        b = nd.b;
-                        cb = nd.cell_base;
-                        int r0[3], r1[3];
-                        for (int l = 0; l < 3; l++) {
-                            r0[l] = cell_coord(__dsub_rn(G.lo[l], G.Ru), nd.lo[l], nd.ext[l], b);
-                            r1[l] = cell_coord(__dadd_rn(G.hi[l], G.Ru), nd.lo[l], nd.ext[l], b);
+            loaded += total;
+            int owner = 0;
+            for (int p0 = 0; p0 < total; p0 += 64) {
+                float4 r[2], of[2];
+                int pos[2];
+                bool valid[2];
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    locate(S, nl, total, p0 + 32 * h, lane, owner, pos[h], of[h], valid[h]);
+                    r[h] = make_float4(inf, inf, inf, 0.f);
+                    if (!mixed) {
+                        if (valid[h]) r[h] = __ldg(&a.rec32[pos[h]]);
+                    } else if (valid[h]) {
+                        if (of[h].w != 0.0f) {
+                            r[h] = __ldg(&a.rec32[pos[h]]);
+                        } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
+                            const double4 d = a.rec[pos[h]];
+                            r[h] = make_float4(__double2float_rn(__dsub_rn(d.x, c0)),
+                                               __double2float_rn(__dsub_rn(d.y, c1)),
+                                               __double2float_rn(__dsub_rn(d.z, c2)),
+                                               __int_as_float((int)__double_as_longlong(d.w)));
+                            of[h].x = of[h].y = of[h].z = 0.0f;
                         }
-                        r0x = r0[0];
-                        r0y = r0[1];
-                        r0z = r0[2];
-                        nx = r1[0] - r0[0] + 1;
-                        ny = r1[1] - r0[1] + 1;
-                        tot = (long long)nx * ny * (r1[2] - r0[2] + 1);
-                    }
-                    // inclusive scan of the cell counts over the lanes
-                    long long inc = tot;
-                    for (int d = 1; d < 32; d <<= 1) {
-                        long long o = __shfl_up_sync(0xffffffffu, inc, d);
-                        if (lane >= d) inc += o;
-                    }
-                    const long long start = inc - tot;
-                    const long long T = __shfl_sync(0xffffffffu, inc, 31);
-                    int owner = 0;
-                    for (long long c0 = 0; c0 < T; c0 += 32) {
-                        // owner lane of cell g = c0 + lane (node starts inside the window)
-                        const long long off = start - c0;
-                        const unsigned bits =
-                            __reduce_or_sync(0xffffffffu, (lane > owner && off >= 1 && off < 32) ? (1u << off) : 0u);
-                        const int o = owner + __popc(bits & ((2u << lane) - 1u));
-                        const unsigned past = __ballot_sync(0xffffffffu, lane > owner && off <= 32);
-                        const int ob = __shfl_sync(0xffffffffu, b, o);
-                        const long long ocb = __shfl_sync(0xffffffffu, cb, o);
-                        const int ox = __shfl_sync(0xffffffffu, r0x, o), oy = __shfl_sync(0xffffffffu, r0y, o),
-                                  oz = __shfl_sync(0xffffffffu, r0z, o);
-                        const int onx = __shfl_sync(0xffffffffu, nx, o), ony = __shfl_sync(0xffffffffu, ny, o);
-                        const long long ostart = __shfl_sync(0xffffffffu, start, o);
-                        owner += __popc(past);
-                        const long long g = c0 + lane;
-                        bool is_leaf = false, is_node = false;
-                        int32_t code = -1;
-                        if (g < T) {
-                            const int local = (int)(g - ostart);
-                            const int cx = ox + local % onx;
-                            const int cy = oy + (local / onx) % ony;
-                            const int cz = oz + local / (onx * ony);
-                            const long long j = cx + (long long)cy * ob + (long long)cz * ob * ob;  // Eq. 3
-                            code = a.cells[ocb + j];
-                            is_leaf = code >= 0;
-                            is_node = code <= -2;
-                        }
-                        const unsigned nm = __ballot_sync(0xffffffffu, is_node);
-                        if (is_node) fnext[nnext + __popc(nm & lt)] = code_node(code);
-                        nnext += __popc(nm);
-                        queue_leaves(S, st, G, lane, a, is_leaf, code);
                     }
                 }
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
+                    // conservative fp32 Minkowski cull against the query box (L3 / L4)
+                    const float ax = __fadd_rn(r[h].x, of[h].x);
+                    const float ay = __fadd_rn(r[h].y, of[h].y);
+                    const float az = __fadd_rn(r[h].z, of[h].z);
+                    const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(blo[0], ax), __fsub_rn(ax, bhi[0])));
+                    const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(blo[1], ay), __fsub_rn(ay, bhi[1])));
+                    const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(blo[2], az), __fsub_rn(az, bhi[2])));
+                    const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
+                    const bool keep = valid[h] && g2 < cull2;
+                    const unsigned km = __ballot_sync(0xffffffffu, keep);
+                    if (keep) {
+                        const int slot = st.nbuf + __popc(km & lt);
+                        S.cx[slot] = ax;
+                        S.cy[slot] = ay;
+                        S.cz[slot] = az;
+                        S.tpos[slot] = pos[h];
+                        const int us = st.nblk * kBlk + slot;  // slot within the unit
+                        if (st.rec_ok) __stcs(&a.cands[st.cand_base + us], __float_as_int(r[h].w));
+                        if ((unsigned)(pos[h] - st.q0) < (unsigned)st.nq) S.self[pos[h] - st.q0] = us;
+                    }
+                    st.nbuf += __popc(km);
+                }
                 __syncwarp();
-                int32_t *tmp = fcur;
-                fcur = fnext;
-                fnext = tmp;
-                nf = nnext;
+                if (st.nbuf >= kBlk) {
+                    test_block(S, st, a, lane, kBlk);
+                    st.nblk++;
+                    // move the overflow (< 64) to the front of the buffer
+                    const int rest = st.nbuf - kBlk;
+                    for (int i = lane; i < rest; i += 32) {
+                        S.cx[i] = S.cx[kBlk + i];
+                        S.cy[i] = S.cy[kBlk + i];
+                        S.cz[i] = S.cz[kBlk + i];
+                        S.tpos[i] = S.tpos[kBlk + i];
+                    }
+                    st.nbuf = rest;
+                    __syncwarp();
+                }
             }
         }
-        if (st.nleaf > 0) stage_leaves(S, st, G, lane, a);
-        close_block(st, lane, a);
-        staged += st.staged;
-        loaded += st.loaded;
+        if (st.nbuf > 0) test_block(S, st, a, lane, st.nbuf);
+        const int nstaged = st.nblk * kBlk + st.nbuf;
+        if (lane < st.nq) a.counts[qo[0]] = st.cnt[0];
+        if (lane + 32 < st.nq) a.counts[qo[1]] = st.cnt[1];
+        if (lane == 0) {
+            UnitRun &W = a.urun[uid];
+            W.cand_base = st.cand_base;
+            W.mask_base = st.mask_base;
+            W.nstaged = nstaged;
+            W.ok = st.rec_ok ? 1 : 0;
+        }
+        cs.cur += nstaged;
+        ms.cur += (long long)((nstaged + 63) >> 6) * st.nq;
+        tests += st.tests;
+        exact += st.exact;
+        staged += nstaged;
         __syncwarp();
     }
     if (lane == 0) {
+        atomicAdd((unsigned long long *)&a.ctr[C_TESTS], (unsigned long long)tests);
+        atomicAdd((unsigned long long *)&a.ctr[C_EXACT], (unsigned long long)exact);
         atomicAdd((unsigned long long *)&a.ctr[C_STAGED], (unsigned long long)staged);
         atomicAdd((unsigned long long *)&a.ctr[C_LOADED], (unsigned long long)loaded);
     }
 }
 
 // ---------------------------------------------------------------------------
-// test_kernel
-// ---------------------------------------------------------------------------
-struct TestSmem {
-    float4 q0[kQ];                         // ax, ax, ay, ay  (fp32, relative to the unit centre)
-    float4 q1[kQ];                         // az, az, A, B    (certain-accept / certain-reject)
-    unsigned long long mask[kChunks][kQ];  // neighbor masks of the block
-};
-
-// The exact band of lemma L4 (rare): redo the block's pairs and let the fp64
-// predicate itself decide every pair with A <= s32 < B.
-__device__ __noinline__ void resolve_band(TestSmem &S, const UnitGeom &G, int lane, const WalkArgs &a,
-                                          const Batch &B, int nch, long long &exact) {
-    for (int k = 0; k < nch; k++) {
-        const int s0 = 64 * k + lane, s1 = s0 + 32;
-        const float inf = __int_as_float(0x7f800000);
-        float4 c0 = make_float4(inf, inf, inf, __int_as_float(-1)), c1 = c0;
-        if (s0 < B.ncand) c0 = a.cand4[B.cand_base + s0];
-        if (s1 < B.ncand) c1 = a.cand4[B.cand_base + s1];
-        const unsigned long long cx = pk(c0.x, c1.x), cy = pk(c0.y, c1.y), cz = pk(c0.z, c1.z);
-        const int cp0 = __float_as_int(c0.w), cp1 = __float_as_int(c1.w);
-        for (int q = 0; q < G.nq; q++) {
-            const float4 Q0 = S.q0[q], Q1 = S.q1[q];
-            const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
-            const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
-            const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
-            unsigned long long s = f2_mul(dx, dx);
-            s = f2_fma(dy, dy, s);
-            s = f2_fma(dz, dz, s);
-            const float v0 = __uint_as_float((unsigned)s), v1 = __uint_as_float((unsigned)(s >> 32));
-            const bool u0 = !(v0 < Q1.z) && v0 < Q1.w, u1 = !(v1 < Q1.z) && v1 < Q1.w;
-            if (!__any_sync(0xffffffffu, u0 || u1)) continue;
-            const int qp = G.q0 + q;
-            const double4 Qr = a.rec[qp];
-            const double t = __dmul_rn(2.0, a.h_tree[qp]);
-            const double T = __dmul_rn(t, t);
-            bool e0 = false, e1 = false;
-            if (u0) e0 = cp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp0]);
-            if (u1) e1 = cp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[cp1]);
-            const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
-            if (lane == 0) S.mask[k][q] |= ((unsigned long long)m1 << 32) | m0;
-            exact += __popc(__ballot_sync(0xffffffffu, u0)) + __popc(__ballot_sync(0xffffffffu, u1));
-            __syncwarp();
-        }
-    }
-    __syncwarp();
-}
-
-__global__ void __launch_bounds__(kTestThreads, 6) test_kernel(WalkArgs a) {
-    __shared__ TestSmem smem[kTestThreads / 32];
-    const int lane = threadIdx.x & 31;
-    TestSmem &S = smem[threadIdx.x >> 5];
-    long long tests = 0, exact = 0;
-    const float inf = __int_as_float(0x7f800000);
-    for (;;) {
-        unsigned long long uid = 0;
-        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK3], 1ull);
-        uid = __shfl_sync(0xffffffffu, uid, 0);
-        if (uid >= (unsigned long long)a.n_units) break;
-        UnitGeom G;
-        unit_setup(a, a.units[uid], lane, G);
-        const int nq = G.nq;
-        long long self[2] = {-1, -1};
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int k = lane + 32 * h;
-            if (k < nq) {
-                const float ax = __double2float_rn(__dsub_rn(G.qx[h], G.c[0]));
-                const float ay = __double2float_rn(__dsub_rn(G.qy[h], G.c[1]));
-                const float az = __double2float_rn(__dsub_rn(G.qz[h], G.c[2]));
-                float A, B;
-                l4_thresholds(G.qT[h], G.E, l4_eps(G.E), a.exact_only != 0, A, B);
-                S.q0[k] = make_float4(ax, ax, ay, ay);
-                S.q1[k] = make_float4(az, az, A, B);
-                self[h] = a.self_slot[G.q0 + k];
-            } else {
-                S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                S.q1[k] = make_float4(0.f, 0.f, 0.f, 0.f);  // A = B = 0: never a neighbor
-            }
-        }
-        int cnt[2] = {0, 0};
-        __syncwarp();
-        // candidate chunk k of block B (padding slots: +inf, s32 = +inf)
-        auto load_chunk = [&](const Batch &Bk, int k, float4 &c0, float4 &c1) {
-            const int s0 = 64 * k + lane, s1 = s0 + 32;
-            c0 = make_float4(inf, inf, inf, 0.f);
-            c1 = c0;
-            if (s0 < Bk.ncand) c0 = __ldcs(&a.cand4[Bk.cand_base + s0]);
-            if (s1 < Bk.ncand) c1 = __ldcs(&a.cand4[Bk.cand_base + s1]);
-        };
-        int b = a.head[uid];
-        Batch B{-1, 0, 0, -1};
-        float4 p0, p1;  // prefetched next chunk
-        if (b >= 0) {
-            B = a.batches[b];
-            load_chunk(B, 0, p0, p1);
-        }
-        while (b >= 0) {
-            const int nch = (B.ncand + 63) >> 6;
-            Batch Bn{-1, 0, 0, -1};
-            if (B.next >= 0) Bn = a.batches[B.next];
-            // Hot loop, branch free: certain accepts (s32 < A) go into the masks;
-            // the ballots of s32 < B are compared with them, and any difference
-            // (a pair in the band [A, B) of lemma L4) is resolved afterwards by
-            // the fp64 predicate.  Queries are padded to a multiple of 4.
-            unsigned diff = 0;
-            for (int k = 0; k < nch; k++) {
-                const float4 c0 = p0, c1 = p1;
-                // prefetch the following chunk (this block's next, or the next block's first)
-                if (k + 1 < nch) load_chunk(B, k + 1, p0, p1);
-                else if (B.next >= 0) load_chunk(Bn, 0, p0, p1);
-                const unsigned long long cx = pk(c0.x, c1.x), cy = pk(c0.y, c1.y), cz = pk(c0.z, c1.z);
-                unsigned long long *mrow = &S.mask[k][0];
-                for (int q = 0; q < nq; q += 4) {
-#pragma unroll
-                    for (int i = 0; i < 4; i++) {
-                        const float4 Q0 = S.q0[q + i], Q1 = S.q1[q + i];
-                        const unsigned long long dx = f2_sub(cx, pk(Q0.x, Q0.y));
-                        const unsigned long long dy = f2_sub(cy, pk(Q0.z, Q0.w));
-                        const unsigned long long dz = f2_sub(cz, pk(Q1.x, Q1.y));
-                        unsigned long long s = f2_mul(dx, dx);
-                        s = f2_fma(dy, dy, s);
-                        s = f2_fma(dz, dz, s);
-                        const float v0 = __uint_as_float((unsigned)s), v1 = __uint_as_float((unsigned)(s >> 32));
-                        const unsigned m0 = __ballot_sync(0xffffffffu, v0 < Q1.z);
-                        const unsigned m1 = __ballot_sync(0xffffffffu, v1 < Q1.z);
-                        const unsigned n0 = __ballot_sync(0xffffffffu, v0 < Q1.w);
-                        const unsigned n1 = __ballot_sync(0xffffffffu, v1 < Q1.w);
-                        diff |= (n0 ^ m0) | (n1 ^ m1);
-                        if (lane == 0) mrow[q + i] = ((unsigned long long)m1 << 32) | m0;
-                    }
-                }
-            }
-            __syncwarp();
-            if (diff) resolve_band(S, G, lane, a, B, nch, exact);
-            // self is never its own neighbor (R12); counts
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int q = lane + 32 * h;
-                if (q < nq) {
-                    const long long sl = self[h] - B.cand_base;
-                    if (sl >= 0 && sl < 64 * nch) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
-                    int c = 0;
-                    for (int k = 0; k < nch; k++) c += __popcll(S.mask[k][q]);
-                    cnt[h] += c;
-                }
-            }
-            // record the masks for the fill pass
-            long long mb = 0;
-            if (lane == 0) mb = atomicAdd((unsigned long long *)&a.ctr[C_MASK], (unsigned long long)(nch * nq));
-            mb = __shfl_sync(0xffffffffu, mb, 0);
-            __syncwarp();
-            if (mb + (long long)nch * nq <= a.mask_cap) {
-                for (int w = lane; w < nch * nq; w += 32) __stcs(&a.masks[mb + w], S.mask[w / nq][w % nq]);
-                if (lane == 0) a.batches[b].mask_base = mb;
-            }
-            tests += (long long)B.ncand * nq;
-            __syncwarp();
-            b = B.next;
-            B = Bn;
-        }
-        if (lane < nq) a.counts[G.qo[0]] = cnt[0];
-        if (lane + 32 < nq) a.counts[G.qo[1]] = cnt[1];
-        __syncwarp();
-    }
-    if (lane == 0) {
-        atomicAdd((unsigned long long *)&a.ctr[C_TESTS], (unsigned long long)tests);
-        atomicAdd((unsigned long long *)&a.ctr[C_EXACT], (unsigned long long)exact);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Fill pass: replay the recorded masks into the CSR rows.  Per unit and batch
-// the candidate indices and masks are staged in shared memory; for each
-// (chunk, query) mask word, lane l owns candidates 64k + l and 64k + 32 + l,
-// and __popc(mask & lanemask_lt) gives its slot in the query's row (row order
-// unspecified, R15).  The next write position of each query lives in shared
-// memory.
+// Fill pass: replay the recorded masks into the CSR rows.  Per unit, rounds
+// of up to 4 chunks: the chunks' candidate indices in registers (chunk k,
+// lane l -> slots 64k + l, 64k + 32 + l), their masks in shared memory; for
+// each (query, chunk) mask word __popc(mask & lanemask_lt) gives each
+// neighbor's slot in the query's row (row order unspecified, R15).
 // ---------------------------------------------------------------------------
 constexpr int kFillWarps = kFillThreads / 32;
 
 struct FillSmem {
-    int32_t *row[kQ];                          // next write address of each query's row
-    unsigned long long mask[kChunks * kQ];     // the block's masks, [k][q]
+    int32_t *row[kQ];                            // next write address of each query's row
+    unsigned long long mask[kFillChunks * kQ];   // the round's masks, [k][q]
 };
 
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
@@ -739,28 +904,30 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
         u = __shfl_sync(0xffffffffu, u, 0);
         if (u >= (unsigned long long)a.n_units) break;
         const int4 U = a.units[u];
+        const UnitRun R = a.urun[u];
         const int nq = U.z;
+        const int nchk = (R.nstaged + 63) >> 6;
         for (int q = lane; q < nq; q += 32)
             F.row[q] = a.nbr + a.offsets[(int32_t)__double_as_longlong(a.rec[U.y + q].w)];
-        for (int b = a.head[u]; b >= 0;) {
-            const Batch B = a.batches[b];
-            const int nch = (B.ncand + 63) >> 6;
-            // the block's candidates in registers: chunk k, lane l -> slots 64k + l, 64k + 32 + l
-            int32_t c0[kChunks], c1[kChunks];
+        for (int kk0 = 0; kk0 < nchk; kk0 += kFillChunks) {
+            const int nk = min(kFillChunks, nchk - kk0);
+            int32_t c0[kFillChunks], c1[kFillChunks];
 #pragma unroll
-            for (int k = 0; k < kChunks; k++) {
-                c0[k] = (k < nch) ? __ldcs(&cands[B.cand_base + 64 * k + lane]) : -1;
-                c1[k] = (k < nch) ? __ldcs(&cands[B.cand_base + 64 * k + 32 + lane]) : -1;
+            for (int k = 0; k < kFillChunks; k++) {
+                const int s0 = 64 * (kk0 + k) + lane, s1 = s0 + 32;
+                c0[k] = (k < nk && s0 < R.nstaged) ? __ldcs(&cands[R.cand_base + s0]) : -1;
+                c1[k] = (k < nk && s1 < R.nstaged) ? __ldcs(&cands[R.cand_base + s1]) : -1;
             }
             __syncwarp();
-            for (int w = lane; w < nch * nq; w += 32) F.mask[w] = __ldcs(&masks[B.mask_base + w]);
+            const unsigned long long *src = masks + R.mask_base + (long long)kk0 * nq;
+            for (int w = lane; w < nk * nq; w += 32) F.mask[w] = __ldcs(&src[w]);
             __syncwarp();
             for (int q = 0; q < nq; q++) {
                 int32_t *dst = F.row[q];
                 int wrote = 0;
 #pragma unroll
-                for (int k = 0; k < kChunks; k++) {
-                    if (k >= nch) break;
+                for (int k = 0; k < kFillChunks; k++) {
+                    if (k >= nk) break;
                     const unsigned long long m = F.mask[k * nq + q];
                     if (m == 0ull) continue;
                     const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
@@ -774,7 +941,6 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
                 if (lane == 0 && wrote) F.row[q] = dst;
             }
             __syncwarp();
-            b = B.next;
         }
     }
 }
@@ -851,14 +1017,11 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
         return (unsigned)(sms * std::max(per_sm, 1));
     };
-    const unsigned grid_g = grid_of((const void *)gather_kernel, kGatherThreads);
-    const unsigned grid_t = grid_of((const void *)test_kernel, kTestThreads);
+    const unsigned grid_d = grid_of((const void *)desc_kernel<false>, kDescThreads);
+    const unsigned grid_w = grid_of((const void *)walk_kernel, kWalkThreads);
     const unsigned grid_f = grid_of((const void *)fill_kernel, kFillThreads);
-    // frontier scratch: a unit's frontier holds each internal node at most once
-    const int64_t front_cap = std::max<int64_t>(t.n_nodes, 1);
-    t.front.reserve((int64_t)grid_g * (kGatherThreads / 32) * 2 * front_cap, 0);
-    t.head.reserve(t.n_units, 0);
-    t.self_slot.reserve(n, 0);
+    const unsigned grid_big = (unsigned)std::min(sms, 32);  // big-unit pass (rare units)
+    t.urun.reserve(t.n_units, 0);
 
     // the recorded masks of a previous test pass are reused by a fill-only
     // call when the tree, h pointer, exactness mode and h checksum all match
@@ -879,13 +1042,10 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     a.M = t.M;
     a.root_is_leaf = t.root_is_leaf ? 1 : 0;
     a.exact_only = g_exact_only;
-    a.front = t.front.p;
-    a.front_cap = front_cap;
+    a.urun = t.urun.p;
     a.offsets = offsets;
     a.nbr = nbr_idx;
     a.ctr = (long long *)t.counters.p;
-    a.head = t.head.p;
-    a.self_slot = (long long *)t.self_slot.p;
 
     auto read_counters = [&](long long *hc) {
         read_back({{t.counters.p, hc, C_N * sizeof(long long)}});
@@ -900,60 +1060,67 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             cnt = tmp_counts.p;
         }
         a.counts = cnt;
-        // arena sized from the previous run on this thread (grown on overflow)
-        static thread_local double cand_per_q = 32.0, batch_per_unit = 3.0, mask_per_q = 12.0;
+        // leaf-list arena: estimated (grown and redone on overflow); candidate
+        // and mask arenas: exact bounds from the descent (no overflow)
+        double list_per_unit = 96.0;
         long long hc[C_N];
         t.rec_valid = false;
-        for (int attempt = 0;; attempt++) {  // A10: gather
-            t.arena_cand4.reserve((long long)(cand_per_q * n) + 4096, 0);
-            t.arena_cands.reserve(t.arena_cand4.n, 0);
-            t.arena_batches.reserve((long long)(batch_per_unit * t.n_units) + 1024, 0);
-            a.cand4 = t.arena_cand4.p;
-            a.cands = t.arena_cands.p;
-            a.cand_cap = (long long)std::min(t.arena_cand4.n, t.arena_cands.n);
-            a.batches = t.arena_batches.p;
-            a.batch_cap = (long long)t.arena_batches.n;
-            for (int c : {C_WORK, C_CAND, C_BATCH, C_STAGED, C_LOADED}) zero(c);
+        const long long warps_d = (long long)grid_d * (kDescThreads / 32);
+        const long long warps_w = (long long)grid_w * (kWalkThreads / 32);
+        for (int attempt = 0;; attempt++) {  // A10: candidate-leaf lists
+            t.ulist.reserve((long long)(list_per_unit * t.n_units) + warps_d * kListSlab, 0);
+            a.ulist = t.ulist.p;
+            a.list_cap = (long long)t.ulist.n;
+            for (int c : {C_WORK, C_LIST, C_BIG, C_WORK4, C_NEEDC, C_NEEDM}) zero(c);
             {
-                Phase ph("search.gather");
-                gather_kernel<<<grid_g, kGatherThreads, 0, st>>>(a);
-                BT_LAUNCH("walk_gather");
+                Phase ph("search.desc");
+                desc_kernel<false><<<grid_d, kDescThreads, 0, st>>>(a);
+                BT_LAUNCH("walk_desc");
             }
             read_counters(hc);
-            cand_per_q = std::max(cand_per_q, 1.1 * (double)hc[C_CAND] / (double)n);
-            batch_per_unit =
-                std::max(batch_per_unit, 1.1 * (double)hc[C_BATCH] / (double)std::max<int64_t>(1, t.n_units));
-            if (hc[C_CAND] <= a.cand_cap && hc[C_BATCH] <= a.batch_cap) break;
-            if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: candidate arena does not converge");
+            t.big_units = hc[C_BIG];
+            if (hc[C_BIG] > 0 && hc[C_LIST] <= a.list_cap) {
+                // units beyond the shared-memory frontier / list reserve
+                t.front.reserve((long long)grid_big * (kDescThreads / 32) * 2 * std::max<int64_t>(t.n_nodes, 1), 0);
+                a.front = t.front.p;
+                a.front_cap = std::max<int64_t>(t.n_nodes, 1);
+                Phase ph("search.desc_big");
+                desc_kernel<true><<<grid_big, kDescThreads, 0, st>>>(a);
+                BT_LAUNCH("walk_desc_big");
+                read_counters(hc);
+            }
+            if (hc[C_LIST] <= a.list_cap) break;
+            list_per_unit = 1.25 * (double)hc[C_LIST] / (double)std::max<int64_t>(1, t.n_units);
+            if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: leaf-list arena does not converge");
         }
-        t.staged = hc[C_STAGED];
-        t.loaded = hc[C_LOADED];
-        t.cand_slots = hc[C_CAND];
-        for (int attempt = 0;; attempt++) {  // A11: pair tests, counts, masks
-            t.arena_masks.reserve((long long)(mask_per_q * n) + 4096, 0);
+        t.list_entries = hc[C_LIST];
+        {  // A10 staging + A11 pair tests, counts, masks
+            t.arena_cands.reserve(hc[C_NEEDC] + warps_w * kCandSlab, 0);
+            t.arena_masks.reserve(hc[C_NEEDM] + warps_w * kMaskSlab, 0);
+            a.cands = t.arena_cands.p;
+            a.cand_cap = (long long)t.arena_cands.n;
             a.masks = t.arena_masks.p;
             a.mask_cap = (long long)t.arena_masks.n;
-            for (int c : {C_WORK3, C_MASK, C_TESTS, C_EXACT}) zero(c);
+            for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero(c);
             {
                 Phase ph("search.count");
-                test_kernel<<<grid_t, kTestThreads, 0, st>>>(a);
+                walk_kernel<<<grid_w, kWalkThreads, 0, st>>>(a);
                 BT_LAUNCH("walk_test");
             }
             read_counters(hc);
-            mask_per_q = std::max(mask_per_q, 1.1 * (double)hc[C_MASK] / (double)n);
-            const bool fits = hc[C_MASK] <= a.mask_cap;
-            if (fits || !fill_pass || nbr_idx == nullptr) {
-                t.rec_valid = fits;
-                t.rec_h = h;
-                t.rec_hsum = hsum;
-                t.rec_exact = g_exact_only;
-                break;
-            }
-            if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: mask arena does not converge");
+            const bool fits = hc[C_CAND] <= a.cand_cap && hc[C_MASK] <= a.mask_cap;
+            if (!fits) throw Error(BT_ERR_CUDA, "bt_find_neighbors: internal: walk arena bound exceeded");
+            t.rec_valid = true;
+            t.rec_h = h;
+            t.rec_hsum = hsum;
+            t.rec_exact = g_exact_only;
         }
+        t.staged = hc[C_STAGED];
+        t.loaded = hc[C_LOADED];
         t.tests = hc[C_TESTS];
         t.exact_tests = hc[C_EXACT];
         t.mask_words = hc[C_MASK];
+        t.cand_slots = hc[C_CAND];
         if (count_pass) {
             DBuf<long long> dtot(1);
             Phase ph("search.scan");
@@ -977,7 +1144,6 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     if (!t.rec_valid) throw Error(BT_ERR_CUDA, "bt_find_neighbors: internal: no recorded test pass");
     a.masks = t.arena_masks.p;
     a.cands = t.arena_cands.p;
-    a.batches = t.arena_batches.p;
     zero(C_WORK2);
     {
         Phase ph("search.fill");
