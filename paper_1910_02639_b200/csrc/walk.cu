@@ -483,9 +483,9 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
 // walk_kernel: staging + pair tests (A10, A11)
 // ---------------------------------------------------------------------------
 struct WalkSmem {
-    float4 q0[kQ];                  // ax, ax, ay, ay  (fp32, relative to the unit centre)
-    float4 q1[kQ];                  // az, az, k, k   (band map d' = s k + c)
-    float2 q2[kQ];                  // c, c
+    float4 q0[kQ + 1];              // ax, ax, ay, ay  (fp32, relative to the unit centre)
+    float4 q1[kQ + 1];              // az, az, k, k   (band map d' = s k + c); [kQ]: look-ahead pad
+    float2 q2[kQ + 1];              // c, c
     int self[kQ];                   // unit slot of each query's own record (-1: none)
     float cx[kBuf], cy[kBuf], cz[kBuf];
     int tpos[kBuf];                 // tree position of each staged candidate
@@ -584,16 +584,23 @@ __device__ __forceinline__ void test_block(WalkSmem &S, WalkState &st, const Wal
     const unsigned aq1 = (unsigned)__cvta_generic_to_shared(&S.q1[0]);
     const unsigned aq2 = (unsigned)__cvta_generic_to_shared(&S.q2[0]);
     float bmin = 2.0f;  // min |d'| over the block's pairs: <= 1 -> some pair is banded
+    // query records, loaded one query ahead of their use (LDS latency)
+    auto ldq = [&](int q, float4 &Q0, float4 &Q1, float2 &Q2) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(Q0.x), "=f"(Q0.y), "=f"(Q0.z), "=f"(Q0.w) : "r"(aq0 + 16 * q));
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(Q1.x), "=f"(Q1.y), "=f"(Q1.z), "=f"(Q1.w) : "r"(aq1 + 16 * q));
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(Q2.x), "=f"(Q2.y) : "r"(aq2 + 8 * q));
+    };
+    float4 N0, N1;
+    float2 N2;
+    ldq(0, N0, N1, N2);
     if (nch == 2) {
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
-            float4 Q0, Q1;
-            float2 Q2;
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(Q0.x), "=f"(Q0.y), "=f"(Q0.z), "=f"(Q0.w) : "r"(aq0 + 16 * q));
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(Q1.x), "=f"(Q1.y), "=f"(Q1.z), "=f"(Q1.w) : "r"(aq1 + 16 * q));
-            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(Q2.x), "=f"(Q2.y) : "r"(aq2 + 8 * q));
+            const float4 Q0 = N0, Q1 = N1;
+            const float2 Q2 = N2;
+            ldq(q + 1, N0, N1, N2);  // q + 1 <= nqp <= 64: within the padded arrays
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
                                      kk = pk(Q1.z, Q1.w), cc = pk(Q2.x, Q2.y);
             unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
@@ -615,13 +622,9 @@ __device__ __forceinline__ void test_block(WalkSmem &S, WalkState &st, const Wal
     } else {
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
-            float4 Q0, Q1;
-            float2 Q2;
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(Q0.x), "=f"(Q0.y), "=f"(Q0.z), "=f"(Q0.w) : "r"(aq0 + 16 * q));
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(Q1.x), "=f"(Q1.y), "=f"(Q1.z), "=f"(Q1.w) : "r"(aq1 + 16 * q));
-            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(Q2.x), "=f"(Q2.y) : "r"(aq2 + 8 * q));
+            const float4 Q0 = N0, Q1 = N1;
+            const float2 Q2 = N2;
+            ldq(q + 1, N0, N1, N2);
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
                                      kk = pk(Q1.z, Q1.w), cc = pk(Q2.x, Q2.y);
             const unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
