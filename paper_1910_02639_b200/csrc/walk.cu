@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kQ = 64;           // queries per unit (== build.cu kUnitQ)
 constexpr int kBlk = 128;        // staged candidates per test block
-constexpr int kBuf = kBlk + 64;  // staging buffer: a block + one staging step
+constexpr int kBuf = kBlk + 32;  // staging buffer: a block + one staging window
 constexpr int kGroup = 32;       // candidate leaves per staging group (one per lane)
 constexpr int kFrontCap = 128;   // shared-memory descent frontier per level
 constexpr int kDescThreads = 128;
@@ -144,6 +144,19 @@ __device__ __forceinline__ float4 lds4(const float4 *p) {
     return v;
 }
 
+__device__ __forceinline__ float4 lds4v(const float4 *p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+__device__ __forceinline__ int2 lds2iv(const int *p) {
+    int2 v;
+    asm volatile("ld.shared.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+
 // Exact predicate (the definition): ((dx*dx + dy*dy) + dz*dz) < T, fp64, no FMA.
 __device__ __forceinline__ bool exact_pair(double qx, double qy, double qz, double T, const double4 &c) {
     double dx = __dsub_rn(qx, c.x), dy = __dsub_rn(qy, c.y), dz = __dsub_rn(qz, c.z);
@@ -190,19 +203,20 @@ __device__ __forceinline__ void l4_thresholds(double T, double E, double eps, bo
 }
 
 // The band [A, B) as one fused multiply-add: fp32
-// A <= Mid <= B, HW >= max(Mid - A, B - Mid), k = the largest power of two
-// <= 1/HW and c = -Mid k (exact: a power-of-two scaling), so the hot loop's
-// d' = fl32(s k + c) = k fl32(s - Mid).  Then
+// A <= Mid <= B, HW >= max(Mid - A, B - Mid), k = a power of two <= 1/HW
+// (per query the largest; a unit uses the minimum over its queries, which
+// only widens the band) and c = -Mid k (exact: a power-of-two scaling), so
+// the hot loop's d' = fl32(s k + c) = k fl32(s - Mid).  Then
 //   s in [A, B)  =>  |s - Mid| <= HW <= 1/k  =>  |d'| <= 1
 // (round-to-nearest is monotone and 1/k is representable), so a pair with
 // |d'| > 1 is certain, and for it d' < 0 <=> s < Mid <=> s < A (a neighbor).
 // k = c = 0 (B = +inf: exact-only) bands every pair ("force": the fp64
 // predicate decides everything, also pairs whose fp32 arithmetic overflowed).
-__device__ __forceinline__ void band_params(float A, float B, float &k, float &c) {
+__device__ __forceinline__ void band_params(float A, float B, float &k, float &Mid) {
     k = 0.0f;
-    c = 0.0f;
+    Mid = 0.0f;
     if (!(B < __int_as_float(0x7f800000))) return;
-    float Mid = __double2float_rn(0.5 * ((double)A + (double)B));
+    Mid = __double2float_rn(0.5 * ((double)A + (double)B));
     Mid = fmaxf(A, fminf(B, Mid));
     // half-width: exact difference of fp32 values rounded up, widened to
     // >= 2^-23 Mid and >= 1e-30 (keeps Mid k <= 2^23 and k <= 2^100)
@@ -211,7 +225,6 @@ __device__ __forceinline__ void band_params(float A, float B, float &k, float &c
     int e;
     frexp(1.0 / (double)HW, &e);  // 1/HW = f 2^e, f in [0.5, 1)
     k = ldexpf(1.0f, e - 1);      // largest power of two <= 1/HW
-    c = -Mid * k;                 // exact
 }
 
 // ---------------------------------------------------------------------------
@@ -482,28 +495,29 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
 // ---------------------------------------------------------------------------
 // walk_kernel: staging + pair tests (A10, A11)
 // ---------------------------------------------------------------------------
-struct WalkSmem {
-    float4 q0[kQ + 1];              // ax, ax, ay, ay  (fp32, relative to the unit centre)
-    float4 q1[kQ + 1];              // az, az, k, k   (band map d' = s k + c); [kQ]: look-ahead pad
-    float2 q2[kQ + 1];              // c, c
-    int self[kQ];                   // unit slot of each query's own record (-1: none)
-    float cx[kBuf], cy[kBuf], cz[kBuf];
-    int tpos[kBuf];                 // tree position of each staged candidate
-    unsigned long long mask[2][kQ]; // the block's neighbor masks [chunk][query]
-    int lbeg[kGroup];               // group leaves: first tree position
-    int lpre[kGroup + 1];           // group leaves: exclusive prefix of counts
-    float4 loff[kGroup];            // group leaves: fl32(c_leaf - c), w = 1 compact / 0 fp64 records
+struct UnitSm {                     // per-warp unit state (shared memory)
+    long long cand_base, mask_base;  // the unit's record bases
+    Slab cs, ms;                     // the warp's candidate / mask slabs
+    long long tests, exact, staged, loaded;  // warp totals
+    double c[3], E;                  // unit centre, coordinate bound (L4)
+    float4 box0, box1;               // fp32 query box relative to c: (lo xyz, cull2), (hi xyz, -)
+    int q0, nq;                      // (8-byte aligned: read as one int2)
+    float k;                         // band scale of the unit (power of two; 0: force)
+    int nblk, rec_ok, force;
 };
 
-struct WalkState {
-    int q0, nq;
-    int nbuf;       // candidates in the staging buffer
-    int nblk;       // blocks tested
-    long long cand_base, mask_base;
-    bool rec_ok;
-    int cnt[2];     // counts of this lane's queries (lane, lane + 32)
-    long long tests, exact;
-    bool force;     // some query has k = 0: every pair goes to the fp64 predicate
+struct WalkSmem {
+    float4 q0[kQ + 1];              // ax, ax, ay, ay  (fp32, relative to the unit centre)
+    float4 q1[kQ + 1];              // az, az, c, c   (band map d' = s k + c); [kQ]: look-ahead pad
+    short self[kQ];                 // unit slot of each query's own record (-1: none)
+    float cx[kBuf], cy[kBuf], cz[kBuf];
+    int tpos[kBuf];                 // tree position of each staged candidate
+    int cidx[kBuf];                 // caller index of each staged candidate
+    unsigned long long mask[2][kQ]; // the block's neighbor masks [chunk][query]
+    int ldel[kGroup];               // group leaves: first tree position - exclusive prefix of counts
+    int lpre[kGroup + 1];           // group leaves: exclusive prefix of counts
+    float4 loff[kGroup];            // group leaves: fl32(c_leaf - c), w = 1 compact / 0 fp64 records
+    UnitSm u;
 };
 
 // The exact band of lemma L4 (rare): recompute the block's pairs with the
@@ -514,6 +528,7 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
                                           long long &exact) {
     const int nch = (n + 63) >> 6;
     const float inf = __int_as_float(0x7f800000);
+    const float ku = S.u.k;
     for (int k = 0; k < nch; k++) {
         float x[2], y[2], z[2];
         int tp[2];
@@ -529,7 +544,6 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
         }
         for (int q = 0; q < nq; q++) {
             const float4 Q0 = S.q0[q], Q1 = S.q1[q];
-            const float2 Q2 = S.q2[q];
             bool flag[2];
 #pragma unroll
             for (int h = 0; h < 2; h++) {
@@ -537,7 +551,7 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
                 float s = __fmul_rn(dx, dx);
                 s = __fmaf_rn(dy, dy, s);
                 s = __fmaf_rn(dz, dz, s);
-                const float d = __fmaf_rn(s, Q1.z, Q2.x);
+                const float d = __fmaf_rn(s, ku, Q1.z);
                 flag[h] = real[h] && (force || fabsf(d) <= 1.0f);
             }
             const unsigned f0 = __ballot_sync(0xffffffffu, flag[0]), f1 = __ballot_sync(0xffffffffu, flag[1]);
@@ -562,10 +576,13 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
     __syncwarp();
 }
 
-// Test the first n (<= kBlk) staged candidates against the unit's queries.
-__device__ __forceinline__ void test_block(WalkSmem &S, WalkState &st, const WalkArgs &a, int lane, int n) {
+// Test the first n (<= kBlk) staged candidates against the unit's queries,
+// record the block's masks and candidate caller indices; returns this lane's
+// count increments for queries (lane, lane + 32).
+__device__ __forceinline__ int2 test_block(WalkSmem &S, const WalkArgs &a, int lane, int n) {
     const float inf = __int_as_float(0x7f800000);
     const int nch = (n + 63) >> 6;  // 1 or 2 chunks of 64
+    const int nq = S.u.nq;
     // this lane's candidates: chunk 0 -> slots (l, l + 32), chunk 1 -> (l + 64, l + 96)
     float c[4][3];
 #pragma unroll
@@ -578,31 +595,29 @@ __device__ __forceinline__ void test_block(WalkSmem &S, WalkState &st, const Wal
     }
     const unsigned long long xa = pk(c[0][0], c[1][0]), ya = pk(c[0][1], c[1][1]), za = pk(c[0][2], c[1][2]);
     const unsigned long long xb = pk(c[2][0], c[3][0]), yb = pk(c[2][1], c[3][1]), zb = pk(c[2][2], c[3][2]);
-    const int nqp = (st.nq + 1) & ~1;  // padded to even (the pad query never matches)
-    // shared addresses of the query records (one LDS.128 / LDS.128 / LDS.64 per query)
+    const int nqp = (nq + 1) & ~1;  // padded to even (the pad query never matches)
+    // shared addresses of the query records (two LDS.128 per query)
     const unsigned aq0 = (unsigned)__cvta_generic_to_shared(&S.q0[0]);
     const unsigned aq1 = (unsigned)__cvta_generic_to_shared(&S.q1[0]);
-    const unsigned aq2 = (unsigned)__cvta_generic_to_shared(&S.q2[0]);
+    const float ku = S.u.k;
+    const unsigned long long kk = pk(ku, ku);
     float bmin = 2.0f;  // min |d'| over the block's pairs: <= 1 -> some pair is banded
     // query records, loaded one query ahead of their use (LDS latency)
-    auto ldq = [&](int q, float4 &Q0, float4 &Q1, float2 &Q2) {
+    auto ldq = [&](int q, float4 &Q0, float4 &Q1) {
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(Q0.x), "=f"(Q0.y), "=f"(Q0.z), "=f"(Q0.w) : "r"(aq0 + 16 * q));
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(Q1.x), "=f"(Q1.y), "=f"(Q1.z), "=f"(Q1.w) : "r"(aq1 + 16 * q));
-        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(Q2.x), "=f"(Q2.y) : "r"(aq2 + 8 * q));
     };
     float4 N0, N1;
-    float2 N2;
-    ldq(0, N0, N1, N2);
+    ldq(0, N0, N1);
     if (nch == 2) {
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
             const float4 Q0 = N0, Q1 = N1;
-            const float2 Q2 = N2;
-            ldq(q + 1, N0, N1, N2);  // q + 1 <= nqp <= 64: within the padded arrays
+            ldq(q + 1, N0, N1);  // q + 1 <= nqp <= 64: within the padded arrays
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
-                                     kk = pk(Q1.z, Q1.w), cc = pk(Q2.x, Q2.y);
+                                     cc = pk(Q1.z, Q1.w);
             unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
             const unsigned long long da = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
             dx = f2_sub(xb, qx);
@@ -623,10 +638,9 @@ __device__ __forceinline__ void test_block(WalkSmem &S, WalkState &st, const Wal
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
             const float4 Q0 = N0, Q1 = N1;
-            const float2 Q2 = N2;
-            ldq(q + 1, N0, N1, N2);
+            ldq(q + 1, N0, N1);
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
-                                     kk = pk(Q1.z, Q1.w), cc = pk(Q2.x, Q2.y);
+                                     cc = pk(Q1.z, Q1.w);
             const unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
             const unsigned long long da = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
             bmin = fminf(bmin, fminf(fabsf(lo_f(da)), fabsf(hi_f(da))));
@@ -635,45 +649,145 @@ __device__ __forceinline__ void test_block(WalkSmem &S, WalkState &st, const Wal
             if (lane == 0) S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
         }
     }
-    const bool band = st.force || bmin <= 1.0f;
+    const bool force = S.u.force != 0;
+    const bool band = force || bmin <= 1.0f;
     __syncwarp();
-    if (__any_sync(0xffffffffu, band)) resolve_band(S, a, lane, st.q0, st.nq, n, st.force, st.exact);
-    // self is never its own neighbor (R12); counts; record the masks
-    const int bs = st.nblk * kBlk;
+    long long exact = 0;
+    if (__any_sync(0xffffffffu, band)) resolve_band(S, a, lane, S.u.q0, nq, n, force, exact);
+    // self is never its own neighbor (R12); counts
+    const int nblk = S.u.nblk;
+    const int bs = nblk * kBlk;
+    int inc[2] = {0, 0};
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int q = lane + 32 * h;
-        if (q < st.nq) {
+        if (q < nq) {
             const int sl = S.self[q] - bs;
             if (sl >= 0 && sl < n) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
-            st.cnt[h] += __popcll(S.mask[0][q]) + (nch > 1 ? __popcll(S.mask[1][q]) : 0);
+            inc[h] = __popcll(S.mask[0][q]) + (nch > 1 ? __popcll(S.mask[1][q]) : 0);
         }
     }
     __syncwarp();
-    if (st.rec_ok) {
-        unsigned long long *dst = a.masks + st.mask_base + (long long)(2 * st.nblk) * st.nq;
+    // record the masks and the candidates' caller indices (the fill pass)
+    if (S.u.rec_ok) {
+        unsigned long long *dst = a.masks + S.u.mask_base + (long long)(2 * nblk) * nq;
         for (int k = 0; k < nch; k++)
-            for (int q = lane; q < st.nq; q += 32) __stcs(&dst[k * st.nq + q], S.mask[k][q]);
+            for (int q = lane; q < nq; q += 32) __stcs(&dst[k * nq + q], S.mask[k][q]);
+        int32_t *cd = a.cands + S.u.cand_base + bs;
+        for (int i = lane; i < n; i += 32) __stcs(&cd[i], S.cidx[i]);
     }
-    st.tests += (long long)n * st.nq;
+    if (lane == 0) {
+        S.u.tests += (long long)n * nq;
+        S.u.exact += exact;
+    }
     __syncwarp();
+    return make_int2(inc[0], inc[1]);
 }
 
-// Flattened position p of the current leaf group -> (tree position, leaf offset)
-// for the 32 positions [w0, w0 + 32); `owner` = leaf holding position w0.
-__device__ __forceinline__ void locate(const WalkSmem &S, int nl, int total, int w0, int lane, int &owner, int &pos,
-                                       float4 &of, bool &valid) {
+// Flattened position p of the current leaf group -> tree position (-1: past
+// the end) and owning leaf, for the 32 positions [w0, w0 + 32); `owner` =
+// leaf holding position w0 (advanced to the leaf holding w0 + 32).
+__device__ __forceinline__ void locate(const WalkSmem &S, int nl, int total, int w0, int lane, unsigned le,
+                                       int &owner, int &pos, int &mine) {
     const int nxt = owner + 1 + lane;
-    const int stt = (nxt <= nl) ? S.lpre[nxt] : 0x7fffffff;
-    const int off = stt - w0;  // >= 1 for leaves after `owner`
-    const unsigned bits = __reduce_or_sync(0xffffffffu, (off >= 1 && off < 32) ? (1u << off) : 0u);
-    const int mine = owner + __popc(bits & ((2u << lane) - 1u));
-    const unsigned past = __ballot_sync(0xffffffffu, off <= 32);
+    const int off = ((nxt <= nl) ? S.lpre[nxt] : 0x7fffffff) - w0;  // >= 1 for leaves after `owner`
+    const unsigned bits = __reduce_or_sync(0xffffffffu, ((unsigned)(off - 1) < 31u) ? (1u << off) : 0u);
+    mine = owner + __popc(bits & le);
+    owner += __popc(__ballot_sync(0xffffffffu, off <= 32));
     const int p = w0 + lane;
-    valid = p < total;
-    pos = valid ? S.lbeg[mine] + (p - S.lpre[mine]) : 0;
-    of = S.loff[mine];
-    owner += __popc(past);
+    pos = (p < total) ? p + S.ldel[mine] : -1;
+}
+
+// Stage the particles of the current leaf group (lemma L3 cull), testing
+// every full block.  kMixed: some leaf of the group is staged from the fp64
+// records (a = fl32(fl64(x - c))), the others from the compact records.
+template <bool kMixed>
+__device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int nl, int total, int &nbuf,
+                                            int &cnt0, int &cnt1) {
+    const unsigned lt = lanemask_lt(), le = lt | (1u << lane);
+    const float4 *__restrict__ rec32 = a.rec32;
+    // record of position pos: the compact record, or (large leaf of a kMixed
+    // group, `rel` set) the fp64 record already relative to the unit centre
+    auto load = [&](int pos, int mine, bool &rel) {
+        float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+        rel = false;
+        if (pos >= 0) {
+            if (!kMixed || S.loff[mine].w != 0.0f) {
+                r = __ldg(&rec32[pos]);
+            } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
+                const double4 d = a.rec[pos];
+                r = make_float4(__double2float_rn(__dsub_rn(d.x, S.u.c[0])), __double2float_rn(__dsub_rn(d.y, S.u.c[1])),
+                                __double2float_rn(__dsub_rn(d.z, S.u.c[2])), __int_as_float((int)__double_as_longlong(d.w)));
+                rel = true;
+            }
+        }
+        return r;
+    };
+    int owner = 0, nblk = S.u.nblk;
+    int pos, mine;
+    bool rel;
+    locate(S, nl, total, 0, lane, le, owner, pos, mine);
+    float4 r = load(pos, mine, rel);
+#pragma unroll 1
+    for (int w0 = 0; w0 < total; w0 += 32) {
+        // the next window's record load is issued before this window is processed
+        int pos_n = -1, mine_n = 0;
+        bool rel_n = false;
+        float4 r_n = r;
+        if (w0 + 32 < total) {
+            locate(S, nl, total, w0 + 32, lane, le, owner, pos_n, mine_n);
+            r_n = load(pos_n, mine_n, rel_n);
+        }
+        // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
+        // conservative fp32 Minkowski cull against the query box (L3 / L4)
+        float4 of = S.loff[mine];
+        if (kMixed && rel) of = make_float4(0.f, 0.f, 0.f, 0.f);
+        // loop invariants re-read from shared memory (cheaper than spilled registers)
+        const float4 B0 = lds4v(&S.u.box0), B1 = lds4v(&S.u.box1);
+        const int2 qn = lds2iv(&S.u.q0);
+        const float ax = __fadd_rn(r.x, of.x);
+        const float ay = __fadd_rn(r.y, of.y);
+        const float az = __fadd_rn(r.z, of.z);
+        const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(B0.x, ax), __fsub_rn(ax, B1.x)));
+        const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(B0.y, ay), __fsub_rn(ay, B1.y)));
+        const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(B0.z, az), __fsub_rn(az, B1.z)));
+        const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
+        const bool keep = pos >= 0 && g2 < B0.w;
+        const unsigned km = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int slot = nbuf + __popc(km & lt);
+            S.cx[slot] = ax;
+            S.cy[slot] = ay;
+            S.cz[slot] = az;
+            S.tpos[slot] = pos;
+            S.cidx[slot] = __float_as_int(r.w);
+            if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = (short)(nblk * kBlk + slot);
+        }
+        nbuf += __popc(km);
+        __syncwarp();
+        if (nbuf >= kBlk) {
+            const int2 inc = test_block(S, a, lane, kBlk);
+            cnt0 += inc.x;
+            cnt1 += inc.y;
+            nblk++;
+            if (lane == 0) S.u.nblk = nblk;
+            // move the overflow (< 32) to the front of the buffer
+            const int rest = nbuf - kBlk;
+            if (lane < rest) {
+                S.cx[lane] = S.cx[kBlk + lane];
+                S.cy[lane] = S.cy[kBlk + lane];
+                S.cz[lane] = S.cz[kBlk + lane];
+                S.tpos[lane] = S.tpos[kBlk + lane];
+                S.cidx[lane] = S.cidx[kBlk + lane];
+            }
+            nbuf = rest;
+            __syncwarp();
+        }
+        pos = pos_n;
+        mine = mine_n;
+        rel = rel_n;
+        r = r_n;
+    }
 }
 
 #ifndef BT_WALK_MIN_BLOCKS
@@ -683,33 +797,42 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
     __shared__ WalkSmem smem[kWalkThreads / 32];
     const int lane = threadIdx.x & 31;
     WalkSmem &S = smem[threadIdx.x >> 5];
-    const unsigned lt = lanemask_lt();
     const float inf = __int_as_float(0x7f800000);
-    Slab cs, ms;
-    long long tests = 0, exact = 0, staged = 0, loaded = 0;
+    if (lane == 0) {
+        S.u.cs = Slab();
+        S.u.ms = Slab();
+        S.u.tests = S.u.exact = S.u.staged = S.u.loaded = 0;
+    }
+    __syncwarp();
     for (;;) {
         unsigned long long uid = 0;
         if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK3], 1ull);
         uid = __shfl_sync(0xffffffffu, uid, 0);
         if (uid >= (unsigned long long)a.n_units) break;
         const UnitRun R = a.urun[uid];
-        WalkState st;
-        double c0, c1, c2, E;
-        float blo[3], bhi[3], cull2;
         int32_t qo[2];
+        int q0, nq;
         {
             UnitGeom G;
             unit_setup(a, a.units[uid], lane, G);
-            st.q0 = G.q0;
-            st.nq = G.nq;
-            c0 = G.c[0];
-            c1 = G.c[1];
-            c2 = G.c[2];
-            E = G.E;
+            q0 = G.q0;
+            nq = G.nq;
             qo[0] = G.qo[0];
             qo[1] = G.qo[1];
             const double eps = l4_eps(G.E);
-            bool force = false;
+            float kq[2] = {INFINITY, INFINITY}, mid[2] = {0.0f, 0.0f};
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                if (lane + 32 * h < G.nq) {
+                    float A, B;
+                    l4_thresholds(G.qT[h], G.E, eps, a.exact_only != 0, A, B);
+                    band_params(A, B, kq[h], mid[h]);
+                }
+            }
+            // unit band scale: the minimum power of two (0 = force)
+            float ku = fminf(kq[0], kq[1]);
+            for (int d = 16; d; d >>= 1) ku = fminf(ku, __shfl_xor_sync(0xffffffffu, ku, d));
+            const bool force = ku == 0.0f;
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const int k = lane + 32 * h;
@@ -717,23 +840,18 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     const float ax = __double2float_rn(__dsub_rn(G.qx[h], G.c[0]));
                     const float ay = __double2float_rn(__dsub_rn(G.qy[h], G.c[1]));
                     const float az = __double2float_rn(__dsub_rn(G.qz[h], G.c[2]));
-                    float A, B, bk, bc;
-                    l4_thresholds(G.qT[h], G.E, eps, a.exact_only != 0, A, B);
-                    band_params(A, B, bk, bc);
-                    force |= bk == 0.0f;
+                    const float cq = -mid[h] * ku;  // exact (power-of-two scaling); 0 when forced
                     S.q0[k] = make_float4(ax, ax, ay, ay);
-                    S.q1[k] = make_float4(az, az, bk, bk);
-                    S.q2[k] = make_float2(bc, bc);
-                } else {  // padding query: d' = 2 (never a neighbor, never banded)
+                    S.q1[k] = make_float4(az, az, cq, cq);
+                } else {  // padding query: d' = s k + 2 >= 2 (never a neighbor, never banded)
                     S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    S.q1[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    S.q2[k] = make_float2(2.f, 2.f);
+                    S.q1[k] = make_float4(0.f, 0.f, 2.f, 2.f);
                 }
                 S.self[k] = -1;
             }
-            st.force = __any_sync(0xffffffffu, force);
             // fp32 images of the query box and the conservative cull radius
             // (R'_u + 4 eps)(1 + 2^-20) (L3 / L4)
+            float blo[3], bhi[3], cull2;
             for (int l = 0; l < 3; l++) {
                 blo[l] = __double2float_rn(__dsub_rn(G.lo[l], G.c[l]));
                 bhi[l] = __double2float_rn(__dsub_rn(G.hi[l], G.c[l]));
@@ -741,19 +859,34 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             const double rc = (G.Ru + 4.0 * eps) * (1.0 + 0x1p-20);
             const double rc2 = rc * rc * (1.0 + 0x1p-40);
             cull2 = (rc2 < 3.0e38) ? __double2float_ru(rc2) : inf;
+            // record space for the unit: at most `loaded` candidates
+            Slab cs = S.u.cs, ms = S.u.ms;
+            const long long need_c = R.loaded, need_m = (long long)((R.loaded + 63) >> 6) * G.nq;
+            const bool okc = slab_reserve(cs, need_c, kCandSlab, a.cand_cap, &a.ctr[C_CAND], lane);
+            const bool okm = slab_reserve(ms, need_m, kMaskSlab, a.mask_cap, &a.ctr[C_MASK], lane);
+            __syncwarp();
+            if (lane == 0) {
+                S.u.cs = cs;
+                S.u.ms = ms;
+                S.u.cand_base = cs.cur;
+                S.u.mask_base = ms.cur;
+                S.u.c[0] = G.c[0];
+                S.u.c[1] = G.c[1];
+                S.u.c[2] = G.c[2];
+                S.u.E = G.E;
+                S.u.q0 = G.q0;
+                S.u.nq = G.nq;
+                S.u.nblk = 0;
+                S.u.rec_ok = okc && okm;
+                S.u.force = force;
+                S.u.k = ku;
+                S.u.box0 = make_float4(blo[0], blo[1], blo[2], cull2);
+                S.u.box1 = make_float4(bhi[0], bhi[1], bhi[2], 0.0f);
+            }
         }
-        // record space for the unit: at most `loaded` candidates
-        const long long need_c = R.loaded, need_m = (long long)((R.loaded + 63) >> 6) * st.nq;
-        const bool okc = slab_reserve(cs, need_c, kCandSlab, a.cand_cap, &a.ctr[C_CAND], lane);
-        const bool okm = slab_reserve(ms, need_m, kMaskSlab, a.mask_cap, &a.ctr[C_MASK], lane);
-        st.rec_ok = okc && okm;
-        st.cand_base = cs.cur;
-        st.mask_base = ms.cur;
-        st.nbuf = 0;
-        st.nblk = 0;
-        st.cnt[0] = st.cnt[1] = 0;
-        st.tests = st.exact = 0;
         __syncwarp();
+        int nbuf = 0, cnt0 = 0, cnt1 = 0;
+        long long loaded = 0;
         const int nleaf = R.nleaf;
         const long long list_off = R.list_off;
         for (int g0 = 0; g0 < nleaf; g0 += kGroup) {
@@ -771,8 +904,9 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                 // compact records are usable when the leaf half-extent H <= 7 E (l4_eps)
                 const double lx = 0.5 * (b0.x + b1.y), ly = 0.5 * (b0.y + b2.x), lz = 0.5 * (b1.x + b2.y);
                 const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
-                off = make_float4(__double2float_rn(__dsub_rn(lx, c0)), __double2float_rn(__dsub_rn(ly, c1)),
-                                  __double2float_rn(__dsub_rn(lz, c2)), (H <= 7.0 * E) ? 1.0f : 0.0f);
+                off = make_float4(__double2float_rn(__dsub_rn(lx, S.u.c[0])),
+                                  __double2float_rn(__dsub_rn(ly, S.u.c[1])),
+                                  __double2float_rn(__dsub_rn(lz, S.u.c[2])), (H <= 7.0 * S.u.E) ? 1.0f : 0.0f);
             }
             int inc = cnt;
             for (int d = 1; d < 32; d <<= 1) {
@@ -781,102 +915,45 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             }
             const int total = __shfl_sync(0xffffffffu, inc, 31);
             const int nl = min(kGroup, nleaf - g0);
-            S.lbeg[lane] = beg;
+            S.ldel[lane] = beg - (inc - cnt);
             S.lpre[lane] = inc - cnt;
             S.loff[lane] = off;
             if (lane == 0) S.lpre[kGroup] = total;
             const bool mixed = __any_sync(0xffffffffu, gi < nleaf && off.w == 0.0f);
             __syncwarp();
             loaded += total;
-            int owner = 0;
-            for (int p0 = 0; p0 < total; p0 += 64) {
-                float4 r[2], of[2];
-                int pos[2];
-                bool valid[2];
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    locate(S, nl, total, p0 + 32 * h, lane, owner, pos[h], of[h], valid[h]);
-                    r[h] = make_float4(inf, inf, inf, 0.f);
-                    if (!mixed) {
-                        if (valid[h]) r[h] = __ldg(&a.rec32[pos[h]]);
-                    } else if (valid[h]) {
-                        if (of[h].w != 0.0f) {
-                            r[h] = __ldg(&a.rec32[pos[h]]);
-                        } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
-                            const double4 d = a.rec[pos[h]];
-                            r[h] = make_float4(__double2float_rn(__dsub_rn(d.x, c0)),
-                                               __double2float_rn(__dsub_rn(d.y, c1)),
-                                               __double2float_rn(__dsub_rn(d.z, c2)),
-                                               __int_as_float((int)__double_as_longlong(d.w)));
-                            of[h].x = of[h].y = of[h].z = 0.0f;
-                        }
-                    }
-                }
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                    // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
-                    // conservative fp32 Minkowski cull against the query box (L3 / L4)
-                    const float ax = __fadd_rn(r[h].x, of[h].x);
-                    const float ay = __fadd_rn(r[h].y, of[h].y);
-                    const float az = __fadd_rn(r[h].z, of[h].z);
-                    const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(blo[0], ax), __fsub_rn(ax, bhi[0])));
-                    const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(blo[1], ay), __fsub_rn(ay, bhi[1])));
-                    const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(blo[2], az), __fsub_rn(az, bhi[2])));
-                    const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
-                    const bool keep = valid[h] && g2 < cull2;
-                    const unsigned km = __ballot_sync(0xffffffffu, keep);
-                    if (keep) {
-                        const int slot = st.nbuf + __popc(km & lt);
-                        S.cx[slot] = ax;
-                        S.cy[slot] = ay;
-                        S.cz[slot] = az;
-                        S.tpos[slot] = pos[h];
-                        const int us = st.nblk * kBlk + slot;  // slot within the unit
-                        if (st.rec_ok) __stcs(&a.cands[st.cand_base + us], __float_as_int(r[h].w));
-                        if ((unsigned)(pos[h] - st.q0) < (unsigned)st.nq) S.self[pos[h] - st.q0] = us;
-                    }
-                    st.nbuf += __popc(km);
-                }
-                __syncwarp();
-                if (st.nbuf >= kBlk) {
-                    test_block(S, st, a, lane, kBlk);
-                    st.nblk++;
-                    // move the overflow (< 64) to the front of the buffer
-                    const int rest = st.nbuf - kBlk;
-                    for (int i = lane; i < rest; i += 32) {
-                        S.cx[i] = S.cx[kBlk + i];
-                        S.cy[i] = S.cy[kBlk + i];
-                        S.cz[i] = S.cz[kBlk + i];
-                        S.tpos[i] = S.tpos[kBlk + i];
-                    }
-                    st.nbuf = rest;
-                    __syncwarp();
-                }
-            }
+            if (mixed)
+                stage_group<true>(S, a, lane, nl, total, nbuf, cnt0, cnt1);
+            else
+                stage_group<false>(S, a, lane, nl, total, nbuf, cnt0, cnt1);
         }
-        if (st.nbuf > 0) test_block(S, st, a, lane, st.nbuf);
-        const int nstaged = st.nblk * kBlk + st.nbuf;
-        if (lane < st.nq) a.counts[qo[0]] = st.cnt[0];
-        if (lane + 32 < st.nq) a.counts[qo[1]] = st.cnt[1];
+        if (nbuf > 0) {
+            const int2 inc = test_block(S, a, lane, nbuf);
+            cnt0 += inc.x;
+            cnt1 += inc.y;
+        }
+        const int nstaged = S.u.nblk * kBlk + nbuf;
+        if (lane < nq) a.counts[qo[0]] = cnt0;
+        if (lane + 32 < nq) a.counts[qo[1]] = cnt1;
+        __syncwarp();
         if (lane == 0) {
             UnitRun &W = a.urun[uid];
-            W.cand_base = st.cand_base;
-            W.mask_base = st.mask_base;
+            W.cand_base = S.u.cand_base;
+            W.mask_base = S.u.mask_base;
             W.nstaged = nstaged;
-            W.ok = st.rec_ok ? 1 : 0;
+            W.ok = S.u.rec_ok;
+            S.u.cs.cur += nstaged;
+            S.u.ms.cur += (long long)((nstaged + 63) >> 6) * nq;
+            S.u.staged += nstaged;
+            S.u.loaded += loaded;
         }
-        cs.cur += nstaged;
-        ms.cur += (long long)((nstaged + 63) >> 6) * st.nq;
-        tests += st.tests;
-        exact += st.exact;
-        staged += nstaged;
         __syncwarp();
     }
     if (lane == 0) {
-        atomicAdd((unsigned long long *)&a.ctr[C_TESTS], (unsigned long long)tests);
-        atomicAdd((unsigned long long *)&a.ctr[C_EXACT], (unsigned long long)exact);
-        atomicAdd((unsigned long long *)&a.ctr[C_STAGED], (unsigned long long)staged);
-        atomicAdd((unsigned long long *)&a.ctr[C_LOADED], (unsigned long long)loaded);
+        atomicAdd((unsigned long long *)&a.ctr[C_TESTS], (unsigned long long)S.u.tests);
+        atomicAdd((unsigned long long *)&a.ctr[C_EXACT], (unsigned long long)S.u.exact);
+        atomicAdd((unsigned long long *)&a.ctr[C_STAGED], (unsigned long long)S.u.staged);
+        atomicAdd((unsigned long long *)&a.ctr[C_LOADED], (unsigned long long)S.u.loaded);
     }
 }
 
