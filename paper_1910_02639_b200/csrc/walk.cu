@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kQ = 64;           // queries per unit (== build.cu kUnitQ)
 constexpr int kBlk = 128;        // staged candidates per test block
-constexpr int kBuf = kBlk + 32;  // staging buffer: a block + one staging window
+constexpr int kScratch = 4096;   // staged candidates per warp scratch (global, L2-resident); multiple of kBlk
 constexpr int kGroup = 32;       // candidate leaves per staging group (one per lane)
 constexpr int kFrontCap = 128;   // shared-memory descent frontier per level
 constexpr int kDescThreads = 128;
@@ -96,6 +96,7 @@ struct WalkArgs {
     long long cand_cap;
     unsigned long long *masks;
     long long mask_cap;
+    float4 *scratch;          // per walk warp: kScratch staged candidates (ax, ay, az, tree position)
 };
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -503,16 +504,13 @@ struct UnitSm {                     // per-warp unit state (shared memory)
     float4 box0, box1;               // fp32 query box relative to c: (lo xyz, cull2), (hi xyz, -)
     int q0, nq;                      // (8-byte aligned: read as one int2)
     float k;                         // band scale of the unit (power of two; 0: force)
-    int nblk, rec_ok, force;
+    int rec_ok, force;
 };
 
 struct WalkSmem {
     float4 q0[kQ + 1];              // ax, ax, ay, ay  (fp32, relative to the unit centre)
     float4 q1[kQ + 1];              // az, az, c, c   (band map d' = s k + c); [kQ]: look-ahead pad
-    short self[kQ];                 // unit slot of each query's own record (-1: none)
-    float cx[kBuf], cy[kBuf], cz[kBuf];
-    int tpos[kBuf];                 // tree position of each staged candidate
-    int cidx[kBuf];                 // caller index of each staged candidate
+    int self[kQ];                   // unit slot of each query's own record (-1: none)
     unsigned long long mask[2][kQ]; // the block's neighbor masks [chunk][query]
     int ldel[kGroup];               // group leaves: first tree position - exclusive prefix of counts
     int lpre[kGroup + 1];           // group leaves: exclusive prefix of counts
@@ -523,31 +521,29 @@ struct WalkSmem {
 // The exact band of lemma L4 (rare): recompute the block's pairs with the
 // hot loop's fp32 operations and let the fp64 predicate decide every pair
 // with |d'| <= 1 (all pairs when `force`; padding slots >= n are never
-// neighbors).
-__device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int lane, int q0, int nq, int n, bool force,
+// neighbors).  blk: the block's staged candidates (ax, ay, az, tree position).
+__device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int lane, const float4 *blk, int n,
                                           long long &exact) {
     const int nch = (n + 63) >> 6;
     const float inf = __int_as_float(0x7f800000);
     const float ku = S.u.k;
+    const bool force = S.u.force != 0;
+    const int q0 = S.u.q0, nq = S.u.nq;
     for (int k = 0; k < nch; k++) {
-        float x[2], y[2], z[2];
-        int tp[2];
+        float4 c[2];
         bool real[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int s = 64 * k + 32 * h + lane;
             real[h] = s < n;
-            x[h] = real[h] ? S.cx[s] : inf;
-            y[h] = real[h] ? S.cy[s] : inf;
-            z[h] = real[h] ? S.cz[s] : inf;
-            tp[h] = real[h] ? S.tpos[s] : -1;
+            c[h] = real[h] ? blk[s] : make_float4(inf, inf, inf, __int_as_float(-1));
         }
         for (int q = 0; q < nq; q++) {
             const float4 Q0 = S.q0[q], Q1 = S.q1[q];
             bool flag[2];
 #pragma unroll
             for (int h = 0; h < 2; h++) {
-                const float dx = __fsub_rn(x[h], Q0.x), dy = __fsub_rn(y[h], Q0.z), dz = __fsub_rn(z[h], Q1.x);
+                const float dx = __fsub_rn(c[h].x, Q0.x), dy = __fsub_rn(c[h].y, Q0.z), dz = __fsub_rn(c[h].z, Q1.x);
                 float s = __fmul_rn(dx, dx);
                 s = __fmaf_rn(dy, dy, s);
                 s = __fmaf_rn(dz, dz, s);
@@ -561,8 +557,9 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
             const double t = __dmul_rn(2.0, a.h_tree[qp]);
             const double T = __dmul_rn(t, t);
             bool e0 = false, e1 = false;
-            if (flag[0]) e0 = tp[0] != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp[0]]);
-            if (flag[1]) e1 = tp[1] != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp[1]]);
+            const int tp0 = __float_as_int(c[0].w), tp1 = __float_as_int(c[1].w);
+            if (flag[0]) e0 = tp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp0]);
+            if (flag[1]) e1 = tp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp1]);
             const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
             if (lane == 0) {
                 const unsigned long long fm = ((unsigned long long)f1 << 32) | f0;
@@ -576,25 +573,23 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
     __syncwarp();
 }
 
-// Test the first n (<= kBlk) staged candidates against the unit's queries,
-// record the block's masks and candidate caller indices; returns this lane's
-// count increments for queries (lane, lane + 32).
-__device__ __forceinline__ int2 test_block(WalkSmem &S, const WalkArgs &a, int lane, int n) {
+// Test n (<= kBlk) staged candidates (blk, unit slots us0 .. us0 + n) against
+// the unit's queries and record the block's masks; returns this lane's count
+// increments for queries (lane, lane + 32).
+__device__ __forceinline__ int2 test_block(WalkSmem &S, const WalkArgs &a, int lane, const float4 *blk, int n,
+                                           int us0) {
     const float inf = __int_as_float(0x7f800000);
     const int nch = (n + 63) >> 6;  // 1 or 2 chunks of 64
     const int nq = S.u.nq;
     // this lane's candidates: chunk 0 -> slots (l, l + 32), chunk 1 -> (l + 64, l + 96)
-    float c[4][3];
+    float4 c[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int s = 32 * j + lane;
-        const bool real = s < n;
-        c[j][0] = real ? S.cx[s] : inf;
-        c[j][1] = real ? S.cy[s] : inf;
-        c[j][2] = real ? S.cz[s] : inf;
+        c[j] = (s < n) ? blk[s] : make_float4(inf, inf, inf, 0.f);
     }
-    const unsigned long long xa = pk(c[0][0], c[1][0]), ya = pk(c[0][1], c[1][1]), za = pk(c[0][2], c[1][2]);
-    const unsigned long long xb = pk(c[2][0], c[3][0]), yb = pk(c[2][1], c[3][1]), zb = pk(c[2][2], c[3][2]);
+    const unsigned long long xa = pk(c[0].x, c[1].x), ya = pk(c[0].y, c[1].y), za = pk(c[0].z, c[1].z);
+    const unsigned long long xb = pk(c[2].x, c[3].x), yb = pk(c[2].y, c[3].y), zb = pk(c[2].z, c[3].z);
     const int nqp = (nq + 1) & ~1;  // padded to even (the pad query never matches)
     // shared addresses of the query records (two LDS.128 per query)
     const unsigned aq0 = (unsigned)__cvta_generic_to_shared(&S.q0[0]);
@@ -649,32 +644,27 @@ __device__ __forceinline__ int2 test_block(WalkSmem &S, const WalkArgs &a, int l
             if (lane == 0) S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
         }
     }
-    const bool force = S.u.force != 0;
-    const bool band = force || bmin <= 1.0f;
+    const bool band = S.u.force != 0 || bmin <= 1.0f;
     __syncwarp();
     long long exact = 0;
-    if (__any_sync(0xffffffffu, band)) resolve_band(S, a, lane, S.u.q0, nq, n, force, exact);
+    if (__any_sync(0xffffffffu, band)) resolve_band(S, a, lane, blk, n, exact);
     // self is never its own neighbor (R12); counts
-    const int nblk = S.u.nblk;
-    const int bs = nblk * kBlk;
     int inc[2] = {0, 0};
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int q = lane + 32 * h;
         if (q < nq) {
-            const int sl = S.self[q] - bs;
+            const int sl = S.self[q] - us0;
             if (sl >= 0 && sl < n) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
             inc[h] = __popcll(S.mask[0][q]) + (nch > 1 ? __popcll(S.mask[1][q]) : 0);
         }
     }
     __syncwarp();
-    // record the masks and the candidates' caller indices (the fill pass)
+    // record the masks (the fill pass): chunk kk = us0 / 64 + k of the unit
     if (S.u.rec_ok) {
-        unsigned long long *dst = a.masks + S.u.mask_base + (long long)(2 * nblk) * nq;
+        unsigned long long *dst = a.masks + S.u.mask_base + (long long)(us0 >> 6) * nq;
         for (int k = 0; k < nch; k++)
             for (int q = lane; q < nq; q += 32) __stcs(&dst[k * nq + q], S.mask[k][q]);
-        int32_t *cd = a.cands + S.u.cand_base + bs;
-        for (int i = lane; i < n; i += 32) __stcs(&cd[i], S.cidx[i]);
     }
     if (lane == 0) {
         S.u.tests += (long long)n * nq;
@@ -698,14 +688,19 @@ __device__ __forceinline__ void locate(const WalkSmem &S, int nl, int total, int
     pos = (p < total) ? p + S.ldel[mine] : -1;
 }
 
-// Stage the particles of the current leaf group (lemma L3 cull), testing
-// every full block.  kMixed: some leaf of the group is staged from the fp64
-// records (a = fl32(fl64(x - c))), the others from the compact records.
+// Stage the particles of the current leaf group from window w0 on (lemma L3
+// cull) into the warp's scratch at nst, until the group is done or the
+// scratch cannot take another window.  kMixed: some leaf of the group is
+// staged from the fp64 records (a = fl32(fl64(x - c))).
 template <bool kMixed>
-__device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int nl, int total, int &nbuf,
-                                            int &cnt0, int &cnt1) {
+__device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int nl, int total, int &w0,
+                                            int &owner, float4 *scr, int &nst, int slot0) {
     const unsigned lt = lanemask_lt(), le = lt | (1u << lane);
     const float4 *__restrict__ rec32 = a.rec32;
+    const float4 B0 = S.u.box0, B1 = S.u.box1;
+    const int2 qn = lds2iv(&S.u.q0);
+    const bool rec_ok = S.u.rec_ok != 0;
+    int32_t *cands = a.cands + S.u.cand_base + slot0;
     // record of position pos: the compact record, or (large leaf of a kMixed
     // group, `rel` set) the fp64 record already relative to the unit centre
     auto load = [&](int pos, int mine, bool &rel) {
@@ -723,13 +718,17 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         }
         return r;
     };
-    int owner = 0, nblk = S.u.nblk;
     int pos, mine;
     bool rel;
-    locate(S, nl, total, 0, lane, le, owner, pos, mine);
+    locate(S, nl, total, w0, lane, le, owner, pos, mine);
     float4 r = load(pos, mine, rel);
 #pragma unroll 1
-    for (int w0 = 0; w0 < total; w0 += 32) {
+    for (; w0 < total; w0 += 32) {
+        if (nst > kScratch - 32) {  // full: the caller tests the staged blocks and resumes at w0
+            owner = mine;           // leaf holding position w0 (locate advanced it past this window)
+            owner = __shfl_sync(0xffffffffu, owner, 0);
+            break;
+        }
         // the next window's record load is issued before this window is processed
         int pos_n = -1, mine_n = 0;
         bool rel_n = false;
@@ -742,9 +741,6 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         // conservative fp32 Minkowski cull against the query box (L3 / L4)
         float4 of = S.loff[mine];
         if (kMixed && rel) of = make_float4(0.f, 0.f, 0.f, 0.f);
-        // loop invariants re-read from shared memory (cheaper than spilled registers)
-        const float4 B0 = lds4v(&S.u.box0), B1 = lds4v(&S.u.box1);
-        const int2 qn = lds2iv(&S.u.q0);
         const float ax = __fadd_rn(r.x, of.x);
         const float ay = __fadd_rn(r.y, of.y);
         const float az = __fadd_rn(r.z, of.z);
@@ -755,34 +751,12 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         const bool keep = pos >= 0 && g2 < B0.w;
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
-            const int slot = nbuf + __popc(km & lt);
-            S.cx[slot] = ax;
-            S.cy[slot] = ay;
-            S.cz[slot] = az;
-            S.tpos[slot] = pos;
-            S.cidx[slot] = __float_as_int(r.w);
-            if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = (short)(nblk * kBlk + slot);
+            const int slot = nst + __popc(km & lt);
+            scr[slot] = make_float4(ax, ay, az, __int_as_float(pos));
+            if (rec_ok) __stcs(&cands[slot], __float_as_int(r.w));
+            if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
         }
-        nbuf += __popc(km);
-        __syncwarp();
-        if (nbuf >= kBlk) {
-            const int2 inc = test_block(S, a, lane, kBlk);
-            cnt0 += inc.x;
-            cnt1 += inc.y;
-            nblk++;
-            if (lane == 0) S.u.nblk = nblk;
-            // move the overflow (< 32) to the front of the buffer
-            const int rest = nbuf - kBlk;
-            if (lane < rest) {
-                S.cx[lane] = S.cx[kBlk + lane];
-                S.cy[lane] = S.cy[kBlk + lane];
-                S.cz[lane] = S.cz[kBlk + lane];
-                S.tpos[lane] = S.tpos[kBlk + lane];
-                S.cidx[lane] = S.cidx[kBlk + lane];
-            }
-            nbuf = rest;
-            __syncwarp();
-        }
+        nst += __popc(km);
         pos = pos_n;
         mine = mine_n;
         rel = rel_n;
@@ -798,6 +772,8 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
     const int lane = threadIdx.x & 31;
     WalkSmem &S = smem[threadIdx.x >> 5];
     const float inf = __int_as_float(0x7f800000);
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    float4 *const scr = a.scratch + gwarp * kScratch;
     if (lane == 0) {
         S.u.cs = Slab();
         S.u.ms = Slab();
@@ -811,11 +787,10 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         if (uid >= (unsigned long long)a.n_units) break;
         const UnitRun R = a.urun[uid];
         int32_t qo[2];
-        int q0, nq;
+        int nq;
         {
             UnitGeom G;
             unit_setup(a, a.units[uid], lane, G);
-            q0 = G.q0;
             nq = G.nq;
             qo[0] = G.qo[0];
             qo[1] = G.qo[1];
@@ -876,7 +851,6 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                 S.u.E = G.E;
                 S.u.q0 = G.q0;
                 S.u.nq = G.nq;
-                S.u.nblk = 0;
                 S.u.rec_ok = okc && okm;
                 S.u.force = force;
                 S.u.k = ku;
@@ -885,54 +859,86 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             }
         }
         __syncwarp();
-        int nbuf = 0, cnt0 = 0, cnt1 = 0;
+        int cnt0 = 0, cnt1 = 0;
         long long loaded = 0;
         const int nleaf = R.nleaf;
         const long long list_off = R.list_off;
-        for (int g0 = 0; g0 < nleaf; g0 += kGroup) {
-            // ---- the group's leaves: first position, count, offset of the centre
-            const int gi = g0 + lane;
-            int cnt = 0, beg = 0;
-            float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gi < nleaf) {
-                const int leaf = a.ulist[list_off + gi];
-                beg = a.leaf_begin[leaf];
-                cnt = a.leaf_count[leaf];
-                const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
-                const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
-                // leaf centre (as build.cu computed it) relative to the unit centre; the
-                // compact records are usable when the leaf half-extent H <= 7 E (l4_eps)
-                const double lx = 0.5 * (b0.x + b1.y), ly = 0.5 * (b0.y + b2.x), lz = 0.5 * (b1.x + b2.y);
-                const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
-                off = make_float4(__double2float_rn(__dsub_rn(lx, S.u.c[0])),
-                                  __double2float_rn(__dsub_rn(ly, S.u.c[1])),
-                                  __double2float_rn(__dsub_rn(lz, S.u.c[2])), (H <= 7.0 * S.u.E) ? 1.0f : 0.0f);
+        int nst = 0, slot0 = 0;            // candidates in the scratch; unit slot of scratch[0]
+        int g0 = 0, w0 = 0, owner = 0, total = 0, nl = 0;
+        bool mixed = false, have_group = false;
+        for (;;) {
+            // ---- staging phase: fill the scratch
+            while (g0 < nleaf) {
+                if (!have_group) {
+                    // the group's leaves: first position, count, offset of the centre
+                    const int gi = g0 + lane;
+                    int cnt = 0, beg = 0;
+                    float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (gi < nleaf) {
+                        const int leaf = a.ulist[list_off + gi];
+                        beg = a.leaf_begin[leaf];
+                        cnt = a.leaf_count[leaf];
+                        const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
+                        const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
+                        // leaf centre (as build.cu computed it) relative to the unit centre; the
+                        // compact records are usable when the leaf half-extent H <= 7 E (l4_eps)
+                        const double lx = 0.5 * (b0.x + b1.y), ly = 0.5 * (b0.y + b2.x), lz = 0.5 * (b1.x + b2.y);
+                        const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
+                        off = make_float4(__double2float_rn(__dsub_rn(lx, S.u.c[0])),
+                                          __double2float_rn(__dsub_rn(ly, S.u.c[1])),
+                                          __double2float_rn(__dsub_rn(lz, S.u.c[2])),
+                                          (H <= 7.0 * S.u.E) ? 1.0f : 0.0f);
+                    }
+                    int inc = cnt;
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int o = __shfl_up_sync(0xffffffffu, inc, d);
+                        if (lane >= d) inc += o;
+                    }
+                    total = __shfl_sync(0xffffffffu, inc, 31);
+                    nl = min(kGroup, nleaf - g0);
+                    S.ldel[lane] = beg - (inc - cnt);
+                    S.lpre[lane] = inc - cnt;
+                    S.loff[lane] = off;
+                    if (lane == 0) S.lpre[kGroup] = total;
+                    mixed = __any_sync(0xffffffffu, gi < nleaf && off.w == 0.0f);
+                    __syncwarp();
+                    w0 = 0;
+                    owner = 0;
+                    have_group = true;
+                }
+                if (mixed)
+                    stage_group<true>(S, a, lane, nl, total, w0, owner, scr, nst, slot0);
+                else
+                    stage_group<false>(S, a, lane, nl, total, w0, owner, scr, nst, slot0);
+                if (w0 < total) break;  // scratch full
+                loaded += total;
+                g0 += kGroup;
+                have_group = false;
             }
-            int inc = cnt;
-            for (int d = 1; d < 32; d <<= 1) {
-                const int o = __shfl_up_sync(0xffffffffu, inc, d);
-                if (lane >= d) inc += o;
-            }
-            const int total = __shfl_sync(0xffffffffu, inc, 31);
-            const int nl = min(kGroup, nleaf - g0);
-            S.ldel[lane] = beg - (inc - cnt);
-            S.lpre[lane] = inc - cnt;
-            S.loff[lane] = off;
-            if (lane == 0) S.lpre[kGroup] = total;
-            const bool mixed = __any_sync(0xffffffffu, gi < nleaf && off.w == 0.0f);
+            const bool done = g0 >= nleaf;
             __syncwarp();
-            loaded += total;
-            if (mixed)
-                stage_group<true>(S, a, lane, nl, total, nbuf, cnt0, cnt1);
-            else
-                stage_group<false>(S, a, lane, nl, total, nbuf, cnt0, cnt1);
+            // ---- test phase: the staged blocks (all but a partial last one unless done)
+            const int ntest = done ? nst : nst - nst % kBlk;
+#ifdef BT_DIAG_NO_TEST
+            if (true) {} else
+#endif
+            for (int b0 = 0; b0 < ntest; b0 += kBlk) {
+                const int2 inc = test_block(S, a, lane, scr + b0, min(kBlk, ntest - b0), slot0 + b0);
+                cnt0 += inc.x;
+                cnt1 += inc.y;
+            }
+            if (done) {
+                slot0 += nst;
+                break;
+            }
+            // move the partial block to the front of the scratch
+            const int rest = nst - ntest;
+            for (int i = lane; i < rest; i += 32) scr[i] = scr[ntest + i];
+            slot0 += ntest;
+            nst = rest;
+            __syncwarp();
         }
-        if (nbuf > 0) {
-            const int2 inc = test_block(S, a, lane, nbuf);
-            cnt0 += inc.x;
-            cnt1 += inc.y;
-        }
-        const int nstaged = S.u.nblk * kBlk + nbuf;
+        const int nstaged = slot0;
         if (lane < nq) a.counts[qo[0]] = cnt0;
         if (lane + 32 < nq) a.counts[qo[1]] = cnt1;
         __syncwarp();
@@ -1181,6 +1187,8 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             a.cand_cap = (long long)t.arena_cands.n;
             a.masks = t.arena_masks.p;
             a.mask_cap = (long long)t.arena_masks.n;
+            t.scratch.reserve(warps_w * kScratch, 0);
+            a.scratch = t.scratch.p;
             for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero(c);
             {
                 Phase ph("search.count");

@@ -20,6 +20,7 @@ ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--exact", action="store_true")
 ap.add_argument("--ngmax", type=int, default=512)
+ap.add_argument("--count-only", action="store_true")
 args = ap.parse_args()
 
 pos_np, h_np = datagen.make_config(args.config, n=args.n)
@@ -38,7 +39,10 @@ for r in range(args.reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     t = P.Tree(pos, 64, 0.5)
-    t.find_neighbors(h, args.ngmax, counts=counts, offsets=offsets, nbr_idx=nbr)
+    if args.count_only:
+        t.count(h)
+    else:
+        t.find_neighbors(h, args.ngmax, counts=counts, offsets=offsets, nbr_idx=nbr)
     st = t.stats()
     t.free()
     torch.cuda.synchronize()
