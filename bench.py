@@ -264,8 +264,9 @@ def run_b200(args):
         return prof.get(name, (0.0, 0))[0] / args.steps
 
     launches = sum(v[1] for k, v in prof.items() if k.startswith("kernel.")) // args.steps
-    kern = {"build": ph("build.total"), "walk_gather": ph("search.gather"), "walk_test": ph("search.count"),
-            "scan": ph("search.scan"), "walk_fill": ph("search.fill"), "gather_h": ph("search.gather_h")}
+    kern = {"build": ph("build.total"), "walk_desc": ph("search.desc") + ph("search.desc_big"),
+            "walk_test": ph("search.count"), "scan": ph("search.scan"), "walk_fill": ph("search.fill"),
+            "gather_h": ph("search.gather_h")}
 
     # ---- roofline of the dominant kernel -----------------
     peaks = {}
@@ -276,26 +277,28 @@ def run_b200(args):
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     hbm_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else "fallback (B200_PROFILING.md)"
     loaded, staged, tests = int(st["loaded"]), int(st["staged"]), int(st["tests"])
-    dom = max(("walk_gather", "walk_test", "walk_fill", "build"), key=lambda k: kern[k])
+    dom = max(("walk_desc", "walk_test", "walk_fill", "build"), key=lambda k: kern[k])
     if dom == "walk_test":
-        # pair tests are fp32 ALU work: 3 sub + 1 mul + 2 fma + 1 compare = 7
-        # lane-ops per pair test; peak = 148 SMs x 128 fp32 lanes x max SM clock
+        # walk_kernel: staging + pair tests, bound by fp32 ALU issue.  Algorithmic
+        # work = 8 fp32 ops per pair test (3 differences, 3 squares, 2 sums:
+        # ((dx*dx + dy*dy) + dz*dz)); peak = 148 SMs x 128 fp32 lanes x max SM
+        # clock (B200_PROFILING.md unit counts, MEASURED_PEAKS sm_max_mhz)
         sm_mhz = peaks.get("sm_max_mhz", 1965.0)
         alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
-        achieved = tests * 7 / (kern[dom] * 1e-3) / 1e12
-        roofline = {"kernel": dom, "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "T lane-op/s",
-                    "frac": achieved / alu_peak, "traffic": None,
+        achieved = tests * 8 / (kern[dom] * 1e-3) / 1e12
+        roofline = {"kernel": "walk_kernel (A10 staging + A11 pair tests)", "bound": "alu", "achieved": achieved,
+                    "peak": alu_peak, "unit": "T fp32 op/s", "frac": achieved / alu_peak, "traffic": None,
                     "peak_source": "derived: 148 SM x 128 fp32 lanes x sm_max_mhz (B200_PROFILING.md / MEASURED_PEAKS)",
-                    "algorithmic_ops": tests * 7}
+                    "algorithmic_ops": tests * 8}
     else:
-        if dom == "walk_gather":
-            # candidate records read (16-B compact record per loaded particle) +
-            # candidate slots written (16-B coordinates + 4-B caller index)
-            alg_bytes = loaded * 16 + staged * 20
+        if dom == "walk_desc":
+            # descent: per unit the query records (32 B) + h (8 B), per listed leaf
+            # its box (48 B) + count (4 B) read and its id (4 B) written
+            alg_bytes = n * 40 + int(st.get("list_entries", 0)) * 56
         elif dom == "walk_fill":
             # recorded masks (8 B/word) + candidate indices (4 B/slot) read, per
             # particle record + offset read, 4-B output index per neighbor pair
-            alg_bytes = int(st["mask_words"]) * 8 + int(st["cand_slots"]) * 4 + n * (32 + 8) + 4 * total_pairs
+            alg_bytes = int(st["mask_words"]) * 8 + staged * 4 + n * (32 + 8) + 4 * total_pairs
         else:
             # build: per particle pos read (24 B) + records written / re-read over
             # the levels and the final sort (~4 x 32 B)
@@ -315,7 +318,7 @@ def run_b200(args):
     # by the walk (16-B compact records loaded by the gather) over the whole walk
     # time (gather + test + fill) and peak HBM bandwidth
     bcand = loaded * 16
-    walk_ms = kern["walk_gather"] + kern["walk_test"] + kern["walk_fill"]
+    walk_ms = kern["walk_desc"] + kern["walk_test"] + kern["walk_fill"]
     bj_roof = {"B_cand_bytes": bcand, "walk_ms": walk_ms,
                "frac": (bcand / (walk_ms * 1e-3) / 1e9) / hbm_peak if walk_ms > 0 else None}
 
@@ -360,8 +363,8 @@ def run_b200(args):
                 "build_ms": kern["build"], "kernel_ms": kern, "gpu_launches": launches,
                 "roofline": roofline, "bj_hbm_roofline": bj_roof,
                 "tree": {k: st[k] for k in ("depth", "root_b", "nodes", "leaves", "halvings", "units")},
-                "walk_counters": {k: st[k] for k in ("loaded", "staged", "tests", "exact_tests", "mask_words",
-                                                     "cand_slots")},
+                "walk_counters": {k: st.get(k) for k in ("loaded", "staged", "tests", "exact_tests", "mask_words",
+                                                         "cand_slots", "list_entries", "big_units")},
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if ws > 1:

@@ -175,9 +175,11 @@ typedef struct bt_stats {
     int64_t staged;       /* candidate records staged by the count pass       */
     int64_t tests;        /* pair tests issued by the count pass              */
     int64_t exact_tests;  /* pairs decided by the fp64 predicate itself       */
-    int64_t loaded;       /* particle records read by the gather (before the cull) */
-    int64_t mask_words;   /* 64-bit neighbor masks recorded for the fill pass   */
+    int64_t loaded;       /* particle records read by the staging (before the cull) */
+    int64_t mask_words;   /* 64-bit neighbor mask words allocated for the fill pass */
     int64_t cand_slots;   /* candidate arena slots allocated                     */
+    int64_t list_entries; /* candidate-leaf list entries allocated by the descent */
+    int64_t big_units;    /* units redone by the global-frontier descent pass    */
 } bt_stats;
 
 int bt_tree_stats(const bt_tree *t, bt_stats *out);

@@ -38,7 +38,8 @@ class Stats(C.Structure):
                 ("box_lo", C.c_double * 3), ("box_hi", C.c_double * 3),
                 ("total_pairs", C.c_int64), ("max_count", C.c_int64), ("staged", C.c_int64),
                 ("tests", C.c_int64), ("exact_tests", C.c_int64), ("loaded", C.c_int64),
-                ("mask_words", C.c_int64), ("cand_slots", C.c_int64)]
+                ("mask_words", C.c_int64), ("cand_slots", C.c_int64), ("list_entries", C.c_int64),
+                ("big_units", C.c_int64)]
 
     def as_dict(self):
         d = {}

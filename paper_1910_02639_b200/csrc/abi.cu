@@ -397,6 +397,8 @@ int bt_tree_stats(const bt_tree *t, bt_stats *out) {
     out->loaded = d.loaded;
     out->mask_words = d.mask_words;
     out->cand_slots = d.cand_slots;
+    out->list_entries = d.list_entries;
+    out->big_units = d.big_units;
     return BT_OK;
 }
 
