@@ -283,6 +283,48 @@ __device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, in
     G.E = (E + G.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
 }
 
+// The unit's query box and R'_u only (the descent): the same operations as
+// unit_setup (min / max are exact and order independent), so both kernels
+// see bit-identical boxes.  A whole-leaf unit needs only its queries' h.
+__device__ __forceinline__ void unit_box(const WalkArgs &a, const int4 &UU, int lane, double (&lo)[3], double (&hi)[3],
+                                         double &Ru) {
+    const int q0 = UU.y, nq = UU.z;
+    const bool whole = nq == a.leaf_count[UU.x];
+    double r = 0.0;
+    for (int l = 0; l < 3; l++) {
+        lo[l] = INFINITY;
+        hi[l] = -INFINITY;
+    }
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int k = lane + 32 * h;
+        if (k < nq) {
+            const double t = __dmul_rn(2.0, a.h_tree[q0 + k]);  // 2h (exact)
+            r = fmax(r, __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M)));
+            if (!whole) {
+                const double4 p = a.rec[q0 + k];
+                lo[0] = fmin(lo[0], p.x); lo[1] = fmin(lo[1], p.y); lo[2] = fmin(lo[2], p.z);
+                hi[0] = fmax(hi[0], p.x); hi[1] = fmax(hi[1], p.y); hi[2] = fmax(hi[2], p.z);
+            }
+        }
+    }
+    const double *lb = a.leaf_box + 6 * (int64_t)UU.x;
+    for (int l = 0; l < 3; l++) {
+        lo[l] = whole ? lb[l] : warp_min(lo[l]);
+        hi[l] = whole ? lb[3 + l] : warp_max(hi[l]);
+    }
+    Ru = warp_max(r);
+}
+
+// x / d for 0 <= x < 2^20, d >= 1 (inv = fl32(1/d)): the fp32 quotient is off
+// by at most one, fixed by one remainder test
+__device__ __forceinline__ int small_div(int x, int d, float inv) {
+    int q = __float2int_rz(__fmul_rn(__int2float_rn(x), inv));
+    const int r = x - q * d;
+    q += (r < 0) ? -1 : ((r >= d) ? 1 : 0);
+    return q;
+}
+
 // Warp-uniform allocation from a per-warp slab [cur, end) refilled from a
 // global counter; returns false when the arena capacity was exceeded.
 struct Slab {
@@ -312,8 +354,10 @@ struct DescOut {
 
 // Breadth-first descent of one unit; appends the kept leaves to out[0, lim)
 // (when out != nullptr) and returns how many there are.
-__device__ __forceinline__ DescOut descend(const WalkArgs &a, const UnitGeom &G, int lane, int32_t *fcur,
-                                           int32_t *fnext, long long fcap, int32_t *out, long long lim) {
+__device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo)[3], const double (&qhi)[3],
+                                           double Ru, int lane, int32_t *fcur, int32_t *fnext, long long fcap,
+                                           int32_t *out, long long lim) {
+    const double Ru2 = __dmul_rn(Ru, Ru);
     const unsigned lt = lanemask_lt();
     DescOut r{0, 0, false};
     long long loaded = 0;
@@ -324,11 +368,11 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const UnitGeom &G,
         if (is_leaf) {
             const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
             const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
-            double gx = fmax(0.0, fmax(__dsub_rn(b0.x, G.hi[0]), __dsub_rn(G.lo[0], b1.y)));
-            double gy = fmax(0.0, fmax(__dsub_rn(b0.y, G.hi[1]), __dsub_rn(G.lo[1], b2.x)));
-            double gz = fmax(0.0, fmax(__dsub_rn(b1.x, G.hi[2]), __dsub_rn(G.lo[2], b2.y)));
+            double gx = fmax(0.0, fmax(__dsub_rn(b0.x, qhi[0]), __dsub_rn(qlo[0], b1.y)));
+            double gy = fmax(0.0, fmax(__dsub_rn(b0.y, qhi[1]), __dsub_rn(qlo[1], b2.x)));
+            double gz = fmax(0.0, fmax(__dsub_rn(b1.x, qhi[2]), __dsub_rn(qlo[2], b2.y)));
             double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
-            keep = g2 < G.Ru2;
+            keep = g2 < Ru2;
         }
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
@@ -356,8 +400,8 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const UnitGeom &G,
                     cb = nd.cell_base;
                     int r0[3], r1[3];
                     for (int l = 0; l < 3; l++) {  // Eq. 5 with R'_u (lemma L2)
-                        r0[l] = cell_coord(__dsub_rn(G.lo[l], G.Ru), nd.lo[l], nd.ext[l], b);
-                        r1[l] = cell_coord(__dadd_rn(G.hi[l], G.Ru), nd.lo[l], nd.ext[l], b);
+                        r0[l] = cell_coord(__dsub_rn(qlo[l], Ru), nd.lo[l], nd.ext[l], b);
+                        r1[l] = cell_coord(__dadd_rn(qhi[l], Ru), nd.lo[l], nd.ext[l], b);
                     }
                     r0x = r0[0];
                     r0y = r0[1];
@@ -394,9 +438,11 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const UnitGeom &G,
                     int32_t code = -1;
                     if (g < T) {
                         const int local = (int)(g - ostart);
-                        const int cx = ox + local % onx;
-                        const int cy = oy + (local / onx) % ony;
-                        const int cz = oz + local / (onx * ony);
+                        const int qx = small_div(local, onx, 1.0f / (float)onx);
+                        const int qy = small_div(qx, ony, 1.0f / (float)ony);
+                        const int cx = ox + (local - qx * onx);
+                        const int cy = oy + (qx - qy * ony);
+                        const int cz = oz + qy;
                         const long long j = cx + (long long)cy * ob + (long long)cz * ob * ob;  // Eq. 3
                         code = a.cells[ocb + j];
                         is_leaf = code >= 0;
@@ -459,34 +505,35 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
         uid = __shfl_sync(0xffffffffu, uid, 0);
         if (uid >= (unsigned long long)a.n_units) break;
         if (kBig && a.urun[uid].nleaf >= 0) continue;
-        UnitGeom G;
-        unit_setup(a, a.units[uid], lane, G);
+        const int4 U = a.units[uid];
+        double qlo[3], qhi[3], Ru;
+        unit_box(a, U, lane, qlo, qhi, Ru);
         UnitRun &R = a.urun[uid];
         if (!kBig) {
             const bool ok = slab_reserve(ls, kListReserve, kListSlab, a.list_cap, &a.ctr[C_LIST], lane);
             const long long lim = ls.end - ls.cur;
-            DescOut d = descend(a, G, lane, f0, f1, fcap, ok ? a.ulist + ls.cur : nullptr, lim);
+            DescOut d = descend(a, qlo, qhi, Ru, lane, f0, f1, fcap, ok ? a.ulist + ls.cur : nullptr, lim);
             const bool fits = ok && !d.overflow && d.nleaf <= lim;
             if (lane == 0) {
                 R.list_off = ls.cur;
                 R.nleaf = fits ? d.nleaf : -1;
                 R.loaded = (int)d.loaded;
                 if (!fits) atomicAdd((unsigned long long *)&a.ctr[C_BIG], 1ull);
-                else add_need(a, d.loaded, G.nq);
+                else add_need(a, d.loaded, U.z);
             }
             if (fits) ls.cur += d.nleaf;
         } else {
-            DescOut d = descend(a, G, lane, f0, f1, fcap, nullptr, 0);
+            DescOut d = descend(a, qlo, qhi, Ru, lane, f0, f1, fcap, nullptr, 0);
             long long base = 0;
             if (lane == 0) base = (long long)atomicAdd((unsigned long long *)&a.ctr[C_LIST], (unsigned long long)d.nleaf);
             base = __shfl_sync(0xffffffffu, base, 0);
             const bool ok = !d.overflow && base + d.nleaf <= a.list_cap;
-            if (ok) descend(a, G, lane, f0, f1, fcap, a.ulist + base, d.nleaf);
+            if (ok) descend(a, qlo, qhi, Ru, lane, f0, f1, fcap, a.ulist + base, d.nleaf);
             if (lane == 0) {
                 R.list_off = base;
                 R.nleaf = ok ? d.nleaf : -2;  // -2: list arena too small (host grows it and redoes the pass)
                 R.loaded = (int)d.loaded;
-                add_need(a, d.loaded, G.nq);
+                add_need(a, d.loaded, U.z);
             }
         }
         __syncwarp();
