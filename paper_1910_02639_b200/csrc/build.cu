@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const LevelNode *__restr
                                                         NodeRec *nodes, int32_t *cells, int64_t cells_base,
                                                         LevelNode *ln_next, int32_t next_gid_base, int32_t *leaf_begin,
                                                         int32_t *leaf_count, int32_t *leaf_depth, int64_t leaf_base,
-                                                        int32_t child_depth, int32_t *cdst, int32_t s) {
+                                                        int32_t child_depth, int2 *cmove, int32_t s) {
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ncells; g += (int64_t)gridDim.x * blockDim.x) {
         int64_t node = find_node(ln, nn, g);
         const LevelNode &L = ln[node];
@@ -310,14 +310,14 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const LevelNode *__restr
                 R.b = 0;
                 R.cell_base = 0;
                 code = node_code(gid);
-                cdst[g] = cact[g];
+                cmove[g] = make_int2(cact[g], id);  // next-level position, child node (level-local)
             } else {
                 int64_t leaf = leaf_base + id;
                 leaf_begin[leaf] = final_pos;
                 leaf_count[leaf] = c;
                 leaf_depth[leaf] = child_depth;
                 code = (int32_t)leaf;
-                cdst[g] = final_pos;
+                cmove[g] = make_int2(final_pos, -1);  // final tree position, leaf
             }
         }
         cells[cells_base + g] = code;
@@ -339,22 +339,21 @@ __global__ void finalize_level_nodes_kernel(const LevelNode *ln, int64_t nn, Nod
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__restrict__ act, const int32_t *__restrict__ act_node,
                                                            int64_t n_act, const LevelNode *__restrict__ ln,
                                                            const uint32_t *__restrict__ keys, int32_t *__restrict__ cursor,
-                                                           const int32_t *__restrict__ cells, int64_t cells_base,
-                                                           const int32_t *__restrict__ cdst, const int32_t *__restrict__ cid,
+                                                           const int2 *__restrict__ cmove,
                                                            double4 *__restrict__ out_final, double4 *__restrict__ act_next,
                                                            int32_t *__restrict__ act_node_next) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_act; p += (int64_t)gridDim.x * blockDim.x) {
         int32_t node = act_node[p];
         int64_t g = ln[node].cell_base + keys[p];
         int32_t r = atomicAdd(&cursor[g], 1);
-        int32_t code = cells[cells_base + g];
+        const int2 mv = cmove[g];  // one random 8-byte load per particle
         double4 v = act[p];
-        int32_t dst = cdst[g] + r;
-        if (code >= 0) {
+        int32_t dst = mv.x + r;
+        if (mv.y < 0) {
             out_final[dst] = v;
         } else {
             act_next[dst] = v;
-            act_node_next[dst] = cid[g];
+            act_node_next[dst] = mv.y;
         }
     }
 }
@@ -371,8 +370,54 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
     int lane = threadIdx.x & 31;
     int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    int wmax = 0, wover = 0;
     for (int64_t L = warp; L < n_leaves; L += nwarps) {
         int32_t b0 = leaf_begin[L], m = leaf_count[L];
+        if (m <= 64) {
+            // single pass, the leaf's records in registers (two per lane)
+            const bool ok0 = lane < m, ok1 = lane + 32 < m;
+            const double4 v0 = ok0 ? src[b0 + lane] : make_double4(0, 0, 0, 0);
+            const double4 v1 = ok1 ? src[b0 + 32 + lane] : make_double4(0, 0, 0, 0);
+            double mn[3], mx[3];
+            mn[0] = fmin(ok0 ? v0.x : INFINITY, ok1 ? v1.x : INFINITY);
+            mn[1] = fmin(ok0 ? v0.y : INFINITY, ok1 ? v1.y : INFINITY);
+            mn[2] = fmin(ok0 ? v0.z : INFINITY, ok1 ? v1.z : INFINITY);
+            mx[0] = fmax(ok0 ? v0.x : -INFINITY, ok1 ? v1.x : -INFINITY);
+            mx[1] = fmax(ok0 ? v0.y : -INFINITY, ok1 ? v1.y : -INFINITY);
+            mx[2] = fmax(ok0 ? v0.z : -INFINITY, ok1 ? v1.z : -INFINITY);
+            double c[3];
+            for (int l = 0; l < 3; l++) {
+                double a = mn[l], b = mx[l];
+                for (int d = 16; d; d >>= 1) {
+                    a = fmin(a, __shfl_xor_sync(0xffffffffu, a, d));
+                    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, d));
+                }
+                if (lane == 0) { leaf_box[6 * L + l] = a; leaf_box[6 * L + 3 + l] = b; }
+                c[l] = 0.5 * (a + b);  // leaf centre for the compact fp32 records
+            }
+            // canonical order: rank(e) = #{k : idx_k < idx_e} (caller indices < 2^31, distinct)
+            const int i0 = ok0 ? (int)__double_as_longlong(v0.w) : 0x7fffffff;
+            const int i1 = ok1 ? (int)__double_as_longlong(v1.w) : 0x7fffffff;
+            int r0 = 0, r1 = 0;
+            for (int j = 0; j < 32; j++) {
+                const int o0 = __shfl_sync(0xffffffffu, i0, j), o1 = __shfl_sync(0xffffffffu, i1, j);
+                r0 += (o0 < i0) + (o1 < i0);
+                r1 += (o0 < i1) + (o1 < i1);
+            }
+            if (ok0) {
+                dst[b0 + r0] = v0;
+                dst32[b0 + r0] = make_float4(__double2float_rn(__dsub_rn(v0.x, c[0])), __double2float_rn(__dsub_rn(v0.y, c[1])),
+                                             __double2float_rn(__dsub_rn(v0.z, c[2])), __int_as_float(i0));
+            }
+            if (ok1) {
+                dst[b0 + r1] = v1;
+                dst32[b0 + r1] = make_float4(__double2float_rn(__dsub_rn(v1.x, c[0])), __double2float_rn(__dsub_rn(v1.y, c[1])),
+                                             __double2float_rn(__dsub_rn(v1.z, c[2])), __int_as_float(i1));
+            }
+            wmax = max(wmax, m);
+            wover += (m > s) ? 1 : 0;  // over-full leaf (depth cap, R14)
+            continue;
+        }
         // tight box (exact fp64 min / max)
         double mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
         for (int32_t e = lane; e < m; e += 32) {
@@ -417,10 +462,13 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
                                                __double2float_rn(__dsub_rn(v.z, c[2])), __int_as_float((int)my));
             }
         }
-        if (lane == 0) {
-            atomicMax(max_leaf, (unsigned long long)m);
-            if (m > s) atomicAdd(max_leaf + 1, 1ull);  // over-full leaf (depth cap, R14)
-        }
+        wmax = max(wmax, m);
+        wover += (m > s) ? 1 : 0;
+    }
+    // one atomic per warp (a per-leaf atomic on one address serialises 10^6 updates)
+    if (lane == 0 && wmax > 0) {
+        atomicMax(max_leaf, (unsigned long long)wmax);
+        if (wover) atomicAdd(max_leaf + 1, (unsigned long long)wover);
     }
 }
 
@@ -619,7 +667,8 @@ void build_tree(TreeDev &t, const double *pos) {
         int level = 0;
         DBuf<int32_t> hist;
         DBuf<int64_t> cpre;
-        DBuf<int32_t> cid, cact, cdst;
+        DBuf<int32_t> cid, cact;
+        DBuf<int2> cmove;
         DBuf<long long> dtotal(1);
         DBuf<CellScan> dcs(1);
         while (nn > 0) {
@@ -635,7 +684,7 @@ void build_tree(TreeDev &t, const double *pos) {
             cpre.reserve(ncells, 0);
             cid.reserve(ncells, 0);
             cact.reserve(ncells, 0);
-            cdst.reserve(ncells, 0);
+            cmove.reserve(ncells, 0);
             t.cells.reserve(t.n_cells + ncells, t.n_cells);
             BT_CUDA(cudaMemsetAsync(hist.p, 0, ncells * sizeof(int32_t), st));
             const unsigned gridC = grid_for(ncells, kThreads, (int64_t)sms * 16);
@@ -680,14 +729,13 @@ void build_tree(TreeDev &t, const double *pos) {
             emit_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, cpre.p, cid.p, cact.p, t.nodes.p, t.cells.p,
                                                     t.n_cells, child_ok ? ln_next.p : nullptr, (int32_t)t.n_nodes,
                                                     t.leaf_begin.p, t.leaf_count.p, t.leaf_depth.p, t.n_leaves,
-                                                    level + 1, cdst.p, t.s);
+                                                    level + 1, cmove.p, t.s);
             BT_LAUNCH("emit");
 
             // A7: scatter (cursor = zeroed histogram)
             BT_CUDA(cudaMemsetAsync(hist.p, 0, ncells * sizeof(int32_t), st));
-            scatter_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, keys.p, hist.p, t.cells.p,
-                                                       t.n_cells, cdst.p, cid.p, fin.p, act[cur ^ 1].p,
-                                                       act_node[cur ^ 1].p);
+            scatter_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, keys.p, hist.p, cmove.p,
+                                                       fin.p, act[cur ^ 1].p, act_node[cur ^ 1].p);
             BT_LAUNCH("scatter");
 
             if (nleaf > 0) t.depth = level + 1;
