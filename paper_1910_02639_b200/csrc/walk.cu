@@ -97,6 +97,7 @@ struct WalkArgs {
     unsigned long long *masks;
     long long mask_cap;
     float4 *scratch;          // per walk warp: kScratch staged candidates (ax, ay, az, tree position)
+    int desc_batch;           // units claimed per atomic by the descent warps
 };
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -325,6 +326,23 @@ __device__ __forceinline__ int small_div(int x, int d, float inv) {
     return q;
 }
 
+// Persistent warps claim work units in batches of consecutive (Morton-ordered,
+// so spatially adjacent) units: one returning atomic per batch instead of one
+// per unit on a single address, which serialised ~10^6 atomics per launch.
+struct WorkBatch {
+    long long next = 0, end = 0;
+};
+__device__ __forceinline__ long long next_unit(WorkBatch &w, long long *ctr, long long n, int batch, int lane) {
+    if (w.next >= w.end) {
+        long long b = 0;
+        if (lane == 0) b = (long long)atomicAdd((unsigned long long *)ctr, (unsigned long long)batch);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        w.next = b;
+        w.end = b + batch < n ? b + batch : n;
+    }
+    return w.next < w.end ? w.next++ : n;
+}
+
 // Warp-uniform allocation from a per-warp slab [cur, end) refilled from a
 // global counter; returns false when the arena capacity was exceeded.
 struct Slab {
@@ -499,11 +517,10 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
         fcap = kFrontCap;
     }
     Slab ls;
+    WorkBatch wb;
     for (;;) {
-        unsigned long long uid = 0;
-        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[kBig ? C_WORK4 : C_WORK], 1ull);
-        uid = __shfl_sync(0xffffffffu, uid, 0);
-        if (uid >= (unsigned long long)a.n_units) break;
+        const long long uid = next_unit(wb, &a.ctr[kBig ? C_WORK4 : C_WORK], a.n_units, kBig ? 1 : a.desc_batch, lane);
+        if (uid >= a.n_units) break;
         if (kBig && a.urun[uid].nleaf >= 0) continue;
         const int4 U = a.units[uid];
         double qlo[3], qhi[3], Ru;
@@ -827,11 +844,10 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         S.u.tests = S.u.exact = S.u.staged = S.u.loaded = 0;
     }
     __syncwarp();
+    WorkBatch wb;
     for (;;) {
-        unsigned long long uid = 0;
-        if (lane == 0) uid = atomicAdd((unsigned long long *)&a.ctr[C_WORK3], 1ull);
-        uid = __shfl_sync(0xffffffffu, uid, 0);
-        if (uid >= (unsigned long long)a.n_units) break;
+        const long long uid = next_unit(wb, &a.ctr[C_WORK3], a.n_units, 1, lane);
+        if (uid >= a.n_units) break;
         const UnitRun R = a.urun[uid];
         int32_t qo[2];
         int nq;
@@ -1029,13 +1045,12 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt(), lanebit = 1u << lane;
     FillSmem &F = fsm[threadIdx.x >> 5];
+    WorkBatch wb;
     const int32_t *__restrict__ cands = a.cands;
     const unsigned long long *__restrict__ masks = a.masks;
     for (;;) {
-        unsigned long long u = 0;
-        if (lane == 0) u = atomicAdd((unsigned long long *)&a.ctr[C_WORK2], 1ull);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= (unsigned long long)a.n_units) break;
+        const long long u = next_unit(wb, &a.ctr[C_WORK2], a.n_units, 1, lane);
+        if (u >= a.n_units) break;
         const int4 U = a.units[u];
         const UnitRun R = a.urun[u];
         const int nq = U.z;
@@ -1176,6 +1191,8 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     a.root_is_leaf = t.root_is_leaf ? 1 : 0;
     a.exact_only = g_exact_only;
     a.urun = t.urun.p;
+    // descent batches: up to 8 units per claim while every warp still gets >= 8 claims
+    a.desc_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, t.n_units / ((int64_t)grid_d * (kDescThreads / 32) * 8)));
     a.offsets = offsets;
     a.nbr = nbr_idx;
     a.ctr = (long long *)t.counters.p;
