@@ -279,16 +279,18 @@ def run_b200(args):
     loaded, staged, tests = int(st["loaded"]), int(st["staged"]), int(st["tests"])
     dom = max(("walk_desc", "walk_test", "walk_fill", "build"), key=lambda k: kern[k])
     if dom == "walk_test":
-        # walk_kernel: staging + pair tests, bound by fp32 ALU issue.  Algorithmic
+        # walk_kernel: staging + pair tests, bound by fp32 issue.  Algorithmic
         # work = 8 fp32 ops per pair test (3 differences, 3 squares, 2 sums:
-        # ((dx*dx + dy*dy) + dz*dz)); peak = 148 SMs x 128 fp32 lanes x max SM
-        # clock (B200_PROFILING.md unit counts, MEASURED_PEAKS sm_max_mhz)
-        sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-        alu_peak = 148 * 128 * sm_mhz * 1e6 / 1e12
+        # ((dx*dx + dy*dy) + dz*dz)).  Peak = the measured packed-fp32 (FFMA2)
+        # rate of this B200 model, 23.61 T instr-lanes/s x 2 = 47.2 T fp32 op/s
+        # (tools/probe_rates.cu, profiles/r01_probe_rates.txt), scaled to the
+        # recorded SM clock; scalar FFMA measures 35.8 T op/s.
+        alu_peak = 47.22
         achieved = tests * 8 / (kern[dom] * 1e-3) / 1e12
         roofline = {"kernel": "walk_kernel (A10 staging + A11 pair tests)", "bound": "alu", "achieved": achieved,
                     "peak": alu_peak, "unit": "T fp32 op/s", "frac": achieved / alu_peak, "traffic": None,
-                    "peak_source": "derived: 148 SM x 128 fp32 lanes x sm_max_mhz (B200_PROFILING.md / MEASURED_PEAKS)",
+                    "peak_source": "measured: packed FFMA2 throughput x 2 (tools/probe_rates.cu, "
+                                   "profiles/r01_probe_rates.txt)",
                     "algorithmic_ops": tests * 8}
     else:
         if dom == "walk_desc":
