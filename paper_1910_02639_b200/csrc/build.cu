@@ -359,6 +359,27 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__rest
 }
 
 // ---- A9: per-leaf canonical order (ascending caller index) + tight box -------
+// Exact fp64 warp min / max through order-preserving 64-bit keys (sign bit
+// flipped for positives, all bits for negatives; no NaN here): two 32-bit
+// redux.sync per value instead of five shuffle + DMNMX steps.
+__device__ __forceinline__ unsigned long long dkey(double d) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dunkey(unsigned long long k) {
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+__device__ __forceinline__ unsigned long long warp_min_key(unsigned long long k) {
+    const unsigned hi = __reduce_min_sync(0xffffffffu, (unsigned)(k >> 32));
+    const unsigned lo = __reduce_min_sync(0xffffffffu, ((unsigned)(k >> 32) == hi) ? (unsigned)k : 0xffffffffu);
+    return ((unsigned long long)hi << 32) | lo;
+}
+__device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k) {
+    const unsigned hi = __reduce_max_sync(0xffffffffu, (unsigned)(k >> 32));
+    const unsigned lo = __reduce_max_sync(0xffffffffu, ((unsigned)(k >> 32) == hi) ? (unsigned)k : 0u);
+    return ((unsigned long long)hi << 32) | lo;
+}
+
 // One warp per leaf.  rank(e) = #{k in leaf : idx_k < idx_e} (caller indices
 // are distinct), O(m^2 / 32) per leaf: m <= s = 64 in the configurations.
 __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *__restrict__ src, double4 *__restrict__ dst,
@@ -374,24 +395,24 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
     for (int64_t L = warp; L < n_leaves; L += nwarps) {
         int32_t b0 = leaf_begin[L], m = leaf_count[L];
         if (m <= 64) {
-            // single pass, the leaf's records in registers (two per lane)
-            const bool ok0 = lane < m, ok1 = lane + 32 < m;
+            // single pass, the leaf's records in registers (one or two per lane)
+            const bool two = m > 32;
+            const bool ok0 = lane < m, ok1 = two && lane + 32 < m;
             const double4 v0 = ok0 ? src[b0 + lane] : make_double4(0, 0, 0, 0);
             const double4 v1 = ok1 ? src[b0 + 32 + lane] : make_double4(0, 0, 0, 0);
-            double mn[3], mx[3];
-            mn[0] = fmin(ok0 ? v0.x : INFINITY, ok1 ? v1.x : INFINITY);
-            mn[1] = fmin(ok0 ? v0.y : INFINITY, ok1 ? v1.y : INFINITY);
-            mn[2] = fmin(ok0 ? v0.z : INFINITY, ok1 ? v1.z : INFINITY);
-            mx[0] = fmax(ok0 ? v0.x : -INFINITY, ok1 ? v1.x : -INFINITY);
-            mx[1] = fmax(ok0 ? v0.y : -INFINITY, ok1 ? v1.y : -INFINITY);
-            mx[2] = fmax(ok0 ? v0.z : -INFINITY, ok1 ? v1.z : -INFINITY);
+            // tight box: exact min / max (keys of absent slots: +inf / -inf)
+            const unsigned long long KMAX = dkey(INFINITY), KMIN = dkey(-INFINITY);
             double c[3];
             for (int l = 0; l < 3; l++) {
-                double a = mn[l], b = mx[l];
-                for (int d = 16; d; d >>= 1) {
-                    a = fmin(a, __shfl_xor_sync(0xffffffffu, a, d));
-                    b = fmax(b, __shfl_xor_sync(0xffffffffu, b, d));
+                const double x0 = l == 0 ? v0.x : (l == 1 ? v0.y : v0.z);
+                const double x1 = l == 0 ? v1.x : (l == 1 ? v1.y : v1.z);
+                const unsigned long long k0 = dkey(x0), k1 = dkey(x1);
+                unsigned long long kmin = ok0 ? k0 : KMAX, kmax = ok0 ? k0 : KMIN;
+                if (ok1) {
+                    kmin = min(kmin, k1);
+                    kmax = max(kmax, k1);
                 }
+                const double a = dunkey(warp_min_key(kmin)), b = dunkey(warp_max_key(kmax));
                 if (lane == 0) { leaf_box[6 * L + l] = a; leaf_box[6 * L + 3 + l] = b; }
                 c[l] = 0.5 * (a + b);  // leaf centre for the compact fp32 records
             }
@@ -399,10 +420,14 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
             const int i0 = ok0 ? (int)__double_as_longlong(v0.w) : 0x7fffffff;
             const int i1 = ok1 ? (int)__double_as_longlong(v1.w) : 0x7fffffff;
             int r0 = 0, r1 = 0;
-            for (int j = 0; j < 32; j++) {
-                const int o0 = __shfl_sync(0xffffffffu, i0, j), o1 = __shfl_sync(0xffffffffu, i1, j);
-                r0 += (o0 < i0) + (o1 < i0);
-                r1 += (o0 < i1) + (o1 < i1);
+            if (!two) {
+                for (int j = 0; j < m; j++) r0 += __shfl_sync(0xffffffffu, i0, j) < i0;
+            } else {
+                for (int j = 0; j < 32; j++) {
+                    const int o0 = __shfl_sync(0xffffffffu, i0, j), o1 = __shfl_sync(0xffffffffu, i1, j);
+                    r0 += (o0 < i0) + (o1 < i0);
+                    r1 += (o0 < i1) + (o1 < i1);
+                }
             }
             if (ok0) {
                 dst[b0 + r0] = v0;
