@@ -304,3 +304,26 @@ def test_octree_policy_parity(P, oracle, cfg, n):
     ot = oracle.Tree(pos, 64, 0.5, policy="octree")
     assert_same(gpu, ot.neighbors(h))
     assert_same_tree(t, ot)
+
+
+# ---- rare walk paths: big-unit descent, scratch-full resume ----------------------
+def test_big_unit_descent_pass(P, oracle):
+    """s = 1 (one particle per leaf) and ~3000 neighbors per particle: units list
+    more than 2048 candidate leaves, so the descent's global-frontier pass
+    (desc_kernel<true>) redoes them; results must equal brute force."""
+    pos, h = datagen.uniform(20_000, 41, 0.17)
+    t, gpu = gpu_run(P, pos, h, s=1)
+    assert t.stats()["big_units"] > 0
+    assert_same(gpu, oracle.brute_force(pos, h))
+
+
+def test_scratch_full_resume(P, oracle):
+    """2h > domain with n = 6000: every unit stages all 6000 particles, more than
+    the walk's per-warp scratch (4096), so staging stops, tests the full
+    blocks and resumes; every particle sees the other n - 1."""
+    pos, h = datagen.uniform(6000, 43, 2.0)
+    t, gpu = gpu_run(P, pos, h, s=64)
+    assert np.all(gpu[0] == 5999)
+    assert_same(gpu, oracle.brute_force(pos, h))
+    st = t.stats()
+    assert st["staged"] == st["units"] * 6000  # every unit staged every particle
