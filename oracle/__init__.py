@@ -88,6 +88,12 @@ def lib():
         L.orc_brute_count.restype = None
         L.orc_brute_rows.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, _P, _P, C.c_int]
         L.orc_brute_rows.restype = C.c_int
+        L.orc_w_m4.argtypes = [C.c_double]
+        L.orc_w_m4.restype = C.c_double
+        L.orc_density.argtypes = [_P, _P, _P, _P, _P, C.c_int64, _P, C.c_int]
+        L.orc_density.restype = None
+        L.orc_brute_density.argtypes = [_P, _P, _P, C.c_int64, _P, C.c_int64, _P, C.c_int]
+        L.orc_brute_density.restype = None
         L.orc_max_threads.argtypes = []
         L.orc_max_threads.restype = C.c_int
         _lib = L
@@ -206,6 +212,37 @@ class Tree:
         if rc != 0:
             raise RuntimeError("oracle: row length changed between passes")
         return counts, offsets, idx
+
+    def density(self, h, mass, queries=None, threads: int | None = None):
+        """SPH density (reading R21: M4 cubic spline, support 2h, gather h):
+        rho_i = m_i W(0, h_i) + sum over the tree walk's N(i) of m_j W(r_ij, h_i)."""
+        h = _f64(h)
+        mass = _f64(mass)
+        q = None if queries is None else np.ascontiguousarray(queries, dtype=np.int64)
+        nq = self.n if q is None else q.size
+        rho = np.empty(nq, dtype=np.float64)
+        lib().orc_density(self._h, _ptr(self.pos), _ptr(h), _ptr(mass), _ptr(q), nq, _ptr(rho),
+                          threads or default_threads())
+        return rho
+
+
+def w_m4(q: float) -> float:
+    """The M4 cubic spline shape w(q) of the density consumer (R21)."""
+    return lib().orc_w_m4(float(q))
+
+
+def brute_density(pos, h, mass, queries=None, threads: int | None = None):
+    """SPH density by the plain definition (every j != i passing the predicate)."""
+    pos = _f64(pos, (-1, 3))
+    h = _f64(h)
+    mass = _f64(mass)
+    n = pos.shape[0]
+    q = None if queries is None else np.ascontiguousarray(queries, dtype=np.int64)
+    nq = n if q is None else q.size
+    rho = np.empty(nq, dtype=np.float64)
+    lib().orc_brute_density(_ptr(pos), _ptr(h), _ptr(mass), n, _ptr(q), nq, _ptr(rho),
+                            threads or default_threads())
+    return rho
 
 
 def brute_force(pos, h, queries=None, threads: int | None = None):

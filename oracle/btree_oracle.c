@@ -552,6 +552,87 @@ int orc_brute_rows(const double *pos, const double *h, int64_t n,
     return bad ? -1 : 0;
 }
 
+/* ------------------------------------------------------------------ */
+/* SPH density consumer (the paper's use of the     */
+/* neighbor lists, Sec. I P:50-56 and Sec. IV-H).  Reading    */
+/* R21 (not in the paper): the M4 cubic spline of compact support 2h,   */
+/*   W(r, h) = w(r / h) / (pi h^3),                                     */
+/*   w(q) = 1 - 1.5 q^2 + 0.75 q^3 (0 <= q < 1),  0.25 (2 - q)^3        */
+/*   (1 <= q < 2),  0 (q >= 2),                                         */
+/* and rho_i = m_i W(0, h_i) + sum_{j in N(i)} m_j W(r_ij, h_i), the     */
+/* gather form with the query's h (R13), r_ij = sqrt of the predicate's */
+/* d^2 = ((dx*dx + dy*dy) + dz*dz).  Plain fp64.                         */
+/* ------------------------------------------------------------------ */
+#define ORC_PI 3.14159265358979323846
+
+double orc_w_m4(double q)
+{
+    if (q < 1.0)
+        return 1.0 - 1.5 * q * q + 0.75 * q * q * q;
+    if (q < 2.0) {
+        double t = 2.0 - q;
+        return 0.25 * t * t * t;
+    }
+    return 0.0;
+}
+
+static double pair_r(const double *xi, const double *xj)
+{
+    double dx = xi[0] - xj[0];
+    double dy = xi[1] - xj[1];
+    double dz = xi[2] - xj[2];
+    return sqrt((dx * dx + dy * dy) + dz * dz);
+}
+
+/* rho of the listed queries through the tree walk (rows ascending). */
+void orc_density(const orc_tree *t, const double *pos, const double *h, const double *mass,
+                 const int64_t *queries, int64_t nq, double *rho, int nthreads)
+{
+    (void)nthreads;
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t k = 0; k < nq; k++) {
+        int64_t i = queries ? queries[k] : k;
+        orc_row row = {NULL, 0, 0};
+        one_row(t, pos, h, i, &row); /* count */
+        int32_t *buf = (int32_t *)malloc(sizeof(int32_t) * (size_t)(row.len > 0 ? row.len : 1));
+        orc_row full = {buf, row.len, 0};
+        one_row(t, pos, h, i, &full);
+        qsort(buf, (size_t)full.len, sizeof(int32_t), cmp_i32);
+        double sum = mass[i] * orc_w_m4(0.0);
+        for (int64_t a = 0; a < full.len; a++) {
+            int64_t j = buf[a];
+            sum += mass[j] * orc_w_m4(pair_r(pos + 3 * i, pos + 3 * j) / h[i]);
+        }
+        free(buf);
+        rho[k] = sum / (ORC_PI * h[i] * h[i] * h[i]);
+    }
+}
+
+/* The same sum by the plain definition: every j != i passing the predicate. */
+void orc_brute_density(const double *pos, const double *h, const double *mass, int64_t n,
+                       const int64_t *queries, int64_t nq, double *rho, int nthreads)
+{
+    (void)nthreads;
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t k = 0; k < nq; k++) {
+        int64_t i = queries ? queries[k] : k;
+        double two_h = 2.0 * h[i];
+        double T = two_h * two_h;
+        double sum = mass[i] * orc_w_m4(0.0);
+        for (int64_t j = 0; j < n; j++) {
+            if (j == i)
+                continue;
+            double dx = pos[3 * i + 0] - pos[3 * j + 0];
+            double dy = pos[3 * i + 1] - pos[3 * j + 1];
+            double dz = pos[3 * i + 2] - pos[3 * j + 2];
+            double d2 = (dx * dx + dy * dy) + dz * dz;
+            if (d2 < T)
+                sum += mass[j] * orc_w_m4(sqrt(d2) / h[i]);
+        }
+        rho[k] = sum / (ORC_PI * h[i] * h[i] * h[i]);
+    }
+}
+
 int orc_max_threads(void)
 {
 #ifdef _OPENMP

@@ -300,3 +300,48 @@ def test_octree_same_neighbors_deeper_tree(oracle):
     assert oc.stats()["depth"] >= bt.stats()["depth"]
     perm, lb, lc, _ = oc.order()
     assert np.array_equal(np.sort(perm), np.arange(len(pos))) and np.all(lc <= 16)
+
+
+# ---- SPH density consumer (reading R21: M4 cubic spline) -----
+def test_density_kernel_normalisation_and_shape(oracle):
+    """W(r, h) = w(r/h) / (pi h^3) integrates to one over its support 2h (the
+    defining normalisation of an SPH kernel), w and w' are continuous at q = 1
+    and q = 2, and hand-computed values hold."""
+    from scipy.integrate import quad
+    for h in (0.3, 1.0, 2.5):
+        tot, _ = quad(lambda r: 4.0 * np.pi * r * r * oracle.w_m4(r / h) / (np.pi * h ** 3), 0.0, 2.0 * h,
+                      points=[h], epsabs=1e-13)
+        assert abs(tot - 1.0) < 1e-10
+    e = 1e-7
+    for q in (1.0, 2.0):
+        assert abs(oracle.w_m4(q - e) - oracle.w_m4(q + e)) < 1e-6
+        d_left = (oracle.w_m4(q - e) - oracle.w_m4(q - 2 * e)) / e
+        d_right = (oracle.w_m4(q + 2 * e) - oracle.w_m4(q + e)) / e
+        assert abs(d_left - d_right) < 1e-5
+    assert oracle.w_m4(0.0) == 1.0
+    assert abs(oracle.w_m4(0.7) - 0.52225) < 1e-15   # 1 - 1.5*0.49 + 0.75*0.343 (by hand)
+    assert oracle.w_m4(1.5) == 0.03125                # 0.25 * 0.5^3
+    assert oracle.w_m4(2.0) == 0.0 and oracle.w_m4(3.0) == 0.0
+
+
+def test_density_closed_forms(oracle):
+    # an isolated particle sees only itself: rho = m W(0, h) = m / (pi h^3)
+    pos = np.array([[0.1, 0.2, 0.3]])
+    rho = oracle.Tree(pos, 8).density(np.array([0.5]), np.array([2.0]))
+    assert rho[0] == 2.0 / (np.pi * 0.125)
+    # a fine unit lattice, unit masses, h = 3 lattice spacings: an interior
+    # particle's kernel sum approximates the continuum density 1 / a^3
+    m = 21
+    pos = datagen.lattice(m, 1.0)
+    h = np.full(len(pos), 3.0)
+    centre = (m // 2) * (m * m + m + 1)
+    rho = oracle.Tree(pos, 64).density(h, np.ones(len(pos)), queries=np.array([centre]))
+    assert abs(rho[0] - 1.0) < 2e-3
+
+
+def test_density_tree_equals_brute_force(oracle):
+    pos, h = datagen.uniform(3000, 17, 0.05, 0.08)
+    mass = np.random.default_rng(3).uniform(0.5, 1.5, len(pos))
+    a = oracle.Tree(pos, 16).density(h, mass)
+    b = oracle.brute_density(pos, h, mass)
+    assert np.array_equal(a, b)   # same terms, same (ascending j) order
