@@ -120,6 +120,28 @@ int bt_find_neighbors(const bt_tree *t, const double *h, int32_t ngmax, int32_t 
 int bt_fill_neighbors(const bt_tree *t, const double *h, const int64_t *offsets,
                       int32_t *nbr_idx, int64_t capacity);
 
+/*
+ * bt_density -- SPH density with the neighbor search fused in (SURVEY 8(f)
+ * row 3: the use the paper builds the lists for, Sec. I, Sec. IV-H
+ * P:540-549), without materialising the CSR.  Reading R21 (the
+ * paper does not fix a kernel): the M4 cubic spline of compact support 2h,
+ *   rho_i = ( m_i w(0) + sum_{j in N(i)} m_j w(r_ij / h_i) ) / (pi h_i^3),
+ *   w(q) = 1 - 1.5 q^2 + 0.75 q^3 (q < 1),  0.25 (2 - q)^3 (1 <= q < 2),
+ * with N(i) exactly the neighbor set of bt_find_neighbors (the same walk and
+ * exact predicate).  The pair distances r_ij are evaluated in fp32 from the
+ * unit-relative coordinates of lemma L4 and the sum of each 128-candidate
+ * block in fp32, blocks accumulated in fp64: relative error <= 1e-4 of rho
+ * (DESIGN.md section 11c).
+ *   h    DEVICE, n fp64, caller order, finite, > 0 (as bt_find_neighbors)
+ *   mass DEVICE, n fp64, caller order, finite
+ *   rho  DEVICE out, n fp64, caller order
+ * Errors: BT_ERR_ARG (NULL tree / pointers), BT_ERR_INPUT (bad h or mass),
+ * BT_ERR_CUDA / BT_ERR_OOM.  Enqueued on the thread's stream; returns after
+ * completion.  Does not touch the masks a previous count pass recorded
+ * (a later bt_fill_neighbors recomputes them).
+ */
+int bt_density(const bt_tree *t, const double *h, const double *mass, double *rho);
+
 /* Frees all tree-owned device memory (into this thread's block cache).  NULL-safe. */
 void bt_free(bt_tree *t);
 

@@ -20,7 +20,8 @@ _NAMES = {0: "BT_OK", 1: "BT_ERR_ARG", 2: "BT_ERR_INPUT", 3: "BT_ERR_CAPACITY", 
           5: "BT_ERR_OOM"}
 
 # every symbol include/btree.h declares
-EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "bt_fill_neighbors", "bt_free",
+EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "bt_fill_neighbors", "bt_density",
+           "bt_free",
            "bt_search_host", "bt_set_stream", "bt_set_exact_only", "bt_release_cache", "bt_last_error", "bt_last_status", "bt_tree_stats",
            "bt_tree_order", "bt_profile_enable", "bt_profile_reset", "bt_profile_get"]
 
@@ -71,6 +72,8 @@ def lib():
         L.bt_find_neighbors.restype = C.c_int
         L.bt_fill_neighbors.argtypes = [_P, _P, _P, _P, C.c_int64]
         L.bt_fill_neighbors.restype = C.c_int
+        L.bt_density.argtypes = [_P, _P, _P, _P]
+        L.bt_density.restype = C.c_int
         L.bt_free.argtypes = [_P]
         L.bt_free.restype = None
         L.bt_search_host.argtypes = [_P, _P, C.c_int64, C.c_int32, C.c_double, _P, _P, _P, C.c_int64]
@@ -180,6 +183,16 @@ class Tree:
         _use_current_stream()
         _check(lib().bt_fill_neighbors(self._handle(), _ptr(h), _ptr(offsets), _ptr(out), out.numel()))
         return out[:total]
+
+    def density(self, h: torch.Tensor, mass: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """SPH density rho [n] fp64 (bt_density: M4 spline, neighbor search fused in)."""
+        h = _dev_f64(h)
+        mass = _dev_f64(mass)
+        if out is None:
+            out = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        _use_current_stream()
+        _check(lib().bt_density(self._handle(), _ptr(h), _ptr(mass), _ptr(out)))
+        return out
 
     def find_neighbors(self, h: torch.Tensor, ngmax: int | None = None,
                        counts=None, offsets=None, nbr_idx=None):

@@ -294,6 +294,19 @@ int bt_fill_neighbors(const bt_tree *tc, const double *h, const int64_t *offsets
     });
 }
 
+int bt_density(const bt_tree *tc, const double *h, const double *mass, double *rho) {
+    bt_tree *t = const_cast<bt_tree *>(tc);
+    if (!t || (t->t.n > 0 && (!h || !mass || !rho))) {
+        set_error(BT_ERR_ARG, "bt_density: need a tree, h, mass and rho");
+        return BT_ERR_ARG;
+    }
+    return guarded([&] {
+        Phase ph("density.total");
+        density(t->t, h, mass, rho);
+        BT_CUDA(cudaStreamSynchronize(stream()));
+    });
+}
+
 void bt_free(bt_tree *t) {
     if (!t) return;
     delete t;  // DBuf destructors return the blocks to this thread's cache

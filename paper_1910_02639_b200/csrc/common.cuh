@@ -155,6 +155,7 @@ struct TreeDev {
     bool root_is_leaf = true;
     // search scratch
     DBuf<double> h_tree;       // h in tree order
+    DBuf<double> m_tree;       // masses in tree order (density consumer)
     DBuf<UnitRun> urun;                    // per-unit walk record
     DBuf<int32_t> ulist;                   // candidate leaf lists of all units
     DBuf<unsigned long long> arena_masks;  // neighbor masks per (64-candidate chunk, query)
@@ -174,6 +175,8 @@ struct TreeDev {
 void build_tree(TreeDev &t, const double *pos);
 void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets,
                     int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass);
+
+void density(TreeDev &t, const double *h, const double *mass, double *rho);
 
 void set_exact_only(int on);
 int release_cache();

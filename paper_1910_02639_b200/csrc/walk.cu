@@ -98,6 +98,8 @@ struct WalkArgs {
     long long mask_cap;
     float4 *scratch;          // per walk warp: kScratch staged candidates (ax, ay, az, tree position)
     int desc_batch;           // units claimed per atomic by the descent warps
+    const double *m_tree;     // density mode: masses in tree order
+    double *rho;              // density mode: output, caller order
 };
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -582,6 +584,28 @@ struct WalkSmem {
     UnitSm u;
 };
 
+// density mode (consumer fusion): per-query 1/h and the
+// block's candidates with their masses
+template <bool kDensity>
+struct DensitySm {};
+template <>
+struct DensitySm<true> {
+    float hinv[kQ];
+    float4 dc[kBlk];  // ax, ay, az (fp32, relative to the unit centre), m_j
+};
+template <bool kDensity>
+struct WalkSmemT : WalkSmem {
+    DensitySm<kDensity> d;
+};
+
+// M4 cubic spline shape (reading R21), fp32
+__device__ __forceinline__ float w_m4f(float q) {
+    const float t = 2.0f - q;
+    const float far = 0.25f * t * t * t;
+    const float near = __fmaf_rn(q * q, __fmaf_rn(0.75f, q, -1.5f), 1.0f);
+    return q < 1.0f ? near : (q < 2.0f ? far : 0.0f);
+}
+
 // The exact band of lemma L4 (rare): recompute the block's pairs with the
 // hot loop's fp32 operations and let the fp64 predicate decide every pair
 // with |d'| <= 1 (all pairs when `force`; padding slots >= n are never
@@ -640,8 +664,9 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
 // Test n (<= kBlk) staged candidates (blk, unit slots us0 .. us0 + n) against
 // the unit's queries and record the block's masks; returns this lane's count
 // increments for queries (lane, lane + 32).
-__device__ __forceinline__ int2 test_block(WalkSmem &S, const WalkArgs &a, int lane, const float4 *blk, int n,
-                                           int us0) {
+template <bool kDensity>
+__device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArgs &a, int lane, const float4 *blk,
+                                           int n, int us0, double (&dacc)[2]) {
     const float inf = __int_as_float(0x7f800000);
     const int nch = (n + 63) >> 6;  // 1 or 2 chunks of 64
     const int nq = S.u.nq;
@@ -724,8 +749,39 @@ __device__ __forceinline__ int2 test_block(WalkSmem &S, const WalkArgs &a, int l
         }
     }
     __syncwarp();
-    // record the masks (the fill pass): chunk kk = us0 / 64 + k of the unit
-    if (S.u.rec_ok) {
+    if constexpr (kDensity) {
+        // consumer fusion: the block's candidates (coordinates, masses) to shared
+        // memory, then lanes = queries sum m_j w(r_ij / h_i) over their set bits
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int sl = 32 * j + lane;
+            if (sl < n) S.d.dc[sl] = make_float4(c[j].x, c[j].y, c[j].z, (float)a.m_tree[__float_as_int(c[j].w)]);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            const int q = lane + 32 * h;
+            if (q < nq) {
+                const float qx = S.q0[q].x, qy = S.q0[q].z, qz = S.q1[q].x, hinv = S.d.hinv[q];
+                float acc = 0.0f;
+                for (int k = 0; k < 2 * nch; k++) {  // 32-bit halves of the chunk masks
+                    unsigned m = (unsigned)(S.mask[k >> 1][q] >> (32 * (k & 1)));
+                    while (m) {
+                        const int sl = 32 * k + __ffs(m) - 1;
+                        m &= m - 1u;
+                        const float4 cd = S.d.dc[sl];
+                        const float dx = cd.x - qx, dy = cd.y - qy, dz = cd.z - qz;
+                        const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+                        const float qq = r2 > 0.0f ? r2 * rsqrtf(r2) * hinv : 0.0f;  // r / h (coincident: 0)
+                        acc = __fmaf_rn(cd.w, w_m4f(qq), acc);
+                    }
+                }
+                dacc[h] += (double)acc;
+            }
+        }
+        __syncwarp();
+    } else if (S.u.rec_ok) {
+        // record the masks (the fill pass): chunk kk = us0 / 64 + k of the unit
         unsigned long long *dst = a.masks + S.u.mask_base + (long long)(us0 >> 6) * nq;
         for (int k = 0; k < nch; k++)
             for (int q = lane; q < nq; q += 32) __stcs(&dst[k * nq + q], S.mask[k][q]);
@@ -831,10 +887,11 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
 #ifndef BT_WALK_MIN_BLOCKS
 #define BT_WALK_MIN_BLOCKS 7
 #endif
+template <bool kDensity>
 __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(WalkArgs a) {
-    __shared__ WalkSmem smem[kWalkThreads / 32];
+    __shared__ WalkSmemT<kDensity> smem[kWalkThreads / 32];
     const int lane = threadIdx.x & 31;
-    WalkSmem &S = smem[threadIdx.x >> 5];
+    WalkSmemT<kDensity> &S = smem[threadIdx.x >> 5];
     const float inf = __int_as_float(0x7f800000);
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     float4 *const scr = a.scratch + gwarp * kScratch;
@@ -850,11 +907,12 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         if (uid >= a.n_units) break;
         const UnitRun R = a.urun[uid];
         int32_t qo[2];
-        int nq;
+        int nq, q0;
         {
             UnitGeom G;
             unit_setup(a, a.units[uid], lane, G);
             nq = G.nq;
+            q0 = G.q0;
             qo[0] = G.qo[0];
             qo[1] = G.qo[1];
             const double eps = l4_eps(G.E);
@@ -881,6 +939,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     const float cq = -mid[h] * ku;  // exact (power-of-two scaling); 0 when forced
                     S.q0[k] = make_float4(ax, ax, ay, ay);
                     S.q1[k] = make_float4(az, az, cq, cq);
+                    if constexpr (kDensity) S.d.hinv[k] = (float)(1.0 / a.h_tree[G.q0 + k]);
                 } else {  // padding query: d' = s k + 2 >= 2 (never a neighbor, never banded)
                     S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
                     S.q1[k] = make_float4(0.f, 0.f, 2.f, 2.f);
@@ -900,8 +959,11 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             // record space for the unit: at most `loaded` candidates
             Slab cs = S.u.cs, ms = S.u.ms;
             const long long need_c = R.loaded, need_m = (long long)((R.loaded + 63) >> 6) * G.nq;
-            const bool okc = slab_reserve(cs, need_c, kCandSlab, a.cand_cap, &a.ctr[C_CAND], lane);
-            const bool okm = slab_reserve(ms, need_m, kMaskSlab, a.mask_cap, &a.ctr[C_MASK], lane);
+            bool okc = false, okm = false;
+            if (!kDensity) {  // the density mode records nothing
+                okc = slab_reserve(cs, need_c, kCandSlab, a.cand_cap, &a.ctr[C_CAND], lane);
+                okm = slab_reserve(ms, need_m, kMaskSlab, a.mask_cap, &a.ctr[C_MASK], lane);
+            }
             __syncwarp();
             if (lane == 0) {
                 S.u.cs = cs;
@@ -923,6 +985,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         }
         __syncwarp();
         int cnt0 = 0, cnt1 = 0;
+        double dacc[2] = {0.0, 0.0};  // density mode: sum of m_j w(r_ij / h_i) of this lane's queries
         long long loaded = 0;
         const int nleaf = R.nleaf;
         const long long list_off = R.list_off;
@@ -986,7 +1049,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             if (true) {} else
 #endif
             for (int b0 = 0; b0 < ntest; b0 += kBlk) {
-                const int2 inc = test_block(S, a, lane, scr + b0, min(kBlk, ntest - b0), slot0 + b0);
+                const int2 inc = test_block<kDensity>(S, a, lane, scr + b0, min(kBlk, ntest - b0), slot0 + b0, dacc);
                 cnt0 += inc.x;
                 cnt1 += inc.y;
             }
@@ -1002,8 +1065,20 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             __syncwarp();
         }
         const int nstaged = slot0;
-        if (lane < nq) a.counts[qo[0]] = cnt0;
-        if (lane + 32 < nq) a.counts[qo[1]] = cnt1;
+        if constexpr (kDensity) {
+            // rho_i = (m_i w(0) + sum_j m_j w(r_ij / h_i)) / (pi h_i^3)   (R21)
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int k = lane + 32 * h;
+                if (k < nq) {
+                    const double hi = a.h_tree[q0 + k];
+                    a.rho[qo[h]] = (a.m_tree[q0 + k] + dacc[h]) / (3.14159265358979323846 * hi * hi * hi);
+                }
+            }
+        } else {
+            if (lane < nq) a.counts[qo[0]] = cnt0;
+            if (lane + 32 < nq) a.counts[qo[1]] = cnt1;
+        }
         __syncwarp();
         if (lane == 0) {
             UnitRun &W = a.urun[uid];
@@ -1132,17 +1207,39 @@ thread_local int g_exact_only = 0;
 
 void set_exact_only(int on) { g_exact_only = on; }
 
-void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
-                    int64_t capacity, bool count_pass, bool fill_pass) {
+namespace {
+
+// masses in tree order + validation (finite, |m| <= 1e150)
+__global__ void gather_m_kernel(const double4 *__restrict__ rec, const double *__restrict__ m, int64_t n,
+                                double *__restrict__ m_tree, int *bad) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const double v = m[__double_as_longlong(rec[k].w)];
+        if (!(fabs(v) <= 1e150)) atomicOr(bad, 1);
+        m_tree[k] = v;
+    }
+}
+
+struct Grids {
+    unsigned d, w, f, big;
+};
+
+template <bool kDensity>
+Grids walk_grids() {
+    const int sms = num_sms();
+    auto grid_of = [&](const void *fn, int threads) {
+        int per_sm = 0;
+        BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
+        return (unsigned)(sms * std::max(per_sm, 1));
+    };
+    return Grids{grid_of((const void *)desc_kernel<false>, kDescThreads),
+                 grid_of((const void *)walk_kernel<kDensity>, kWalkThreads),
+                 grid_of((const void *)fill_kernel, kFillThreads), (unsigned)std::min(sms, 32)};
+}
+
+// h in tree order (validated) + its checksum
+long long gather_h(TreeDev &t, const double *h, const char *who) {
     cudaStream_t st = stream();
     const int64_t n = t.n;
-    if (n == 0) {
-        if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
-        t.total_pairs = t.max_count = t.staged = t.loaded = t.tests = t.exact_tests = 0;
-        BT_CUDA(cudaStreamSynchronize(st));
-        return;
-    }
-    const int sms = num_sms();
     DBuf<int> dbad(1);
     t.h_tree.reserve(n, 0);
     t.counters.reserve(C_N, 0);
@@ -1150,33 +1247,20 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     BT_CUDA(cudaMemsetAsync(t.counters.p + C_HSUM, 0, sizeof(int64_t), st));
     {
         Phase ph("search.gather_h");
-        gather_h_kernel<<<grid_for(n, 256, (int64_t)sms * 16), 256, 0, st>>>(t.rec.p, h, n, t.h_tree.p, dbad.p,
-                                                                            (long long *)t.counters.p + C_HSUM);
+        gather_h_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec.p, h, n, t.h_tree.p, dbad.p,
+                                                                                  (long long *)t.counters.p + C_HSUM);
         BT_LAUNCH("gather_h");
     }
     int hbad = 0;
     long long hsum = 0;
     read_back({{dbad.p, &hbad, sizeof(int)}, {t.counters.p + C_HSUM, &hsum, sizeof(long long)}});
-    if (hbad) throw Error(BT_ERR_INPUT, "bt_find_neighbors: h must be finite, > 0 and <= 1e150");
+    if (hbad) throw Error(BT_ERR_INPUT, std::string(who) + ": h must be finite, > 0 and <= 1e150");
+    return hsum;
+}
 
-    // persistent grids: all resident warps of each kernel
-    auto grid_of = [&](const void *fn, int threads) {
-        int per_sm = 0;
-        BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
-        return (unsigned)(sms * std::max(per_sm, 1));
-    };
-    const unsigned grid_d = grid_of((const void *)desc_kernel<false>, kDescThreads);
-    const unsigned grid_w = grid_of((const void *)walk_kernel, kWalkThreads);
-    const unsigned grid_f = grid_of((const void *)fill_kernel, kFillThreads);
-    const unsigned grid_big = (unsigned)std::min(sms, 32);  // big-unit pass (rare units)
-    t.urun.reserve(t.n_units, 0);
-
-    // the recorded masks of a previous test pass are reused by a fill-only
-    // call when the tree, h pointer, exactness mode and h checksum all match
-    const bool have_record = t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only;
-    const bool run_test = count_pass || !have_record;
-
+WalkArgs walk_args(TreeDev &t, const Grids &g) {
     WalkArgs a{};
+    t.urun.reserve(t.n_units, 0);
     a.rec = t.rec.p;
     a.rec32 = t.rec32.p;
     a.h_tree = t.h_tree.p;
@@ -1192,15 +1276,74 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     a.exact_only = g_exact_only;
     a.urun = t.urun.p;
     // descent batches: up to 8 units per claim while every warp still gets >= 8 claims
-    a.desc_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, t.n_units / ((int64_t)grid_d * (kDescThreads / 32) * 8)));
+    a.desc_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, t.n_units / ((int64_t)g.d * (kDescThreads / 32) * 8)));
+    a.ctr = (long long *)t.counters.p;
+    return a;
+}
+
+void read_counters(TreeDev &t, long long *hc) { read_back({{t.counters.p, hc, C_N * sizeof(long long)}}); }
+void zero_counter(TreeDev &t, int c) { BT_CUDA(cudaMemsetAsync(t.counters.p + c, 0, sizeof(int64_t), stream())); }
+
+// A10: candidate-leaf lists of all units; the leaf-list arena is estimated
+// (grown and redone on overflow).  Leaves the counters in hc.
+void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
+    cudaStream_t st = stream();
+    double list_per_unit = 96.0;
+    const long long warps_d = (long long)g.d * (kDescThreads / 32);
+    for (int attempt = 0;; attempt++) {
+        t.ulist.reserve((long long)(list_per_unit * t.n_units) + warps_d * kListSlab, 0);
+        a.ulist = t.ulist.p;
+        a.list_cap = (long long)t.ulist.n;
+        for (int c : {C_WORK, C_LIST, C_BIG, C_WORK4, C_NEEDC, C_NEEDM}) zero_counter(t, c);
+        {
+            Phase ph("search.desc");
+            desc_kernel<false><<<g.d, kDescThreads, 0, st>>>(a);
+            BT_LAUNCH("walk_desc");
+        }
+        read_counters(t, hc);
+        t.big_units = hc[C_BIG];
+        if (hc[C_BIG] > 0 && hc[C_LIST] <= a.list_cap) {
+            // units beyond the shared-memory frontier / list reserve
+            t.front.reserve((long long)g.big * (kDescThreads / 32) * 2 * std::max<int64_t>(t.n_nodes, 1), 0);
+            a.front = t.front.p;
+            a.front_cap = std::max<int64_t>(t.n_nodes, 1);
+            Phase ph("search.desc_big");
+            desc_kernel<true><<<g.big, kDescThreads, 0, st>>>(a);
+            BT_LAUNCH("walk_desc_big");
+            read_counters(t, hc);
+        }
+        if (hc[C_LIST] <= a.list_cap) break;
+        list_per_unit = 1.25 * (double)hc[C_LIST] / (double)std::max<int64_t>(1, t.n_units);
+        if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: leaf-list arena does not converge");
+    }
+    t.list_entries = hc[C_LIST];
+}
+
+}  // namespace
+
+void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
+                    int64_t capacity, bool count_pass, bool fill_pass) {
+    cudaStream_t st = stream();
+    const int64_t n = t.n;
+    if (n == 0) {
+        if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
+        t.total_pairs = t.max_count = t.staged = t.loaded = t.tests = t.exact_tests = 0;
+        BT_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    const int sms = num_sms();
+    const long long hsum = gather_h(t, h, "bt_find_neighbors");
+    const Grids g = walk_grids<false>();
+
+    // the recorded masks of a previous test pass are reused by a fill-only
+    // call when the tree, h pointer, exactness mode and h checksum all match
+    const bool have_record = t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only;
+    const bool run_test = count_pass || !have_record;
+
+    WalkArgs a = walk_args(t, g);
     a.offsets = offsets;
     a.nbr = nbr_idx;
-    a.ctr = (long long *)t.counters.p;
-
-    auto read_counters = [&](long long *hc) {
-        read_back({{t.counters.p, hc, C_N * sizeof(long long)}});
-    };
-    auto zero = [&](int c) { BT_CUDA(cudaMemsetAsync(t.counters.p + c, 0, sizeof(int64_t), st)); };
+    auto zero = [&](int c) { zero_counter(t, c); };
 
     DBuf<int32_t> tmp_counts;
     if (run_test) {
@@ -1210,41 +1353,11 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             cnt = tmp_counts.p;
         }
         a.counts = cnt;
-        // leaf-list arena: estimated (grown and redone on overflow); candidate
-        // and mask arenas: exact bounds from the descent (no overflow)
-        double list_per_unit = 96.0;
         long long hc[C_N];
         t.rec_valid = false;
-        const long long warps_d = (long long)grid_d * (kDescThreads / 32);
-        const long long warps_w = (long long)grid_w * (kWalkThreads / 32);
-        for (int attempt = 0;; attempt++) {  // A10: candidate-leaf lists
-            t.ulist.reserve((long long)(list_per_unit * t.n_units) + warps_d * kListSlab, 0);
-            a.ulist = t.ulist.p;
-            a.list_cap = (long long)t.ulist.n;
-            for (int c : {C_WORK, C_LIST, C_BIG, C_WORK4, C_NEEDC, C_NEEDM}) zero(c);
-            {
-                Phase ph("search.desc");
-                desc_kernel<false><<<grid_d, kDescThreads, 0, st>>>(a);
-                BT_LAUNCH("walk_desc");
-            }
-            read_counters(hc);
-            t.big_units = hc[C_BIG];
-            if (hc[C_BIG] > 0 && hc[C_LIST] <= a.list_cap) {
-                // units beyond the shared-memory frontier / list reserve
-                t.front.reserve((long long)grid_big * (kDescThreads / 32) * 2 * std::max<int64_t>(t.n_nodes, 1), 0);
-                a.front = t.front.p;
-                a.front_cap = std::max<int64_t>(t.n_nodes, 1);
-                Phase ph("search.desc_big");
-                desc_kernel<true><<<grid_big, kDescThreads, 0, st>>>(a);
-                BT_LAUNCH("walk_desc_big");
-                read_counters(hc);
-            }
-            if (hc[C_LIST] <= a.list_cap) break;
-            list_per_unit = 1.25 * (double)hc[C_LIST] / (double)std::max<int64_t>(1, t.n_units);
-            if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: leaf-list arena does not converge");
-        }
-        t.list_entries = hc[C_LIST];
-        {  // A10 staging + A11 pair tests, counts, masks
+        run_descent(t, a, g, hc);
+        const long long warps_w = (long long)g.w * (kWalkThreads / 32);
+        {  // A10 staging + A11 pair tests, counts, masks; candidate and mask arenas: exact bounds from the descent
             t.arena_cands.reserve(hc[C_NEEDC] + warps_w * kCandSlab, 0);
             t.arena_masks.reserve(hc[C_NEEDM] + warps_w * kMaskSlab, 0);
             a.cands = t.arena_cands.p;
@@ -1256,10 +1369,10 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero(c);
             {
                 Phase ph("search.count");
-                walk_kernel<<<grid_w, kWalkThreads, 0, st>>>(a);
+                walk_kernel<false><<<g.w, kWalkThreads, 0, st>>>(a);
                 BT_LAUNCH("walk_test");
             }
-            read_counters(hc);
+            read_counters(t, hc);
             const bool fits = hc[C_CAND] <= a.cand_cap && hc[C_MASK] <= a.mask_cap;
             if (!fits) throw Error(BT_ERR_CUDA, "bt_find_neighbors: internal: walk arena bound exceeded");
             t.rec_valid = true;
@@ -1299,10 +1412,55 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     zero(C_WORK2);
     {
         Phase ph("search.fill");
-        fill_kernel<<<grid_f, kFillThreads, 0, st>>>(a);
+        fill_kernel<<<g.f, kFillThreads, 0, st>>>(a);
         BT_LAUNCH("walk_fill");
     }
     BT_CUDA(cudaStreamSynchronize(st));
+}
+
+
+// SPH density with the neighbor search fused in: the
+// descent and the walk as in find_neighbors, the walk in density mode (no
+// masks, no candidate records, no CSR); rho in caller order.
+void density(TreeDev &t, const double *h, const double *mass, double *rho) {
+    cudaStream_t st = stream();
+    const int64_t n = t.n;
+    if (n == 0) {
+        BT_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    gather_h(t, h, "bt_density");
+    {
+        DBuf<int> dbad(1);
+        BT_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
+        t.m_tree.reserve(n, 0);
+        gather_m_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec.p, mass, n, t.m_tree.p, dbad.p);
+        BT_LAUNCH("gather_m");
+        int mbad = 0;
+        read_back({{dbad.p, &mbad, sizeof(int)}});
+        if (mbad) throw Error(BT_ERR_INPUT, "bt_density: masses must be finite and |m| <= 1e150");
+    }
+    const Grids g = walk_grids<true>();
+    WalkArgs a = walk_args(t, g);
+    a.m_tree = t.m_tree.p;
+    a.rho = rho;
+    long long hc[C_N];
+    t.rec_valid = false;  // the density walk records no masks
+    run_descent(t, a, g, hc);
+    const long long warps_w = (long long)g.w * (kWalkThreads / 32);
+    t.scratch.reserve(warps_w * kScratch, 0);
+    a.scratch = t.scratch.p;
+    for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero_counter(t, c);
+    {
+        Phase ph("density.walk");
+        walk_kernel<true><<<g.w, kWalkThreads, 0, st>>>(a);
+        BT_LAUNCH("walk_density");
+    }
+    read_counters(t, hc);
+    t.staged = hc[C_STAGED];
+    t.loaded = hc[C_LOADED];
+    t.tests = hc[C_TESTS];
+    t.exact_tests = hc[C_EXACT];
 }
 
 }  // namespace bt

@@ -327,3 +327,48 @@ def test_scratch_full_resume(P, oracle):
     assert_same(gpu, oracle.brute_force(pos, h))
     st = t.stats()
     assert st["staged"] == st["units"] * 6000  # every unit staged every particle
+
+
+# ---- SPH density consumer (bt_density; reading R21) ------------------------------
+DENSITY_RTOL = 1e-4  # fp32 pair distances and block sums
+
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, 100_000), (4, 100_000), (5, 200_000)])
+def test_density_parity(P, oracle, cfg, n):
+    pos, h = datagen.make_config(cfg, n=n)
+    mass = np.random.default_rng(5).uniform(0.5, 1.5, len(pos))
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd, md = torch.from_numpy(h).to(DEV), torch.from_numpy(mass).to(DEV)
+    rho = t.density(hd, md).cpu().numpy()
+    ref = oracle.Tree(pos, 64).density(h, mass)
+    rel = np.abs(rho - ref) / ref
+    assert rel.max() < DENSITY_RTOL, (rel.max(), int(rel.argmax()))
+    # the density walk records nothing: a later count + fill is still exact
+    c, off, nb = t.find_neighbors(hd)
+    ot = oracle.Tree(pos, 64)
+    assert_same((c.cpu().numpy(), off.cpu().numpy(), sort_rows(c, off, nb)), ot.neighbors(h))
+
+
+def test_density_exact_only_and_boundary(P, oracle):
+    pos, h = datagen.near_boundary(512, 64, 29)
+    mass = np.random.default_rng(6).uniform(0.5, 1.5, len(pos))
+    ref = oracle.brute_density(pos, h, mass)
+    t = P.build(torch.from_numpy(pos).to(DEV), 8)
+    hd, md = torch.from_numpy(h).to(DEV), torch.from_numpy(mass).to(DEV)
+    for exact in (False, True):
+        try:
+            P.set_exact_only(exact)
+            rho = t.density(hd, md).cpu().numpy()
+        finally:
+            P.set_exact_only(False)
+        assert (np.abs(rho - ref) / ref).max() < DENSITY_RTOL
+
+
+def test_density_errors(P):
+    pos, h = datagen.uniform(1000, 9, 0.05)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    m = np.ones(1000)
+    m[7] = np.inf
+    with pytest.raises(P.BtreeError) as e:
+        t.density(torch.from_numpy(h).to(DEV), torch.from_numpy(m).to(DEV))
+    assert e.value.code == 2
