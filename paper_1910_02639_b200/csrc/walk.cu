@@ -1131,7 +1131,7 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
         const int nq = U.z;
         const int nchk = (R.nstaged + 63) >> 6;
         for (int q = lane; q < nq; q += 32)
-            F.row[q] = a.nbr + a.offsets[(int32_t)__double_as_longlong(a.rec[U.y + q].w)];
+            F.row[q] = a.nbr + a.offsets[__float_as_int(a.rec32[U.y + q].w)];  // caller index (16-B record)
         for (int kk0 = 0; kk0 < nchk; kk0 += kFillChunks) {
             const int nk = min(kFillChunks, nchk - kk0);
             int32_t c0[kFillChunks], c1[kFillChunks];
@@ -1169,11 +1169,11 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
 }
 
 // h in tree order + validation (h finite, > 0, <= 1e150) + checksum of h
-__global__ void gather_h_kernel(const double4 *__restrict__ rec, const double *__restrict__ h, int64_t n,
+__global__ void gather_h_kernel(const float4 *__restrict__ rec32, const double *__restrict__ h, int64_t n,
                                 double *__restrict__ h_tree, int *bad, long long *hsum) {
     long long acc = 0;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        long long i = __double_as_longlong(rec[k].w);
+        long long i = __float_as_int(rec32[k].w);  // caller index (16-B compact record)
         double v = h[i];
         if (!(v > 0.0 && v <= 1e150)) atomicOr(bad, 1);
         h_tree[k] = v;
@@ -1210,10 +1210,10 @@ void set_exact_only(int on) { g_exact_only = on; }
 namespace {
 
 // masses in tree order + validation (finite, |m| <= 1e150)
-__global__ void gather_m_kernel(const double4 *__restrict__ rec, const double *__restrict__ m, int64_t n,
+__global__ void gather_m_kernel(const float4 *__restrict__ rec32, const double *__restrict__ m, int64_t n,
                                 double *__restrict__ m_tree, int *bad) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const double v = m[__double_as_longlong(rec[k].w)];
+        const double v = m[__float_as_int(rec32[k].w)];
         if (!(fabs(v) <= 1e150)) atomicOr(bad, 1);
         m_tree[k] = v;
     }
@@ -1247,7 +1247,7 @@ long long gather_h(TreeDev &t, const double *h, const char *who) {
     BT_CUDA(cudaMemsetAsync(t.counters.p + C_HSUM, 0, sizeof(int64_t), st));
     {
         Phase ph("search.gather_h");
-        gather_h_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec.p, h, n, t.h_tree.p, dbad.p,
+        gather_h_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec32.p, h, n, t.h_tree.p, dbad.p,
                                                                                   (long long *)t.counters.p + C_HSUM);
         BT_LAUNCH("gather_h");
     }
@@ -1434,7 +1434,7 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
         DBuf<int> dbad(1);
         BT_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
         t.m_tree.reserve(n, 0);
-        gather_m_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec.p, mass, n, t.m_tree.p, dbad.p);
+        gather_m_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec32.p, mass, n, t.m_tree.p, dbad.p);
         BT_LAUNCH("gather_m");
         int mbad = 0;
         read_back({{dbad.p, &mbad, sizeof(int)}});
