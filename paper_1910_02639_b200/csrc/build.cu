@@ -576,10 +576,62 @@ __global__ void unit_scatter_kernel(const int4 *__restrict__ units, int64_t nu, 
 }
 
 constexpr int kUnitQ = 64;  // queries per walk work unit
+#ifndef BT_SMALL_LEAF
+#define BT_SMALL_LEAF 16
+#endif
+constexpr int kSmallLeaf = BT_SMALL_LEAF;  // leaves this small are paired into one unit
+
+// Work units (the paper's "blocked approach", Sec. IV-E; reading R16):
+// one unit per leaf (leaves above 64 split into 64-query units), except that
+// consecutive small leaves (<= 16 particles, adjacent in depth-first order,
+// whose union box is at most twice as wide as the wider of the two) are
+// paired: a descent and a staging pass per leaf would otherwise serve only a
+// handful of queries.  Runs of small leaves pair (0,1), (2,3), ... by rank.
+struct MaxScan {
+    long long v;
+    __host__ __device__ MaxScan operator+(const MaxScan &o) const { return MaxScan{v > o.v ? v : o.v}; }
+};
+struct RunStartIn {
+    const int32_t *cnt;
+    __device__ MaxScan operator()(int64_t L) const {
+        const bool cont = L > 0 && cnt[L] <= kSmallLeaf && cnt[L - 1] <= kSmallLeaf;
+        return MaxScan{cont ? 0 : L};
+    }
+};
+struct RunStartOut {
+    int32_t *rs;
+    __device__ void operator()(int64_t L, const MaxScan &exc, const MaxScan &v) const {
+        rs[L] = (int32_t)(exc.v > v.v ? exc.v : v.v);  // inclusive max
+    }
+};
+
+__global__ void pair_leaves_kernel(const int32_t *__restrict__ cnt, const double *__restrict__ box,
+                                   const int32_t *__restrict__ rs, int64_t nl, int32_t *__restrict__ merge) {
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < nl; L += (int64_t)gridDim.x * blockDim.x) {
+        int m = 0;
+        if (L + 1 < nl && cnt[L] <= kSmallLeaf && cnt[L + 1] <= kSmallLeaf && rs[L + 1] == rs[L] &&
+            ((L - rs[L]) & 1) == 0) {
+            const double *a = box + 6 * L, *b = box + 6 * (L + 1);
+            double wa = 0.0, wb = 0.0, wu = 0.0;
+            for (int l = 0; l < 3; l++) {
+                wa = fmax(wa, a[3 + l] - a[l]);
+                wb = fmax(wb, b[3 + l] - b[l]);
+                wu = fmax(wu, fmax(a[3 + l], b[3 + l]) - fmin(a[l], b[l]));
+            }
+            m = wu <= 2.0 * fmax(wa, wb) ? 1 : 0;
+        }
+        merge[L] = m;
+    }
+}
 
 struct UnitsOfLeaf {
     const int32_t *cnt;
-    __device__ long long operator()(int64_t L) const { return (cnt[L] + kUnitQ - 1) / kUnitQ; }
+    const int32_t *merge;
+    __device__ long long operator()(int64_t L) const {
+        if (L > 0 && merge[L - 1]) return 0;  // paired into the previous leaf's unit
+        const int q = cnt[L] + (merge[L] ? cnt[L + 1] : 0);
+        return (q + kUnitQ - 1) / kUnitQ;
+    }
 };
 struct NullOut {
     __device__ void operator()(int64_t, long long, long long) const {}
@@ -587,11 +639,13 @@ struct NullOut {
 struct UnitsOut {
     const int32_t *begin;
     const int32_t *cnt;
+    const int32_t *merge;
     int4 *units;
     __device__ void operator()(int64_t L, long long exc, long long v) const {
+        const int q = cnt[L] + ((v > 0 && merge[L]) ? cnt[L + 1] : 0);
         for (long long u = 0; u < v; u++) {
             int q0 = (int)(u * kUnitQ);
-            units[exc + u] = make_int4((int)L, begin[L] + q0, min(kUnitQ, cnt[L] - q0), 0);
+            units[exc + u] = make_int4((int)L, begin[L] + q0, min(kUnitQ, q - q0), 0);
         }
     }
 };
@@ -809,15 +863,20 @@ void build_tree(TreeDev &t, const double *pos) {
             fin.p, t.rec.p, t.rec32.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
         BT_LAUNCH("leaf_finalize");
         DBuf<long long> dtot(1);
+        // small leaves paired (runs of small leaves, pair by rank, box check)
+        DBuf<int32_t> rs(t.n_leaves), merge(t.n_leaves);
+        device_scan<MaxScan>(RunStartIn{t.leaf_count.p}, RunStartOut{rs.p}, t.n_leaves, (MaxScan *)nullptr);
+        pair_leaves_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
+            t.leaf_count.p, t.leaf_box.p, rs.p, t.n_leaves, merge.p);
+        BT_LAUNCH("pair_leaves");
         // units: count first (to size the array), then write
-        // (two scans over the leaves; cheap: L <= n / 1)
-        device_scan<long long>(UnitsOfLeaf{t.leaf_count.p}, NullOut{}, t.n_leaves, dtot.p);
+        device_scan<long long>(UnitsOfLeaf{t.leaf_count.p, merge.p}, NullOut{}, t.n_leaves, dtot.p);
         long long nu = 0;
         read_back({{dtot.p, &nu, sizeof(long long)}});
         t.units.alloc(nu);
         t.n_units = nu;
-        device_scan<long long>(UnitsOfLeaf{t.leaf_count.p}, UnitsOut{t.leaf_begin.p, t.leaf_count.p, t.units.p},
-                               t.n_leaves, dtot.p);
+        device_scan<long long>(UnitsOfLeaf{t.leaf_count.p, merge.p},
+                               UnitsOut{t.leaf_begin.p, t.leaf_count.p, merge.p, t.units.p}, t.n_leaves, dtot.p);
         if (nu > 1) {  // Morton order of the units (walk locality)
             DBuf<unsigned> key(nu);
             DBuf<int32_t> bucket(1u << kMortonBits);

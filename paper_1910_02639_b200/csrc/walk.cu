@@ -38,7 +38,7 @@ constexpr int kQ = 64;           // queries per unit (== build.cu kUnitQ)
 constexpr int kBlk = 128;        // staged candidates per test block
 constexpr int kScratch = 4096;   // staged candidates per warp scratch (global, L2-resident); multiple of kBlk
 constexpr int kGroup = 32;       // candidate leaves per staging group (one per lane)
-constexpr int kFrontCap = 128;   // shared-memory descent frontier per level
+constexpr int kFrontCap = 512;   // shared-memory descent frontier per level
 constexpr int kDescThreads = 128;
 constexpr int kWalkThreads = 128;
 constexpr int kFillThreads = 256;
