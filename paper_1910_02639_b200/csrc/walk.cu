@@ -177,58 +177,49 @@ __device__ __forceinline__ bool exact_pair(double qx, double qy, double qz, doub
 // (D = |c_leaf - c| <= H + E, so H + D <= 15 E).  One bound covers both.
 __device__ __forceinline__ double l4_eps(double E) { return 16.02 * 0x1p-24 * E + 0x1p-146; }
 
-// Lemma L4: thresholds A <= B (fp32) such that for the
-// fp32 squared distance s32 of a pair whose coordinates relative to the unit
-// centre carry error <= eps (E: coordinate bound),
-//   s32 <  A  =>  fp64 predicate true,     s32 >= B  =>  fp64 predicate false.
-// All slack factors round the bounds outward.
-__device__ __forceinline__ void l4_thresholds(double T, double E, double eps, bool exact_only, float &A, float &B) {
-    const double u = 0x1p-53, w = 0x1p-24;
-    if (exact_only || !(E < 1e15)) {
-        A = 0.0f;
-        B = __int_as_float(0x7f800000);  // +inf: every pair goes to the fp64 predicate
-        return;
-    }
-    const double a0 = 2.0 * eps * (1.0 + w) + 0x1p-150;  // |d - D| <= a0 + w |D|
-    const double g3 = 3.0 * w / (1.0 - 3.0 * w);
-    auto err = [&](double S) {
-        double D = 3.0 * a0 * a0 + 2.0 * 1.7320508075688775 * a0 * (1.0 + w) * sqrt(S) + (2.0 * w + w * w) * S;
-        return (D + g3 * (S + D) + 3.0 * 0x1p-150) * 1.0001;
-    };
-    const double Tm = T * (1.0 - 8.0 * u);  // <= T / (1 + gamma_5)
-    const double Tp = T * (1.0 + 8.0 * u);  // >= T / (1 - gamma_5)
-    A = 0.0f;
-    if (a0 <= 0.01 * sqrt(Tm)) {  // S - err(S) increasing on [Tm, inf)
-        double g = (Tm - err(Tm)) * (1.0 - 0x1p-40);
-        if (g > 0.0) A = __double2float_rd(g);
-    }
-    double hb = (Tp + err(Tp)) * (1.0 + 0x1p-40);
-    B = (hb < 3.0e38) ? __double2float_ru(hb) : __int_as_float(0x7f800000);
-}
-
-// The band [A, B) as one fused multiply-add: fp32
-// A <= Mid <= B, HW >= max(Mid - A, B - Mid), k = a power of two <= 1/HW
-// (per query the largest; a unit uses the minimum over its queries, which
-// only widens the band) and c = -Mid k (exact: a power-of-two scaling), so
-// the hot loop's d' = fl32(s k + c) = k fl32(s - Mid).  Then
-//   s in [A, B)  =>  |s - Mid| <= HW <= 1/k  =>  |d'| <= 1
-// (round-to-nearest is monotone and 1/k is representable), so a pair with
-// |d'| > 1 is certain, and for it d' < 0 <=> s < Mid <=> s < A (a neighbor).
-// k = c = 0 (B = +inf: exact-only) bands every pair ("force": the fp64
-// predicate decides everything, also pairs whose fp32 arithmetic overflowed).
-__device__ __forceinline__ void band_params(float A, float B, float &k, float &Mid) {
+// Lemma L4, expanded form.  The hot loop evaluates, per
+// (candidate c, query q) with fp32 unit-relative coordinates,
+//   v = fl(cx Qx + fl(cy Qy + fl(cz Qz + fl(Ac + Bq))))      (3 FMA + 1 add)
+// with Ac = k fl(|c|^2) (per candidate), Q = -2 k q and Bq = fl32(k (|q|^2 -
+// Mid)) (per query), k a power of two (exact scalings).  In exact arithmetic
+// v = k (|c - q|^2 - Mid).  With E' >= every |coordinate| (E' = E(1 + 1e-6) +
+// 5 eps: queries and kept candidates lie within E + 4 eps of the unit centre)
+// the fp32 arithmetic errs by at most k G, G = u (60.1 E'^2 + 5.01 Mid_max)
+// (u = 2^-24: |c|^2 in three roundings <= 9.01 u E'^2, Bq <= u (3E'^2 + Mid),
+// four roundings of partial sums bounded by k (12 E'^2 + Mid)), and the inputs'
+// representation error (<= eps per coordinate, so <= 2 eps per axis of c - q)
+// moves |c - q|^2 from the exact S by <= 4 sqrt(3) eps sqrt(S) + 12 eps^2.
+// So Err(S) = 4 sqrt3 eps sqrt(S) + 12 eps^2 + G bounds |v/k + Mid - S|; with
+// T- = T (1 - 8 u64), T+ = T (1 + 8 u64) (the fp64 predicate's rounding) and
+// S - Err(S) increasing on [T-, inf):
+//   A = T- - Err(T-),  B = T+ + Err(T+),  HW >= max(|Mid - A|, |B - Mid|),
+//   k = largest power of two <= 1/HW  =>  [t_acc, t_rej) = k [A - Mid, B - Mid)
+//   lies inside [-1, 1], so |v| > 1 is certain: v < -1 => S < T- => neighbor,
+//   v > 1 => S >= T+ => not; the band |v| <= 1 goes to the fp64 predicate.
+// k = 0 ("force": exact-only, E >= 1e15, or a bound that fails) sends every
+// pair to the fp64 predicate.  A unit uses the minimum k over its queries
+// (1/k only grows, the band only widens).
+__device__ __forceinline__ void l4_band(double T, double E, double eps, bool exact_only, float &k, float &Mid) {
     k = 0.0f;
     Mid = 0.0f;
-    if (!(B < __int_as_float(0x7f800000))) return;
-    Mid = __double2float_rn(0.5 * ((double)A + (double)B));
-    Mid = fmaxf(A, fminf(B, Mid));
-    // half-width: exact difference of fp32 values rounded up, widened to
-    // >= 2^-23 Mid and >= 1e-30 (keeps Mid k <= 2^23 and k <= 2^100)
-    float HW = __double2float_ru(fmax((double)Mid - (double)A, (double)B - (double)Mid));
-    HW = fmaxf(HW, fmaxf(Mid * 0x1p-23f, 1e-30f));
+    if (exact_only || !(E < 1e15)) return;
+    const double u = 0x1p-24, u64 = 0x1p-53, s3 = 1.7320508075688775;
+    const double Ep = E * (1.0 + 1e-6) + 5.0 * eps;
+    const double Tm = T * (1.0 - 8.0 * u64), Tp = T * (1.0 + 8.0 * u64);
+    const double G = u * (60.1 * Ep * Ep + 5.01 * (2.0 * Tp));  // Mid <= B <= 2 T+ (checked below)
+    auto err = [&](double S) { return (4.0 * s3 * eps * sqrt(S) + 12.0 * eps * eps + G) * 1.0001; };
+    if (!(2.0 * s3 * eps * 1.0001 <= 0.5 * sqrt(Tm))) return;  // S - Err(S) increasing on [T-, inf)
+    const double A = Tm - err(Tm), B = Tp + err(Tp);
+    if (!(A > 0.0) || !(B <= 2.0 * Tp)) return;
+    const float M = __double2float_rn(0.5 * (A + B));
+    double hw = fmax(fmax((double)M - A, B - (double)M), (double)M * 0x1p-23) * (1.0 + 0x1p-40);
     int e;
-    frexp(1.0 / (double)HW, &e);  // 1/HW = f 2^e, f in [0.5, 1)
-    k = ldexpf(1.0f, e - 1);      // largest power of two <= 1/HW
+    frexp(1.0 / hw, &e);                       // 1/hw = f 2^e, f in [0.5, 1)
+    const double kd = ldexp(1.0, e - 1);       // largest power of two <= 1/hw
+    // the expanded form's magnitudes stay far below fp32 overflow
+    if (!(kd * (12.0 * Ep * Ep + (double)M) < 1e36) || !(2.0 * kd * Ep < 1e36)) return;
+    k = (float)kd;
+    Mid = M;
 }
 
 // ---------------------------------------------------------------------------
@@ -591,6 +582,7 @@ struct DensitySm {};
 template <>
 struct DensitySm<true> {
     float hinv[kQ];
+    float4 qraw[kQ];  // fp32 query coordinates relative to the unit centre
     float4 dc[kBlk];  // ax, ay, az (fp32, relative to the unit centre), m_j
 };
 template <bool kDensity>
@@ -615,28 +607,28 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
     const int nch = (n + 63) >> 6;
     const float inf = __int_as_float(0x7f800000);
     const float ku = S.u.k;
-    const bool force = S.u.force != 0;
+    const bool force = S.u.force != 0;  // (inf used for padding Ac)
     const int q0 = S.u.q0, nq = S.u.nq;
     for (int k = 0; k < nch; k++) {
         float4 c[2];
+        float ac[2];
         bool real[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
             const int s = 64 * k + 32 * h + lane;
             real[h] = s < n;
-            c[h] = real[h] ? blk[s] : make_float4(inf, inf, inf, __int_as_float(-1));
+            c[h] = real[h] ? blk[s] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+            const float nc = __fmaf_rn(c[h].z, c[h].z, __fmaf_rn(c[h].y, c[h].y, __fmul_rn(c[h].x, c[h].x)));
+            ac[h] = real[h] ? __fmul_rn(ku, nc) : inf;  // identical to test_block
         }
         for (int q = 0; q < nq; q++) {
             const float4 Q0 = S.q0[q], Q1 = S.q1[q];
             bool flag[2];
 #pragma unroll
             for (int h = 0; h < 2; h++) {
-                const float dx = __fsub_rn(c[h].x, Q0.x), dy = __fsub_rn(c[h].y, Q0.z), dz = __fsub_rn(c[h].z, Q1.x);
-                float s = __fmul_rn(dx, dx);
-                s = __fmaf_rn(dy, dy, s);
-                s = __fmaf_rn(dz, dz, s);
-                const float d = __fmaf_rn(s, ku, Q1.z);
-                flag[h] = real[h] && (force || fabsf(d) <= 1.0f);
+                // the hot loop's v, operation for operation
+                const float v = __fmaf_rn(c[h].x, Q0.x, __fmaf_rn(c[h].y, Q0.z, __fmaf_rn(c[h].z, Q1.x, __fadd_rn(ac[h], Q1.z))));
+                flag[h] = real[h] && (force || fabsf(v) <= 1.0f);
             }
             const unsigned f0 = __ballot_sync(0xffffffffu, flag[0]), f1 = __ballot_sync(0xffffffffu, flag[1]);
             if (!(f0 | f1)) continue;
@@ -670,23 +662,28 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     const float inf = __int_as_float(0x7f800000);
     const int nch = (n + 63) >> 6;  // 1 or 2 chunks of 64
     const int nq = S.u.nq;
-    // this lane's candidates: chunk 0 -> slots (l, l + 32), chunk 1 -> (l + 64, l + 96)
+    // this lane's candidates: chunk 0 -> slots (l, l + 32), chunk 1 -> (l + 64, l + 96);
+    // padding slots: c = 0, Ac = +inf (v = +inf: never a neighbor, never banded)
+    const float ku = S.u.k;
     float4 c[4];
+    float ac[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int s = 32 * j + lane;
-        c[j] = (s < n) ? blk[s] : make_float4(inf, inf, inf, 0.f);
+        c[j] = (s < n) ? blk[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float nc = __fmaf_rn(c[j].z, c[j].z, __fmaf_rn(c[j].y, c[j].y, __fmul_rn(c[j].x, c[j].x)));
+        ac[j] = (s < n) ? __fmul_rn(ku, nc) : inf;  // k |c|^2 (exact scaling)
     }
-    const unsigned long long xa = pk(c[0].x, c[1].x), ya = pk(c[0].y, c[1].y), za = pk(c[0].z, c[1].z);
-    const unsigned long long xb = pk(c[2].x, c[3].x), yb = pk(c[2].y, c[3].y), zb = pk(c[2].z, c[3].z);
+    const unsigned long long xa = pk(c[0].x, c[1].x), ya = pk(c[0].y, c[1].y), za = pk(c[0].z, c[1].z),
+                             aa = pk(ac[0], ac[1]);
+    const unsigned long long xb = pk(c[2].x, c[3].x), yb = pk(c[2].y, c[3].y), zb = pk(c[2].z, c[3].z),
+                             ab = pk(ac[2], ac[3]);
     const int nqp = (nq + 1) & ~1;  // padded to even (the pad query never matches)
     // shared addresses of the query records (two LDS.128 per query)
     const unsigned aq0 = (unsigned)__cvta_generic_to_shared(&S.q0[0]);
     const unsigned aq1 = (unsigned)__cvta_generic_to_shared(&S.q1[0]);
-    const float ku = S.u.k;
-    const unsigned long long kk = pk(ku, ku);
-    float bmin = 2.0f;  // min |d'| over the block's pairs: <= 1 -> some pair is banded
-    // query records, loaded one query ahead of their use (LDS latency)
+    float bmin = 2.0f;  // min |v| over the block's pairs: <= 1 -> some pair is banded
+    // query records (-2k q, k(|q|^2 - Mid)), loaded one query ahead of their use (LDS latency)
     auto ldq = [&](int q, float4 &Q0, float4 &Q1) {
         asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                      : "=f"(Q0.x), "=f"(Q0.y), "=f"(Q0.z), "=f"(Q0.w) : "r"(aq0 + 16 * q));
@@ -701,14 +698,11 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             const float4 Q0 = N0, Q1 = N1;
             ldq(q + 1, N0, N1);  // q + 1 <= nqp <= 64: within the padded arrays
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
-                                     cc = pk(Q1.z, Q1.w);
-            unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
-            const unsigned long long da = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
-            dx = f2_sub(xb, qx);
-            dy = f2_sub(yb, qy);
-            dz = f2_sub(zb, qz);
-            const unsigned long long db = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
-            bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(da)), fabsf(hi_f(da))), fminf(fabsf(lo_f(db)), fabsf(hi_f(db)))));
+                                     bq = pk(Q1.z, Q1.w);
+            // v = k (|c - q|^2 - Mid) expanded: one add + three FMA per packed pair (lemma L4)
+            const unsigned long long da = f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq))));
+            const unsigned long long db = f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq))));
+            bmin = fminf(fminf(bmin, fminf(fabsf(lo_f(da)), fabsf(hi_f(da)))), fminf(fabsf(lo_f(db)), fabsf(hi_f(db))));
             const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(da) < 0.0f);
             const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(da) < 0.0f);
             const unsigned m2 = __ballot_sync(0xffffffffu, lo_f(db) < 0.0f);
@@ -724,9 +718,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             const float4 Q0 = N0, Q1 = N1;
             ldq(q + 1, N0, N1);
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
-                                     cc = pk(Q1.z, Q1.w);
-            const unsigned long long dx = f2_sub(xa, qx), dy = f2_sub(ya, qy), dz = f2_sub(za, qz);
-            const unsigned long long da = f2_fma(f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx))), kk, cc);
+                                     bq = pk(Q1.z, Q1.w);
+            const unsigned long long da = f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq))));
             bmin = fminf(bmin, fminf(fabsf(lo_f(da)), fabsf(hi_f(da))));
             const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(da) < 0.0f);
             const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(da) < 0.0f);
@@ -762,7 +755,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
         for (int h = 0; h < 2; h++) {
             const int q = lane + 32 * h;
             if (q < nq) {
-                const float qx = S.q0[q].x, qy = S.q0[q].z, qz = S.q1[q].x, hinv = S.d.hinv[q];
+                const float4 qr = S.d.qraw[q];
+                const float qx = qr.x, qy = qr.y, qz = qr.z, hinv = S.d.hinv[q];
                 float acc = 0.0f;
                 for (int k = 0; k < 2 * nch; k++) {  // 32-bit halves of the chunk masks
                     unsigned m = (unsigned)(S.mask[k >> 1][q] >> (32 * (k & 1)));
@@ -918,13 +912,8 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             const double eps = l4_eps(G.E);
             float kq[2] = {INFINITY, INFINITY}, mid[2] = {0.0f, 0.0f};
 #pragma unroll
-            for (int h = 0; h < 2; h++) {
-                if (lane + 32 * h < G.nq) {
-                    float A, B;
-                    l4_thresholds(G.qT[h], G.E, eps, a.exact_only != 0, A, B);
-                    band_params(A, B, kq[h], mid[h]);
-                }
-            }
+            for (int h = 0; h < 2; h++)
+                if (lane + 32 * h < G.nq) l4_band(G.qT[h], G.E, eps, a.exact_only != 0, kq[h], mid[h]);
             // unit band scale: the minimum power of two (0 = force)
             float ku = fminf(kq[0], kq[1]);
             for (int d = 16; d; d >>= 1) ku = fminf(ku, __shfl_xor_sync(0xffffffffu, ku, d));
@@ -936,11 +925,17 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     const float ax = __double2float_rn(__dsub_rn(G.qx[h], G.c[0]));
                     const float ay = __double2float_rn(__dsub_rn(G.qy[h], G.c[1]));
                     const float az = __double2float_rn(__dsub_rn(G.qz[h], G.c[2]));
-                    const float cq = -mid[h] * ku;  // exact (power-of-two scaling); 0 when forced
-                    S.q0[k] = make_float4(ax, ax, ay, ay);
-                    S.q1[k] = make_float4(az, az, cq, cq);
-                    if constexpr (kDensity) S.d.hinv[k] = (float)(1.0 / a.h_tree[G.q0 + k]);
-                } else {  // padding query: d' = s k + 2 >= 2 (never a neighbor, never banded)
+                    // Q = -2 k q (exact), Bq = fl32(k (|q|^2 - Mid)), |q|^2 in fp64 from the fp32 q
+                    const float m2k = -2.0f * ku;
+                    const double qq = (double)ax * ax + (double)ay * ay + (double)az * az;
+                    const float bq = force ? 0.0f : __double2float_rn((double)ku * (qq - (double)mid[h]));
+                    S.q0[k] = make_float4(m2k * ax, m2k * ax, m2k * ay, m2k * ay);
+                    S.q1[k] = make_float4(m2k * az, m2k * az, bq, bq);
+                    if constexpr (kDensity) {
+                        S.d.hinv[k] = (float)(1.0 / a.h_tree[G.q0 + k]);
+                        S.d.qraw[k] = make_float4(ax, ay, az, 0.f);
+                    }
+                } else {  // padding query: v = Ac + 2 >= 2 (never a neighbor, never banded)
                     S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
                     S.q1[k] = make_float4(0.f, 0.f, 2.f, 2.f);
                 }
