@@ -189,7 +189,7 @@ typedef struct bt_stats {
     int64_t max_leaf;
     int32_t depth;        /* leaf depth maximum; a root leaf has depth 0      */
     int32_t root_b;       /* accepted branching factor of the root (0: leaf)  */
-    int64_t units;        /* walk work units (<= 64 queries of one leaf)      */
+    int64_t units;        /* walk work units (a leaf, a 64-query part of one, or two small leaves) */
     double box_lo[3], box_hi[3];
     /* last bt_find_neighbors on this tree */
     int64_t total_pairs;
