@@ -42,6 +42,7 @@ struct LevelNode {
     int32_t halvings;
     int64_t cell_base;   // level-local first cell
     int64_t under;       // #{j < b^3 : n_j <= alpha s}   (Eq. 4 numerator)
+    double bx[3];        // fl(b / ext) of the current b (cell_coord_fast)
 };
 
 struct CellScan {  // per-cell values scanned in one pass (A6)
@@ -144,13 +145,14 @@ __device__ __forceinline__ int eq1_branching(int64_t n, int64_t s) {
     return (int)b;
 }
 
-__global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s, int octree) {
+__global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s, int octree, const NodeRec *nodes) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nn) return;
     // FixedOctree policy (the paper's comparison baseline): b = 2
     int b = octree ? 2 : eq1_branching(ln[i].count, s);
     ln[i].b0 = b;
     ln[i].b = b;
+    for (int l = 0; l < 3; l++) ln[i].bx[l] = __ddiv_rn((double)b, nodes[ln[i].gid].ext[l]);
     ln[i].flag = 1;
     ln[i].halvings = 0;
     ln[i].under = 0;
@@ -177,9 +179,10 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__res
         const NodeRec &nr = nodes[L.gid];
         double4 r = act[p];
         int b = L.b;
-        int c1 = cell_coord(r.x, nr.lo[0], nr.ext[0], b);
-        int c2 = cell_coord(r.y, nr.lo[1], nr.ext[1], b);
-        int c3 = cell_coord(r.z, nr.lo[2], nr.ext[2], b);
+        // Eq. 2 (cell_coord_fast: identical results, division only near cell faces)
+        int c1 = cell_coord_fast(r.x, nr.lo[0], nr.ext[0], L.bx[0], b);
+        int c2 = cell_coord_fast(r.y, nr.lo[1], nr.ext[1], L.bx[1], b);
+        int c3 = cell_coord_fast(r.z, nr.lo[2], nr.ext[2], L.bx[2], b);
         uint32_t j = (uint32_t)c1 + (uint32_t)c2 * (uint32_t)b + (uint32_t)c3 * (uint32_t)b * (uint32_t)b;
         keys[p] = j;
         atomicAdd(&hist[L.cell_base + j], 1);
@@ -220,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) under_count_kernel(LevelNode *ln, in
 }
 
 // r = u / b^3 (Eq. 4); halve iff r >= beta and b > 2 (readings R3, R7)
-__global__ void ratio_decide_kernel(LevelNode *ln, int64_t nn, double beta, int *any) {
+__global__ void ratio_decide_kernel(LevelNode *ln, int64_t nn, double beta, int *any, const NodeRec *nodes) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nn) return;
     LevelNode &L = ln[i];
@@ -229,6 +232,7 @@ __global__ void ratio_decide_kernel(LevelNode *ln, int64_t nn, double beta, int 
     double r = __ddiv_rn((double)L.under, B);
     if (r >= beta && L.b > 2) {
         L.b = max(2, L.b / 2);
+        for (int l = 0; l < 3; l++) L.bx[l] = __ddiv_rn((double)L.b, nodes[L.gid].ext[l]);
         L.halvings++;
         L.under = 0;
         L.flag = 1;
@@ -332,6 +336,7 @@ __global__ void finalize_level_nodes_kernel(const LevelNode *ln, int64_t nn, Nod
     NodeRec &R = nodes[ln[i].gid];
     R.b = ln[i].b;
     R.cell_base = cells_base + ln[i].cell_base;
+    for (int l = 0; l < 3; l++) R.bx[l] = __ddiv_rn((double)R.b, R.ext[l]);
     if (ln[i].halvings) atomicAdd(halvings, (unsigned long long)ln[i].halvings);
 }
 
@@ -753,7 +758,7 @@ void build_tree(TreeDev &t, const double *pos) {
         while (nn > 0) {
             Phase ph("build.level");
             // A2: Eq. 1 and the level's cell layout
-            level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s, t.octree ? 1 : 0);
+            level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s, t.octree ? 1 : 0, t.nodes.p);
             BT_LAUNCH("level_b");
             device_scan<long long>(CellsOfNode{ln.p}, CellBaseOut{ln.p}, nn, dtotal.p);
             long long ncells_h = 0;
@@ -782,7 +787,7 @@ void build_tree(TreeDev &t, const double *pos) {
                 under_count_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, t.alpha * (double)t.s);
                 BT_LAUNCH("under_count");
                 BT_CUDA(cudaMemsetAsync(dflags.p + 1, 0, sizeof(int), st));
-                ratio_decide_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.beta, dflags.p + 1);
+                ratio_decide_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.beta, dflags.p + 1, t.nodes.p);
                 BT_LAUNCH("ratio_decide");
                 int any = 0;
                 read_back({{dflags.p + 1, &any, sizeof(int)}});

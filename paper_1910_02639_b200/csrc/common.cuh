@@ -110,6 +110,7 @@ struct NodeRec {      // one internal node
     int32_t b;        // accepted branching factor per dimension
     int32_t depth;
     int64_t cell_base;  // first entry of this node's b^3 cells in the cell table
+    double bx[3];     // fl(b / ext): cell_coord_fast's multiplier (set with b)
 };
 
 // cell table code: -1 empty, >= 0 leaf id, <= -2 internal node (id = -2 - code)
@@ -195,6 +196,23 @@ __device__ __forceinline__ int cell_coord(double x, double lo, double ext, int b
     if (!(f >= 0.0)) return 0;
     if (f > (double)(b - 1)) return b - 1;
     return (int)f;
+}
+
+// cell_coord without the division in the common case: q = fl(fl(x - lo) *
+// fl(b / ext)) differs from Eq. 2's fl(fl(fl(x - lo) / ext) * b) by at most a
+// few ulps of q (|q - q_eq2| <= |q| 2^-50.9), so the two floors agree unless q
+// lies within |q| 2^-45 of an integer; there (and for non-finite q) the exact
+// Eq. 2 evaluation decides.  Results are identical to cell_coord's.
+__device__ __forceinline__ int cell_coord_fast(double x, double lo, double ext, double bx, int b) {
+    const double q = __dmul_rn(__dsub_rn(x, lo), bx);
+    const double f = floor(q);
+    const double m = fabs(q) * 0x1p-45 + 0x1p-1000;
+    if (__dsub_rn(q, f) > m && __dsub_rn(__dadd_rn(f, 1.0), q) > m) {  // false for NaN / inf
+        if (!(f >= 0.0)) return 0;
+        if (f > (double)(b - 1)) return b - 1;
+        return (int)f;
+    }
+    return cell_coord(x, lo, ext, b);
 }
 
 constexpr int kWarp = 32;

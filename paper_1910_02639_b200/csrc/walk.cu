@@ -411,8 +411,8 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
                     cb = nd.cell_base;
                     int r0[3], r1[3];
                     for (int l = 0; l < 3; l++) {  // Eq. 5 with R'_u (lemma L2)
-                        r0[l] = cell_coord(__dsub_rn(qlo[l], Ru), nd.lo[l], nd.ext[l], b);
-                        r1[l] = cell_coord(__dadd_rn(qhi[l], Ru), nd.lo[l], nd.ext[l], b);
+                        r0[l] = cell_coord_fast(__dsub_rn(qlo[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], b);
+                        r1[l] = cell_coord_fast(__dadd_rn(qhi[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], b);
                     }
                     r0x = r0[0];
                     r0y = r0[1];
