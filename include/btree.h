@@ -142,6 +142,33 @@ int bt_fill_neighbors(const bt_tree *t, const double *h, const int64_t *offsets,
  */
 int bt_density(const bt_tree *t, const double *h, const double *mass, double *rho);
 
+/*
+ * bt_find_neighbors_sym -- the symmetric criterion (the
+ * paper's Alg. 2 uses the query's h only; the open question of
+ * SPEC S:273; reading R22 in DESIGN.md): j != i is a neighbor of i iff
+ *   ((dx*dx + dy*dy) + dz*dz) < (2 max(h_i, h_j)) * (2 max(h_i, h_j))
+ * in fp64 (no FMA), dx = x_i - x_j.  Equivalently N_sym(i) = N(i) u
+ * {j : i in N(j)} with N the gather sets of bt_find_neighbors, which is how it
+ * is computed: the gather walk, then a pass over its recorded masks that adds
+ * every one-sided pair to the other row.  The relation is symmetric.
+ * Arguments, layouts, ownership, synchrony, row order (unspecified), the
+ * count-only call (nbr_idx NULL) and the errors are those of
+ * bt_find_neighbors (capacity n*ngmax; BT_ERR_CAPACITY leaves counts and
+ * offsets valid and nbr_idx untouched).  Uses internal device memory of
+ * 3 n int32 + (n+1) int64 besides the gather pass's.
+ */
+int bt_find_neighbors_sym(const bt_tree *t, const double *h, int32_t ngmax, int32_t *counts,
+                          int64_t *offsets, int32_t *nbr_idx);
+
+/*
+ * bt_fill_neighbors_sym -- the fill of bt_find_neighbors_sym alone, with the
+ * offsets of a previous symmetric count on the same tree and h (the count
+ * pass is reused when nothing ran in between, else redone).  capacity =
+ * int32 slots of nbr_idx; BT_ERR_CAPACITY if offsets[n] > capacity.
+ */
+int bt_fill_neighbors_sym(const bt_tree *t, const double *h, const int64_t *offsets,
+                          int32_t *nbr_idx, int64_t capacity);
+
 /* Frees all tree-owned device memory (into this thread's block cache).  NULL-safe. */
 void bt_free(bt_tree *t);
 

@@ -88,6 +88,10 @@ def lib():
         L.orc_brute_count.restype = None
         L.orc_brute_rows.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, _P, _P, C.c_int]
         L.orc_brute_rows.restype = C.c_int
+        L.orc_brute_count_sym.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, _P, C.c_int]
+        L.orc_brute_count_sym.restype = None
+        L.orc_brute_rows_sym.argtypes = [_P, _P, C.c_int64, _P, C.c_int64, _P, _P, C.c_int]
+        L.orc_brute_rows_sym.restype = C.c_int
         L.orc_w_m4.argtypes = [C.c_double]
         L.orc_w_m4.restype = C.c_double
         L.orc_density.argtypes = [_P, _P, _P, _P, _P, C.c_int64, _P, C.c_int]
@@ -245,21 +249,22 @@ def brute_density(pos, h, mass, queries=None, threads: int | None = None):
     return rho
 
 
-def brute_force(pos, h, queries=None, threads: int | None = None):
-    """O(n^2) plain definition: (counts, offsets, idx), rows ascending."""
+def brute_force(pos, h, queries=None, threads: int | None = None, symmetric: bool = False):
+    """O(n^2) plain definition: (counts, offsets, idx), rows ascending.
+    symmetric: the max(h_i, h_j) criterion (reading R22)."""
     pos = _f64(pos, (-1, 3))
     h = _f64(h)
     n = pos.shape[0]
     q = None if queries is None else np.ascontiguousarray(queries, dtype=np.int64)
     nq = n if q is None else q.size
     counts = np.empty(nq, dtype=np.int32)
-    lib().orc_brute_count(_ptr(pos), _ptr(h), n, _ptr(q), nq, _ptr(counts),
-                          threads or default_threads())
+    count_fn = lib().orc_brute_count_sym if symmetric else lib().orc_brute_count
+    rows_fn = lib().orc_brute_rows_sym if symmetric else lib().orc_brute_rows
+    count_fn(_ptr(pos), _ptr(h), n, _ptr(q), nq, _ptr(counts), threads or default_threads())
     offsets = np.zeros(nq + 1, dtype=np.int64)
     np.cumsum(counts, out=offsets[1:])
     idx = np.empty(int(offsets[-1]), dtype=np.int32)
-    rc = lib().orc_brute_rows(_ptr(pos), _ptr(h), n, _ptr(q), nq, _ptr(offsets), _ptr(idx),
-                              threads or default_threads())
+    rc = rows_fn(_ptr(pos), _ptr(h), n, _ptr(q), nq, _ptr(offsets), _ptr(idx), threads or default_threads())
     if rc != 0:
         raise RuntimeError("oracle brute force: row length changed between passes")
     return counts, offsets, idx

@@ -553,6 +553,60 @@ int orc_brute_rows(const double *pos, const double *h, int64_t n,
 }
 
 /* ------------------------------------------------------------------ */
+/* Symmetric criterion (reading R22, not in the      */
+/* paper, whose Alg. 2 uses the query's h_p only  */
+/* leaves it open): j != i is a neighbor of i iff                       */
+/*   ((dx*dx + dy*dy) + dz*dz) < t*t,  t = 2 max(h_i, h_j)             */
+/* in fp64 (max is exact).  The plain definition, O(n^2), every j.      */
+/* ------------------------------------------------------------------ */
+static int orc_sym_pair(const double *pos, const double *h, int64_t i, int64_t j)
+{
+    double hm = h[i] > h[j] ? h[i] : h[j];
+    double t = 2.0 * hm;
+    double dx = pos[3 * i + 0] - pos[3 * j + 0];
+    double dy = pos[3 * i + 1] - pos[3 * j + 1];
+    double dz = pos[3 * i + 2] - pos[3 * j + 2];
+    return (dx * dx + dy * dy) + dz * dz < t * t;
+}
+
+void orc_brute_count_sym(const double *pos, const double *h, int64_t n,
+                         const int64_t *queries, int64_t nq, int32_t *counts, int nthreads)
+{
+    (void)nthreads;
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1)
+    for (int64_t k = 0; k < nq; k++) {
+        int64_t i = queries ? queries[k] : k;
+        int32_t c = 0;
+        for (int64_t j = 0; j < n; j++)
+            if (j != i && orc_sym_pair(pos, h, i, j))
+                c++;
+        counts[k] = c;
+    }
+}
+
+int orc_brute_rows_sym(const double *pos, const double *h, int64_t n,
+                       const int64_t *queries, int64_t nq, const int64_t *offsets,
+                       int32_t *idx, int nthreads)
+{
+    int bad = 0;
+    (void)nthreads;
+#pragma omp parallel for schedule(static) num_threads(nthreads > 0 ? nthreads : 1) reduction(| : bad)
+    for (int64_t k = 0; k < nq; k++) {
+        int64_t i = queries ? queries[k] : k;
+        int64_t w = offsets[k], end = offsets[k + 1];
+        for (int64_t j = 0; j < n; j++) {
+            if (j != i && orc_sym_pair(pos, h, i, j)) {
+                if (w < end) idx[w] = (int32_t)j;
+                w++;
+            }
+        }
+        if (w != end)
+            bad |= 1;
+    }
+    return bad ? -1 : 0;
+}
+
+/* ------------------------------------------------------------------ */
 /* SPH density consumer (the paper's use of the     */
 /* neighbor lists, Sec. I P:50-56 and Sec. IV-H).  Reading    */
 /* R21 (not in the paper): the M4 cubic spline of compact support 2h,   */

@@ -20,8 +20,8 @@ _NAMES = {0: "BT_OK", 1: "BT_ERR_ARG", 2: "BT_ERR_INPUT", 3: "BT_ERR_CAPACITY", 
           5: "BT_ERR_OOM"}
 
 # every symbol include/btree.h declares
-EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "bt_fill_neighbors", "bt_density",
-           "bt_free",
+EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "bt_fill_neighbors",
+           "bt_find_neighbors_sym", "bt_fill_neighbors_sym", "bt_density", "bt_free",
            "bt_search_host", "bt_set_stream", "bt_set_exact_only", "bt_release_cache", "bt_last_error", "bt_last_status", "bt_tree_stats",
            "bt_tree_order", "bt_profile_enable", "bt_profile_reset", "bt_profile_get"]
 
@@ -72,6 +72,10 @@ def lib():
         L.bt_find_neighbors.restype = C.c_int
         L.bt_fill_neighbors.argtypes = [_P, _P, _P, _P, C.c_int64]
         L.bt_fill_neighbors.restype = C.c_int
+        L.bt_find_neighbors_sym.argtypes = [_P, _P, C.c_int32, _P, _P, _P]
+        L.bt_find_neighbors_sym.restype = C.c_int
+        L.bt_fill_neighbors_sym.argtypes = [_P, _P, _P, _P, C.c_int64]
+        L.bt_fill_neighbors_sym.restype = C.c_int
         L.bt_density.argtypes = [_P, _P, _P, _P]
         L.bt_density.restype = C.c_int
         L.bt_free.argtypes = [_P]
@@ -166,22 +170,26 @@ class Tree:
             raise BtreeError(BT_ERR_ARG, "tree already freed")
         return self._h
 
-    def count(self, h: torch.Tensor):
-        """Count-only call: (counts int32 [n], offsets int64 [n+1])."""
+    def count(self, h: torch.Tensor, symmetric: bool = False):
+        """Count-only call: (counts int32 [n], offsets int64 [n+1]).  symmetric:
+        the max(h_i, h_j) criterion (bt_find_neighbors_sym)."""
         h = _dev_f64(h)
         counts = torch.empty(self.n, dtype=torch.int32, device=self.device)
         offsets = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
         _use_current_stream()
-        _check(lib().bt_find_neighbors(self._handle(), _ptr(h), 1, _ptr(counts), _ptr(offsets), None))
+        fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
+        _check(fn(self._handle(), _ptr(h), 1, _ptr(counts), _ptr(offsets), None))
         return counts, offsets
 
-    def fill(self, h: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None):
+    def fill(self, h: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,
+             symmetric: bool = False):
         h = _dev_f64(h)
         total = int(offsets[-1].item())
         if out is None:
             out = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
         _use_current_stream()
-        _check(lib().bt_fill_neighbors(self._handle(), _ptr(h), _ptr(offsets), _ptr(out), out.numel()))
+        fn = lib().bt_fill_neighbors_sym if symmetric else lib().bt_fill_neighbors
+        _check(fn(self._handle(), _ptr(h), _ptr(offsets), _ptr(out), out.numel()))
         return out[:total]
 
     def density(self, h: torch.Tensor, mass: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
@@ -195,17 +203,18 @@ class Tree:
         return out
 
     def find_neighbors(self, h: torch.Tensor, ngmax: int | None = None,
-                       counts=None, offsets=None, nbr_idx=None):
+                       counts=None, offsets=None, nbr_idx=None, symmetric: bool = False):
         """(counts, offsets, nbr_idx) for every particle.
 
         ngmax given: one bt_find_neighbors call into a buffer of n*ngmax slots
         (or the caller's nbr_idx).  ngmax None: count-only call, exact
-        allocation, then bt_fill_neighbors.
+        allocation, then bt_fill_neighbors.  symmetric: the max(h_i, h_j)
+        criterion (bt_find_neighbors_sym / bt_fill_neighbors_sym).
         """
         h = _dev_f64(h)
         if ngmax is None:
-            counts, offsets = self.count(h)
-            return counts, offsets, self.fill(h, offsets)
+            counts, offsets = self.count(h, symmetric)
+            return counts, offsets, self.fill(h, offsets, symmetric=symmetric)
         if counts is None:
             counts = torch.empty(self.n, dtype=torch.int32, device=self.device)
         if offsets is None:
@@ -213,8 +222,8 @@ class Tree:
         if nbr_idx is None:
             nbr_idx = torch.empty(max(self.n * int(ngmax), 1), dtype=torch.int32, device=self.device)
         _use_current_stream()
-        _check(lib().bt_find_neighbors(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets),
-                                       _ptr(nbr_idx)))
+        fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
+        _check(fn(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets), _ptr(nbr_idx)))
         return counts, offsets, nbr_idx
 
     def stats(self) -> dict:

@@ -294,6 +294,34 @@ int bt_fill_neighbors(const bt_tree *tc, const double *h, const int64_t *offsets
     });
 }
 
+int bt_find_neighbors_sym(const bt_tree *tc, const double *h, int32_t ngmax, int32_t *counts, int64_t *offsets,
+                          int32_t *nbr_idx) {
+    bt_tree *t = const_cast<bt_tree *>(tc);
+    if (!t || ngmax < 1 || (t->t.n > 0 && (!h || !counts || !offsets)) || (t->t.n == 0 && !offsets)) {
+        set_error(BT_ERR_ARG, "bt_find_neighbors_sym: need a tree, h, counts, offsets and ngmax >= 1");
+        return BT_ERR_ARG;
+    }
+    return guarded([&] {
+        Phase ph("search.total");
+        const int64_t cap = t->t.n * (int64_t)ngmax;
+        find_neighbors_sym(t->t, h, counts, offsets, nbr_idx, cap, true, nbr_idx != nullptr);
+    });
+}
+
+int bt_fill_neighbors_sym(const bt_tree *tc, const double *h, const int64_t *offsets, int32_t *nbr_idx,
+                          int64_t capacity) {
+    bt_tree *t = const_cast<bt_tree *>(tc);
+    if (!t || (t->t.n > 0 && (!h || !offsets || (!nbr_idx && capacity > 0))) || capacity < 0) {
+        set_error(BT_ERR_ARG, "bt_fill_neighbors_sym: need a tree, h, offsets, nbr_idx and capacity >= 0");
+        return BT_ERR_ARG;
+    }
+    return guarded([&] {
+        Phase ph("search.total");
+        if (t->t.n == 0) return;
+        find_neighbors_sym(t->t, h, nullptr, const_cast<int64_t *>(offsets), nbr_idx, capacity, false, true);
+    });
+}
+
 int bt_density(const bt_tree *tc, const double *h, const double *mass, double *rho) {
     bt_tree *t = const_cast<bt_tree *>(tc);
     if (!t || (t->t.n > 0 && (!h || !mass || !rho))) {

@@ -66,7 +66,8 @@ enum {
     C_WORK4 = 13,    // unit counter (big-unit descent)
     C_NEEDC = 14,    // sum over units of `loaded` (bound on candidate slots)
     C_NEEDM = 15,    // sum over units of ceil(loaded / 64) * nq (bound on mask words)
-    C_N = 16
+    C_WORK5 = 16,    // unit counter (symmetric-criterion pass)
+    C_N = 17
 };
 
 struct WalkArgs {
@@ -1163,6 +1164,121 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric criterion (reading R22): j is a neighbor of i
+// iff d2 < (2 max(h_i, h_j))^2.  fl(t^2) is monotone in t and d2 is the same
+// bits for (i, j) and (j, i), so N_sym(i) = N(i) u {j : i in N(j)}: the gather
+// sets plus their transpose.  The pass replays the recorded gather masks
+// (query i = unit query, candidate j = lane's slot): a pair (i, j) of N(i)
+// with NOT d2 < T_j is one-sided, and i is added to row j.  Lanes = candidates,
+// so a lane collects its candidate's one-sided queries in a 64-bit mask and
+// touches j's counter once per (unit, chunk).
+// ---------------------------------------------------------------------------
+__global__ void inverse_order_kernel(const float4 *__restrict__ rec32, int64_t n, int32_t *__restrict__ inv) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+        inv[__float_as_int(rec32[p].w)] = (int32_t)p;
+}
+
+__global__ void add_counts_kernel(const int32_t *__restrict__ g, const int32_t *__restrict__ x, int64_t n,
+                                  int32_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = g[i] + x[i];
+}
+
+// kFill = false: extra[j] += one-sided pairs (i, j).  kFill = true: append i
+// to row j at offsets[j] + gcnt[j] + (cursor extra[j], zeroed by the caller).
+template <bool kFill>
+__global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int32_t *__restrict__ inv,
+                                                           const int32_t *__restrict__ gcnt, int32_t *__restrict__ extra) {
+    __shared__ double4 qs[kFillWarps][kQ];
+    __shared__ double qT[kFillWarps][kQ];
+    const int lane = threadIdx.x & 31;
+    double4 *Q = qs[threadIdx.x >> 5];
+    double *TQ = qT[threadIdx.x >> 5];
+    WorkBatch wb;
+    for (;;) {
+        const long long u = next_unit(wb, &a.ctr[C_WORK5], a.n_units, 1, lane);
+        if (u >= a.n_units) break;
+        const int4 U = a.units[u];
+        const UnitRun R = a.urun[u];
+        const int nq = U.z;
+        __syncwarp();
+        // the queries' exact records and T_i = fl((2 h_i)^2); a pair can only be
+        // one-sided when T_j < T_i, so candidates with T_j >= max_i T_i are idle
+        double tmax = 0.0;
+        for (int q = lane; q < nq; q += 32) {
+            Q[q] = a.rec[U.y + q];
+            const double t = __dmul_rn(2.0, a.h_tree[U.y + q]);
+            TQ[q] = __dmul_rn(t, t);
+            tmax = fmax(tmax, TQ[q]);
+        }
+        tmax = warp_max(tmax);
+        __syncwarp();
+        const int nchk = (R.nstaged + 63) >> 6;
+        for (int k = 0; k < nchk; k++) {
+            const unsigned long long *mw = a.masks + R.mask_base + (long long)k * nq;
+            const unsigned long long w0 = lane < nq ? mw[lane] : 0ull, w1 = lane + 32 < nq ? mw[lane + 32] : 0ull;
+            if (!__any_sync(0xffffffffu, (w0 | w1) != 0ull)) continue;
+            int32_t j[2];
+            double4 c[2];
+            double T[2];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int slot = 64 * k + 32 * h + lane;
+                j[h] = slot < R.nstaged ? a.cands[R.cand_base + slot] : -1;
+                if (j[h] >= 0) {
+                    const int32_t tp = inv[j[h]];
+                    c[h] = a.rec[tp];
+                    const double t = __dmul_rn(2.0, a.h_tree[tp]);  // 2 h_j (exact)
+                    T[h] = __dmul_rn(t, t);
+                } else {
+                    c[h] = make_double4(0.0, 0.0, 0.0, 0.0);
+                    T[h] = 0.0;
+                }
+            }
+            const bool act0 = j[0] >= 0 && T[0] < tmax, act1 = j[1] >= 0 && T[1] < tmax;
+            if (!__any_sync(0xffffffffu, act0 || act1)) continue;
+            unsigned long long os[2] = {0ull, 0ull};  // bit q: (query q, this lane's candidate) one-sided
+            for (int q = 0; q < nq; q++) {
+                const unsigned long long m = __shfl_sync(0xffffffffu, q < 32 ? w0 : w1, q & 31);
+                if (m == 0ull) continue;
+                const double Ti = TQ[q];
+                const bool b0 = act0 && ((m >> lane) & 1ull) && T[0] < Ti;
+                const bool b1 = act1 && ((m >> (32 + lane)) & 1ull) && T[1] < Ti;
+                if (b0 || b1) {
+                    const double4 qr = Q[q];
+#pragma unroll
+                    for (int h = 0; h < 2; h++) {
+                        if (h == 0 ? b0 : b1) {
+                            // the predicate's d2, bit for bit (no contraction)
+                            const double dx = __dsub_rn(qr.x, c[h].x), dy = __dsub_rn(qr.y, c[h].y),
+                                         dz = __dsub_rn(qr.z, c[h].z);
+                            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+                            if (!(d2 < T[h])) os[h] |= 1ull << q;
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                if (!os[h]) continue;
+                const int cnt = __popcll(os[h]);
+                if constexpr (!kFill) {
+                    atomicAdd(&extra[j[h]], cnt);
+                } else {
+                    int32_t *dst = a.nbr + a.offsets[j[h]] + gcnt[j[h]] + atomicAdd(&extra[j[h]], cnt);
+                    unsigned long long m = os[h];
+                    while (m) {
+                        const int q = __ffsll((long long)m) - 1;
+                        m &= m - 1ull;
+                        *dst++ = (int32_t)__double_as_longlong(Q[q].w);  // caller index of query q
+                    }
+                }
+            }
+        }
+    }
+}
+
 // h in tree order + validation (h finite, > 0, <= 1e150) + checksum of h
 __global__ void gather_h_kernel(const float4 *__restrict__ rec32, const double *__restrict__ h, int64_t n,
                                 double *__restrict__ h_tree, int *bad, long long *hsum) {
@@ -1350,6 +1466,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         a.counts = cnt;
         long long hc[C_N];
         t.rec_valid = false;
+        t.sym_valid = false;
         run_descent(t, a, g, hc);
         const long long warps_w = (long long)g.w * (kWalkThreads / 32);
         {  // A10 staging + A11 pair tests, counts, masks; candidate and mask arenas: exact bounds from the descent
@@ -1414,6 +1531,94 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
 }
 
 
+// Symmetric criterion (reading R22): the gather test pass (recorded masks,
+// gather counts in t.sym_g), then sym_kernel<false> counts the one-sided pairs
+// per row (t.sym_x); counts = gather + extra.  The fill writes each row's
+// gather part with fill_kernel at the symmetric offsets and appends the
+// transposed one-sided pairs with sym_kernel<true>.
+void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
+                        int64_t capacity, bool count_pass, bool fill_pass) {
+    cudaStream_t st = stream();
+    const int64_t n = t.n;
+    if (n == 0) {
+        if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
+        t.total_pairs = t.max_count = 0;
+        BT_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    const int sms = num_sms();
+    const Grids g = walk_grids<false>();
+    t.sym_g.reserve(n, 0);
+    t.sym_x.reserve(n, 0);
+    t.sym_off.reserve(n + 1, 0);
+    bool have = false;
+    if (!count_pass) {
+        const long long hsum = gather_h(t, h, "bt_fill_neighbors_sym");
+        have = t.sym_valid && t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only;
+    }
+    if (!have) {
+        find_neighbors(t, h, t.sym_g.p, t.sym_off.p, nullptr, 0, true, false);  // gather counts + recorded masks
+        if (!t.inv_valid) {
+            t.inv.reserve(n, 0);
+            inverse_order_kernel<<<grid_for(n, 256, (int64_t)sms * 16), 256, 0, st>>>(t.rec32.p, n, t.inv.p);
+            BT_LAUNCH("inverse_order");
+            t.inv_valid = true;
+        }
+        WalkArgs a = walk_args(t, g);
+        a.masks = t.arena_masks.p;
+        a.cands = t.arena_cands.p;
+        BT_CUDA(cudaMemsetAsync(t.sym_x.p, 0, n * sizeof(int32_t), st));
+        zero_counter(t, C_WORK5);
+        {
+            Phase ph("search.sym_count");
+            sym_kernel<false><<<g.f, kFillThreads, 0, st>>>(a, t.inv.p, t.sym_g.p, t.sym_x.p);
+            BT_LAUNCH("sym_count");
+        }
+        t.sym_valid = true;
+    }
+    if (count_pass) {
+        add_counts_kernel<<<grid_for(n, 256, (int64_t)sms * 16), 256, 0, st>>>(t.sym_g.p, t.sym_x.p, n, counts);
+        BT_LAUNCH("sym_add_counts");
+        DBuf<long long> dtot(1);
+        Phase ph("search.scan");
+        device_scan<long long>(CountIn{counts}, OffsetOut{offsets}, n, dtot.p);
+        write_total_kernel<<<1, 1, 0, st>>>(offsets, n, dtot.p);
+        BT_LAUNCH("write_total");
+        zero_counter(t, C_MAXC);
+        max_count_kernel<<<grid_for(n, 256, (int64_t)sms * 8), 256, 0, st>>>(counts, n, (long long *)t.counters.p + C_MAXC);
+        BT_LAUNCH("max_count");
+    }
+    int64_t total = 0, maxc = 0;
+    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)}});
+    if (count_pass) t.max_count = maxc;
+    t.total_pairs = total;
+    if (!fill_pass || nbr_idx == nullptr) return;
+    if (total > capacity)
+        throw Error(BT_ERR_CAPACITY, "bt_find_neighbors_sym: " + std::to_string(total) +
+                                         " neighbor pairs exceed capacity " + std::to_string(capacity));
+    WalkArgs a = walk_args(t, g);
+    a.masks = t.arena_masks.p;
+    a.cands = t.arena_cands.p;
+    a.offsets = offsets;
+    a.nbr = nbr_idx;
+    zero_counter(t, C_WORK2);
+    zero_counter(t, C_WORK5);
+    BT_CUDA(cudaMemsetAsync(t.sym_x.p, 0, n * sizeof(int32_t), st));  // append cursors
+    {
+        Phase ph("search.fill");
+        fill_kernel<<<g.f, kFillThreads, 0, st>>>(a);
+        BT_LAUNCH("walk_fill");
+    }
+    {
+        Phase ph("search.sym_fill");
+        sym_kernel<true><<<g.f, kFillThreads, 0, st>>>(a, t.inv.p, t.sym_g.p, t.sym_x.p);
+        BT_LAUNCH("sym_fill");
+    }
+    t.sym_valid = false;  // the cursors overwrote the extra counts
+    BT_CUDA(cudaStreamSynchronize(st));
+}
+
+
 // SPH density with the neighbor search fused in: the
 // descent and the walk as in find_neighbors, the walk in density mode (no
 // masks, no candidate records, no CSR); rho in caller order.
@@ -1441,6 +1646,7 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
     a.rho = rho;
     long long hc[C_N];
     t.rec_valid = false;  // the density walk records no masks
+    t.sym_valid = false;
     run_descent(t, a, g, hc);
     const long long warps_w = (long long)g.w * (kWalkThreads / 32);
     t.scratch.reserve(warps_w * kScratch, 0);

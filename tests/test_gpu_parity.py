@@ -372,3 +372,122 @@ def test_density_errors(P):
     with pytest.raises(P.BtreeError) as e:
         t.density(torch.from_numpy(h).to(DEV), torch.from_numpy(m).to(DEV))
     assert e.value.code == 2
+
+
+# ---- symmetric criterion (reading R22) -----------------------
+def sym_union_ref(oracle, pos, h, s=64):
+    """Oracle symmetric sets as N u N^T of the oracle's own tree walk (pinned
+    equal to the symmetric brute force in test_oracle_pins); rows ascending."""
+    c, off, idx = oracle.Tree(pos, s, 0.5).neighbors(h)
+    n = len(pos)
+    rows = np.repeat(np.arange(n, dtype=np.int64), c)
+    cols = idx.astype(np.int64)
+    key = np.unique(np.concatenate([rows * (1 << 32) + cols, cols * (1 << 32) + rows]))
+    r = key >> 32
+    counts = np.bincount(r, minlength=n).astype(np.int32)
+    offsets = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    return counts, offsets, (key & 0xFFFFFFFF).astype(np.int32)
+
+
+def gpu_sym(P, pos, h, s=64, ngmax=None):
+    t = P.build(torch.from_numpy(pos).to(DEV), s, 0.5)
+    hd = torch.from_numpy(h).to(DEV)
+    counts, offsets, nbr = t.find_neighbors(hd, ngmax, symmetric=True)
+    torch.cuda.synchronize()
+    return t, (counts.cpu().numpy(), offsets.cpu().numpy(), sort_rows(counts, offsets, nbr))
+
+
+@pytest.mark.parametrize("cfg,n", [(1, None), (2, 100_000), (4, 100_000), (5, 200_000)])
+def test_symmetric_parity(P, oracle, cfg, n):
+    pos, h = datagen.make_config(cfg, n=n)
+    _, gpu = gpu_sym(P, pos, h)
+    ref = sym_union_ref(oracle, pos, h)
+    assert_same(gpu, ref)
+    if cfg == 1:  # the plain definition itself at cfg 1
+        assert_same(gpu, oracle.brute_force(pos, h, symmetric=True))
+    # gather sets are a subset; the relation is symmetric
+    if cfg in (2, 4, 5):
+        assert int(ref[1][-1]) > int(oracle.Tree(pos, 64).count(h).sum())
+
+
+def test_symmetric_closed_forms_and_edges(P, oracle):
+    # hand pair (0.6, 0.1) at d = 1, and the chain of test_symmetric_chain_closed_form
+    pos = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    _, gpu = gpu_sym(P, pos, np.array([0.6, 0.1]), s=1)
+    assert gpu[0].tolist() == [1, 1] and gpu[2].tolist() == [1, 0]
+    m = 101
+    pos = np.zeros((m, 3))
+    pos[:, 0] = np.arange(m, dtype=np.float64)
+    h = np.where(np.arange(m) % 2 == 0, 0.3, 0.55)
+    for s in (1, 4, 64):
+        _, gpu = gpu_sym(P, pos, h, s=s)
+        expect = np.full(m, 2)
+        expect[0] = expect[-1] = 1
+        assert np.array_equal(gpu[0], expect)
+        assert_same(gpu, oracle.brute_force(pos, h, symmetric=True))
+    # constant h: identical to the gather result
+    pos, h = datagen.make_config(3, n=50_000)
+    _, g = gpu_run(P, pos, h)
+    _, s_ = gpu_sym(P, pos, h)
+    assert_same(s_, g)
+    # n = 1 and the adversarial near-boundary set with variable h
+    _, gpu = gpu_sym(P, np.zeros((1, 3)), np.array([1.0]))
+    assert gpu[0].tolist() == [0]
+    pos, h = datagen.near_boundary(64, 64, 77)
+    h = h * np.random.default_rng(78).choice([1.0, 1.0 + 2.0 ** -50, 0.5], len(h))
+    _, gpu = gpu_sym(P, pos, h)
+    assert_same(gpu, oracle.brute_force(pos, h, symmetric=True))
+
+
+def test_symmetric_one_call_capacity_and_reuse(P, oracle):
+    pos, h = datagen.make_config(4, n=60_000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd = torch.from_numpy(h).to(DEV)
+    c1, o1, n1 = t.find_neighbors(hd, symmetric=True)              # count-only + exact fill
+    c2, o2, n2 = t.find_neighbors(hd, ngmax=512, symmetric=True)   # single call
+    assert torch.equal(c1, c2) and torch.equal(o1, o2)
+    assert np.array_equal(sort_rows(c1, o1, n1), sort_rows(c2, o2, n2))
+    # a gather call in between invalidates nothing the symmetric fill relies on
+    cs, os_ = t.count(hd, symmetric=True)
+    t.find_neighbors(hd, ngmax=512)
+    t.density(hd, torch.ones_like(hd))
+    n3 = t.fill(hd, os_, symmetric=True)
+    assert np.array_equal(sort_rows(cs, os_, n3), sort_rows(c1, o1, n1))
+    # capacity: counts/offsets valid, nbr untouched
+    n = pos.shape[0]
+    counts = torch.empty(n, dtype=torch.int32, device=DEV)
+    offsets = torch.empty(n + 1, dtype=torch.int64, device=DEV)
+    nbr = torch.full((n,), -7, dtype=torch.int32, device=DEV)
+    with pytest.raises(P.BtreeError) as e:
+        t.find_neighbors(hd, ngmax=1, counts=counts, offsets=offsets, nbr_idx=nbr, symmetric=True)
+    assert e.value.code == 3
+    assert torch.equal(counts, c1) and torch.equal(offsets, o1)
+    assert bool((nbr == -7).all())
+    ref = sym_union_ref(oracle, pos, h)
+    assert_same((c1.cpu().numpy(), o1.cpu().numpy(), sort_rows(c1, o1, n1)), ref)
+
+
+def test_symmetric_cfg5_full_size_sampled(P, oracle):
+    """Symmetric criterion at full cfg 5 (2^25): counts of sampled rows and
+    their sorted rows against the symmetric brute force; CSR invariants."""
+    pos, h = datagen.make_config(5)
+    n = pos.shape[0]
+    t = P.build(torch.from_numpy(pos).to(DEV), 64, 0.5)
+    hd = torch.from_numpy(h).to(DEV)
+    counts, offsets = t.count(hd, symmetric=True)
+    nbr = t.fill(hd, offsets, symmetric=True)
+    torch.cuda.synchronize()
+    c = counts.cpu().numpy()
+    off = offsets.cpu().numpy()
+    assert off[0] == 0 and np.all(np.diff(off) == c) and off[-1] == c.sum()
+    cg, _ = t.count(hd)
+    assert bool((counts >= cg).all()) and int(offsets[-1]) > int(cg.sum())
+    rng = np.random.default_rng(199)
+    q = np.sort(rng.choice(n, 300, replace=False)).astype(np.int64)
+    bc, boff, bidx = oracle.brute_force(pos, h, queries=q, symmetric=True)
+    assert np.array_equal(c[q], bc)
+    for k in range(q.size):
+        s0 = int(off[q[k]])
+        row = nbr[s0:s0 + int(c[q[k]])].cpu().numpy()
+        assert np.array_equal(np.sort(row), bidx[boff[k]:boff[k + 1]])

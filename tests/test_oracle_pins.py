@@ -345,3 +345,58 @@ def test_density_tree_equals_brute_force(oracle):
     a = oracle.Tree(pos, 16).density(h, mass)
     b = oracle.brute_density(pos, h, mass)
     assert np.array_equal(a, b)   # same terms, same (ascending j) order
+
+
+# ---- symmetric criterion (reading R22) ---------------------
+def test_symmetric_hand_values(oracle):
+    # d = 1, h = (0.6, 0.1): gather gives 0 -> 1 only (1 < 1.2, 1 >= 0.2); the
+    # max(h_i, h_j) criterion gives both directions
+    pos = np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 0.0]])
+    h = np.array([0.6, 0.1])
+    c, off, idx = oracle.brute_force(pos, h)
+    assert c.tolist() == [1, 0] and idx.tolist() == [1]
+    c, off, idx = oracle.brute_force(pos, h, symmetric=True)
+    assert c.tolist() == [1, 1] and idx.tolist() == [1, 0]
+    # strict at d = 2 max(h): d^2 = 1 = (2 * 0.5)^2 -> not neighbors
+    h = np.array([0.5, 0.1])
+    assert oracle.brute_force(pos, h, symmetric=True)[0].tolist() == [0, 0]
+    h = np.array([0.1, np.nextafter(0.5, 1.0)])
+    assert oracle.brute_force(pos, h, symmetric=True)[0].tolist() == [1, 1]
+
+
+def test_symmetric_chain_closed_form(oracle):
+    # unit-spaced chain, h alternating 0.3 (2h = 0.6 < 1) and 0.55 (2h = 1.1 < 2):
+    # gather: odd points see their two neighbours, even points none; symmetric:
+    # every point sees its two neighbours (ends: one)
+    m = 101
+    pos = np.zeros((m, 3))
+    pos[:, 0] = np.arange(m, dtype=np.float64)
+    h = np.where(np.arange(m) % 2 == 0, 0.3, 0.55)
+    cg = oracle.brute_force(pos, h)[0]
+    cs = oracle.brute_force(pos, h, symmetric=True)[0]
+    expect_g = np.where(np.arange(m) % 2 == 1, 2, 0)
+    expect_s = np.full(m, 2)
+    expect_s[0] = expect_s[-1] = 1
+    assert np.array_equal(cg, expect_g)
+    assert np.array_equal(cs, expect_s)
+
+
+def test_symmetric_is_gather_union_transpose(oracle):
+    # N_sym(i) = N(i) u {j : i in N(j)} (d^2 is the same bits both ways and
+    # fl(t^2) is monotone), with N from the tree walk (Alg. 2), an independent
+    # code path from the symmetric brute force; constant h: N_sym = N
+    pos, h = datagen.clustered(3000, 61, h=0.012)
+    h = h * np.random.default_rng(62).uniform(0.5, 2.0, len(h))
+    c, off, idx = oracle.Tree(pos, 16).neighbors(h)
+    rows = np.repeat(np.arange(len(pos)), c)
+    union = set(zip(rows.tolist(), idx.tolist())) | set(zip(idx.tolist(), rows.tolist()))
+    cs, offs, idxs = oracle.brute_force(pos, h, symmetric=True)
+    rs = np.repeat(np.arange(len(pos)), cs)
+    sym = set(zip(rs.tolist(), idxs.tolist()))
+    assert sym == union
+    assert len(sym) > c.sum()  # variable h: some pairs are one-sided
+    assert all((j, i) in sym for i, j in sym)
+    hc = np.full(len(pos), 0.02)
+    g = oracle.brute_force(pos, hc)
+    s = oracle.brute_force(pos, hc, symmetric=True)
+    _assert_same(g, s)

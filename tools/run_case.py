@@ -21,6 +21,7 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--exact", action="store_true")
 ap.add_argument("--ngmax", type=int, default=512)
 ap.add_argument("--count-only", action="store_true")
+ap.add_argument("--symmetric", action="store_true", help="max(h_i, h_j) criterion (bt_find_neighbors_sym)")
 args = ap.parse_args()
 
 pos_np, h_np = datagen.make_config(args.config, n=args.n)
@@ -40,9 +41,9 @@ for r in range(args.reps):
     t0 = time.perf_counter()
     t = P.Tree(pos, 64, 0.5)
     if args.count_only:
-        t.count(h)
+        t.count(h, symmetric=args.symmetric)
     else:
-        t.find_neighbors(h, args.ngmax, counts=counts, offsets=offsets, nbr_idx=nbr)
+        t.find_neighbors(h, args.ngmax, counts=counts, offsets=offsets, nbr_idx=nbr, symmetric=args.symmetric)
     st = t.stats()
     t.free()
     torch.cuda.synchronize()
