@@ -81,10 +81,17 @@ bt_tree *bt_build_ex(const double *pos, int64_t n, int32_t bucket_size, double m
  *   BT_POLICY_BTREE   the paper's adaptive b (Eq. 1 + the Eq. 4 halving loop);
  *   BT_POLICY_OCTREE  the classical octree the paper compares against (Sec. II,
  *                     P:98-103; Table II): b = 2 at every node, no ratio test
- *                     (max_empty and alpha are ignored).
- * The neighbor sets found through either tree are identical.
+ *                     (max_empty and alpha are ignored);
+ *   BT_POLICY_BTREE_2D  the b-tree with k = 2 (the paper is k-generic, Table I
+ *                     P:140; reading R23): Eq. 1 with b^2 s >= n_i, b^2
+ *                     sub-cells per node (x and y divided, z one slab), the
+ *                     Eq. 4 ratio over the b^2 sub-cells;
+ *   BT_POLICY_QUADTREE  b = 2 with k = 2, no ratio test.
+ * pos stays [n,3]; the k = 2 trees suit planar (2-D) particle sets and are
+ * valid for any input.  The neighbor sets found through any of these trees
+ * are identical.
  */
-enum { BT_POLICY_BTREE = 0, BT_POLICY_OCTREE = 1 };
+enum { BT_POLICY_BTREE = 0, BT_POLICY_OCTREE = 1, BT_POLICY_BTREE_2D = 2, BT_POLICY_QUADTREE = 3 };
 bt_tree *bt_build_policy(const double *pos, int64_t n, int32_t bucket_size, double max_empty,
                          double alpha, int32_t depth_cap, int32_t policy);
 

@@ -56,6 +56,8 @@ def lib():
         build()
         L = C.CDLL(_LIB)
         L.orc_branching_factor.argtypes = [C.c_int64, C.c_int64]
+        L.orc_branching_factor_k.argtypes = [C.c_int64, C.c_int64, C.c_int]
+        L.orc_branching_factor_k.restype = C.c_int
         L.orc_branching_factor.restype = C.c_int
         L.orc_cell_coord.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int]
         L.orc_cell_coord.restype = C.c_int
@@ -120,6 +122,13 @@ def default_threads() -> int:
 
 
 # ---- Eq. 1 - 5 helpers (exposed for the pins) -------------------------------
+POLICIES = {"btree": 0, "octree": 1, "btree2d": 2, "quadtree": 3}
+
+
+def branching_factor_k(n: int, s: int, k: int) -> int:
+    return lib().orc_branching_factor_k(n, s, k)
+
+
 def branching_factor(n: int, s: int) -> int:
     return lib().orc_branching_factor(n, s)
 
@@ -160,7 +169,7 @@ class Tree:
         self.pos = _f64(pos, (-1, 3))
         self.n = self.pos.shape[0]
         self._h = lib().orc_build_policy(_ptr(self.pos), self.n, bucket_size, max_empty, alpha, depth_cap,
-                                         1 if policy == "octree" else 0)
+                                         POLICIES[policy])
         if not self._h:
             raise ValueError("oracle: invalid build arguments")
 

@@ -45,6 +45,17 @@ int orc_branching_factor(int64_t n, int64_t s)
     return (int)b;
 }
 
+/* Eq. 1 for k dimensions (the paper is k-generic, Table I): the    */
+/* smallest integer b >= 2 with b^k * s >= n, k in {2, 3} (R23).          */
+int orc_branching_factor_k(int64_t n, int64_t s, int k)
+{
+    int64_t m = (n + s - 1) / s;
+    int64_t b = 2;
+    while ((k == 3 ? b * b * b : b * b) < m)
+        b++;
+    return (int)b;
+}
+
 /* ------------------------------------------------------------------ */
 /* Eq. 2 (Sec. III-A Step 2):                               */
 /*   x'_l = floor( (x_l - x_{l,min}) / (x_{l,max} - x_{l,min}) * b )   */
@@ -128,6 +139,7 @@ void orc_root_box(const double *pos, int64_t n, double *lo, double *hi)
 typedef struct orc_node {
     double lo[3], hi[3];
     int b;          /* accepted branching factor (internal nodes) */
+    int bz;         /* sub-cells along z: b, or 1 for k = 2 */
     int depth;
     int halvings;   /* redistribution rounds that halved b */
     int is_leaf;
@@ -145,6 +157,7 @@ typedef struct {
     double beta, alpha;
     int32_t depth_cap;
     int octree; /* FixedOctree policy: b = 2, no ratio loop (Sec. II) */
+    int k;      /* dimensions subdivided: 3, or 2 (x, y only; z is one slab) (R23) */
     double box_lo[3], box_hi[3];
     double M;       /* max |root box coordinate|, for the radius margin */
     orc_node *root; /* NULL iff n == 0 */
@@ -197,20 +210,22 @@ static orc_node *build_tree(orc_tree *t, const double *pos, const double *lo,
 
     /* Step 1: branching factor, Eq. 1 (computed once, then only halved: R6). */
     /* The octree policy fixes b = 2 and skips Step 3.                       */
-    int b = t->octree ? 2 : orc_branching_factor(n, t->s);
+    int b = t->octree ? 2 : orc_branching_factor_k(n, t->s, t->k);
     int64_t *cell = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
     int64_t *cnt = NULL;
     int64_t B = 0;
     for (;;) {
         /* Step 2: create b^k sub-cells and distribute the particles (Eq. 2, 3). */
-        B = (int64_t)b * b * b;
+        /* k = 2: the z axis is not divided (one slab, b_z = 1, so c3 = 0).      */
+        int bz = t->k == 3 ? b : 1;
+        B = (int64_t)b * b * bz;
         free(cnt);
         cnt = (int64_t *)calloc((size_t)B, sizeof(int64_t));
         for (int64_t p = 0; p < n; p++) {
             const double *x = pos + 3 * (int64_t)idx[p];
             int c1 = orc_cell_coord(x[0], lo[0], hi[0], b);
             int c2 = orc_cell_coord(x[1], lo[1], hi[1], b);
-            int c3 = orc_cell_coord(x[2], lo[2], hi[2], b);
+            int c3 = orc_cell_coord(x[2], lo[2], hi[2], bz);
             int64_t j = orc_cell_id(c1, c2, c3, b);
             cell[p] = j;
             cnt[j]++; /* "Update n_j" */
@@ -228,6 +243,7 @@ static orc_node *build_tree(orc_tree *t, const double *pos, const double *lo,
         }
     }
     nd->b = b;
+    nd->bz = t->k == 3 ? b : 1;
     t->halvings += nd->halvings;
 
     /* Stable distribution into per-cell lists (ascending original index). */
@@ -261,8 +277,9 @@ static orc_node *build_tree(orc_tree *t, const double *pos, const double *lo,
         c[2] = (int)(j / ((int64_t)b * b));
         double clo[3], chi[3];
         for (int l = 0; l < 3; l++) {
-            clo[l] = lo[l] + ((double)c[l] * (hi[l] - lo[l])) / (double)b;
-            chi[l] = lo[l] + ((double)(c[l] + 1) * (hi[l] - lo[l])) / (double)b;
+            double bl = (l == 2 && t->k == 2) ? 1.0 : (double)b; /* b_z = 1 for k = 2 */
+            clo[l] = lo[l] + ((double)c[l] * (hi[l] - lo[l])) / bl;
+            chi[l] = lo[l] + ((double)(c[l] + 1) * (hi[l] - lo[l])) / bl;
         }
         nd->child_j[k] = j;
         nd->child[k] = build_tree(t, pos, clo, chi, sorted + start[j], cnt[j], depth + 1);
@@ -275,7 +292,7 @@ static orc_node *build_tree(orc_tree *t, const double *pos, const double *lo,
 }
 
 orc_tree *orc_build_policy(const double *pos, int64_t n, int32_t s, double beta,
-                           double alpha, int32_t depth_cap, int octree);
+                           double alpha, int32_t depth_cap, int policy);
 
 orc_tree *orc_build(const double *pos, int64_t n, int32_t s, double beta,
                     double alpha, int32_t depth_cap)
@@ -283,10 +300,12 @@ orc_tree *orc_build(const double *pos, int64_t n, int32_t s, double beta,
     return orc_build_policy(pos, n, s, beta, alpha, depth_cap, 0);
 }
 
+/* policy: 0 b-tree (k = 3), 1 octree (b = 2, k = 3), 2 b-tree with k = 2, */
+/* 3 quadtree (b = 2, k = 2).                                             */
 orc_tree *orc_build_policy(const double *pos, int64_t n, int32_t s, double beta,
-                           double alpha, int32_t depth_cap, int octree)
+                           double alpha, int32_t depth_cap, int policy)
 {
-    if (n < 0 || s < 1 || !(beta > 0.0 && beta <= 1.0) || depth_cap < 0)
+    if (n < 0 || s < 1 || !(beta > 0.0 && beta <= 1.0) || depth_cap < 0 || policy < 0 || policy > 3)
         return NULL;
     orc_tree *t = (orc_tree *)calloc(1, sizeof(orc_tree));
     t->n = n;
@@ -294,7 +313,8 @@ orc_tree *orc_build_policy(const double *pos, int64_t n, int32_t s, double beta,
     t->beta = beta;
     t->alpha = alpha;
     t->depth_cap = depth_cap;
-    t->octree = octree != 0;
+    t->octree = policy == 1 || policy == 3;
+    t->k = policy >= 2 ? 2 : 3;
     if (n == 0)
         return t;
     orc_root_box(pos, n, t->box_lo, t->box_hi);
@@ -421,8 +441,8 @@ static void find_neighbors(const orc_node *nd, const double *pos, int64_t p,
     }
     const double *x = pos + 3 * p;
     int r[3][2];
-    for (int l = 0; l < 3; l++)
-        orc_range(x[l], Rp, nd->lo[l], nd->hi[l], nd->b, &r[l][0], &r[l][1]);
+    for (int l = 0; l < 3; l++) /* Eq. 5 per axis; k = 2: one z slab (b_z = 1) */
+        orc_range(x[l], Rp, nd->lo[l], nd->hi[l], (l == 2 && nd->bz == 1) ? 1 : nd->b, &r[l][0], &r[l][1]);
     int64_t lo_k = 0;
     for (int c3 = r[2][0]; c3 <= r[2][1]; c3++)
         for (int c2 = r[1][0]; c2 <= r[1][1]; c2++)

@@ -26,6 +26,10 @@ EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "b
            "bt_tree_order", "bt_profile_enable", "bt_profile_reset", "bt_profile_get"]
 
 
+# bt_build_policy's policies (include/btree.h)
+POLICIES = {"btree": 0, "octree": 1, "btree2d": 2, "quadtree": 3}
+
+
 class BtreeError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"{_NAMES.get(code, code)}: {msg}")
@@ -137,12 +141,12 @@ class Tree:
         self.n = pos.shape[0]
         self.device = pos.device
         _use_current_stream()
-        if policy not in ("btree", "octree"):
-            raise ValueError("policy must be 'btree' or 'octree'")
-        if policy == "octree":
+        if policy not in POLICIES:
+            raise ValueError(f"policy must be one of {sorted(POLICIES)}")
+        if policy != "btree":
             h = lib().bt_build_policy(_ptr(pos), self.n, int(bucket_size), float(max_empty),
                                       0.5 if alpha is None else float(alpha),
-                                      64 if depth_cap is None else int(depth_cap), 1)
+                                      64 if depth_cap is None else int(depth_cap), POLICIES[policy])
         elif alpha is None and depth_cap is None:
             h = lib().bt_build(_ptr(pos), self.n, int(bucket_size), float(max_empty))
         else:

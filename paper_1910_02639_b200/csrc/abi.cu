@@ -221,8 +221,8 @@ extern "C" {
 
 bt_tree *bt_build_policy(const double *pos, int64_t n, int32_t bucket_size, double max_empty, double alpha,
                          int32_t depth_cap, int32_t policy) {
-    if (policy != BT_POLICY_BTREE && policy != BT_POLICY_OCTREE) {
-        set_error(BT_ERR_ARG, "bt_build_policy: policy must be BT_POLICY_BTREE or BT_POLICY_OCTREE");
+    if (policy < BT_POLICY_BTREE || policy > BT_POLICY_QUADTREE) {
+        set_error(BT_ERR_ARG, "bt_build_policy: policy must be BT_POLICY_BTREE, _OCTREE, _BTREE_2D or _QUADTREE");
         return nullptr;
     }
     if (n < 0 || n > 2147483647LL || (pos == nullptr && n > 0) || bucket_size < 1 || !(max_empty > 0.0 && max_empty <= 1.0) ||
@@ -240,7 +240,8 @@ bt_tree *bt_build_policy(const double *pos, int64_t n, int32_t bucket_size, doub
         t->t.beta = max_empty;
         t->t.alpha = alpha;
         t->t.depth_cap = depth_cap;
-        t->t.octree = policy == BT_POLICY_OCTREE;
+        t->t.octree = policy == BT_POLICY_OCTREE || policy == BT_POLICY_QUADTREE;
+        t->t.dims = (policy == BT_POLICY_BTREE_2D || policy == BT_POLICY_QUADTREE) ? 2 : 3;
         Phase ph("build.total");
         build_tree(t->t, pos);
         BT_CUDA(cudaStreamSynchronize(stream()));

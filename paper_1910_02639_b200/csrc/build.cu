@@ -40,6 +40,8 @@ struct LevelNode {
     int32_t b;           // current / accepted branching factor
     int32_t flag;        // (re)distribute in this round
     int32_t halvings;
+    int32_t kz;          // 1: z is divided like x, y (k = 3); 0: one z slab (k = 2, R23)
+    int32_t pad_;
     int64_t cell_base;   // level-local first cell
     int64_t under;       // #{j < b^3 : n_j <= alpha s}   (Eq. 4 numerator)
     double bx[3];        // fl(b / ext) of the current b (cell_coord_fast)
@@ -136,23 +138,32 @@ __global__ void copy_rec_kernel(const double4 *__restrict__ src, double4 *__rest
 }
 
 // ---- A2: Eq. 1 --------------------------------------------------------------
-__device__ __forceinline__ int eq1_branching(int64_t n, int64_t s) {
-    int64_t m = (n + s - 1) / s;  // b^3 s >= n  <=>  b^3 >= ceil(n/s)   (R6)
-    int64_t b = (int64_t)cbrt((double)m);
+__device__ __forceinline__ int64_t ipow_k(int64_t b, int k) { return k == 3 ? b * b * b : b * b; }
+
+// smallest integer b >= 2 with b^k s >= n (R6; k = 2: R23)
+__device__ __forceinline__ int eq1_branching(int64_t n, int64_t s, int k) {
+    int64_t m = (n + s - 1) / s;  // b^k s >= n  <=>  b^k >= ceil(n/s)
+    int64_t b = (int64_t)(k == 3 ? cbrt((double)m) : sqrt((double)m));
     if (b < 2) b = 2;
-    while (b > 2 && (b - 1) * (b - 1) * (b - 1) >= m) b--;
-    while (b * b * b < m) b++;
+    while (b > 2 && ipow_k(b - 1, k) >= m) b--;
+    while (ipow_k(b, k) < m) b++;
     return (int)b;
 }
 
-__global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s, int octree, const NodeRec *nodes) {
+// sub-cells along z: b (k = 3) or 1 (k = 2: the z axis is one slab)
+__device__ __forceinline__ int bz_of(int b, int kz) { return kz ? b : 1; }
+
+__global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s, int octree, int dims, const NodeRec *nodes) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= nn) return;
-    // FixedOctree policy (the paper's comparison baseline): b = 2
-    int b = octree ? 2 : eq1_branching(ln[i].count, s);
+    // FixedOctree / quadtree policies (the paper's comparison baseline): b = 2
+    int b = octree ? 2 : eq1_branching(ln[i].count, s, dims);
+    const int kz = dims == 3 ? 1 : 0;
     ln[i].b0 = b;
     ln[i].b = b;
-    for (int l = 0; l < 3; l++) ln[i].bx[l] = __ddiv_rn((double)b, nodes[ln[i].gid].ext[l]);
+    ln[i].kz = kz;
+    for (int l = 0; l < 3; l++)
+        ln[i].bx[l] = __ddiv_rn((double)(l == 2 ? bz_of(b, kz) : b), nodes[ln[i].gid].ext[l]);
     ln[i].flag = 1;
     ln[i].halvings = 0;
     ln[i].under = 0;
@@ -182,7 +193,7 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__res
         // Eq. 2 (cell_coord_fast: identical results, division only near cell faces)
         int c1 = cell_coord_fast(r.x, nr.lo[0], nr.ext[0], L.bx[0], b);
         int c2 = cell_coord_fast(r.y, nr.lo[1], nr.ext[1], L.bx[1], b);
-        int c3 = cell_coord_fast(r.z, nr.lo[2], nr.ext[2], L.bx[2], b);
+        int c3 = cell_coord_fast(r.z, nr.lo[2], nr.ext[2], L.bx[2], bz_of(b, L.kz));
         uint32_t j = (uint32_t)c1 + (uint32_t)c2 * (uint32_t)b + (uint32_t)c3 * (uint32_t)b * (uint32_t)b;
         keys[p] = j;
         atomicAdd(&hist[L.cell_base + j], 1);
@@ -209,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) under_count_kernel(LevelNode *ln, in
         if (g < ncells) {
             node = find_node(ln, nn, g);
             const LevelNode &L = ln[node];
-            int64_t B = (int64_t)L.b * L.b * L.b;
+            int64_t B = (int64_t)L.b * L.b * bz_of(L.b, L.kz);
             under = L.flag && (g - L.cell_base) < B && (double)hist[g] <= alpha_s;
         }
         unsigned m = __ballot_sync(0xffffffffu, under);
@@ -228,11 +239,12 @@ __global__ void ratio_decide_kernel(LevelNode *ln, int64_t nn, double beta, int 
     if (i >= nn) return;
     LevelNode &L = ln[i];
     if (!L.flag) return;
-    double B = (double)((int64_t)L.b * L.b * L.b);
+    double B = (double)((int64_t)L.b * L.b * bz_of(L.b, L.kz));
     double r = __ddiv_rn((double)L.under, B);
     if (r >= beta && L.b > 2) {
         L.b = max(2, L.b / 2);
-        for (int l = 0; l < 3; l++) L.bx[l] = __ddiv_rn((double)L.b, nodes[L.gid].ext[l]);
+        for (int l = 0; l < 3; l++)
+            L.bx[l] = __ddiv_rn((double)(l == 2 ? bz_of(L.b, L.kz) : L.b), nodes[L.gid].ext[l]);
         L.halvings++;
         L.under = 0;
         L.flag = 1;
@@ -266,7 +278,9 @@ struct CellOut {
 };
 struct CellsOfNode {
     const LevelNode *ln;
-    __device__ long long operator()(int64_t i) const { return (long long)ln[i].b0 * ln[i].b0 * ln[i].b0; }
+    __device__ long long operator()(int64_t i) const {
+        return (long long)ln[i].b0 * ln[i].b0 * bz_of(ln[i].b0, ln[i].kz);
+    }
 };
 struct CellBaseOut {
     LevelNode *ln;
@@ -304,9 +318,10 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const LevelNode *__restr
                 int b = L.b;
                 int cc[3] = {(int)(j % b), (int)((j / b) % b), (int)(j / ((int64_t)b * b))};
                 for (int l = 0; l < 3; l++) {
-                    // child box = equal 1/b slice of the parent (Sec. III-A Step 1)
-                    double lo = __dadd_rn(P.lo[l], __ddiv_rn(__dmul_rn((double)cc[l], P.ext[l]), (double)b));
-                    double hi = __dadd_rn(P.lo[l], __ddiv_rn(__dmul_rn((double)(cc[l] + 1), P.ext[l]), (double)b));
+                    // child box = equal 1/b slice of the parent (Sec. III-A Step 1); k = 2: whole z slab
+                    const double bl = (double)(l == 2 ? bz_of(b, L.kz) : b);
+                    double lo = __dadd_rn(P.lo[l], __ddiv_rn(__dmul_rn((double)cc[l], P.ext[l]), bl));
+                    double hi = __dadd_rn(P.lo[l], __ddiv_rn(__dmul_rn((double)(cc[l] + 1), P.ext[l]), bl));
                     R.lo[l] = lo;
                     R.ext[l] = __dsub_rn(hi, lo);
                 }
@@ -335,8 +350,9 @@ __global__ void finalize_level_nodes_kernel(const LevelNode *ln, int64_t nn, Nod
     if (i >= nn) return;
     NodeRec &R = nodes[ln[i].gid];
     R.b = ln[i].b;
+    R.bz = bz_of(R.b, ln[i].kz);
     R.cell_base = cells_base + ln[i].cell_base;
-    for (int l = 0; l < 3; l++) R.bx[l] = __ddiv_rn((double)R.b, R.ext[l]);
+    for (int l = 0; l < 3; l++) R.bx[l] = __ddiv_rn((double)(l == 2 ? R.bz : R.b), R.ext[l]);
     if (ln[i].halvings) atomicAdd(halvings, (unsigned long long)ln[i].halvings);
 }
 
@@ -758,7 +774,8 @@ void build_tree(TreeDev &t, const double *pos) {
         while (nn > 0) {
             Phase ph("build.level");
             // A2: Eq. 1 and the level's cell layout
-            level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s, t.octree ? 1 : 0, t.nodes.p);
+            level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s, t.octree ? 1 : 0, t.dims,
+                                                                        t.nodes.p);
             BT_LAUNCH("level_b");
             device_scan<long long>(CellsOfNode{ln.p}, CellBaseOut{ln.p}, nn, dtotal.p);
             long long ncells_h = 0;

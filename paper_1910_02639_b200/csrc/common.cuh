@@ -110,7 +110,9 @@ struct NodeRec {      // one internal node
     int32_t b;        // accepted branching factor per dimension
     int32_t depth;
     int64_t cell_base;  // first entry of this node's b^3 cells in the cell table
-    double bx[3];     // fl(b / ext): cell_coord_fast's multiplier (set with b)
+    double bx[3];     // fl(b_l / ext): cell_coord_fast's multiplier (set with b)
+    int32_t bz;       // sub-cells along z: b, or 1 for the k = 2 policies (R23)
+    int32_t pad_;
 };
 
 // cell table code: -1 empty, >= 0 leaf id, <= -2 internal node (id = -2 - code)
@@ -132,7 +134,8 @@ struct TreeDev {
     int32_t s = 64;
     double beta = 0.5, alpha = 0.5;
     int32_t depth_cap = 64;
-    bool octree = false;       // FixedOctree policy: b = 2 at every node, no ratio test
+    bool octree = false;       // FixedOctree / quadtree policy: b = 2 at every node, no ratio test
+    int32_t dims = 3;          // k: 3, or 2 (x, y subdivided, z one slab; R23)
     // records in tree (depth-first leaf) order: x, y, z, caller index (bits)
     DBuf<double4> rec;
     // compact records in tree order: fl32(fl64(x - c_leaf)) per axis, caller index (int bits)

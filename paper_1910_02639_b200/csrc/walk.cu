@@ -411,9 +411,10 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
                     b = nd.b;
                     cb = nd.cell_base;
                     int r0[3], r1[3];
-                    for (int l = 0; l < 3; l++) {  // Eq. 5 with R'_u (lemma L2)
-                        r0[l] = cell_coord_fast(__dsub_rn(qlo[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], b);
-                        r1[l] = cell_coord_fast(__dadd_rn(qhi[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], b);
+                    for (int l = 0; l < 3; l++) {  // Eq. 5 with R'_u (lemma L2); b_z = nd.bz
+                        const int bl = l == 2 ? nd.bz : b;
+                        r0[l] = cell_coord_fast(__dsub_rn(qlo[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], bl);
+                        r1[l] = cell_coord_fast(__dadd_rn(qhi[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], bl);
                     }
                     r0x = r0[0];
                     r0y = r0[1];

@@ -491,3 +491,54 @@ def test_symmetric_cfg5_full_size_sampled(P, oracle):
         s0 = int(off[q[k]])
         row = nbr[s0:s0 + int(c[q[k]])].cpu().numpy()
         assert np.array_equal(np.sort(row), bidx[boff[k]:boff[k + 1]])
+
+
+# ---- k = 2 policies (b-tree with b^2 sub-cells, quadtree; reading R23) -----------
+def _plane(n, seed):
+    rng = np.random.default_rng(seed)
+    pos = np.zeros((n, 3))
+    pos[:, :2] = rng.random((n, 2))
+    h = 0.5 * np.sqrt(100.0 / (np.pi * n)) * rng.uniform(0.8, 1.2, n)  # ~100 neighbours in 2-D
+    return pos, h
+
+
+@pytest.mark.parametrize("policy", ["btree2d", "quadtree"])
+@pytest.mark.parametrize("case", ["plane", "cfg2", "cfg5"])
+def test_k2_policy_parity(P, oracle, policy, case):
+    if case == "plane":
+        pos, h = _plane(200_003, 7)
+    elif case == "cfg2":
+        pos, h = datagen.make_config(2, n=100_000)
+    else:
+        pos, h = datagen.make_config(5, n=200_000)
+    t = P.build(torch.from_numpy(pos).to(DEV), 64, 0.5, policy=policy)
+    hd = torch.from_numpy(h).to(DEV)
+    counts, offsets, nbr = t.find_neighbors(hd)
+    gpu = (counts.cpu().numpy(), offsets.cpu().numpy(), sort_rows(counts, offsets, nbr))
+    ot = oracle.Tree(pos, 64, 0.5, policy=policy)
+    assert_same(gpu, ot.neighbors(h))
+    assert_same_tree(t, ot)
+
+
+def test_k2_plane_lattice_and_halving(P, oracle):
+    # the oracle-pinned shapes: 16^2 plane lattice at s = 4 (depth 1, b = 8) and
+    # the 12 -> 6 -> 3 -> 2 halving sequence; 2-D lattice closed form: 2h = 2.5
+    # gives the 20 integer offsets with a^2 + b^2 <= 6 in the interior
+    g = np.arange(16, dtype=np.float64)
+    gx, gy = np.meshgrid(g, g, indexing="ij")
+    pos = np.ascontiguousarray(np.stack([gx.ravel(), gy.ravel(), np.zeros(256)], axis=1))
+    for pol in ("btree2d", "quadtree"):
+        t = P.build(torch.from_numpy(pos).to(DEV), 4, 0.5, policy=pol)
+        assert_same_tree(t, oracle.Tree(pos, 4, 0.5, policy=pol))
+        hd = torch.full((256,), 1.25, dtype=torch.float64, device=DEV)
+        c = t.count(hd)[0].cpu().numpy().reshape(16, 16)
+        assert np.all(c[2:-2, 2:-2] == 20)
+    rng = np.random.default_rng(4)
+    pts = rng.random((1000, 3)) * np.array([0.01, 0.01, 1.0])
+    pos = np.concatenate([pts, [[1.0, 1.0, 1.0]]])
+    t = P.build(torch.from_numpy(pos).to(DEV), 8, 0.5, policy="btree2d")
+    ot = oracle.Tree(pos, 8, 0.5, policy="btree2d")
+    assert t.stats()["root_b"] == 2
+    assert_same_tree(t, ot)
+    with pytest.raises(ValueError):
+        P.build(torch.from_numpy(pos).to(DEV), 8, 0.5, policy="k3")

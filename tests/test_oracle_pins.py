@@ -400,3 +400,69 @@ def test_symmetric_is_gather_union_transpose(oracle):
     g = oracle.brute_force(pos, hc)
     s = oracle.brute_force(pos, hc, symmetric=True)
     _assert_same(g, s)
+
+
+# ---- k = 2 (the paper's k-generic b-tree, Table I; reading R23) ---------
+def _plane_lattice(m, z=0.0):
+    g = np.arange(m, dtype=np.float64)
+    gx, gy = np.meshgrid(g, g, indexing="ij")
+    return np.ascontiguousarray(np.stack([gx.ravel(), gy.ravel(), np.full(m * m, z)], axis=1))
+
+
+def test_eq1_two_dimensions(oracle):
+    # b = smallest integer >= 2 with b^2 s >= n, by integer arithmetic
+    assert oracle.branching_factor_k(10**6, 64, 2) == 125      # 125^2 = 15625 = 10^6 / 64
+    assert oracle.branching_factor_k(10**6 + 1, 64, 2) == 126
+    assert oracle.branching_factor_k(5, 8, 2) == 2
+    assert oracle.branching_factor_k(2**25, 64, 2) == 725    # 724^2 < 524288 <= 725^2
+    rng = np.random.default_rng(17)
+    for _ in range(500):
+        n, s = int(rng.integers(1, 10**9)), int(rng.integers(1, 5000))
+        b = oracle.branching_factor_k(n, s, 2)
+        m = -(-n // s)
+        assert b * b >= m and (b == 2 or (b - 1) ** 2 < m)
+        assert oracle.branching_factor_k(n, s, 3) == oracle.branching_factor(n, s)
+
+
+@pytest.mark.parametrize("m", [4, 8, 16])
+def test_plane_lattice_best_case_k2(oracle, m):
+    # m^2 plane lattice, s = 4: Eq. 1 (k = 2) gives b = m/2, every cell 2x2 =
+    # 4 points = s: depth 1, no halving, (m/2)^2 leaves of 4 -- the 2-D analogue
+    # of the Table II best case; the quadtree reaches it only at depth log2(m/2)
+    pos = _plane_lattice(m)
+    st = oracle.Tree(pos, 4, policy="btree2d").stats()
+    assert st["depth"] == 1 and st["halvings"] == 0 and st["nodes"] == 1
+    assert st["root_b"] == m // 2 and st["leaves"] == (m // 2) ** 2
+    _, _, lc, _ = oracle.Tree(pos, 4, policy="btree2d").order()
+    assert np.all(lc == 4)
+    q = oracle.Tree(pos, 4, policy="quadtree").stats()
+    assert q["root_b"] == 2 and q["leaves"] == (m // 2) ** 2
+    assert q["depth"] == int(np.log2(m // 2)) and q["nodes"] == sum(4 ** d for d in range(q["depth"]))
+
+
+def test_halving_hand_derived_k2(oracle):
+    """1000 points in [0,0.01)^2 x [0,1) plus one at (1,1,1), s = 8, k = 2:
+    Eq. 1 gives b = 12 (11^2 < 126 <= 12^2); r = 142/144 -> b = 6; r = 34/36 ->
+    b = 3; r = 7/9 -> b = 2; at b = 2 the loop stops: 3 halvings at the root."""
+    rng = np.random.default_rng(4)
+    pts = rng.random((1000, 3)) * np.array([0.01, 0.01, 1.0])
+    pos = np.concatenate([pts, [[1.0, 1.0, 1.0]]])
+    st = oracle.Tree(pos, 8, 0.5, policy="btree2d").stats()
+    assert st["root_b"] == 2
+    t = oracle.Tree(pos, 8, 1.0, policy="btree2d")
+    assert t.stats()["root_b"] == 12 and t.stats()["halvings"] == 0
+
+
+def test_k2_trees_same_neighbors(oracle):
+    # the neighbor sets do not depend on the tree: k = 2 (slabs through z) and the
+    # quadtree give the brute-force sets on 3-D and planar inputs
+    pos, h = datagen.clustered(5000, 93, h=0.012)
+    ref = oracle.brute_force(pos, h)
+    for pol in ("btree2d", "quadtree"):
+        for s in (4, 16, 64):
+            _assert_same(oracle.Tree(pos, s, 0.5, policy=pol).neighbors(h), ref)
+    flat = pos.copy()
+    flat[:, 2] = 0.25
+    ref = oracle.brute_force(flat, h)
+    for pol in ("btree", "btree2d", "quadtree"):
+        _assert_same(oracle.Tree(flat, 16, 0.5, policy=pol).neighbors(h), ref)

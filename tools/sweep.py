@@ -28,10 +28,19 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--ngmax", type=int, default=512)
+ap.add_argument("--plane", type=int, default=0,
+                help="planar input of this many particles (z = 0, ~100 2-D neighbours) instead of a config")
 ap.add_argument("--out", default=None)
 args = ap.parse_args()
 
-pos_np, h_np = datagen.make_config(args.config, n=args.n)
+if args.plane:
+    import numpy as np
+    rng = np.random.default_rng(7)
+    pos_np = np.zeros((args.plane, 3))
+    pos_np[:, :2] = rng.random((args.plane, 2))
+    h_np = 0.5 * np.sqrt(100.0 / (np.pi * args.plane)) * rng.uniform(0.8, 1.2, args.plane)
+else:
+    pos_np, h_np = datagen.make_config(args.config, n=args.n)
 n = pos_np.shape[0]
 dev = torch.device("cuda:0")
 pos = torch.from_numpy(pos_np).to(dev)
@@ -70,16 +79,24 @@ def run(s, beta, policy):
 
 rows = []
 t0 = time.time()
-for s in (8, 16, 32, 64, 128, 256):
-    rows.append(run(s, 0.5, "btree"))
-for beta in (0.1, 0.25, 0.75, 1.0):
-    rows.append(run(64, beta, "btree"))
-for s in (8, 32, 64):
-    rows.append(run(s, 0.5, "octree"))
+if args.plane:  # k = 2 policies (R23) against the 3-D ones on a planar set
+    for pol in ("btree", "octree", "btree2d", "quadtree"):
+        for s in (16, 64):
+            rows.append(run(s, 0.5, pol))
+else:
+    for s in (8, 16, 32, 64, 128, 256):
+        rows.append(run(s, 0.5, "btree"))
+    for beta in (0.1, 0.25, 0.75, 1.0):
+        rows.append(run(64, beta, "btree"))
+    for s in (8, 32, 64):
+        rows.append(run(s, 0.5, "octree"))
+    if n <= 4_000_000:  # k = 2 trees on 3-D data: columns through z (at cfg 5 the walk arena exceeds HBM)
+        rows.append(run(64, 0.5, "btree2d"))
+        rows.append(run(64, 0.5, "quadtree"))
 ref = rows[0]["count_checksum"]
 for r in rows:
     r["same_counts_as_first"] = r["count_checksum"] == ref
-out = {"config": args.config, "n": n, "reps": args.reps, "device": torch.cuda.get_device_name(0),
+out = {"config": "plane" if args.plane else args.config, "n": n, "reps": args.reps, "device": torch.cuda.get_device_name(0),
        "wall_s": time.time() - t0, "rows": rows}
 text = json.dumps(out, indent=1)
 print(text)
