@@ -559,6 +559,8 @@ struct UnitSm {                     // per-warp unit state (shared memory)
     long long cand_base, mask_base;  // the unit's record bases
     Slab cs, ms;                     // the warp's candidate / mask slabs
     long long tests, exact, staged, loaded;  // warp totals
+    float4 *scr;                     // the warp's staging scratch (read from here: not rematerialised)
+    int32_t *cand_ptr;               // the unit's candidate-index records (a.cands + cand_base)
     double c[3], E;                  // unit centre, coordinate bound (L4)
     float4 box0, box1;               // fp32 query box relative to c: (lo xyz, cull2), (hi xyz, -)
     int q0, nq;                      // (8-byte aligned: read as one int2)
@@ -619,7 +621,7 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
         for (int h = 0; h < 2; h++) {
             const int s = 64 * k + 32 * h + lane;
             real[h] = s < n;
-            c[h] = real[h] ? blk[s] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+            c[h] = real[h] ? __ldcg(&blk[s]) : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
             const float nc = __fmaf_rn(c[h].z, c[h].z, __fmaf_rn(c[h].y, c[h].y, __fmul_rn(c[h].x, c[h].x)));
             ac[h] = real[h] ? __fmul_rn(ku, nc) : inf;  // identical to test_block
         }
@@ -672,7 +674,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int s = 32 * j + lane;
-        c[j] = (s < n) ? blk[s] : make_float4(0.f, 0.f, 0.f, 0.f);
+        c[j] = (s < n) ? __ldcg(&blk[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
         const float nc = __fmaf_rn(c[j].z, c[j].z, __fmaf_rn(c[j].y, c[j].y, __fmul_rn(c[j].x, c[j].x)));
         ac[j] = (s < n) ? __fmul_rn(ku, nc) : inf;  // k |c|^2 (exact scaling)
     }
@@ -810,13 +812,14 @@ __device__ __forceinline__ void locate(const WalkSmem &S, int nl, int total, int
 // staged from the fp64 records (a = fl32(fl64(x - c))).
 template <bool kMixed>
 __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int nl, int total, int &w0,
-                                            int &owner, float4 *scr, int &nst, int slot0) {
+                                            int &owner, int &nst, int slot0) {
     const unsigned lt = lanemask_lt(), le = lt | (1u << lane);
     const float4 *__restrict__ rec32 = a.rec32;
     const float4 B0 = S.u.box0, B1 = S.u.box1;
     const int2 qn = lds2iv(&S.u.q0);
     const bool rec_ok = S.u.rec_ok != 0;
-    int32_t *cands = a.cands + S.u.cand_base + slot0;
+    float4 *const scr = S.u.scr;
+    int32_t *const cands = S.u.cand_ptr + slot0;
     // record of position pos: the compact record, or (large leaf of a kMixed
     // group, `rel` set) the fp64 record already relative to the unit centre
     auto load = [&](int pos, int mine, bool &rel) {
@@ -868,7 +871,7 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             const int slot = nst + __popc(km & lt);
-            scr[slot] = make_float4(ax, ay, az, __int_as_float(pos));
+            __stcg(&scr[slot], make_float4(ax, ay, az, __int_as_float(pos)));  // L2-resident scratch
             if (rec_ok) __stcs(&cands[slot], __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
         }
@@ -890,8 +893,8 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
     WalkSmemT<kDensity> &S = smem[threadIdx.x >> 5];
     const float inf = __int_as_float(0x7f800000);
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    float4 *const scr = a.scratch + gwarp * kScratch;
     if (lane == 0) {
+        S.u.scr = a.scratch + gwarp * kScratch;
         S.u.cs = Slab();
         S.u.ms = Slab();
         S.u.tests = S.u.exact = S.u.staged = S.u.loaded = 0;
@@ -966,6 +969,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                 S.u.cs = cs;
                 S.u.ms = ms;
                 S.u.cand_base = cs.cur;
+                S.u.cand_ptr = a.cands + cs.cur;
                 S.u.mask_base = ms.cur;
                 S.u.c[0] = G.c[0];
                 S.u.c[1] = G.c[1];
@@ -1030,9 +1034,9 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     have_group = true;
                 }
                 if (mixed)
-                    stage_group<true>(S, a, lane, nl, total, w0, owner, scr, nst, slot0);
+                    stage_group<true>(S, a, lane, nl, total, w0, owner, nst, slot0);
                 else
-                    stage_group<false>(S, a, lane, nl, total, w0, owner, scr, nst, slot0);
+                    stage_group<false>(S, a, lane, nl, total, w0, owner, nst, slot0);
                 if (w0 < total) break;  // scratch full
                 loaded += total;
                 g0 += kGroup;
@@ -1046,7 +1050,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             if (true) {} else
 #endif
             for (int b0 = 0; b0 < ntest; b0 += kBlk) {
-                const int2 inc = test_block<kDensity>(S, a, lane, scr + b0, min(kBlk, ntest - b0), slot0 + b0, dacc);
+                const int2 inc = test_block<kDensity>(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0), slot0 + b0, dacc);
                 cnt0 += inc.x;
                 cnt1 += inc.y;
             }
@@ -1056,7 +1060,8 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             }
             // move the partial block to the front of the scratch
             const int rest = nst - ntest;
-            for (int i = lane; i < rest; i += 32) scr[i] = scr[ntest + i];
+            float4 *const scr = S.u.scr;
+            for (int i = lane; i < rest; i += 32) __stcg(&scr[i], __ldcg(&scr[ntest + i]));
             slot0 += ntest;
             nst = rest;
             __syncwarp();
