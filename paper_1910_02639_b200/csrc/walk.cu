@@ -734,15 +734,30 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     __syncwarp();
     long long exact = 0;
     if (__any_sync(0xffffffffu, band)) resolve_band(S, a, lane, blk, n, exact);
-    // self is never its own neighbor (R12); counts
+    // self is never its own neighbor (R12); counts; the final masks recorded
+    // for the fill pass (chunk kk = us0 / 64 + k of the unit) straight from
+    // the lanes that own the queries
     int inc[2] = {0, 0};
+    unsigned long long *const dst =
+        (!kDensity && S.u.rec_ok) ? a.masks + S.u.mask_base + (long long)(us0 >> 6) * nq : nullptr;
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int q = lane + 32 * h;
         if (q < nq) {
             const int sl = S.self[q] - us0;
-            if (sl >= 0 && sl < n) S.mask[sl >> 6][q] &= ~(1ull << (sl & 63));
-            inc[h] = __popcll(S.mask[0][q]) + (nch > 1 ? __popcll(S.mask[1][q]) : 0);
+            unsigned long long m0 = S.mask[0][q], m1 = nch > 1 ? S.mask[1][q] : 0ull;
+            if (sl >= 0 && sl < n) {
+                if (sl < 64) m0 &= ~(1ull << sl);
+                else m1 &= ~(1ull << (sl - 64));
+            }
+            inc[h] = __popcll(m0) + __popcll(m1);
+            if constexpr (kDensity) {
+                S.mask[0][q] = m0;
+                S.mask[1][q] = m1;
+            } else if (dst) {
+                __stcs(&dst[q], m0);
+                if (nch > 1) __stcs(&dst[nq + q], m1);
+            }
         }
     }
     __syncwarp();
@@ -778,11 +793,6 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             }
         }
         __syncwarp();
-    } else if (S.u.rec_ok) {
-        // record the masks (the fill pass): chunk kk = us0 / 64 + k of the unit
-        unsigned long long *dst = a.masks + S.u.mask_base + (long long)(us0 >> 6) * nq;
-        for (int k = 0; k < nch; k++)
-            for (int q = lane; q < nq; q += 32) __stcs(&dst[k * nq + q], S.mask[k][q]);
     }
     if (lane == 0) {
         S.u.tests += (long long)n * nq;
