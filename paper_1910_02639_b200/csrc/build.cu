@@ -404,7 +404,7 @@ __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k)
 // One warp per leaf.  rank(e) = #{k in leaf : idx_k < idx_e} (caller indices
 // are distinct), O(m^2 / 32) per leaf: m <= s = 64 in the configurations.
 __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *__restrict__ src, double4 *__restrict__ dst,
-                                                                 float4 *__restrict__ dst32,
+                                                                 float4 *__restrict__ dst32, int32_t *__restrict__ perm,
                                                                  const int32_t *__restrict__ leaf_begin,
                                                                  const int32_t *__restrict__ leaf_count, int64_t n_leaves,
                                                                  double *__restrict__ leaf_box,
@@ -452,11 +452,13 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
             }
             if (ok0) {
                 dst[b0 + r0] = v0;
+                perm[b0 + r0] = i0;
                 dst32[b0 + r0] = make_float4(__double2float_rn(__dsub_rn(v0.x, c[0])), __double2float_rn(__dsub_rn(v0.y, c[1])),
                                              __double2float_rn(__dsub_rn(v0.z, c[2])), __int_as_float(i0));
             }
             if (ok1) {
                 dst[b0 + r1] = v1;
+                perm[b0 + r1] = i1;
                 dst32[b0 + r1] = make_float4(__double2float_rn(__dsub_rn(v1.x, c[0])), __double2float_rn(__dsub_rn(v1.y, c[1])),
                                              __double2float_rn(__dsub_rn(v1.z, c[2])), __int_as_float(i1));
             }
@@ -503,6 +505,7 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
             if (e < m) {
                 dst[b0 + rank] = v;
                 // compact record: fl32(fl64(x - c_L)), caller index (walk staging, lemma L4)
+                perm[b0 + rank] = (int32_t)my;
                 dst32[b0 + rank] = make_float4(__double2float_rn(__dsub_rn(v.x, c[0])),
                                                __double2float_rn(__dsub_rn(v.y, c[1])),
                                                __double2float_rn(__dsub_rn(v.z, c[2])), __int_as_float((int)my));
@@ -881,8 +884,9 @@ void build_tree(TreeDev &t, const double *pos) {
         Phase ph("build.leaves");
         t.leaf_box.alloc(6 * (size_t)t.n_leaves);
         t.rec32.alloc(n);
+        t.perm.alloc(n);
         leaf_finalize_kernel<<<grid_for(t.n_leaves * 32, kThreads, (int64_t)sms * 32), kThreads, 0, st>>>(
-            fin.p, t.rec.p, t.rec32.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
+            fin.p, t.rec.p, t.rec32.p, t.perm.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
         BT_LAUNCH("leaf_finalize");
         DBuf<long long> dtot(1);
         // small leaves paired (runs of small leaves, pair by rank, box check)

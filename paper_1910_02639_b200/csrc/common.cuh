@@ -140,6 +140,7 @@ struct TreeDev {
     DBuf<double4> rec;
     // compact records in tree order: fl32(fl64(x - c_leaf)) per axis, caller index (int bits)
     DBuf<float4> rec32;
+    DBuf<int32_t> perm;        // caller index of each tree position (as rec / rec32 .w)
     DBuf<NodeRec> nodes;       // internal nodes, all levels
     int64_t n_nodes = 0;
     DBuf<int32_t> cells;       // cell table, all levels

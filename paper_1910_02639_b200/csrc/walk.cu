@@ -73,6 +73,7 @@ enum {
 struct WalkArgs {
     const double4 *rec;
     const float4 *rec32;
+    const int32_t *perm;      // caller index of each tree position
     const double *h_tree;
     const NodeRec *nodes;
     const int32_t *cells;
@@ -1143,7 +1144,7 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
         const int nq = U.z;
         const int nchk = (R.nstaged + 63) >> 6;
         for (int q = lane; q < nq; q += 32)
-            F.row[q] = a.nbr + a.offsets[__float_as_int(a.rec32[U.y + q].w)];  // caller index (16-B record)
+            F.row[q] = a.nbr + a.offsets[a.perm[U.y + q]];
         for (int kk0 = 0; kk0 < nchk; kk0 += kFillChunks) {
             const int nk = min(kFillChunks, nchk - kk0);
             int32_t c0[kFillChunks], c1[kFillChunks];
@@ -1190,9 +1191,9 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
 // so a lane collects its candidate's one-sided queries in a 64-bit mask and
 // touches j's counter once per (unit, chunk).
 // ---------------------------------------------------------------------------
-__global__ void inverse_order_kernel(const float4 *__restrict__ rec32, int64_t n, int32_t *__restrict__ inv) {
+__global__ void inverse_order_kernel(const int32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ inv) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-        inv[__float_as_int(rec32[p].w)] = (int32_t)p;
+        inv[perm[p]] = (int32_t)p;
 }
 
 __global__ void add_counts_kernel(const int32_t *__restrict__ g, const int32_t *__restrict__ x, int64_t n,
@@ -1296,16 +1297,35 @@ __global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int
 }
 
 // h in tree order + validation (h finite, > 0, <= 1e150) + checksum of h
-__global__ void gather_h_kernel(const float4 *__restrict__ rec32, const double *__restrict__ h, int64_t n,
+// four independent gathers in flight per thread (the h loads are random 8-B reads)
+__global__ void gather_h_kernel(const int32_t *__restrict__ perm, const double *__restrict__ h, int64_t n,
                                 double *__restrict__ h_tree, int *bad, long long *hsum) {
     long long acc = 0;
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        long long i = __float_as_int(rec32[k].w);  // caller index (16-B compact record)
-        double v = h[i];
-        if (!(v > 0.0 && v <= 1e150)) atomicOr(bad, 1);
+    bool ok = true;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (; k + 3 * stride < n; k += 4 * stride) {
+        long long i[4];
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) i[u] = perm[k + u * stride];
+#pragma unroll
+        for (int u = 0; u < 4; u++) v[u] = h[i[u]];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            ok = ok && (v[u] > 0.0 && v[u] <= 1e150);
+            h_tree[k + u * stride] = v[u];
+            acc += __double_as_longlong(v[u]) * (2 * i[u] + 1);
+        }
+    }
+    for (; k < n; k += stride) {
+        const long long i = perm[k];
+        const double v = h[i];
+        ok = ok && (v > 0.0 && v <= 1e150);
         h_tree[k] = v;
         acc += __double_as_longlong(v) * (2 * i + 1);
     }
+    if (!ok) atomicOr(bad, 1);
     for (int d = 16; d; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
     if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long *)hsum, (unsigned long long)acc);
 }
@@ -1337,10 +1357,10 @@ void set_exact_only(int on) { g_exact_only = on; }
 namespace {
 
 // masses in tree order + validation (finite, |m| <= 1e150)
-__global__ void gather_m_kernel(const float4 *__restrict__ rec32, const double *__restrict__ m, int64_t n,
+__global__ void gather_m_kernel(const int32_t *__restrict__ perm, const double *__restrict__ m, int64_t n,
                                 double *__restrict__ m_tree, int *bad) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const double v = m[__float_as_int(rec32[k].w)];
+        const double v = m[perm[k]];
         if (!(fabs(v) <= 1e150)) atomicOr(bad, 1);
         m_tree[k] = v;
     }
@@ -1374,7 +1394,7 @@ long long gather_h(TreeDev &t, const double *h, const char *who) {
     BT_CUDA(cudaMemsetAsync(t.counters.p + C_HSUM, 0, sizeof(int64_t), st));
     {
         Phase ph("search.gather_h");
-        gather_h_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec32.p, h, n, t.h_tree.p, dbad.p,
+        gather_h_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.perm.p, h, n, t.h_tree.p, dbad.p,
                                                                                   (long long *)t.counters.p + C_HSUM);
         BT_LAUNCH("gather_h");
     }
@@ -1390,6 +1410,7 @@ WalkArgs walk_args(TreeDev &t, const Grids &g) {
     t.urun.reserve(t.n_units, 0);
     a.rec = t.rec.p;
     a.rec32 = t.rec32.p;
+    a.perm = t.perm.p;
     a.h_tree = t.h_tree.p;
     a.nodes = t.nodes.p;
     a.cells = t.cells.p;
@@ -1576,7 +1597,7 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
         find_neighbors(t, h, t.sym_g.p, t.sym_off.p, nullptr, 0, true, false);  // gather counts + recorded masks
         if (!t.inv_valid) {
             t.inv.reserve(n, 0);
-            inverse_order_kernel<<<grid_for(n, 256, (int64_t)sms * 16), 256, 0, st>>>(t.rec32.p, n, t.inv.p);
+            inverse_order_kernel<<<grid_for(n, 256, (int64_t)sms * 16), 256, 0, st>>>(t.perm.p, n, t.inv.p);
             BT_LAUNCH("inverse_order");
             t.inv_valid = true;
         }
@@ -1650,7 +1671,7 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
         DBuf<int> dbad(1);
         BT_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
         t.m_tree.reserve(n, 0);
-        gather_m_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.rec32.p, mass, n, t.m_tree.p, dbad.p);
+        gather_m_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.perm.p, mass, n, t.m_tree.p, dbad.p);
         BT_LAUNCH("gather_m");
         int mbad = 0;
         read_back({{dbad.p, &mbad, sizeof(int)}});
