@@ -11,6 +11,10 @@ N = 2^25, ngmax = 512, count-then-fill CSR), seeded synthetic data.
 Multi-GPU (torchrun): every rank searches its own independently drawn
 sub-domain of the same recipe (the paper's per-node sub-domain, P:366-369);
 no data-path collective; weak scaling; time = max over ranks.
+--mode replicated: one particle set of the cfg size for the whole job (SURVEY
+8(e) variant (i)): each step rank 0 broadcasts pos and h (NCCL), every rank
+builds the same tree and searches only its share of the work units
+(bt_set_partition); strong scaling.
 --impl reference runs the CPU oracle (oracle/, the paper's Alg. 1 + Alg. 2 in
 plain C) on a bounded sample, rank 0 only.
 """
@@ -52,6 +56,8 @@ def parse():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--n", type=int, default=None, help="override particle count (not a bench line)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--mode", default="subdomain", choices=["subdomain", "replicated"],
+                    help="subdomain: one sub-domain per rank (weak); replicated: one set, units sharded (strong)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -82,16 +88,42 @@ def subdomain(cfg: int, n, rank: int):
     return datagen.make_config(cfg, n=n, seed_offset=rank)
 
 
+def replicated_inputs(cfg: int, n, rank: int, device):
+    """--mode replicated: rank 0 draws the job's one particle set; the other
+    ranks allocate buffers that the per-step broadcast fills."""
+    import torch
+    if rank == 0:
+        pos_np, h_np = subdomain(cfg, n, 0)
+        return pos_np, h_np, torch.from_numpy(pos_np).to(device), torch.from_numpy(h_np).to(device)
+    nn = n if n is not None else datagen.FULL_N[cfg]
+    return (None, None, torch.empty((nn, 3), dtype=torch.float64, device=device),
+            torch.empty(nn, dtype=torch.float64, device=device))
+
+
+def broadcast_inputs(pos, h):
+    """The step's particle set from rank 0 to every rank (NCCL over NVLink on the GPUs)."""
+    import torch.distributed as dist
+    dist.broadcast(pos, 0)
+    dist.broadcast(h, 0)
+
+
+def strong_value(n_total: int, ms: float) -> float:
+    """Whole-job throughput of one shared particle set over the max-over-ranks step time."""
+    return n_total / (ms * 1e-3)
+
+
 def weak_value(n_per_rank: int, ws: int, ms: float) -> float:
     """Whole-job throughput: all ranks' particles over the max-over-ranks step time."""
     return n_per_rank * ws / (ms * 1e-3)
 
 
-def config_block(cfg, n, ws):
+def config_block(cfg, n, ws, mode="subdomain"):
+    nn = n if n is not None else datagen.FULL_N[cfg]
+    par = f"sub-domain x{ws}" if mode == "subdomain" else f"replicated tree, units sharded x{ws} (pos/h broadcast per step)"
     return {"workload": (f"BASELINE.json configs[{cfg - 1}] (cfg {cfg}): {WORKLOADS[cfg]}"
                          + ("" if n is None else f" [n overridden to {n}: not a bench line]")),
-            "N_per_gpu": n if n is not None else datagen.FULL_N[cfg], "bucket_size": datagen.BUCKET_SIZE,
-            "max_empty": datagen.MAX_EMPTY, "alpha": 0.5, "ngmax": datagen.NGMAX, "parallelism": f"sub-domain x{ws}",
+            ("N_per_gpu" if mode == "subdomain" else "N_total"): nn, "bucket_size": datagen.BUCKET_SIZE,
+            "max_empty": datagen.MAX_EMPTY, "alpha": 0.5, "ngmax": datagen.NGMAX, "parallelism": par,
             "l2": "inputs larger than L2 (pos 805 MB + h 268 MB at cfg 5); no flush"}
 
 
@@ -216,18 +248,26 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=dev)
     P.lib()
 
-    pos_np, h_np = subdomain(args.config, args.n, rank)
-    n = pos_np.shape[0]
+    replicated = args.mode == "replicated"
+    if replicated:  # rank 0's particle set arrives by broadcast every step
+        pos_np, h_np, pos, h = replicated_inputs(args.config, args.n, rank, dev)
+    else:
+        pos_np, h_np = subdomain(args.config, args.n, rank)
+        pos = torch.from_numpy(pos_np).to(dev)
+        h = torch.from_numpy(h_np).to(dev)
+    n = pos.shape[0]
     ngmax = datagen.NGMAX
-    pos = torch.from_numpy(pos_np).to(dev)
-    h = torch.from_numpy(h_np).to(dev)
     counts = torch.empty(n, dtype=torch.int32, device=dev)
     offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
     nbr = torch.empty(n * ngmax, dtype=torch.int32, device=dev)  # capacity n * ngmax (BJ)
     stream = torch.cuda.current_stream()
 
     def step():
+        if replicated and ws > 1:  # the step's particle set, from rank 0 (NVLink)
+            broadcast_inputs(pos, h)
         t = P.Tree(pos, datagen.BUCKET_SIZE, datagen.MAX_EMPTY)
+        if replicated:
+            t.set_partition(rank, ws)
         t.find_neighbors(h, ngmax, counts=counts, offsets=offsets, nbr_idx=nbr)
         st = t.stats()
         t.free()
@@ -326,7 +366,9 @@ def run_b200(args):
 
     # ---- end to end through the public API on host buffers --------------------
     e2e = None
-    if not args.no_e2e and args.e2e_steps > 0:
+    if replicated:
+        e2e = {"value": None, "note": "not measured in --mode replicated (bt_search_host searches the whole set)"}
+    elif not args.no_e2e and args.e2e_steps > 0:
         pos_h = torch.from_numpy(pos_np).pin_memory()
         h_h = torch.from_numpy(h_np).pin_memory()
         c_h = torch.empty(n, dtype=torch.int32).pin_memory()
@@ -357,11 +399,14 @@ def run_b200(args):
         cpu = {"value": n / step_s, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": weak_value(n, ws, ms), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        value = strong_value(n, ms) if replicated else weak_value(n, ws, ms)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if replicated else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy PCG64, SURVEY 8(d) recipe)",
-                "config": config_block(args.config, args.n, ws),
-                "pairs_per_s": total_pairs * ws / (ms * 1e-3), "total_pairs_per_gpu": total_pairs,
+                "config": config_block(args.config, args.n, ws, args.mode),
+                "pairs_per_s": (None if replicated else total_pairs * ws / (ms * 1e-3)),
+                ("total_pairs_rank0" if replicated else "total_pairs_per_gpu"): total_pairs,
                 "build_ms": kern["build"], "kernel_ms": kern, "gpu_launches": launches,
                 "roofline": roofline, "bj_hbm_roofline": bj_roof,
                 "tree": {k: st[k] for k in ("depth", "root_b", "nodes", "leaves", "halvings", "units")},

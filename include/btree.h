@@ -176,6 +176,22 @@ int bt_find_neighbors_sym(const bt_tree *t, const double *h, int32_t ngmax, int3
 int bt_fill_neighbors_sym(const bt_tree *t, const double *h, const int64_t *offsets,
                           int32_t *nbr_idx, int64_t capacity);
 
+/*
+ * bt_set_partition -- restrict this tree's later searches to part `part` of
+ * `nparts` (the replicated-tree multi-GPU variant of SURVEY 8(e): every rank
+ * builds the same tree from the same positions and searches only its share).
+ * The parts are contiguous ranges of the Morton-ordered work units (units
+ * [U*part/nparts, U*(part+1)/nparts) of U), i.e. spatially compact sets of
+ * whole leaves; every particle belongs to exactly one part.  Afterwards
+ * bt_find_neighbors / bt_fill_neighbors return counts[i] = |N(i)| and row i
+ * for the particles of the part and counts 0 (empty rows) for all others, so
+ * the CSR sizes to the part; bt_density writes rho only for the part's
+ * particles.  The symmetric criterion needs the whole tree (BT_ERR_ARG when
+ * nparts > 1).  nparts = 1 restores the whole tree.  BT_ERR_ARG for
+ * nparts < 1 or part outside [0, nparts).  No device work.
+ */
+int bt_set_partition(bt_tree *t, int32_t part, int32_t nparts);
+
 /* Frees all tree-owned device memory (into this thread's block cache).  NULL-safe. */
 void bt_free(bt_tree *t);
 

@@ -21,7 +21,7 @@ _NAMES = {0: "BT_OK", 1: "BT_ERR_ARG", 2: "BT_ERR_INPUT", 3: "BT_ERR_CAPACITY", 
 
 # every symbol include/btree.h declares
 EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "bt_fill_neighbors",
-           "bt_find_neighbors_sym", "bt_fill_neighbors_sym", "bt_density", "bt_free",
+           "bt_find_neighbors_sym", "bt_fill_neighbors_sym", "bt_density", "bt_set_partition", "bt_free",
            "bt_search_host", "bt_set_stream", "bt_set_exact_only", "bt_release_cache", "bt_last_error", "bt_last_status", "bt_tree_stats",
            "bt_tree_order", "bt_profile_enable", "bt_profile_reset", "bt_profile_get"]
 
@@ -80,6 +80,8 @@ def lib():
         L.bt_find_neighbors_sym.restype = C.c_int
         L.bt_fill_neighbors_sym.argtypes = [_P, _P, _P, _P, C.c_int64]
         L.bt_fill_neighbors_sym.restype = C.c_int
+        L.bt_set_partition.argtypes = [_P, C.c_int32, C.c_int32]
+        L.bt_set_partition.restype = C.c_int
         L.bt_density.argtypes = [_P, _P, _P, _P]
         L.bt_density.restype = C.c_int
         L.bt_free.argtypes = [_P]
@@ -229,6 +231,12 @@ class Tree:
         fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
         _check(fn(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets), _ptr(nbr_idx)))
         return counts, offsets, nbr_idx
+
+    def set_partition(self, part: int, nparts: int):
+        """Restrict later searches to part `part` of `nparts` (bt_set_partition):
+        rows of other parts' particles come back empty."""
+        _check(lib().bt_set_partition(self._handle(), int(part), int(nparts)))
+        return self
 
     def stats(self) -> dict:
         s = Stats()

@@ -323,6 +323,18 @@ int bt_fill_neighbors_sym(const bt_tree *tc, const double *h, const int64_t *off
     });
 }
 
+int bt_set_partition(bt_tree *t, int32_t part, int32_t nparts) {
+    if (!t || nparts < 1 || part < 0 || part >= nparts) {
+        set_error(BT_ERR_ARG, "bt_set_partition: need a tree, nparts >= 1 and 0 <= part < nparts");
+        return BT_ERR_ARG;
+    }
+    t->t.part = part;
+    t->t.nparts = nparts;
+    t->t.rec_valid = false;  // the recorded masks belong to the previous unit range
+    t->t.sym_valid = false;
+    return BT_OK;
+}
+
 int bt_density(const bt_tree *tc, const double *h, const double *mass, double *rho) {
     bt_tree *t = const_cast<bt_tree *>(tc);
     if (!t || (t->t.n > 0 && (!h || !mass || !rho))) {

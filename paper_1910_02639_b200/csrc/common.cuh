@@ -153,6 +153,7 @@ struct TreeDev {
     DBuf<int32_t> leaf_id_of_level;  // scratch
     DBuf<int4> units;          // {leaf, first query (tree pos), n queries, 0}
     int64_t n_units = 0;
+    int32_t part = 0, nparts = 1;  // bt_set_partition: searches cover units [n_units part / nparts, n_units (part+1) / nparts)
     double box_lo[3] = {0, 0, 0}, box_hi[3] = {0, 0, 0};
     double M = 0.0;            // max |root box coordinate|
     int32_t depth = 0, root_b = 0;

@@ -1408,6 +1408,9 @@ long long gather_h(TreeDev &t, const double *h, const char *who) {
 WalkArgs walk_args(TreeDev &t, const Grids &g) {
     WalkArgs a{};
     t.urun.reserve(t.n_units, 0);
+    // this tree's partition (bt_set_partition): a contiguous range of the
+    // Morton-ordered units; the kernels see it as units [0, n_units)
+    const int64_t u0 = t.n_units * t.part / t.nparts, u1 = t.n_units * (t.part + 1) / t.nparts;
     a.rec = t.rec.p;
     a.rec32 = t.rec32.p;
     a.perm = t.perm.p;
@@ -1417,14 +1420,14 @@ WalkArgs walk_args(TreeDev &t, const Grids &g) {
     a.leaf_begin = t.leaf_begin.p;
     a.leaf_count = t.leaf_count.p;
     a.leaf_box = t.leaf_box.p;
-    a.units = t.units.p;
-    a.n_units = t.n_units;
+    a.units = t.units.p + u0;
+    a.n_units = u1 - u0;
     a.M = t.M;
     a.root_is_leaf = t.root_is_leaf ? 1 : 0;
     a.exact_only = g_exact_only;
-    a.urun = t.urun.p;
+    a.urun = t.urun.p + u0;
     // descent batches: up to 8 units per claim while every warp still gets >= 8 claims
-    a.desc_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, t.n_units / ((int64_t)g.d * (kDescThreads / 32) * 8)));
+    a.desc_batch = (int)std::max<int64_t>(1, std::min<int64_t>(8, a.n_units / ((int64_t)g.d * (kDescThreads / 32) * 8)));
     a.ctr = (long long *)t.counters.p;
     return a;
 }
@@ -1439,7 +1442,7 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
     double list_per_unit = 96.0;
     const long long warps_d = (long long)g.d * (kDescThreads / 32);
     for (int attempt = 0;; attempt++) {
-        t.ulist.reserve((long long)(list_per_unit * t.n_units) + warps_d * kListSlab, 0);
+        t.ulist.reserve((long long)(list_per_unit * a.n_units) + warps_d * kListSlab, 0);
         a.ulist = t.ulist.p;
         a.list_cap = (long long)t.ulist.n;
         for (int c : {C_WORK, C_LIST, C_BIG, C_WORK4, C_NEEDC, C_NEEDM}) zero_counter(t, c);
@@ -1461,7 +1464,7 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
             read_counters(t, hc);
         }
         if (hc[C_LIST] <= a.list_cap) break;
-        list_per_unit = 1.25 * (double)hc[C_LIST] / (double)std::max<int64_t>(1, t.n_units);
+        list_per_unit = 1.25 * (double)hc[C_LIST] / (double)std::max<int64_t>(1, a.n_units);
         if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: leaf-list arena does not converge");
     }
     t.list_entries = hc[C_LIST];
@@ -1500,6 +1503,8 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             tmp_counts.alloc(n);
             cnt = tmp_counts.p;
         }
+        // partitioned tree: particles of other parts keep count 0 (empty rows)
+        if (t.nparts > 1) BT_CUDA(cudaMemsetAsync(cnt, 0, n * sizeof(int32_t), st));
         a.counts = cnt;
         long long hc[C_N];
         t.rec_valid = false;
@@ -1583,6 +1588,8 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
         BT_CUDA(cudaStreamSynchronize(st));
         return;
     }
+    if (t.nparts > 1)
+        throw Error(BT_ERR_ARG, "bt_find_neighbors_sym: the symmetric criterion needs the whole tree (bt_set_partition 0, 1)");
     const int sms = num_sms();
     const Grids g = walk_grids<false>();
     t.sym_g.reserve(n, 0);

@@ -542,3 +542,47 @@ def test_k2_plane_lattice_and_halving(P, oracle):
     assert_same_tree(t, ot)
     with pytest.raises(ValueError):
         P.build(torch.from_numpy(pos).to(DEV), 8, 0.5, policy="k3")
+
+
+# ---- replicated-tree partition (SURVEY 8(e) variant (i), bt_set_partition) -------
+@pytest.mark.parametrize("cfg,n,nparts", [(2, 100_000, 3), (4, 100_000, 2), (5, 200_000, 5)])
+def test_partitioned_search_is_a_disjoint_cover(P, oracle, cfg, n, nparts):
+    """Each part's search returns exactly the full rows of its particles and
+    empty rows elsewhere; the parts are disjoint and cover all particles (the
+    density written per part marks membership)."""
+    pos, h = datagen.make_config(cfg, n=n)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd = torch.from_numpy(h).to(DEV)
+    mass = torch.ones_like(hd)
+    fc, fo, fn = t.find_neighbors(hd)
+    full_rows = sort_rows(fc, fo, fn)
+    full_rho = t.density(hd, mass)
+    ref = oracle.Tree(pos, 64, 0.5).neighbors(h)
+    assert_same((fc.cpu().numpy(), fo.cpu().numpy(), full_rows), ref)
+    owner = np.full(n, -1)
+    fcn = fc.cpu().numpy()
+    for p in range(nparts):
+        t.set_partition(p, nparts)
+        rho = torch.full_like(hd, float("nan"))
+        t.density(hd, mass, out=rho)
+        mine = ~torch.isnan(rho).cpu().numpy()
+        assert np.all(owner[mine] == -1)
+        owner[mine] = p
+        torch.testing.assert_close(rho[torch.from_numpy(mine).to(DEV)], full_rho[torch.from_numpy(mine).to(DEV)],
+                                   rtol=0, atol=0)
+        c, o, nb = t.find_neighbors(hd)
+        cn = c.cpu().numpy()
+        assert np.array_equal(cn[mine], fcn[mine]) and not np.any(cn[~mine])
+        # the part's sorted rows are the full rows of its particles
+        rows = sort_rows(c, o, nb)
+        keep = np.repeat(mine, fcn)
+        assert np.array_equal(rows, full_rows[keep])
+        with pytest.raises(P.BtreeError) as e:
+            t.count(hd, symmetric=True)
+        assert e.value.code == 1
+    assert np.all(owner >= 0)
+    t.set_partition(0, 1)
+    c, o, nb = t.find_neighbors(hd)
+    assert np.array_equal(sort_rows(c, o, nb), full_rows)
+    with pytest.raises(P.BtreeError):
+        t.set_partition(2, 2)

@@ -52,6 +52,43 @@ def test_two_ranks_gloo():
     assert v0 == v1 == pytest.approx(2 * 2000 / 15e-3)
 
 
+def _worker_replicated(rank, ws, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(ws),
+                      LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    import bench
+    _, rank_, _ = bench.dist_env()
+    pos_np, h_np, pos, h = bench.replicated_inputs(2, 3000, rank_, "cpu")
+    had_data = pos_np is not None
+    bench.broadcast_inputs(pos, h)        # gloo stands in for NCCL here
+    ms = bench.max_over_ranks(8.0 + rank_)
+    cfg = bench.config_block(2, 3000, ws, "replicated")
+    q.put((rank_, had_data, float(pos.sum()), float(h.sum()), ms, bench.strong_value(pos.shape[0], ms),
+           cfg["parallelism"], cfg.get("N_total")))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_ranks_replicated_gloo():
+    """--mode replicated: rank 0 alone draws the set, the broadcast gives every
+    rank the same bits, the value is the one set over the max step time."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_replicated, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, d0, ps0, hs0, m0, v0, par0, n0), (r1, d1, ps1, hs1, m1, v1, par1, n1) = res
+    assert d0 and not d1
+    assert ps0 == ps1 and hs0 == hs1                  # identical particle sets after the broadcast
+    assert m0 == m1 == 9.0 and v0 == v1 == pytest.approx(3000 / 9e-3)
+    assert "replicated" in par0 and n0 == n1 == 3000
+
+
 def test_single_process_identity():
     import bench
     assert bench.max_over_ranks(3.5) == 3.5
