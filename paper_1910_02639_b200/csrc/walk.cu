@@ -1255,10 +1255,16 @@ __global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int
             }
             const bool act0 = j[0] >= 0 && T[0] < tmax, act1 = j[1] >= 0 && T[1] < tmax;
             if (!__any_sync(0xffffffffu, act0 || act1)) continue;
+            // queries worth a visit: a non-empty mask word and T_i above the
+            // smallest T_j of an active candidate (lanes = queries here)
+            const double tlo = warp_min(fmin(act0 ? T[0] : INFINITY, act1 ? T[1] : INFINITY));
+            const unsigned long long qv =
+                (unsigned long long)__ballot_sync(0xffffffffu, w0 != 0ull && TQ[lane] > tlo) |
+                ((unsigned long long)__ballot_sync(0xffffffffu, w1 != 0ull && TQ[lane + 32] > tlo) << 32);
             unsigned long long os[2] = {0ull, 0ull};  // bit q: (query q, this lane's candidate) one-sided
-            for (int q = 0; q < nq; q++) {
+            for (unsigned long long qq = qv; qq; qq &= qq - 1ull) {
+                const int q = __ffsll((long long)qq) - 1;
                 const unsigned long long m = __shfl_sync(0xffffffffu, q < 32 ? w0 : w1, q & 31);
-                if (m == 0ull) continue;
                 const double Ti = TQ[q];
                 const bool b0 = act0 && ((m >> lane) & 1ull) && T[0] < Ti;
                 const bool b1 = act1 && ((m >> (32 + lane)) & 1ull) && T[1] < Ti;
