@@ -183,6 +183,17 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle: cpu_baseline / --impl reference
 # ---------------------------------------------------------------------------
+def cpu_model() -> str:
+    """The host CPU's model name (/proc/cpuinfo), for the CPU-baseline line."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def oracle_sample(pos, h, sample_queries: int):
     """Time the oracle as it stands on this host: full BuildTree + the
     FindNeighbors count and row passes for a random sample of queries, all
@@ -202,7 +213,8 @@ def oracle_sample(pos, h, sample_queries: int):
     build_s = t1 - t0
     search_s = (t2 - t1) * n / k
     desc = (f"oracle BuildTree on all {n} particles ({build_s:.2f} s, 1 thread) + count and row passes for "
-            f"{k} random queries ({t2 - t1:.2f} s, {cores} threads), search scaled x{n / k:.1f} to all queries")
+            f"{k} random queries ({t2 - t1:.2f} s, {cores} threads), search scaled x{n / k:.1f} to all queries; "
+            f"host CPU: {cpu_model()}")
     return build_s + search_s, desc, cores, build_s, search_s
 
 
