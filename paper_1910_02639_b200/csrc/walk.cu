@@ -569,6 +569,13 @@ struct WalkSmemT : WalkSmem {
     DensitySm<kDensity> d;
 };
 
+// fp32 square root on the SFU (sqrt.approx: relative error ~2^-22, sqrt(0) = 0)
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // M4 cubic spline shape (reading R21), fp32
 __device__ __forceinline__ float w_m4f(float q) {
     const float t = 2.0f - q;
@@ -760,7 +767,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
                         const float4 cd = S.d.dc[sl];
                         const float dx = cd.x - qx, dy = cd.y - qy, dz = cd.z - qz;
                         const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-                        const float qq = r2 > 0.0f ? r2 * rsqrtf(r2) * hinv : 0.0f;  // r / h (coincident: 0)
+                        const float qq = sqrt_approx(r2) * hinv;  // r / h (MUFU.SQRT; coincident: 0)
                         acc = __fmaf_rn(cd.w, w_m4f(qq), acc);
                     }
                 }
