@@ -38,6 +38,7 @@ constexpr int kQ = 64;           // queries per unit (== build.cu kUnitQ)
 constexpr int kBlk = 128;        // staged candidates per test block
 constexpr int kScratch = 4096;   // staged candidates per warp scratch (global, L2-resident); multiple of kBlk
 constexpr int kGroup = 32;       // candidate leaves per staging group (one per lane)
+constexpr int kGroupPos = 2048;  // positions a multi-leaf group may span (its leaf-start bitmap)
 constexpr int kFrontCap = 512;   // shared-memory descent frontier per level
 constexpr int kDescThreads = 128;
 constexpr int kWalkThreads = 128;
@@ -549,7 +550,8 @@ struct WalkSmem {
     int self[kQ];                   // unit slot of each query's own record (-1: none)
     unsigned long long mask[2][kQ]; // the block's neighbor masks [chunk][query]
     int ldel[kGroup];               // group leaves: first tree position - exclusive prefix of counts
-    int lpre[kGroup + 1];           // group leaves: exclusive prefix of counts
+    unsigned lstart[kGroupPos / 32];       // group positions: bit p set where a leaf starts (p = 32 w + bit)
+    unsigned char lwpre[kGroupPos / 32];   // leaves starting before word w
     float4 loff[kGroup];            // group leaves: fl32(c_leaf - c), w = 1 compact / 0 fp64 records
     UnitSm u;
 };
@@ -784,16 +786,14 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     return make_int2(inc[0], inc[1]);
 }
 
-// Flattened position p of the current leaf group -> tree position (-1: past
-// the end) and owning leaf, for the 32 positions [w0, w0 + 32); `owner` =
-// leaf holding position w0 (advanced to the leaf holding w0 + 32).
-__device__ __forceinline__ void locate(const WalkSmem &S, int nl, int total, int w0, int lane, unsigned le,
-                                       int &owner, int &pos, int &mine) {
-    const int nxt = owner + 1 + lane;
-    const int off = ((nxt <= nl) ? S.lpre[nxt] : 0x7fffffff) - w0;  // >= 1 for leaves after `owner`
-    const unsigned bits = __reduce_or_sync(0xffffffffu, ((unsigned)(off - 1) < 31u) ? (1u << off) : 0u);
-    mine = owner + __popc(bits & le);
-    owner += __popc(__ballot_sync(0xffffffffu, off <= 32));
+// Flattened position p = w0 + lane of the current leaf group (w0 a multiple
+// of 32) -> owning leaf (leaf starts up to p, from the group's start bitmap;
+// a one-leaf group, which may be an over-full leaf, has none) and tree
+// position (-1: past the end).
+__device__ __forceinline__ void locate(const WalkSmem &S, int total, bool single, int w0, int lane, unsigned le,
+                                       int &pos, int &mine) {
+    const int w = w0 >> 5;
+    mine = single ? 0 : (int)S.lwpre[w] + __popc(S.lstart[w] & le) - 1;
     const int p = w0 + lane;
     pos = (p < total) ? p + S.ldel[mine] : -1;
 }
@@ -803,8 +803,8 @@ __device__ __forceinline__ void locate(const WalkSmem &S, int nl, int total, int
 // scratch cannot take another window.  kMixed: some leaf of the group is
 // staged from the fp64 records (a = fl32(fl64(x - c))).
 template <bool kMixed>
-__device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int nl, int total, int &w0,
-                                            int &owner, int &nst, int slot0) {
+__device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int total, bool single,
+                                            int &w0, int &nst, int slot0) {
     const unsigned lt = lanemask_lt(), le = lt | (1u << lane);
     const float4 *__restrict__ rec32 = a.rec32;
     const float4 B0 = S.u.box0, B1 = S.u.box1;
@@ -831,21 +831,17 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
     };
     int pos, mine;
     bool rel;
-    locate(S, nl, total, w0, lane, le, owner, pos, mine);
+    locate(S, total, single, w0, lane, le, pos, mine);
     float4 r = load(pos, mine, rel);
 #pragma unroll 1
     for (; w0 < total; w0 += 32) {
-        if (nst > kScratch - 32) {  // full: the caller tests the staged blocks and resumes at w0
-            owner = mine;           // leaf holding position w0 (locate advanced it past this window)
-            owner = __shfl_sync(0xffffffffu, owner, 0);
-            break;
-        }
+        if (nst > kScratch - 32) break;  // full: the caller tests the staged blocks and resumes at w0
         // the next window's record load is issued before this window is processed
         int pos_n = -1, mine_n = 0;
         bool rel_n = false;
         float4 r_n = r;
         if (w0 + 32 < total) {
-            locate(S, nl, total, w0 + 32, lane, le, owner, pos_n, mine_n);
+            locate(S, total, single, w0 + 32, lane, le, pos_n, mine_n);
             r_n = load(pos_n, mine_n, rel_n);
         }
         // fp32 relative coordinates (compact: fl32(r32 + fl32(c_leaf - c))) and the
@@ -983,7 +979,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         const int nleaf = R.nleaf;
         const long long list_off = R.list_off;
         int nst = 0, slot0 = 0;            // candidates in the scratch; unit slot of scratch[0]
-        int g0 = 0, w0 = 0, owner = 0, total = 0, nl = 0;
+        int g0 = 0, w0 = 0, total = 0, nl = 0;
         bool mixed = false, have_group = false;
         for (;;) {
             // ---- staging phase: fill the scratch
@@ -1013,25 +1009,44 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                         const int o = __shfl_up_sync(0xffffffffu, inc, d);
                         if (lane >= d) inc += o;
                     }
-                    total = __shfl_sync(0xffffffffu, inc, 31);
-                    nl = min(kGroup, nleaf - g0);
+                    // the group: the leading leaves within kGroupPos positions (at least one)
+                    nl = max(1, __popc(__ballot_sync(0xffffffffu, gi < nleaf && inc <= kGroupPos)));
+                    total = __shfl_sync(0xffffffffu, inc, nl - 1);
                     S.ldel[lane] = beg - (inc - cnt);
-                    S.lpre[lane] = inc - cnt;
                     S.loff[lane] = off;
-                    if (lane == 0) S.lpre[kGroup] = total;
-                    mixed = __any_sync(0xffffffffu, gi < nleaf && off.w == 0.0f);
+                    // start bitmap of the group's positions and the starts before each word
+                    const int nw = nl > 1 ? (total + 31) >> 5 : 0;  // <= kGroupPos / 32
+                    for (int w = lane; w < nw; w += 32) S.lstart[w] = 0u;
+                    __syncwarp();
+                    if (nl > 1 && lane < nl) atomicOr(&S.lstart[(inc - cnt) >> 5], 1u << ((inc - cnt) & 31));
+                    __syncwarp();
+                    {
+                        const int c0 = lane < nw ? __popc(S.lstart[lane]) : 0;
+                        const int c1 = lane + 32 < nw ? __popc(S.lstart[lane + 32]) : 0;
+                        int i0 = c0, i1 = c1;
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const int o0 = __shfl_up_sync(0xffffffffu, i0, d), o1 = __shfl_up_sync(0xffffffffu, i1, d);
+                            if (lane >= d) {
+                                i0 += o0;
+                                i1 += o1;
+                            }
+                        }
+                        const int t0 = __shfl_sync(0xffffffffu, i0, 31);
+                        if (lane < nw) S.lwpre[lane] = (unsigned char)(i0 - c0);
+                        if (lane + 32 < nw) S.lwpre[lane + 32] = (unsigned char)(t0 + i1 - c1);
+                    }
+                    mixed = __any_sync(0xffffffffu, lane < nl && gi < nleaf && off.w == 0.0f);
                     __syncwarp();
                     w0 = 0;
-                    owner = 0;
                     have_group = true;
                 }
                 if (mixed)
-                    stage_group<true>(S, a, lane, nl, total, w0, owner, nst, slot0);
+                    stage_group<true>(S, a, lane, total, nl == 1, w0, nst, slot0);
                 else
-                    stage_group<false>(S, a, lane, nl, total, w0, owner, nst, slot0);
+                    stage_group<false>(S, a, lane, total, nl == 1, w0, nst, slot0);
                 if (w0 < total) break;  // scratch full
                 loaded += total;
-                g0 += kGroup;
+                g0 += nl;
                 have_group = false;
             }
             const bool done = g0 >= nleaf;
