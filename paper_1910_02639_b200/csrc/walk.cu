@@ -817,7 +817,9 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
     auto load = [&](int pos, int mine, bool &rel) {
         float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
         rel = false;
-        if (pos >= 0) {
+        if (!kMixed) {  // past-the-end lanes read record 0 (never kept): no branch
+            r = __ldg(&rec32[max(pos, 0)]);
+        } else if (pos >= 0) {
             if (!kMixed || S.loff[mine].w != 0.0f) {
                 r = __ldg(&rec32[pos]);
             } else {  // large leaf: exact fp64 record, a = fl32(fl64(x - c))
@@ -859,8 +861,8 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             const int slot = nst + __popc(km & lt);
-            __stcg(&scr[slot], make_float4(ax, ay, az, __int_as_float(pos)));  // L2-resident scratch
-            if (rec_ok) __stcs(&cands[slot], __float_as_int(r.w));
+            __stcg(&scr[(unsigned)slot], make_float4(ax, ay, az, __int_as_float(pos)));  // L2-resident scratch
+            if (rec_ok) __stcs(&cands[(unsigned)slot], __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
         }
         nst += __popc(km);
