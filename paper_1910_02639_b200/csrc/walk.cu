@@ -792,8 +792,9 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
 // position (-1: past the end).
 __device__ __forceinline__ void locate(const WalkSmem &S, int total, bool single, int w0, int lane, unsigned le,
                                        int &pos, int &mine) {
-    const int w = w0 >> 5;
-    mine = single ? 0 : (int)S.lwpre[w] + __popc(S.lstart[w] & le) - 1;
+    const int w = min(w0 >> 5, kGroupPos / 32 - 1);  // (clamped: one-leaf groups ignore the bitmap)
+    const int m = (int)S.lwpre[w] + __popc(S.lstart[w] & le) - 1;
+    mine = single ? 0 : m;
     const int p = w0 + lane;
     pos = (p < total) ? p + S.ldel[mine] : -1;
 }
@@ -811,7 +812,7 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
     const int2 qn = lds2iv(&S.u.q0);
     const bool rec_ok = S.u.rec_ok != 0;
     float4 *const scr = S.u.scr;
-    int32_t *const cands = S.u.cand_ptr + slot0;
+    int32_t *const cands = S.u.cand_ptr + (unsigned)slot0;
     // record of position pos: the compact record, or (large leaf of a kMixed
     // group, `rel` set) the fp64 record already relative to the unit centre
     auto load = [&](int pos, int mine, bool &rel) {
