@@ -851,11 +851,14 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         // conservative fp32 Minkowski cull against the query box (L3 / L4)
         float4 of = S.loff[mine];
         if (kMixed && rel) of = make_float4(0.f, 0.f, 0.f, 0.f);
-        const float ax = __fadd_rn(r.x, of.x);
-        const float ay = __fadd_rn(r.y, of.y);
+        // (x, y) as packed pairs: the same IEEE roundings as the scalar forms
+        const unsigned long long axy = f2_add(pk(r.x, r.y), pk(of.x, of.y));
+        const unsigned long long lxy = f2_add(axy, pk(-B0.x, -B0.y));  // a - lo (fl(lo - a) = -fl(a - lo))
+        const unsigned long long hxy = f2_add(axy, pk(-B1.x, -B1.y));  // a - hi
+        const float ax = lo_f(axy), ay = hi_f(axy);
         const float az = __fadd_rn(r.z, of.z);
-        const float gx = fmaxf(0.0f, fmaxf(__fsub_rn(B0.x, ax), __fsub_rn(ax, B1.x)));
-        const float gy = fmaxf(0.0f, fmaxf(__fsub_rn(B0.y, ay), __fsub_rn(ay, B1.y)));
+        const float gx = fmaxf(0.0f, fmaxf(-lo_f(lxy), lo_f(hxy)));
+        const float gy = fmaxf(0.0f, fmaxf(-hi_f(lxy), hi_f(hxy)));
         const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(B0.z, az), __fsub_rn(az, B1.z)));
         const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
         const bool keep = pos >= 0 && g2 < B0.w;
