@@ -567,6 +567,24 @@ __device__ __forceinline__ unsigned spread3(unsigned v) {  // 10 bits -> every t
     return v;
 }
 
+// per-leaf staging record: centre (the same 0.5 (lo + hi) as the compact
+// records), half-extent, begin, count
+__global__ void leaf_rec_kernel(const double *__restrict__ box, const int32_t *__restrict__ begin,
+                                const int32_t *__restrict__ count, int64_t nl, LeafRec *__restrict__ out) {
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < nl; L += (int64_t)gridDim.x * blockDim.x) {
+        const double *b = box + 6 * L;
+        LeafRec r;
+        r.cx = 0.5 * (b[0] + b[3]);
+        r.cy = 0.5 * (b[1] + b[4]);
+        r.cz = 0.5 * (b[2] + b[5]);
+        r.H = 0.5 * fmax(fmax(b[3] - b[0], b[4] - b[1]), b[5] - b[2]);
+        r.begin = begin[L];
+        r.count = count[L];
+        r.pad_[0] = r.pad_[1] = 0;
+        out[L] = r;
+    }
+}
+
 __global__ void unit_key_kernel(const int4 *__restrict__ units, int64_t nu, const double *__restrict__ leaf_box,
                                 const double *__restrict__ box, unsigned *__restrict__ key, int32_t *__restrict__ hist) {
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
@@ -888,6 +906,10 @@ void build_tree(TreeDev &t, const double *pos) {
         leaf_finalize_kernel<<<grid_for(t.n_leaves * 32, kThreads, (int64_t)sms * 32), kThreads, 0, st>>>(
             fin.p, t.rec.p, t.rec32.p, t.perm.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
         BT_LAUNCH("leaf_finalize");
+        t.leaf_rec.alloc(t.n_leaves);
+        leaf_rec_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
+            t.leaf_box.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_rec.p);
+        BT_LAUNCH("leaf_rec");
         DBuf<long long> dtot(1);
         // small leaves paired (runs of small leaves, pair by rank, box check)
         DBuf<int32_t> rs(t.n_leaves), merge(t.n_leaves);

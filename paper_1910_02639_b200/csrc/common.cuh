@@ -119,6 +119,13 @@ struct NodeRec {      // one internal node
 __host__ __device__ inline int32_t node_code(int32_t node) { return -2 - node; }
 __host__ __device__ inline int32_t code_node(int32_t code) { return -2 - code; }
 
+struct LeafRec {             // per leaf, what a walk staging group reads (one 48-B record)
+    double cx, cy;          // leaf centre 0.5 (lo + hi) per axis (the compact records' origin)
+    double cz, H;           // ... and half-extent 0.5 max_l (hi_l - lo_l)
+    int32_t begin, count;   // first tree position, particles
+    int32_t pad_[2];
+};
+
 struct UnitRun {             // per walk unit, written by the walk kernels
     long long list_off;     // first candidate leaf of the unit in the leaf-list arena
     long long cand_base;    // first candidate slot of the unit (caller indices, for the fill)
@@ -149,6 +156,7 @@ struct TreeDev {
     DBuf<int32_t> leaf_count;
     DBuf<int32_t> leaf_depth;
     DBuf<double> leaf_box;     // [6*L]: lo x,y,z, hi x,y,z (tight, exact min/max)
+    DBuf<LeafRec> leaf_rec;    // [L]: centre, half-extent, begin, count (walk staging)
     int64_t n_leaves = 0;
     DBuf<int32_t> leaf_id_of_level;  // scratch
     DBuf<int4> units;          // {leaf, first query (tree pos), n queries, 0}

@@ -81,6 +81,7 @@ struct WalkArgs {
     const int32_t *leaf_begin;
     const int32_t *leaf_count;
     const double *leaf_box;
+    const LeafRec *leaf_rec;
     const int4 *units;
     int64_t n_units;
     double M;
@@ -996,19 +997,18 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     int cnt = 0, beg = 0;
                     float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (gi < nleaf) {
-                        const int leaf = a.ulist[list_off + gi];
-                        beg = a.leaf_begin[leaf];
-                        cnt = a.leaf_count[leaf];
-                        const double2 *lb = reinterpret_cast<const double2 *>(a.leaf_box + 6 * (int64_t)leaf);
-                        const double2 b0 = lb[0], b1 = lb[1], b2 = lb[2];  // lo x,y | lo z, hi x | hi y,z
-                        // leaf centre (as build.cu computed it) relative to the unit centre; the
+                        const LeafRec *lr = a.leaf_rec + a.ulist[list_off + gi];
+                        const double2 cxy = *reinterpret_cast<const double2 *>(&lr->cx);
+                        const double2 czH = *reinterpret_cast<const double2 *>(&lr->cz);
+                        const int2 bc = *reinterpret_cast<const int2 *>(&lr->begin);
+                        beg = bc.x;
+                        cnt = bc.y;
+                        // leaf centre (as the build computed it) relative to the unit centre; the
                         // compact records are usable when the leaf half-extent H <= 7 E (l4_eps)
-                        const double lx = 0.5 * (b0.x + b1.y), ly = 0.5 * (b0.y + b2.x), lz = 0.5 * (b1.x + b2.y);
-                        const double H = 0.5 * fmax(fmax(b1.y - b0.x, b2.x - b0.y), b2.y - b1.x);
-                        off = make_float4(__double2float_rn(__dsub_rn(lx, S.u.c[0])),
-                                          __double2float_rn(__dsub_rn(ly, S.u.c[1])),
-                                          __double2float_rn(__dsub_rn(lz, S.u.c[2])),
-                                          (H <= 7.0 * S.u.E) ? 1.0f : 0.0f);
+                        off = make_float4(__double2float_rn(__dsub_rn(cxy.x, S.u.c[0])),
+                                          __double2float_rn(__dsub_rn(cxy.y, S.u.c[1])),
+                                          __double2float_rn(__dsub_rn(czH.x, S.u.c[2])),
+                                          (czH.y <= 7.0 * S.u.E) ? 1.0f : 0.0f);
                     }
                     int inc = cnt;
                     for (int d = 1; d < 32; d <<= 1) {
@@ -1428,6 +1428,7 @@ WalkArgs walk_args(TreeDev &t, const Grids &g) {
     a.leaf_begin = t.leaf_begin.p;
     a.leaf_count = t.leaf_count.p;
     a.leaf_box = t.leaf_box.p;
+    a.leaf_rec = t.leaf_rec.p;
     a.units = t.units.p + u0;
     a.n_units = u1 - u0;
     a.M = t.M;
