@@ -361,8 +361,7 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__rest
                                                            int64_t n_act, const LevelNode *__restrict__ ln,
                                                            const uint32_t *__restrict__ keys, int32_t *__restrict__ cursor,
                                                            const int2 *__restrict__ cmove,
-                                                           double4 *__restrict__ out_final, double4 *__restrict__ act_next,
-                                                           int32_t *__restrict__ act_node_next) {
+                                                           double4 *__restrict__ out_final, double4 *__restrict__ act_next) {
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_act; p += (int64_t)gridDim.x * blockDim.x) {
         int32_t node = act_node[p];
         int64_t g = ln[node].cell_base + keys[p];
@@ -370,12 +369,19 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__rest
         const int2 mv = cmove[g];  // one random 8-byte load per particle
         double4 v = act[p];
         int32_t dst = mv.x + r;
-        if (mv.y < 0) {
-            out_final[dst] = v;
-        } else {
-            act_next[dst] = v;
-            act_node_next[dst] = mv.y;
-        }
+        if (mv.y < 0) out_final[dst] = v;
+        else act_next[dst] = v;  // (its node id: node_ids_kernel, coalesced)
+    }
+}
+
+// next level's node id of every active position: one warp per node writes its
+// contiguous range (instead of a random 4-byte store per particle in the scatter)
+__global__ void node_ids_kernel(const LevelNode *__restrict__ ln, int64_t nn, int32_t *__restrict__ act_node) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nn; i += warps) {
+        const int32_t b = ln[i].act_begin, c = ln[i].count;
+        for (int32_t k = lane; k < c; k += 32) act_node[b + k] = (int32_t)i;
     }
 }
 
@@ -857,8 +863,13 @@ void build_tree(TreeDev &t, const double *pos) {
             // A7: scatter (cursor = zeroed histogram)
             BT_CUDA(cudaMemsetAsync(hist.p, 0, ncells * sizeof(int32_t), st));
             scatter_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, keys.p, hist.p, cmove.p,
-                                                       fin.p, act[cur ^ 1].p, act_node[cur ^ 1].p);
+                                                       fin.p, act[cur ^ 1].p);
             BT_LAUNCH("scatter");
+            if (nn_next > 0) {
+                node_ids_kernel<<<grid_for(nn_next * 32, kThreads, (int64_t)sms * 16), kThreads, 0, st>>>(
+                    ln_next.p, nn_next, act_node[cur ^ 1].p);
+                BT_LAUNCH("node_ids");
+            }
 
             if (nleaf > 0) t.depth = level + 1;
             t.n_cells += ncells;
