@@ -1059,9 +1059,6 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             __syncwarp();
             // ---- test phase: the staged blocks (all but a partial last one unless done)
             const int ntest = done ? nst : nst - nst % kBlk;
-#ifdef BT_DIAG_NO_TEST
-            if (true) {} else
-#endif
             for (int b0 = 0; b0 < ntest; b0 += kBlk) {
                 const int2 inc = test_block<kDensity>(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0), slot0 + b0, dacc);
                 cnt0 += inc.x;
