@@ -104,6 +104,18 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(In in, Out out
     }
 }
 
+// in-place exclusive scan of an array of tile sums (the recursive level)
+template <class T>
+struct TileIn {
+    const T *p;
+    __device__ T operator()(int64_t i) const { return p[i]; }
+};
+template <class T>
+struct TileOut {
+    T *p;
+    __device__ void operator()(int64_t i, const T &exc, const T &) const { p[i] = exc; }
+};
+
 // Exclusive scan of n items; total (device pointer, may be null) receives the sum.
 template <class T, class In, class Out>
 void device_scan(In in, Out out, int64_t n, T *total) {
@@ -112,8 +124,12 @@ void device_scan(In in, Out out, int64_t n, T *total) {
     DBuf<T> tiles(ntiles);
     scan_reduce_kernel<T, In><<<(unsigned)ntiles, kScanThreads, 0, stream()>>>(in, n, tiles.p);
     BT_LAUNCH("scan_reduce");
-    scan_tiles_kernel<T><<<1, kScanThreads, 0, stream()>>>(tiles.p, ntiles, total);
-    BT_LAUNCH("scan_tiles");
+    if (ntiles > kScanTile) {  // many tiles: scan the tile sums in parallel, not in one block
+        device_scan<T>(TileIn<T>{tiles.p}, TileOut<T>{tiles.p}, ntiles, total);
+    } else {
+        scan_tiles_kernel<T><<<1, kScanThreads, 0, stream()>>>(tiles.p, ntiles, total);
+        BT_LAUNCH("scan_tiles");
+    }
     scan_apply_kernel<T, In, Out><<<(unsigned)ntiles, kScanThreads, 0, stream()>>>(in, out, n, tiles.p);
     BT_LAUNCH("scan_apply");
 }
