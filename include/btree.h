@@ -162,7 +162,7 @@ int bt_density(const bt_tree *t, const double *h, const double *mass, double *rh
  * count-only call (nbr_idx NULL) and the errors are those of
  * bt_find_neighbors (capacity n*ngmax; BT_ERR_CAPACITY leaves counts and
  * offsets valid and nbr_idx untouched).  Uses internal device memory of
- * 3 n int32 + (n+1) int64 besides the gather pass's.
+ * 2 n int32 + (n+1) int64 besides the gather pass's.
  */
 int bt_find_neighbors_sym(const bt_tree *t, const double *h, int32_t ngmax, int32_t *counts,
                           int64_t *offsets, int32_t *nbr_idx);

@@ -179,14 +179,14 @@ struct TreeDev {
     const double *rec_h = nullptr;
     long long rec_hsum = 0;
     int rec_exact = 0;
+    bool rec_tp = false;       // the candidate records hold tree positions (symmetric pass)
     DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
     DBuf<int32_t> front;       // descent frontier scratch of the big-unit pass (per warp)
     // symmetric criterion (R22): gather counts, one-sided extras / append cursors, gather offsets
     DBuf<int32_t> sym_g, sym_x;
     DBuf<int64_t> sym_off;
     bool sym_valid = false;    // sym_g / sym_x hold the pass of the current recorded masks
-    DBuf<int32_t> inv;         // tree position of each caller index
-    bool inv_valid = false;
+
     int64_t total_pairs = 0, max_count = 0, staged = 0, loaded = 0, tests = 0, exact_tests = 0;
     int64_t mask_words = 0, cand_slots = 0, list_entries = 0, big_units = 0;
 };
@@ -194,7 +194,7 @@ struct TreeDev {
 // Build (build.cu) and search (walk.cu) entry points.
 void build_tree(TreeDev &t, const double *pos);
 void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets,
-                    int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass);
+                    int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass, bool cand_tp = false);
 
 void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
                         int64_t capacity, bool count_pass, bool fill_pass);

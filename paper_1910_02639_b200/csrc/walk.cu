@@ -804,7 +804,7 @@ __device__ __forceinline__ void locate(const WalkSmem &S, int total, bool single
 // cull) into the warp's scratch at nst, until the group is done or the
 // scratch cannot take another window.  kMixed: some leaf of the group is
 // staged from the fp64 records (a = fl32(fl64(x - c))).
-template <bool kMixed>
+template <bool kMixed, bool kTP>
 __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int total, bool single,
                                             int &w0, int &nst, int slot0) {
     const unsigned lt = lanemask_lt(), le = lt | (1u << lane);
@@ -867,7 +867,7 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         if (keep) {
             const int slot = nst + __popc(km & lt);
             __stcg(&scr[(unsigned)slot], make_float4(ax, ay, az, __int_as_float(pos)));  // L2-resident scratch
-            if (rec_ok) __stcs(&cands[(unsigned)slot], __float_as_int(r.w));
+            if (rec_ok) __stcs(&cands[(unsigned)slot], kTP ? pos : __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
         }
         nst += __popc(km);
@@ -881,7 +881,9 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
 #ifndef BT_WALK_MIN_BLOCKS
 #define BT_WALK_MIN_BLOCKS 7
 #endif
-template <bool kDensity>
+// kTP: record each candidate's tree position instead of its caller index
+// (the symmetric pass reads the records; the fill maps them through perm)
+template <bool kDensity, bool kTP>
 __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(WalkArgs a) {
     __shared__ WalkSmemT<kDensity> smem[kWalkThreads / 32];
     const int lane = threadIdx.x & 31;
@@ -1047,9 +1049,9 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     have_group = true;
                 }
                 if (mixed)
-                    stage_group<true>(S, a, lane, total, nl == 1, w0, nst, slot0);
+                    stage_group<true, kTP>(S, a, lane, total, nl == 1, w0, nst, slot0);
                 else
-                    stage_group<false>(S, a, lane, total, nl == 1, w0, nst, slot0);
+                    stage_group<false, kTP>(S, a, lane, total, nl == 1, w0, nst, slot0);
                 if (w0 < total) break;  // scratch full
                 loaded += total;
                 g0 += nl;
@@ -1127,6 +1129,7 @@ struct FillSmem {
     unsigned long long mask[kFillChunks * kQ];   // the round's masks, [k][q]
 };
 
+template <bool kTP>
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     __shared__ FillSmem fsm[kFillWarps];
     const int lane = threadIdx.x & 31;
@@ -1152,6 +1155,10 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
                 const int s0 = 64 * (kk0 + k) + lane, s1 = s0 + 32;
                 c0[k] = (k < nk && s0 < R.nstaged) ? __ldcs(&cands[R.cand_base + s0]) : -1;
                 c1[k] = (k < nk && s1 < R.nstaged) ? __ldcs(&cands[R.cand_base + s1]) : -1;
+                if (kTP) {  // tree positions -> caller indices
+                    if (c0[k] >= 0) c0[k] = a.perm[c0[k]];
+                    if (c1[k] >= 0) c1[k] = a.perm[c1[k]];
+                }
             }
             __syncwarp();
             const unsigned long long *src = masks + R.mask_base + (long long)kk0 * nq;
@@ -1190,11 +1197,6 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
 // so a lane collects its candidate's one-sided queries in a 64-bit mask and
 // touches j's counter once per (unit, chunk).
 // ---------------------------------------------------------------------------
-__global__ void inverse_order_kernel(const int32_t *__restrict__ perm, int64_t n, int32_t *__restrict__ inv) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-        inv[perm[p]] = (int32_t)p;
-}
-
 __global__ void add_counts_kernel(const int32_t *__restrict__ g, const int32_t *__restrict__ x, int64_t n,
                                   int32_t *__restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -1204,8 +1206,8 @@ __global__ void add_counts_kernel(const int32_t *__restrict__ g, const int32_t *
 // kFill = false: extra[j] += one-sided pairs (i, j).  kFill = true: append i
 // to row j at offsets[j] + gcnt[j] + (cursor extra[j], zeroed by the caller).
 template <bool kFill>
-__global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int32_t *__restrict__ inv,
-                                                           const int32_t *__restrict__ gcnt, int32_t *__restrict__ extra) {
+__global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int32_t *__restrict__ gcnt,
+                                                           int32_t *__restrict__ extra) {
     __shared__ double4 qs[kFillWarps][kQ];
     __shared__ double qT[kFillWarps][kQ];
     const int lane = threadIdx.x & 31;
@@ -1241,9 +1243,9 @@ __global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const int slot = 64 * k + 32 * h + lane;
-                j[h] = slot < R.nstaged ? a.cands[R.cand_base + slot] : -1;
-                if (j[h] >= 0) {
-                    const int32_t tp = inv[j[h]];
+                const int32_t tp = slot < R.nstaged ? a.cands[R.cand_base + slot] : -1;  // tree position (kTP records)
+                j[h] = tp >= 0 ? a.perm[tp] : -1;
+                if (tp >= 0) {
                     c[h] = a.rec[tp];
                     const double t = __dmul_rn(2.0, a.h_tree[tp]);  // 2 h_j (exact)
                     T[h] = __dmul_rn(t, t);
@@ -1384,8 +1386,8 @@ Grids walk_grids() {
         return (unsigned)(sms * std::max(per_sm, 1));
     };
     return Grids{grid_of((const void *)desc_kernel<false>, kDescThreads),
-                 grid_of((const void *)walk_kernel<kDensity>, kWalkThreads),
-                 grid_of((const void *)fill_kernel, kFillThreads), (unsigned)std::min(sms, 32)};
+                 grid_of((const void *)walk_kernel<kDensity, false>, kWalkThreads),
+                 grid_of((const void *)fill_kernel<false>, kFillThreads), (unsigned)std::min(sms, 32)};
 }
 
 // h in tree order (validated) + its checksum
@@ -1479,7 +1481,7 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
 }  // namespace
 
 void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
-                    int64_t capacity, bool count_pass, bool fill_pass) {
+                    int64_t capacity, bool count_pass, bool fill_pass, bool cand_tp) {
     cudaStream_t st = stream();
     const int64_t n = t.n;
     if (n == 0) {
@@ -1494,7 +1496,8 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
 
     // the recorded masks of a previous test pass are reused by a fill-only
     // call when the tree, h pointer, exactness mode and h checksum all match
-    const bool have_record = t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only;
+    const bool have_record = t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only &&
+                             t.rec_tp == cand_tp;
     const bool run_test = count_pass || !have_record;
 
     WalkArgs a = walk_args(t, g);
@@ -1529,7 +1532,10 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero(c);
             {
                 Phase ph("search.count");
-                walk_kernel<false><<<g.w, kWalkThreads, 0, st>>>(a);
+                if (cand_tp)
+                    walk_kernel<false, true><<<g.w, kWalkThreads, 0, st>>>(a);
+                else
+                    walk_kernel<false, false><<<g.w, kWalkThreads, 0, st>>>(a);
                 BT_LAUNCH("walk_test");
             }
             read_counters(t, hc);
@@ -1539,6 +1545,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             t.rec_h = h;
             t.rec_hsum = hsum;
             t.rec_exact = g_exact_only;
+            t.rec_tp = cand_tp;
         }
         t.staged = hc[C_STAGED];
         t.loaded = hc[C_LOADED];
@@ -1572,7 +1579,10 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     zero(C_WORK2);
     {
         Phase ph("search.fill");
-        fill_kernel<<<g.f, kFillThreads, 0, st>>>(a);
+        if (t.rec_tp)
+            fill_kernel<true><<<g.f, kFillThreads, 0, st>>>(a);
+        else
+            fill_kernel<false><<<g.f, kFillThreads, 0, st>>>(a);
         BT_LAUNCH("walk_fill");
     }
     BT_CUDA(cudaStreamSynchronize(st));
@@ -1604,16 +1614,12 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
     bool have = false;
     if (!count_pass) {
         const long long hsum = gather_h(t, h, "bt_fill_neighbors_sym");
-        have = t.sym_valid && t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only;
+        have = t.sym_valid && t.rec_valid && t.rec_tp && t.rec_h == h && t.rec_hsum == hsum &&
+               t.rec_exact == g_exact_only;
     }
     if (!have) {
-        find_neighbors(t, h, t.sym_g.p, t.sym_off.p, nullptr, 0, true, false);  // gather counts + recorded masks
-        if (!t.inv_valid) {
-            t.inv.reserve(n, 0);
-            inverse_order_kernel<<<grid_for(n, 256, (int64_t)sms * 16), 256, 0, st>>>(t.perm.p, n, t.inv.p);
-            BT_LAUNCH("inverse_order");
-            t.inv_valid = true;
-        }
+        // gather counts + recorded masks, candidates recorded as tree positions
+        find_neighbors(t, h, t.sym_g.p, t.sym_off.p, nullptr, 0, true, false, true);
         WalkArgs a = walk_args(t, g);
         a.masks = t.arena_masks.p;
         a.cands = t.arena_cands.p;
@@ -1621,7 +1627,7 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
         zero_counter(t, C_WORK5);
         {
             Phase ph("search.sym_count");
-            sym_kernel<false><<<g.f, kFillThreads, 0, st>>>(a, t.inv.p, t.sym_g.p, t.sym_x.p);
+            sym_kernel<false><<<g.f, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
             BT_LAUNCH("sym_count");
         }
         t.sym_valid = true;
@@ -1656,12 +1662,12 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
     BT_CUDA(cudaMemsetAsync(t.sym_x.p, 0, n * sizeof(int32_t), st));  // append cursors
     {
         Phase ph("search.fill");
-        fill_kernel<<<g.f, kFillThreads, 0, st>>>(a);
+        fill_kernel<true><<<g.f, kFillThreads, 0, st>>>(a);  // symmetric pass: tree-position records
         BT_LAUNCH("walk_fill");
     }
     {
         Phase ph("search.sym_fill");
-        sym_kernel<true><<<g.f, kFillThreads, 0, st>>>(a, t.inv.p, t.sym_g.p, t.sym_x.p);
+        sym_kernel<true><<<g.f, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
         BT_LAUNCH("sym_fill");
     }
     t.sym_valid = false;  // the cursors overwrote the extra counts
@@ -1704,7 +1710,7 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
     for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero_counter(t, c);
     {
         Phase ph("density.walk");
-        walk_kernel<true><<<g.w, kWalkThreads, 0, st>>>(a);
+        walk_kernel<true, false><<<g.w, kWalkThreads, 0, st>>>(a);
         BT_LAUNCH("walk_density");
     }
     read_counters(t, hc);
