@@ -586,3 +586,29 @@ def test_partitioned_search_is_a_disjoint_cover(P, oracle, cfg, n, nparts):
     assert np.array_equal(sort_rows(c, o, nb), full_rows)
     with pytest.raises(P.BtreeError):
         t.set_partition(2, 2)
+
+
+def test_parity_cfg5_full_size_every_row(P, oracle):
+    """cfg 5 at full size (2^25 particles): every count against the oracle's
+    own tree walk (memcmp), and every row, compared sorted in chunks of 2^21
+    queries (the oracle recomputes each chunk) -- the whole 4.35e9-pair CSR."""
+    pos, h = datagen.make_config(5)
+    n = pos.shape[0]
+    t = P.build(torch.from_numpy(pos).to(DEV), 64, 0.5)
+    hd = torch.from_numpy(h).to(DEV)
+    counts, offsets = t.count(hd)
+    nbr = t.fill(hd, offsets)
+    torch.cuda.synchronize()
+    t.free()
+    ot = oracle.Tree(pos, 64, 0.5)
+    oc = ot.count(h)
+    c = counts.cpu().numpy()
+    assert np.array_equal(c, oc)
+    chunk = 1 << 21
+    for q0 in range(0, n, chunk):
+        q1 = min(n, q0 + chunk)
+        _, ooff, oidx = ot.neighbors(h, queries=np.arange(q0, q1, dtype=np.int64))
+        s0, s1 = int(offsets[q0]), int(offsets[q1])
+        sub_off = offsets[q0:q1 + 1] - s0
+        rows = sort_rows(counts[q0:q1], sub_off, nbr[s0:s1])
+        assert np.array_equal(rows, oidx), f"rows {q0}..{q1} differ"
