@@ -11,7 +11,7 @@
  *
  * Citations: P:n = line n of the paper text (PAPER.md, arXiv 1910.02639),
  * with the section / equation / algorithm it falls in.  Readings of the paper
- * where it is silent or garbled are numbered R1..R18 in DESIGN.md section 3.
+ * where it is silent or garbled are numbered R1..R23 in DESIGN.md section 3.
  *
  * Build flags (see __graft_entry__.build): gcc -O2 -std=c11 -fPIC -shared
  * -ffp-contract=off -fno-fast-math -fopenmp.  x86-64 SSE2 fp64, no FMA, no
@@ -20,8 +20,10 @@
  *
  * Pinned by tests/test_oracle_pins.py (worked examples of Eq. 2/3, Eq. 1 and
  * Eq. 4 closed forms, Fig. 1 ranges, lattice neighbor counts, boundary
- * convention, brute force vs scipy cKDTree, structural invariants).  Tree
- * shapes at scale are "parity unpinned" beyond those invariants.
+ * convention, brute force vs scipy cKDTree, structural invariants; the k = 2
+ * policies, the symmetric criterion and the density sum by their own closed
+ * forms and cross-checks).  Tree shapes at scale are "parity unpinned"
+ * beyond those invariants.
  */
 #include <math.h>
 #include <stdint.h>
