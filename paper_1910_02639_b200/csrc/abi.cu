@@ -363,35 +363,50 @@ int bt_search_host(const double *pos_h, const double *h_h, int64_t n, int32_t bu
     bt_tree *t = nullptr;
     int rc = guarded([&] {
         cudaStream_t st = stream();
+        // a side stream carries the copies that do not gate the next kernel:
+        // h's upload overlaps the build, counts / offsets go home during the fill
+        static thread_local cudaStream_t side = nullptr;
+        if (!side) BT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        cudaEvent_t ev_h, ev_c;
+        BT_CUDA(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming));
+        BT_CUDA(cudaEventCreateWithFlags(&ev_c, cudaEventDisableTiming));
+        struct Events {
+            cudaEvent_t a, b;
+            ~Events() { cudaEventDestroy(a); cudaEventDestroy(b); }
+        } evs{ev_h, ev_c};
         Phase ph("e2e.total");
         DBuf<double> pos(3 * (size_t)n), h((size_t)n);
         DBuf<int32_t> counts((size_t)n);
         DBuf<int64_t> offsets((size_t)n + 1);
-        {
-            Phase p2("e2e.h2d");
-            if (n) BT_CUDA(cudaMemcpyAsync(pos.p, pos_h, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
-            if (n) BT_CUDA(cudaMemcpyAsync(h.p, h_h, n * sizeof(double), cudaMemcpyHostToDevice, st));
-        }
+        struct SideSync {  // (declared after the buffers: on any exit the side stream drains first)
+            cudaStream_t s;
+            ~SideSync() { cudaStreamSynchronize(s); }
+        } side_sync{side};
+        BT_CUDA(cudaEventRecord(ev_h, st));  // the buffers exist before the side stream writes them
+        BT_CUDA(cudaStreamWaitEvent(side, ev_h, 0));
+        if (n) BT_CUDA(cudaMemcpyAsync(pos.p, pos_h, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+        if (n) BT_CUDA(cudaMemcpyAsync(h.p, h_h, n * sizeof(double), cudaMemcpyHostToDevice, side));
+        BT_CUDA(cudaEventRecord(ev_h, side));
         t = bt_build(pos.p, n, bucket_size, max_empty);
         if (!t) throw Error(g_status, g_err);
+        BT_CUDA(cudaStreamWaitEvent(st, ev_h, 0));  // h has arrived
         find_neighbors(t->t, h.p, counts.p, offsets.p, nullptr, 0, true, false);
         const int64_t total = t->t.total_pairs;
-        {
-            Phase p3("e2e.d2h");
-            if (n) BT_CUDA(cudaMemcpyAsync(counts_h, counts.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-            BT_CUDA(cudaMemcpyAsync(offsets_h, offsets.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        }
+        BT_CUDA(cudaEventRecord(ev_c, st));
+        BT_CUDA(cudaStreamWaitEvent(side, ev_c, 0));
+        if (n) BT_CUDA(cudaMemcpyAsync(counts_h, counts.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, side));
+        BT_CUDA(cudaMemcpyAsync(offsets_h, offsets.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, side));
+        BT_CUDA(cudaEventRecord(ev_c, side));
         if (total > capacity) {
+            BT_CUDA(cudaStreamSynchronize(side));
             BT_CUDA(cudaStreamSynchronize(st));
             throw Error(BT_ERR_CAPACITY, "bt_search_host: " + std::to_string(total) + " pairs exceed capacity " +
                                              std::to_string(capacity));
         }
         DBuf<int32_t> nbr((size_t)(total > 0 ? total : 1));
         find_neighbors(t->t, h.p, nullptr, offsets.p, nbr.p, total, false, true);
-        {
-            Phase p4("e2e.d2h");
-            if (total) BT_CUDA(cudaMemcpyAsync(nbr_h, nbr.p, total * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        }
+        if (total) BT_CUDA(cudaMemcpyAsync(nbr_h, nbr.p, total * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        BT_CUDA(cudaStreamWaitEvent(st, ev_c, 0));  // (buffers are released on st)
         BT_CUDA(cudaStreamSynchronize(st));
     });
     if (t) {
