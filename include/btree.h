@@ -252,6 +252,8 @@ typedef struct bt_stats {
     int64_t cand_slots;   /* candidate arena slots allocated                     */
     int64_t list_entries; /* candidate-leaf list entries allocated by the descent */
     int64_t big_units;    /* units redone by the global-frontier descent pass    */
+    int64_t rows_over_ngmax; /* rows of the last count with more than its ngmax neighbors
+                                (SPH callers sizing fixed-stride tables; counts are never clamped) */
 } bt_stats;
 
 int bt_tree_stats(const bt_tree *t, bt_stats *out);

@@ -44,7 +44,7 @@ class Stats(C.Structure):
                 ("total_pairs", C.c_int64), ("max_count", C.c_int64), ("staged", C.c_int64),
                 ("tests", C.c_int64), ("exact_tests", C.c_int64), ("loaded", C.c_int64),
                 ("mask_words", C.c_int64), ("cand_slots", C.c_int64), ("list_entries", C.c_int64),
-                ("big_units", C.c_int64)]
+                ("big_units", C.c_int64), ("rows_over_ngmax", C.c_int64)]
 
     def as_dict(self):
         d = {}
@@ -176,15 +176,16 @@ class Tree:
             raise BtreeError(BT_ERR_ARG, "tree already freed")
         return self._h
 
-    def count(self, h: torch.Tensor, symmetric: bool = False):
+    def count(self, h: torch.Tensor, symmetric: bool = False, ngmax: int = 512):
         """Count-only call: (counts int32 [n], offsets int64 [n+1]).  symmetric:
-        the max(h_i, h_j) criterion (bt_find_neighbors_sym)."""
+        the max(h_i, h_j) criterion (bt_find_neighbors_sym); ngmax only sets
+        the threshold of stats()["rows_over_ngmax"]."""
         h = _dev_f64(h)
         counts = torch.empty(self.n, dtype=torch.int32, device=self.device)
         offsets = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
         _use_current_stream()
         fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
-        _check(fn(self._handle(), _ptr(h), 1, _ptr(counts), _ptr(offsets), None))
+        _check(fn(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets), None))
         return counts, offsets
 
     def fill(self, h: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,

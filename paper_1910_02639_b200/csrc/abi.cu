@@ -278,6 +278,7 @@ int bt_find_neighbors(const bt_tree *tc, const double *h, int32_t ngmax, int32_t
     return guarded([&] {
         Phase ph("search.total");
         const int64_t cap = t->t.n * (int64_t)ngmax;
+        t->t.ngmax = ngmax;
         find_neighbors(t->t, h, counts, offsets, nbr_idx, cap, true, nbr_idx != nullptr);
     });
 }
@@ -305,6 +306,7 @@ int bt_find_neighbors_sym(const bt_tree *tc, const double *h, int32_t ngmax, int
     return guarded([&] {
         Phase ph("search.total");
         const int64_t cap = t->t.n * (int64_t)ngmax;
+        t->t.ngmax = ngmax;
         find_neighbors_sym(t->t, h, counts, offsets, nbr_idx, cap, true, nbr_idx != nullptr);
     });
 }
@@ -468,6 +470,7 @@ int bt_tree_stats(const bt_tree *t, bt_stats *out) {
     out->cand_slots = d.cand_slots;
     out->list_entries = d.list_entries;
     out->big_units = d.big_units;
+    out->rows_over_ngmax = d.rows_over_ngmax;
     return BT_OK;
 }
 

@@ -188,6 +188,7 @@ struct TreeDev {
     bool sym_valid = false;    // sym_g / sym_x hold the pass of the current recorded masks
 
     int64_t total_pairs = 0, max_count = 0, staged = 0, loaded = 0, tests = 0, exact_tests = 0;
+    int64_t ngmax = 512, rows_over_ngmax = 0;  // the last count's ngmax and its rows above it
     int64_t mask_words = 0, cand_slots = 0, list_entries = 0, big_units = 0;
 };
 

@@ -68,7 +68,8 @@ enum {
     C_NEEDC = 14,    // sum over units of `loaded` (bound on candidate slots)
     C_NEEDM = 15,    // sum over units of ceil(loaded / 64) * nq (bound on mask words)
     C_WORK5 = 16,    // unit counter (symmetric-criterion pass)
-    C_N = 17
+    C_OVER = 17,     // rows with more neighbors than the call's ngmax
+    C_N = 18
 };
 
 struct WalkArgs {
@@ -1347,12 +1348,22 @@ struct OffsetOut {
 };
 __global__ void write_total_kernel(int64_t *off, int64_t n, const long long *total) { off[n] = *total; }
 
-__global__ void max_count_kernel(const int32_t *c, int64_t n, long long *out) {
+// max over the counts and the number of rows above ngmax (out[0], out[C_OVER - C_MAXC])
+__global__ void max_count_kernel(const int32_t *c, int64_t n, int64_t ngmax, long long *out) {
     int m = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    unsigned over = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         m = max(m, c[i]);
-    for (int d = 16; d; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
-    if ((threadIdx.x & 31) == 0) atomicMax((unsigned long long *)out, (unsigned long long)m);
+        over += c[i] > ngmax;
+    }
+    for (int d = 16; d; d >>= 1) {
+        m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+        over += __shfl_xor_sync(0xffffffffu, over, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax((unsigned long long *)out, (unsigned long long)m);
+        if (over) atomicAdd((unsigned long long *)(out + (C_OVER - C_MAXC)), (unsigned long long)over);
+    }
 }
 
 thread_local int g_exact_only = 0;
@@ -1486,7 +1497,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     const int64_t n = t.n;
     if (n == 0) {
         if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
-        t.total_pairs = t.max_count = t.staged = t.loaded = t.tests = t.exact_tests = 0;
+        t.total_pairs = t.max_count = t.staged = t.loaded = t.tests = t.exact_tests = t.rows_over_ngmax = 0;
         BT_CUDA(cudaStreamSynchronize(st));
         return;
     }
@@ -1560,14 +1571,19 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             write_total_kernel<<<1, 1, 0, st>>>(offsets, n, dtot.p);
             BT_LAUNCH("write_total");
             zero(C_MAXC);
-            max_count_kernel<<<grid_for(n, 256, (int64_t)sms * 8), 256, 0, st>>>(cnt, n,
+            zero(C_OVER);
+            max_count_kernel<<<grid_for(n, 256, (int64_t)sms * 8), 256, 0, st>>>(cnt, n, t.ngmax,
                                                                                   (long long *)t.counters.p + C_MAXC);
             BT_LAUNCH("max_count");
         }
     }
-    int64_t total = 0, maxc = 0;
-    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)}});
-    if (count_pass) t.max_count = maxc;
+    int64_t total = 0, maxc = 0, over = 0;
+    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)},
+               {t.counters.p + C_OVER, &over, sizeof(int64_t)}});
+    if (count_pass) {
+        t.max_count = maxc;
+        t.rows_over_ngmax = over;
+    }
     t.total_pairs = total;
     if (!fill_pass || nbr_idx == nullptr) return;
     if (total > capacity)
@@ -1600,7 +1616,7 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
     const int64_t n = t.n;
     if (n == 0) {
         if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
-        t.total_pairs = t.max_count = 0;
+        t.total_pairs = t.max_count = t.rows_over_ngmax = 0;
         BT_CUDA(cudaStreamSynchronize(st));
         return;
     }
@@ -1641,12 +1657,18 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
         write_total_kernel<<<1, 1, 0, st>>>(offsets, n, dtot.p);
         BT_LAUNCH("write_total");
         zero_counter(t, C_MAXC);
-        max_count_kernel<<<grid_for(n, 256, (int64_t)sms * 8), 256, 0, st>>>(counts, n, (long long *)t.counters.p + C_MAXC);
+        zero_counter(t, C_OVER);
+        max_count_kernel<<<grid_for(n, 256, (int64_t)sms * 8), 256, 0, st>>>(counts, n, t.ngmax,
+                                                                              (long long *)t.counters.p + C_MAXC);
         BT_LAUNCH("max_count");
     }
-    int64_t total = 0, maxc = 0;
-    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)}});
-    if (count_pass) t.max_count = maxc;
+    int64_t total = 0, maxc = 0, over = 0;
+    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)},
+               {t.counters.p + C_OVER, &over, sizeof(int64_t)}});
+    if (count_pass) {
+        t.max_count = maxc;
+        t.rows_over_ngmax = over;
+    }
     t.total_pairs = total;
     if (!fill_pass || nbr_idx == nullptr) return;
     if (total > capacity)

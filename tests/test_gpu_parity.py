@@ -612,3 +612,18 @@ def test_parity_cfg5_full_size_every_row(P, oracle):
         sub_off = offsets[q0:q1 + 1] - s0
         rows = sort_rows(counts[q0:q1], sub_off, nbr[s0:s1])
         assert np.array_equal(rows, oidx), f"rows {q0}..{q1} differ"
+
+
+def test_rows_over_ngmax_stat(P, oracle):
+    # bt_tree_stats reports the rows above the call's ngmax (counts never clamped)
+    pos, h = datagen.make_config(5, n=200_000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd = torch.from_numpy(h).to(DEV)
+    c, _ = t.count(hd, ngmax=100)
+    cn = c.cpu().numpy()
+    st = t.stats()
+    assert st["rows_over_ngmax"] == int((cn > 100).sum()) and st["max_count"] == int(cn.max())
+    t.count(hd, ngmax=int(cn.max()))
+    assert t.stats()["rows_over_ngmax"] == 0
+    cs, _ = t.count(hd, symmetric=True, ngmax=100)
+    assert t.stats()["rows_over_ngmax"] == int((cs.cpu().numpy() > 100).sum())
