@@ -5,6 +5,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <cstdio>
 
 #include <stdexcept>
 #include <string>
@@ -237,6 +238,23 @@ __device__ __forceinline__ int cell_coord_fast(double x, double lo, double ext, 
     }
     return cell_coord(x, lo, ext, b);
 }
+
+// Device-side bounds checks of the checked build (nvcc -DBT_CHECKED,
+// tools/gpu_checked.sh): a failed check prints its location and traps, which
+// surfaces as a CUDA error at the ABI.  Compiled out otherwise.
+#ifdef BT_CHECKED
+#define BT_DEV_CHECK(c)                                                                 \
+    do {                                                                                \
+        if (!(c)) {                                                                     \
+            printf("BT_DEV_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);          \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define BT_DEV_CHECK(c) \
+    do {                \
+    } while (0)
+#endif
 
 constexpr int kWarp = 32;
 

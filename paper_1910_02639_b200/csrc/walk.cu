@@ -99,6 +99,8 @@ struct WalkArgs {
     long long *ctr;
     int32_t *cands;           // caller index of each candidate slot
     long long cand_cap;
+    int64_t n_rec;            // particles (tree positions) -- bounds checks
+    int64_t nbr_cap;          // int32 slots of nbr -- bounds checks
     unsigned long long *masks;
     long long mask_cap;
     float4 *scratch;          // per walk warp: kScratch staged candidates (ax, ay, az, tree position)
@@ -741,6 +743,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
                 S.mask[0][q] = m0;
                 S.mask[1][q] = m1;
             } else if (dst) {
+                BT_DEV_CHECK(S.u.mask_base + (long long)(us0 >> 6) * nq + (nch > 1 ? nq : 0) + q < a.mask_cap);
                 __stcs(&dst[q], m0);
                 if (nch > 1) __stcs(&dst[nq + q], m1);
             }
@@ -797,6 +800,7 @@ __device__ __forceinline__ void locate(const WalkSmem &S, int total, bool single
     const int w = min(w0 >> 5, kGroupPos / 32 - 1);  // (clamped: one-leaf groups ignore the bitmap)
     const int m = (int)S.lwpre[w] + __popc(S.lstart[w] & le) - 1;
     mine = single ? 0 : m;
+    BT_DEV_CHECK(mine >= 0 && mine < kGroup);
     const int p = w0 + lane;
     pos = (p < total) ? p + S.ldel[mine] : -1;
 }
@@ -867,6 +871,8 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             const int slot = nst + __popc(km & lt);
+            BT_DEV_CHECK(slot < kScratch && pos >= 0 && pos < a.n_rec);
+            BT_DEV_CHECK(!rec_ok || S.u.cand_base + slot0 + slot < a.cand_cap);
             __stcg(&scr[(unsigned)slot], make_float4(ax, ay, az, __int_as_float(pos)));  // L2-resident scratch
             if (rec_ok) __stcs(&cands[(unsigned)slot], kTP ? pos : __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
@@ -1163,6 +1169,7 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
             }
             __syncwarp();
             const unsigned long long *src = masks + R.mask_base + (long long)kk0 * nq;
+            BT_DEV_CHECK(R.mask_base + (long long)(kk0 + nk) * nq <= a.mask_cap && R.cand_base + R.nstaged <= a.cand_cap);
             for (int w = lane; w < nk * nq; w += 32) F.mask[w] = __ldcs(&src[w]);
             __syncwarp();
             for (int q = 0; q < nq; q++) {
@@ -1175,6 +1182,7 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
                     if (m == 0ull) continue;
                     const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
                     const int plo = __popc(lo);
+                    BT_DEV_CHECK(dst - a.nbr + plo + __popc(hi) <= a.nbr_cap);
                     if (lo & lanebit) __stcs(&dst[__popc(lo & lt)], c0[k]);
                     if (hi & lanebit) __stcs(&dst[plo + __popc(hi & lt)], c1[k]);
                     const int n = plo + __popc(hi);
@@ -1432,6 +1440,9 @@ WalkArgs walk_args(TreeDev &t, const Grids &g) {
     a.rec = t.rec.p;
     a.rec32 = t.rec32.p;
     a.perm = t.perm.p;
+    a.n_rec = t.n;
+    a.cand_cap = (long long)t.arena_cands.n;
+    a.mask_cap = (long long)t.arena_masks.n;
     a.h_tree = t.h_tree.p;
     a.nodes = t.nodes.p;
     a.cells = t.cells.p;
@@ -1514,6 +1525,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     WalkArgs a = walk_args(t, g);
     a.offsets = offsets;
     a.nbr = nbr_idx;
+    a.nbr_cap = capacity;
     auto zero = [&](int c) { zero_counter(t, c); };
 
     DBuf<int32_t> tmp_counts;
@@ -1679,6 +1691,7 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
     a.cands = t.arena_cands.p;
     a.offsets = offsets;
     a.nbr = nbr_idx;
+    a.nbr_cap = capacity;
     zero_counter(t, C_WORK2);
     zero_counter(t, C_WORK5);
     BT_CUDA(cudaMemsetAsync(t.sym_x.p, 0, n * sizeof(int32_t), st));  // append cursors
