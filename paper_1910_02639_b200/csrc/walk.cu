@@ -100,6 +100,7 @@ struct WalkArgs {
     int32_t *cands;           // caller index of each candidate slot
     long long cand_cap;
     int64_t n_rec;            // particles (tree positions) -- bounds checks
+    int64_t n_cells, n_leaves;  // cell-table entries, leaves -- bounds checks
     int64_t nbr_cap;          // int32 slots of nbr -- bounds checks
     unsigned long long *masks;
     long long mask_cap;
@@ -440,6 +441,7 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
                         code = a.cells[ocb + j];
                         is_leaf = code >= 0;
                         is_node = code <= -2;
+                        BT_DEV_CHECK(ocb + j < a.n_cells && code < a.n_leaves);
                     }
                     const unsigned nm = __ballot_sync(0xffffffffu, is_node);
                     const int slot = nnext + __popc(nm & lt);
@@ -1301,6 +1303,7 @@ __global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int
                 } else {
                     int32_t *dst = a.nbr + a.offsets[j[h]] + gcnt[j[h]] + atomicAdd(&extra[j[h]], cnt);
                     unsigned long long m = os[h];
+                    BT_DEV_CHECK(dst - a.nbr + cnt <= a.nbr_cap);
                     while (m) {
                         const int q = __ffsll((long long)m) - 1;
                         m &= m - 1ull;
@@ -1441,6 +1444,8 @@ WalkArgs walk_args(TreeDev &t, const Grids &g) {
     a.rec32 = t.rec32.p;
     a.perm = t.perm.p;
     a.n_rec = t.n;
+    a.n_cells = t.n_cells;
+    a.n_leaves = t.n_leaves;
     a.cand_cap = (long long)t.arena_cands.n;
     a.mask_cap = (long long)t.arena_masks.n;
     a.h_tree = t.h_tree.p;
