@@ -45,7 +45,7 @@ typedef enum bt_status {
     BT_OK = 0,
     BT_ERR_ARG = 1,      /* invalid argument (NULL pointer, range, size)        */
     BT_ERR_INPUT = 2,    /* invalid data (non-finite or |coordinate| > 1e150,
-                            h not finite or h <= 0)                              */
+                            h not finite, h <= 0 or h > 1e150)                   */
     BT_ERR_CAPACITY = 3, /* neighbor output does not fit the given capacity      */
     BT_ERR_CUDA = 4,     /* CUDA runtime / launch failure                        */
     BT_ERR_OOM = 5       /* device memory exhausted                              */
