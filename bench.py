@@ -61,7 +61,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1_000_000, help="oracle queries timed for cpu_baseline")
+    ap.add_argument("--cpu-sample", type=int, default=None,
+                    help="oracle queries timed for cpu_baseline (default: every query up to N = 4.2M, else 1M)")
     return ap.parse_args()
 
 
@@ -194,27 +195,43 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def default_sample(n: int) -> int:
+    """Oracle queries timed per cpu_baseline: the whole workload up to N = 4.2M
+    (cfg 1-4: tens of seconds on the box's cores), a 1M-query sample above."""
+    return n if n <= 4_200_000 else 1_000_000
+
+
 def oracle_sample(pos, h, sample_queries: int):
     """Time the oracle as it stands on this host: full BuildTree + the
-    FindNeighbors count and row passes for a random sample of queries, all
-    host cores (OpenMP over queries).  Returns (est. seconds per full step,
-    description, cores)."""
+    FindNeighbors count and row passes over every query (N <= 4.2M) or a
+    random sample of queries, all host cores (OpenMP over queries).  Returns
+    (seconds per full step -- measured, or scaled from the sample --,
+    description, cores, build s, search s)."""
     import oracle
     n = pos.shape[0]
     cores = oracle.default_threads()
     t0 = time.perf_counter()
     tree = oracle.Tree(pos, datagen.BUCKET_SIZE, datagen.MAX_EMPTY)
     t1 = time.perf_counter()
-    rng = np.random.default_rng(7)
     k = min(sample_queries, n)
-    q = np.sort(rng.choice(n, k, replace=False)).astype(np.int64)
-    tree.neighbors(h, queries=q, threads=cores)
+    if k >= n:
+        tree.neighbors(h, threads=cores)
+    else:
+        rng = np.random.default_rng(7)
+        q = np.sort(rng.choice(n, k, replace=False)).astype(np.int64)
+        tree.neighbors(h, queries=q, threads=cores)
     t2 = time.perf_counter()
     build_s = t1 - t0
     search_s = (t2 - t1) * n / k
-    desc = (f"oracle BuildTree on all {n} particles ({build_s:.2f} s, 1 thread) + count and row passes for "
-            f"{k} random queries ({t2 - t1:.2f} s, {cores} threads), search scaled x{n / k:.1f} to all queries; "
-            f"host CPU: {cpu_model()}")
+    if k >= n:
+        desc = (f"oracle on the whole workload, measured: BuildTree on all {n} particles ({build_s:.2f} s, "
+                f"1 thread) + count and row passes for all {n} queries ({t2 - t1:.2f} s, {cores} threads); "
+                f"host CPU: {cpu_model()}")
+    else:
+        desc = (f"oracle BuildTree on all {n} particles ({build_s:.2f} s, 1 thread) + count and row passes for "
+                f"{k} random queries ({t2 - t1:.2f} s, {cores} threads), search scaled x{n / k:.1f} to all "
+                f"queries (full single-thread and all-core runs: profiles/r02_oracle_baseline.jsonl); "
+                f"host CPU: {cpu_model()}")
     return build_s + search_s, desc, cores, build_s, search_s
 
 
@@ -227,7 +244,8 @@ def run_reference(args):
     steps = []
     desc = cores = None
     for s in range(args.warmup + args.steps):
-        step_s, desc, cores, b, srch = oracle_sample(pos, h, min(args.cpu_sample, 200_000))
+        step_s, desc, cores, b, srch = oracle_sample(pos, h, min(args.cpu_sample or default_sample(n), 200_000)
+                                                     if n > 4_200_000 else default_sample(n))
         if s >= args.warmup:
             steps.append(step_s)
     t = float(np.mean(steps))
@@ -318,7 +336,7 @@ def run_b200(args):
     launches = sum(v[1] for k, v in prof.items() if k.startswith("kernel.")) // args.steps
     kern = {"build": ph("build.total"), "walk_desc": ph("search.desc") + ph("search.desc_big"),
             "walk_test": ph("search.count"), "scan": ph("search.scan"), "walk_fill": ph("search.fill"),
-            "gather_h": ph("search.gather_h")}
+            "gather_h": ph("search.gather_h"), "search_total": ph("search.total")}
 
     # ---- roofline of the dominant kernel -----------------
     peaks = {}
@@ -332,18 +350,19 @@ def run_b200(args):
     dom = max(("walk_desc", "walk_test", "walk_fill", "build"), key=lambda k: kern[k])
     if dom == "walk_test":
         # walk_kernel: staging + pair tests, bound by fp32 issue.  Algorithmic
-        # work = 8 fp32 ops per pair test (3 differences, 3 squares, 2 sums:
-        # ((dx*dx + dy*dy) + dz*dz)).  Peak = the measured packed-fp32 (FFMA2)
-        # rate of this B200 model, 23.61 T instr-lanes/s x 2 = 47.2 T fp32 op/s
-        # (tools/probe_rates.cu, profiles/r01_probe_rates.txt), scaled to the
-        # recorded SM clock; scalar FFMA measures 35.8 T op/s.
-        alu_peak = 47.22
+        # work = the plain predicate's 8 flops per pair test (3 differences, 3
+        # squares, 2 sums), against the measured packed-fp32 peak counted the
+        # same way: 23.61 T FFMA2 instruction-lanes/s x 2 FMAs x 2 flops =
+        # 94.4 TFLOP/s (tools/probe_rates.cu, profiles/r01_probe_rates.txt).
+        # (The kernel issues 4 fp32 element ops per pair -- FADD + 3 FFMA of the
+        # expanded form -- against 47.2 T element-ops/s: the same fraction.)
+        alu_peak = 94.44
         achieved = tests * 8 / (kern[dom] * 1e-3) / 1e12
         roofline = {"kernel": "walk_kernel (A10 staging + A11 pair tests)", "bound": "alu", "achieved": achieved,
-                    "peak": alu_peak, "unit": "T fp32 op/s", "frac": achieved / alu_peak, "traffic": None,
-                    "peak_source": "measured: packed FFMA2 throughput x 2 (tools/probe_rates.cu, "
+                    "peak": alu_peak, "unit": "TFLOP/s", "frac": achieved / alu_peak, "traffic": None,
+                    "peak_source": "measured: packed FFMA2 rate x 2 FMA x 2 flops (tools/probe_rates.cu, "
                                    "profiles/r01_probe_rates.txt)",
-                    "algorithmic_ops": tests * 8}
+                    "algorithmic_flops": tests * 8, "issued_fp32_element_ops": tests * 4}
     else:
         if dom == "walk_desc":
             # descent: per unit the query records (32 B) + h (8 B), per listed leaf
@@ -361,20 +380,25 @@ def run_b200(args):
         roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved / hbm_peak, "traffic": None, "peak_source": hbm_src,
                     "algorithmic_bytes": alg_bytes}
-    try:  # per-launch DRAM bytes from the committed ncu capture (profiles/), if any
+    try:  # per-launch DRAM bytes / L2 hit rate from the committed ncu captures (profiles/), if any
         tr = json.load(open(os.path.join(ROOT, "profiles", "dram_traffic.json")))
         if tr.get("config") == args.config and dom in tr.get("kernels", {}):
             roofline["traffic"] = tr["kernels"][dom]
             roofline["traffic_source"] = tr.get("source")
+        if tr.get("config") == args.config and tr.get("ncu"):
+            roofline["ncu"] = tr["ncu"]
     except Exception:
         pass
     # BASELINE.json's own definition: bytes of candidate positions actually read
-    # by the walk (16-B compact records loaded by the gather) over the whole walk
-    # time (gather + test + fill) and peak HBM bandwidth
+    # by the walk (16-B compact records loaded by the staging) over the time of
+    # the whole bt_find_neighbors call (gather of h, descent, count, offsets
+    # scan, capacity check, fill) and peak HBM bandwidth
     bcand = loaded * 16
-    walk_ms = kern["walk_desc"] + kern["walk_test"] + kern["walk_fill"]
-    bj_roof = {"B_cand_bytes": bcand, "walk_ms": walk_ms,
-               "frac": (bcand / (walk_ms * 1e-3) / 1e9) / hbm_peak if walk_ms > 0 else None}
+    search_ms = ph("search.total")
+    bj_roof = {"B_cand_bytes": bcand, "search_ms": search_ms,
+               "frac": (bcand / (search_ms * 1e-3) / 1e9) / hbm_peak if search_ms > 0 else None,
+               "definition": "16 B x compact records loaded by the walk staging / whole bt_find_neighbors time / "
+                             "measured HBM peak"}
 
     # ---- end to end through the public API on host buffers --------------------
     e2e = None
@@ -407,7 +431,7 @@ def run_b200(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        step_s, desc, cores, _, _ = oracle_sample(pos_np, h_np, args.cpu_sample)
+        step_s, desc, cores, _, _ = oracle_sample(pos_np, h_np, args.cpu_sample or default_sample(n))
         cpu = {"value": n / step_s, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
     if rank == 0:
@@ -423,7 +447,7 @@ def run_b200(args):
                 "roofline": roofline, "bj_hbm_roofline": bj_roof,
                 "tree": {k: st[k] for k in ("depth", "root_b", "nodes", "leaves", "halvings", "units")},
                 "walk_counters": {k: st.get(k) for k in ("loaded", "staged", "tests", "exact_tests", "mask_words",
-                                                         "cand_slots", "list_entries", "big_units")},
+                                                         "cand_slots", "list_entries", "big_units", "mask_words_nonzero")},
                 "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if ws > 1:

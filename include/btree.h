@@ -254,6 +254,7 @@ typedef struct bt_stats {
     int64_t big_units;    /* units redone by the global-frontier descent pass    */
     int64_t rows_over_ngmax; /* rows of the last count with more than its ngmax neighbors
                                 (SPH callers sizing fixed-stride tables; counts are never clamped) */
+    int64_t mask_words_nonzero; /* recorded mask words holding at least one neighbor (the fill's work) */
 } bt_stats;
 
 int bt_tree_stats(const bt_tree *t, bt_stats *out);

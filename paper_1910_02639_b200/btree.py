@@ -44,7 +44,8 @@ class Stats(C.Structure):
                 ("total_pairs", C.c_int64), ("max_count", C.c_int64), ("staged", C.c_int64),
                 ("tests", C.c_int64), ("exact_tests", C.c_int64), ("loaded", C.c_int64),
                 ("mask_words", C.c_int64), ("cand_slots", C.c_int64), ("list_entries", C.c_int64),
-                ("big_units", C.c_int64), ("rows_over_ngmax", C.c_int64)]
+                ("big_units", C.c_int64), ("rows_over_ngmax", C.c_int64),
+                ("mask_words_nonzero", C.c_int64)]
 
     def as_dict(self):
         d = {}
@@ -122,16 +123,35 @@ def _ptr(t):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
-def _use_current_stream():
-    lib().bt_set_stream(C.c_void_p(torch.cuda.current_stream().cuda_stream))
+def _use_current_stream(device=None):
+    """Hand torch's current stream of `device` (the tensors' GPU) to the library."""
+    lib().bt_set_stream(C.c_void_p(torch.cuda.current_stream(device).cuda_stream))
 
 
-def _dev_f64(t, shape_last=None):
+def _dev_f64(t, shape_last=None, n=None, device=None, name="tensor"):
+    """A contiguous CUDA float64 tensor of shape [n, shape_last] (or [n])."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
-        raise TypeError("expected a CUDA float64 tensor")
+        raise TypeError(f"{name}: expected a CUDA float64 tensor")
     if shape_last is not None and (t.dim() != 2 or t.shape[1] != shape_last):
-        raise TypeError(f"expected shape [n, {shape_last}]")
+        raise TypeError(f"{name}: expected shape [n, {shape_last}]")
+    if shape_last is None and t.dim() != 1:
+        raise TypeError(f"{name}: expected a 1-D tensor")
+    if n is not None and t.shape[0] != n:
+        raise ValueError(f"{name}: expected {n} rows, got {t.shape[0]}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name}: on {t.device}, the tree is on {device}")
     return t.contiguous()
+
+
+def _dev_out(t, dtype, numel, device, name):
+    """A caller-supplied CUDA output buffer: dtype, device, contiguity, size >= numel."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous CUDA {dtype} tensor")
+    if t.device != device:
+        raise ValueError(f"{name}: on {t.device}, the tree is on {device}")
+    if t.numel() < numel:
+        raise ValueError(f"{name}: needs >= {numel} elements, has {t.numel()}")
+    return t
 
 
 class Tree:
@@ -139,12 +159,16 @@ class Tree:
 
     def __init__(self, pos: torch.Tensor, bucket_size: int = 64, max_empty: float = 0.5,
                  alpha: float | None = None, depth_cap: int | None = None, policy: str = "btree"):
-        pos = _dev_f64(pos, 3)
+        pos = _dev_f64(pos, 3, name="pos")
         self.n = pos.shape[0]
         self.device = pos.device
-        _use_current_stream()
         if policy not in POLICIES:
             raise ValueError(f"policy must be one of {sorted(POLICIES)}")
+        with torch.cuda.device(self.device):
+            self._h = self._build(pos, bucket_size, max_empty, alpha, depth_cap, policy)
+
+    def _build(self, pos, bucket_size, max_empty, alpha, depth_cap, policy):
+        _use_current_stream(self.device)
         if policy != "btree":
             h = lib().bt_build_policy(_ptr(pos), self.n, int(bucket_size), float(max_empty),
                                       0.5 if alpha is None else float(alpha),
@@ -157,12 +181,14 @@ class Tree:
                                   64 if depth_cap is None else int(depth_cap))
         if not h:
             raise BtreeError(lib().bt_last_status(), lib().bt_last_error().decode())
-        self._h = h
+        return h
 
     def free(self):
         h = getattr(self, "_h", None)
         if h:
-            lib().bt_free(h)
+            with torch.cuda.device(self.device):
+                _use_current_stream(self.device)
+                lib().bt_free(h)
             self._h = None
 
     def __del__(self):
@@ -180,33 +206,41 @@ class Tree:
         """Count-only call: (counts int32 [n], offsets int64 [n+1]).  symmetric:
         the max(h_i, h_j) criterion (bt_find_neighbors_sym); ngmax only sets
         the threshold of stats()["rows_over_ngmax"]."""
-        h = _dev_f64(h)
+        h = _dev_f64(h, n=self.n, device=self.device, name="h")
         counts = torch.empty(self.n, dtype=torch.int32, device=self.device)
         offsets = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
-        _use_current_stream()
-        fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
-        _check(fn(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets), None))
+        with torch.cuda.device(self.device):
+            _use_current_stream(self.device)
+            fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
+            _check(fn(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets), None))
         return counts, offsets
 
     def fill(self, h: torch.Tensor, offsets: torch.Tensor, out: torch.Tensor | None = None,
              symmetric: bool = False):
-        h = _dev_f64(h)
+        h = _dev_f64(h, n=self.n, device=self.device, name="h")
+        _dev_out(offsets, torch.int64, self.n + 1, self.device, "offsets")
+        if offsets.numel() != self.n + 1:
+            raise ValueError(f"offsets: expected {self.n + 1} entries, got {offsets.numel()}")
         total = int(offsets[-1].item())
         if out is None:
             out = torch.empty(max(total, 1), dtype=torch.int32, device=self.device)
-        _use_current_stream()
-        fn = lib().bt_fill_neighbors_sym if symmetric else lib().bt_fill_neighbors
-        _check(fn(self._handle(), _ptr(h), _ptr(offsets), _ptr(out), out.numel()))
+        _dev_out(out, torch.int32, 0, self.device, "out")
+        with torch.cuda.device(self.device):
+            _use_current_stream(self.device)
+            fn = lib().bt_fill_neighbors_sym if symmetric else lib().bt_fill_neighbors
+            _check(fn(self._handle(), _ptr(h), _ptr(offsets), _ptr(out), out.numel()))
         return out[:total]
 
     def density(self, h: torch.Tensor, mass: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """SPH density rho [n] fp64 (bt_density: M4 spline, neighbor search fused in)."""
-        h = _dev_f64(h)
-        mass = _dev_f64(mass)
+        h = _dev_f64(h, n=self.n, device=self.device, name="h")
+        mass = _dev_f64(mass, n=self.n, device=self.device, name="mass")
         if out is None:
             out = torch.empty(self.n, dtype=torch.float64, device=self.device)
-        _use_current_stream()
-        _check(lib().bt_density(self._handle(), _ptr(h), _ptr(mass), _ptr(out)))
+        _dev_out(out, torch.float64, self.n, self.device, "out")
+        with torch.cuda.device(self.device):
+            _use_current_stream(self.device)
+            _check(lib().bt_density(self._handle(), _ptr(h), _ptr(mass), _ptr(out)))
         return out
 
     def find_neighbors(self, h: torch.Tensor, ngmax: int | None = None,
@@ -218,7 +252,7 @@ class Tree:
         allocation, then bt_fill_neighbors.  symmetric: the max(h_i, h_j)
         criterion (bt_find_neighbors_sym / bt_fill_neighbors_sym).
         """
-        h = _dev_f64(h)
+        h = _dev_f64(h, n=self.n, device=self.device, name="h")
         if ngmax is None:
             counts, offsets = self.count(h, symmetric)
             return counts, offsets, self.fill(h, offsets, symmetric=symmetric)
@@ -228,9 +262,14 @@ class Tree:
             offsets = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
         if nbr_idx is None:
             nbr_idx = torch.empty(max(self.n * int(ngmax), 1), dtype=torch.int32, device=self.device)
-        _use_current_stream()
-        fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
-        _check(fn(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets), _ptr(nbr_idx)))
+        _dev_out(counts, torch.int32, self.n, self.device, "counts")
+        _dev_out(offsets, torch.int64, self.n + 1, self.device, "offsets")
+        # the library's capacity is n * ngmax slots (BJ): the buffer must hold them
+        _dev_out(nbr_idx, torch.int32, self.n * int(ngmax), self.device, "nbr_idx")
+        with torch.cuda.device(self.device):
+            _use_current_stream(self.device)
+            fn = lib().bt_find_neighbors_sym if symmetric else lib().bt_find_neighbors
+            _check(fn(self._handle(), _ptr(h), int(ngmax), _ptr(counts), _ptr(offsets), _ptr(nbr_idx)))
         return counts, offsets, nbr_idx
 
     def set_partition(self, part: int, nparts: int):
@@ -251,8 +290,9 @@ class Tree:
         lb = torch.empty(max(L, 1), dtype=torch.int64, device=self.device)
         lc = torch.empty(max(L, 1), dtype=torch.int32, device=self.device)
         ld = torch.empty(max(L, 1), dtype=torch.int32, device=self.device)
-        _use_current_stream()
-        _check(lib().bt_tree_order(self._handle(), _ptr(perm), _ptr(lb), _ptr(lc), _ptr(ld)))
+        with torch.cuda.device(self.device):
+            _use_current_stream(self.device)
+            _check(lib().bt_tree_order(self._handle(), _ptr(perm), _ptr(lb), _ptr(lc), _ptr(ld)))
         return perm[:self.n], lb[:L], lc[:L], ld[:L]
 
 
@@ -263,14 +303,29 @@ def build(pos, bucket_size: int = 64, max_empty: float = 0.5, **kw) -> Tree:
 def search_host(pos, h, bucket_size: int = 64, max_empty: float = 0.5, capacity: int | None = None,
                 counts=None, offsets=None, nbr=None):
     """End-to-end on host (preferably pinned) tensors via bt_search_host."""
+    def host(t, dtype, shape, name):
+        if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != dtype or not t.is_contiguous():
+            raise TypeError(f"{name}: expected a contiguous CPU {dtype} tensor")
+        if shape is not None and tuple(t.shape) != shape:
+            raise ValueError(f"{name}: expected shape {shape}, got {tuple(t.shape)}")
+        return t
+    if not isinstance(pos, torch.Tensor) or pos.dim() != 2:
+        raise TypeError("pos: expected a CPU float64 tensor [n, 3]")
     n = pos.shape[0]
+    host(pos, torch.float64, (n, 3), "pos")
+    host(h, torch.float64, (n,), "h")
     if counts is None:
         counts = torch.empty(n, dtype=torch.int32).pin_memory()
     if offsets is None:
         offsets = torch.empty(n + 1, dtype=torch.int64).pin_memory()
     if nbr is None:
         nbr = torch.empty(max(capacity or 1, 1), dtype=torch.int32).pin_memory()
-    cap = nbr.numel() if capacity is None else capacity
+    host(counts, torch.int32, (n,), "counts")
+    host(offsets, torch.int64, (n + 1,), "offsets")
+    host(nbr, torch.int32, None, "nbr")
+    cap = nbr.numel() if capacity is None else int(capacity)
+    if cap > nbr.numel() or cap < 0:
+        raise ValueError(f"capacity {cap} exceeds nbr's {nbr.numel()} elements")
     _use_current_stream()
     _check(lib().bt_search_host(_ptr(pos), _ptr(h), n, int(bucket_size), float(max_empty), _ptr(counts),
                                 _ptr(offsets), _ptr(nbr), cap))

@@ -110,26 +110,40 @@ Phase::~Phase() {
 
 // Device memory: a per-thread caching allocator over cudaMalloc.  Freed blocks
 // are kept and handed out again (best fit, at most 2x the request) to later
-// calls of the same thread, whose work is ordered on the same stream -- the
-// stream-ordered pool (cudaMallocAsync) re-mapped physical memory on every
-// build here (~5 ms per GB), which dominated small steps.  On OOM the cache
-// is released and the allocation retried once.
+// calls of the same thread on the same device, whose work is ordered on the
+// same stream -- the stream-ordered pool (cudaMallocAsync) re-mapped physical
+// memory on every build here (~5 ms per GB), which dominated small steps.
+// Blocks are keyed by the device current at allocation (cudaGetDevice), so a
+// thread that switches devices never receives another GPU's memory.  On OOM
+// the cache is released and the allocation retried once.
 namespace {
+int current_device() {
+    int d = 0;
+    BT_CUDA(cudaGetDevice(&d));
+    return d;
+}
 struct BlockCache {
-    std::multimap<size_t, void *> free_blocks;
-    std::unordered_map<void *, size_t> size_of;
-    size_t cached = 0;
+    std::map<int, std::multimap<size_t, void *>> free_blocks;    // per device
+    std::unordered_map<void *, std::pair<int, size_t>> owner;    // block -> (device, size)
     void release_all() {
         cudaStreamSynchronize(g_stream);
-        for (auto &kv : free_blocks) {
-            cudaFree(kv.second);
-            size_of.erase(kv.second);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (auto &dv : free_blocks) {
+            cudaSetDevice(dv.first);
+            for (auto &kv : dv.second) {
+                cudaFree(kv.second);
+                owner.erase(kv.second);
+            }
+            dv.second.clear();
         }
-        free_blocks.clear();
-        cached = 0;
+        cudaSetDevice(cur);
     }
     ~BlockCache() {
-        for (auto &kv : free_blocks) cudaFree(kv.second);
+        for (auto &dv : free_blocks) {
+            cudaSetDevice(dv.first);
+            for (auto &kv : dv.second) cudaFree(kv.second);
+        }
     }
 };
 BlockCache &block_cache() {
@@ -145,12 +159,13 @@ size_t round_block(size_t bytes) {
 
 void *dmalloc(size_t bytes) {
     BlockCache &C = block_cache();
+    const int dev = current_device();
     const size_t want = round_block(bytes);
-    auto it = C.free_blocks.lower_bound(want);
-    if (it != C.free_blocks.end() && it->first <= 2 * want) {
+    auto &fb = C.free_blocks[dev];
+    auto it = fb.lower_bound(want);
+    if (it != fb.end() && it->first <= 2 * want) {
         void *p = it->second;
-        C.cached -= it->first;
-        C.free_blocks.erase(it);
+        fb.erase(it);
         return p;
     }
     static const bool trace = getenv("BT_TRACE") != nullptr;
@@ -164,27 +179,34 @@ void *dmalloc(size_t bytes) {
     }
     if (trace) {
         double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
-        fprintf(stderr, "[bt] cudaMalloc %zu bytes: %.1f us\n", want, us);
+        fprintf(stderr, "[bt] cudaMalloc %zu bytes on device %d: %.1f us\n", want, dev, us);
     }
     if (e != cudaSuccess) {
         cudaGetLastError();
         throw Error(e == cudaErrorMemoryAllocation ? BT_ERR_OOM : BT_ERR_CUDA,
                     "device allocation of " + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e));
     }
-    C.size_of[p] = want;
+    C.owner[p] = {dev, want};
     return p;
 }
 void dfree(void *p) {
     if (!p) return;
     BlockCache &C = block_cache();
-    auto it = C.size_of.find(p);
-    if (it == C.size_of.end()) {  // allocated by another thread: return it to the driver
+    auto it = C.owner.find(p);
+    if (it == C.owner.end()) {  // allocated by another thread: return it to the driver
         cudaStreamSynchronize(g_stream);
         cudaFree(p);
         return;
     }
-    C.free_blocks.emplace(it->second, p);
-    C.cached += it->second;
+    C.free_blocks[it->second.first].emplace(it->second.second, p);
+}
+
+int num_sms() {
+    static int v[128] = {0};
+    const int dev = current_device();
+    if (dev < 0 || dev >= 128) throw Error(BT_ERR_CUDA, "device ordinal out of range");
+    if (!v[dev]) BT_CUDA(cudaDeviceGetAttribute(&v[dev], cudaDevAttrMultiProcessorCount, dev));
+    return v[dev];
 }
 
 int release_cache() {
@@ -367,7 +389,8 @@ int bt_search_host(const double *pos_h, const double *h_h, int64_t n, int32_t bu
         cudaStream_t st = stream();
         // a side stream carries the copies that do not gate the next kernel:
         // h's upload overlaps the build, counts / offsets go home during the fill
-        static thread_local cudaStream_t side = nullptr;
+        static thread_local std::map<int, cudaStream_t> sides;  // one per device
+        cudaStream_t &side = sides[current_device()];
         if (!side) BT_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
         cudaEvent_t ev_h, ev_c;
         BT_CUDA(cudaEventCreateWithFlags(&ev_h, cudaEventDisableTiming));
@@ -471,6 +494,7 @@ int bt_tree_stats(const bt_tree *t, bt_stats *out) {
     out->list_entries = d.list_entries;
     out->big_units = d.big_units;
     out->rows_over_ngmax = d.rows_over_ngmax;
+    out->mask_words_nonzero = d.mask_words_nz;
     return BT_OK;
 }
 

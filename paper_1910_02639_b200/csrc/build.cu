@@ -22,6 +22,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <cub/device/device_segmented_sort.cuh>
+
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -409,6 +411,10 @@ __device__ __forceinline__ unsigned long long warp_max_key(unsigned long long k)
 
 // One warp per leaf.  rank(e) = #{k in leaf : idx_k < idx_e} (caller indices
 // are distinct), O(m^2 / 32) per leaf: m <= s = 64 in the configurations.
+// Leaves above kBigLeaf particles (only at the depth cap, R14: e.g. many
+// coincident points) get their box here and their order from a segmented
+// radix sort afterwards (big_leaf_*), which keeps the build O(m log m).
+constexpr int kBigLeaf = 1024;
 __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *__restrict__ src, double4 *__restrict__ dst,
                                                                  float4 *__restrict__ dst32, int32_t *__restrict__ perm,
                                                                  const int32_t *__restrict__ leaf_begin,
@@ -489,6 +495,9 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
             if (lane == 0) { leaf_box[6 * L + l] = a; leaf_box[6 * L + 3 + l] = b; }
             c[l] = 0.5 * (a + b);  // leaf centre for the compact fp32 records
         }
+        wmax = max(wmax, m);
+        wover += (m > s) ? 1 : 0;
+        if (m > kBigLeaf) continue;  // ordered by big_leaf_write_kernel
         // canonical order: rank(e) = #{k : idx_k < idx_e}
         for (int32_t e0 = 0; e0 < m; e0 += 32) {
             int32_t e = e0 + lane;
@@ -517,8 +526,6 @@ __global__ void __launch_bounds__(kThreads) leaf_finalize_kernel(const double4 *
                                                __double2float_rn(__dsub_rn(v.z, c[2])), __int_as_float((int)my));
             }
         }
-        wmax = max(wmax, m);
-        wover += (m > s) ? 1 : 0;
     }
     // one atomic per warp (a per-leaf atomic on one address serialises 10^6 updates)
     if (lane == 0 && wmax > 0) {
@@ -575,6 +582,47 @@ __device__ __forceinline__ unsigned spread3(unsigned v) {  // 10 bits -> every t
 
 // per-leaf staging record: centre (the same 0.5 (lo + hi) as the compact
 // records), half-extent, begin, count
+// ---- leaves above kBigLeaf particles: segmented sort by caller index -------
+__global__ void big_leaf_list_kernel(const int32_t *__restrict__ begin, const int32_t *__restrict__ count, int64_t n_leaves,
+                                     int32_t *__restrict__ ids, int32_t *__restrict__ seg_b, int32_t *__restrict__ seg_e,
+                                     int *n_big) {
+    for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n_leaves; L += (int64_t)gridDim.x * blockDim.x)
+        if (count[L] > kBigLeaf) {
+            const int k = atomicAdd(n_big, 1);
+            ids[k] = (int32_t)L;
+            seg_b[k] = begin[L];
+            seg_e[k] = begin[L] + count[L];
+        }
+}
+// keys = caller index, values = position, over each big leaf's positions (one block per leaf)
+__global__ void big_leaf_keys_kernel(const double4 *__restrict__ src, const int32_t *__restrict__ seg_b,
+                                     const int32_t *__restrict__ seg_e, int nbig, int32_t *__restrict__ key,
+                                     int32_t *__restrict__ val) {
+    for (int k = blockIdx.x; k < nbig; k += gridDim.x)
+        for (int32_t p = seg_b[k] + threadIdx.x; p < seg_e[k]; p += blockDim.x) {
+            key[p] = (int32_t)__double_as_longlong(src[p].w);
+            val[p] = p;
+        }
+}
+// records of each big leaf in ascending caller index (compact records relative to its centre)
+__global__ void big_leaf_write_kernel(const double4 *__restrict__ src, const int32_t *__restrict__ ids,
+                                      const int32_t *__restrict__ seg_b, const int32_t *__restrict__ seg_e, int nbig,
+                                      const int32_t *__restrict__ val, const double *__restrict__ leaf_box,
+                                      double4 *__restrict__ dst, float4 *__restrict__ dst32, int32_t *__restrict__ perm) {
+    for (int k = blockIdx.x; k < nbig; k += gridDim.x) {
+        const double *bx = leaf_box + 6 * (int64_t)ids[k];
+        const double c0 = 0.5 * (bx[0] + bx[3]), c1 = 0.5 * (bx[1] + bx[4]), c2 = 0.5 * (bx[2] + bx[5]);
+        for (int32_t p = seg_b[k] + threadIdx.x; p < seg_e[k]; p += blockDim.x) {
+            const double4 v = src[val[p]];
+            const int i = (int)__double_as_longlong(v.w);
+            dst[p] = v;
+            perm[p] = i;
+            dst32[p] = make_float4(__double2float_rn(__dsub_rn(v.x, c0)), __double2float_rn(__dsub_rn(v.y, c1)),
+                                   __double2float_rn(__dsub_rn(v.z, c2)), __int_as_float(i));
+        }
+    }
+}
+
 __global__ void leaf_rec_kernel(const double *__restrict__ box, const int32_t *__restrict__ begin,
                                 const int32_t *__restrict__ count, int64_t nl, LeafRec *__restrict__ out) {
     for (int64_t L = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; L < nl; L += (int64_t)gridDim.x * blockDim.x) {
@@ -699,6 +747,34 @@ struct UnitsOut {
 };
 
 }  // namespace
+
+// Leaves above kBigLeaf particles (depth cap): canonical order by a segmented
+// radix sort of their caller indices (cub), then their records are written.
+void order_big_leaves(TreeDev &t, const double4 *fin, int *dcount) {
+    cudaStream_t st = stream();
+    const int64_t n = t.n;
+    DBuf<int32_t> ids(t.n_leaves), sb(t.n_leaves), se(t.n_leaves);
+    BT_CUDA(cudaMemsetAsync(dcount, 0, sizeof(int), st));
+    big_leaf_list_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)num_sms() * 8), kThreads, 0, st>>>(
+        t.leaf_begin.p, t.leaf_count.p, t.n_leaves, ids.p, sb.p, se.p, dcount);
+    BT_LAUNCH("big_leaf_list");
+    int nbig = 0;
+    read_back({{dcount, &nbig, sizeof(int)}});
+    if (nbig == 0) return;
+    DBuf<int32_t> kin(n), kout(n), vin(n), vout(n);
+    const unsigned gb = (unsigned)std::min<int64_t>(nbig, (int64_t)num_sms() * 8);
+    big_leaf_keys_kernel<<<gb, kThreads, 0, st>>>(fin, sb.p, se.p, nbig, kin.p, vin.p);
+    BT_LAUNCH("big_leaf_keys");
+    size_t tmp_bytes = 0;
+    BT_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, tmp_bytes, kin.p, kout.p, vin.p, vout.p, (int)n, nbig, sb.p,
+                                                se.p, st));
+    DBuf<unsigned char> tmp(tmp_bytes > 0 ? tmp_bytes : 1);
+    BT_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp.p, tmp_bytes, kin.p, kout.p, vin.p, vout.p, (int)n, nbig, sb.p,
+                                                se.p, st));
+    big_leaf_write_kernel<<<gb, kThreads, 0, st>>>(fin, ids.p, sb.p, se.p, nbig, vout.p, t.leaf_box.p, t.rec.p,
+                                                   t.rec32.p, t.perm.p);
+    BT_LAUNCH("big_leaf_write");
+}
 
 // ---------------------------------------------------------------------------
 // Host driver (K12): level loop.  Reads back a few scalars per level (total
@@ -917,6 +993,11 @@ void build_tree(TreeDev &t, const double *pos) {
         leaf_finalize_kernel<<<grid_for(t.n_leaves * 32, kThreads, (int64_t)sms * 32), kThreads, 0, st>>>(
             fin.p, t.rec.p, t.rec32.p, t.perm.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
         BT_LAUNCH("leaf_finalize");
+        {
+            unsigned long long ml = 0;
+            read_back({{dstat.p + 1, &ml, sizeof(ml)}});
+            if (ml > (unsigned long long)kBigLeaf) order_big_leaves(t, fin.p, dflags.p + 2);
+        }
         t.leaf_rec.alloc(t.n_leaves);
         leaf_rec_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
             t.leaf_box.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_rec.p);

@@ -179,6 +179,7 @@ struct TreeDev {
     bool rec_valid = false;    // arena holds the test pass of (rec_h, rec_hsum, rec_exact)
     const double *rec_h = nullptr;
     long long rec_hsum = 0;
+    long long rec_csum = 0;    // checksum of the recorded pass's counts (fill-only offsets validation)
     int rec_exact = 0;
     bool rec_tp = false;       // the candidate records hold tree positions (symmetric pass)
     DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
@@ -190,7 +191,7 @@ struct TreeDev {
 
     int64_t total_pairs = 0, max_count = 0, staged = 0, loaded = 0, tests = 0, exact_tests = 0;
     int64_t ngmax = 512, rows_over_ngmax = 0;  // the last count's ngmax and its rows above it
-    int64_t mask_words = 0, cand_slots = 0, list_entries = 0, big_units = 0;
+    int64_t mask_words = 0, cand_slots = 0, list_entries = 0, big_units = 0, mask_words_nz = 0;
 };
 
 // Build (build.cu) and search (walk.cu) entry points.
@@ -264,15 +265,7 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return m;
 }
 
-inline int num_sms() {
-    static int v = 0;
-    if (!v) {
-        int dev;
-        BT_CUDA(cudaGetDevice(&dev));
-        BT_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
-    }
-    return v;
-}
+int num_sms();  // SM count of the current device (abi.cu; cached per device)
 
 inline unsigned grid_for(int64_t n, int threads, int64_t max_blocks = 1 << 20) {
     int64_t b = (n + threads - 1) / threads;

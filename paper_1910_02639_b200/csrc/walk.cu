@@ -69,7 +69,11 @@ enum {
     C_NEEDM = 15,    // sum over units of ceil(loaded / 64) * nq (bound on mask words)
     C_WORK5 = 16,    // unit counter (symmetric-criterion pass)
     C_OVER = 17,     // rows with more neighbors than the call's ngmax
-    C_N = 18
+    C_CSUM = 18,     // checksum of the test pass's counts: sum of counts[i] (2i + 1) mod 2^64
+    C_OSUM = 19,     // the same checksum of a fill-only call's offsets differences
+    C_OBAD = 20,     // a fill-only call's offsets are not a valid scan of the counts
+    C_NZW = 21,      // recorded mask words with at least one neighbor
+    C_N = 22
 };
 
 struct WalkArgs {
@@ -292,13 +296,16 @@ __device__ __forceinline__ void unit_box(const WalkArgs &a, const int4 &UU, int 
     Ru = warp_max(r);
 }
 
-// x / d for 0 <= x < 2^20, d >= 1 (inv = fl32(1/d)): the fp32 quotient is off
-// by at most one, fixed by one remainder test
-__device__ __forceinline__ int small_div(int x, int d, float inv) {
-    int q = __float2int_rz(__fmul_rn(__int2float_rn(x), inv));
-    const int r = x - q * d;
-    q += (r < 0) ? -1 : ((r >= d) ? 1 : 0);
-    return q;
+// x / d for d >= 1 (inv = fl32(1/d)): for x < 2^22 x is exact in fp32 and the
+// rounded quotient is within one of the true one, fixed by one remainder
+// test; larger x (a range of >= 2^22 cells of one node: huge b at tiny s,
+// ADVICE r1) takes the exact integer division.
+__device__ __forceinline__ unsigned small_div(unsigned x, unsigned d, float inv) {
+    if (x >= (1u << 22)) return x / d;
+    int q = __float2int_rz(__fmul_rn(__uint2float_rn(x), inv));
+    const int r = (int)x - q * (int)d;
+    q += (r < 0) ? -1 : ((r >= (int)d) ? 1 : 0);
+    return (unsigned)q;
 }
 
 // Persistent warps claim work units in batches of consecutive (Morton-ordered,
@@ -431,12 +438,13 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
                     bool is_leaf = false, is_node = false;
                     int32_t code = -1;
                     if (g < T) {
-                        const int local = (int)(g - ostart);
-                        const int qx = small_div(local, onx, 1.0f / (float)onx);
-                        const int qy = small_div(qx, ony, 1.0f / (float)ony);
-                        const int cx = ox + (local - qx * onx);
-                        const int cy = oy + (qx - qy * ony);
-                        const int cz = oz + qy;
+                        // cell offset inside the node's range (< b^3 < 2^32 for n < 2^31)
+                        const unsigned local = (unsigned)(g - ostart);
+                        const unsigned qx = small_div(local, onx, 1.0f / (float)onx);
+                        const unsigned qy = small_div(qx, ony, 1.0f / (float)ony);
+                        const int cx = ox + (int)(local - qx * onx);
+                        const int cy = oy + (int)(qx - qy * ony);
+                        const int cz = oz + (int)qy;
                         const long long j = cx + (long long)cy * ob + (long long)cz * ob * ob;  // Eq. 3
                         code = a.cells[ocb + j];
                         is_leaf = code >= 0;
@@ -540,7 +548,7 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
 struct UnitSm {                     // per-warp unit state (shared memory)
     long long cand_base, mask_base;  // the unit's record bases
     Slab cs, ms;                     // the warp's candidate / mask slabs
-    long long tests, exact, staged, loaded;  // warp totals
+    long long tests, exact, staged, loaded, nzw;  // warp totals
     float4 *scr;                     // the warp's staging scratch (read from here: not rematerialised)
     int32_t *cand_ptr;               // the unit's candidate-index records (a.cands + cand_base)
     double c[3], E;                  // unit centre, coordinate bound (L4)
@@ -728,6 +736,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     // for the fill pass (chunk kk = us0 / 64 + k of the unit) straight from
     // the lanes that own the queries
     int inc[2] = {0, 0};
+    int nzw = 0;  // non-zero mask words of this lane's queries
     unsigned long long *const dst =
         (!kDensity && S.u.rec_ok) ? a.masks + S.u.mask_base + (long long)(us0 >> 6) * nq : nullptr;
 #pragma unroll
@@ -741,6 +750,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
                 else m1 &= ~(1ull << (sl - 64));
             }
             inc[h] = __popcll(m0) + __popcll(m1);
+            nzw += (m0 != 0ull) + (m1 != 0ull);
             if constexpr (kDensity) {
                 S.mask[0][q] = m0;
                 S.mask[1][q] = m1;
@@ -785,9 +795,11 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
         }
         __syncwarp();
     }
+    nzw = (int)__reduce_add_sync(0xffffffffu, (unsigned)nzw);
     if (lane == 0) {
         S.u.tests += (long long)n * nq;
         S.u.exact += exact;
+        S.u.nzw += nzw;
     }
     __syncwarp();
     return make_int2(inc[0], inc[1]);
@@ -903,10 +915,11 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         S.u.scr = a.scratch + gwarp * kScratch;
         S.u.cs = Slab();
         S.u.ms = Slab();
-        S.u.tests = S.u.exact = S.u.staged = S.u.loaded = 0;
+        S.u.tests = S.u.exact = S.u.staged = S.u.loaded = S.u.nzw = 0;
     }
     __syncwarp();
     WorkBatch wb;
+    unsigned long long csum = 0;  // checksum of this lane's counts (fill-only offsets validation)
     for (;;) {
         const long long uid = next_unit(wb, &a.ctr[C_WORK3], a.n_units, 1, lane);
         if (uid >= a.n_units) break;
@@ -1099,8 +1112,14 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                 }
             }
         } else {
-            if (lane < nq) a.counts[qo[0]] = cnt0;
-            if (lane + 32 < nq) a.counts[qo[1]] = cnt1;
+            if (lane < nq) {
+                a.counts[qo[0]] = cnt0;
+                csum += (unsigned long long)cnt0 * (2ull * (unsigned)qo[0] + 1ull);
+            }
+            if (lane + 32 < nq) {
+                a.counts[qo[1]] = cnt1;
+                csum += (unsigned long long)cnt1 * (2ull * (unsigned)qo[1] + 1ull);
+            }
         }
         __syncwarp();
         if (lane == 0) {
@@ -1116,7 +1135,10 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         }
         __syncwarp();
     }
+    for (int d = 16; d; d >>= 1) csum += __shfl_xor_sync(0xffffffffu, csum, d);
     if (lane == 0) {
+        if (!kDensity) atomicAdd((unsigned long long *)&a.ctr[C_CSUM], csum);
+        atomicAdd((unsigned long long *)&a.ctr[C_NZW], (unsigned long long)S.u.nzw);
         atomicAdd((unsigned long long *)&a.ctr[C_TESTS], (unsigned long long)S.u.tests);
         atomicAdd((unsigned long long *)&a.ctr[C_EXACT], (unsigned long long)S.u.exact);
         atomicAdd((unsigned long long *)&a.ctr[C_STAGED], (unsigned long long)S.u.staged);
@@ -1125,13 +1147,19 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
 }
 
 // ---------------------------------------------------------------------------
-// Fill pass: replay the recorded masks into the CSR rows.  Per unit, rounds
+// Fill pass (A13, Alg. 2 "Add q to NeighborsOf(p)" P:294): replay the
+// recorded masks into the CSR rows.  (Bounded by the DRAM cost of writing
+// rows at random CSR positions: tools/probe_csr.py measured a plain
+// warp-per-row writer of the same rows at 8.7 ms of this pass's 11.1 ms at
+// cfg 5; fewer instructions per mask word did not
+// shorten it.)  Per unit, rounds
 // of up to kFillChunks (6) chunks: the chunks' candidate indices in registers (chunk k,
 // lane l -> slots 64k + l, 64k + 32 + l), their masks in shared memory; for
 // each (query, chunk) mask word __popc(mask & lanemask_lt) gives each
 // neighbor's slot in the query's row (row order unspecified, R15).
 // ---------------------------------------------------------------------------
 constexpr int kFillWarps = kFillThreads / 32;
+constexpr int kCsrThreads = kFillThreads;
 
 struct FillSmem {
     int32_t *row[kQ];                            // next write address of each query's row
@@ -1377,6 +1405,25 @@ __global__ void max_count_kernel(const int32_t *c, int64_t n, int64_t ngmax, lon
     }
 }
 
+// A fill-only call's offsets must be the exclusive scan of the counts of the
+// recorded test pass (else rows would overlap): offsets[0] = 0, differences
+// >= 0 and, when the counts are at hand (c1 [+ c2]), equal to them; the
+// checksum sum_i d_i (2i + 1) mod 2^64 is compared with the walk's C_CSUM.
+__global__ void check_offsets_kernel(const int64_t *__restrict__ off, int64_t n, const int32_t *__restrict__ c1,
+                                     const int32_t *__restrict__ c2, long long *ctr) {
+    unsigned long long s = 0;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t d = off[i + 1] - off[i];
+        bad = bad || d < 0 || (i == 0 && off[0] != 0);
+        if (c1) bad = bad || d != (int64_t)c1[i] + (c2 ? (int64_t)c2[i] : 0);
+        s += (unsigned long long)d * (2ull * (unsigned long long)i + 1ull);
+    }
+    for (int d = 16; d; d >>= 1) s += __shfl_xor_sync(0xffffffffu, s, d);
+    if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long *)&ctr[C_OSUM], s);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr((int *)&ctr[C_OBAD], 1);
+}
+
 thread_local int g_exact_only = 0;
 
 }  // namespace
@@ -1396,7 +1443,7 @@ __global__ void gather_m_kernel(const int32_t *__restrict__ perm, const double *
 }
 
 struct Grids {
-    unsigned d, w, f, big;
+    unsigned d, w, f, big, s;
 };
 
 template <bool kDensity>
@@ -1409,7 +1456,8 @@ Grids walk_grids() {
     };
     return Grids{grid_of((const void *)desc_kernel<false>, kDescThreads),
                  grid_of((const void *)walk_kernel<kDensity, false>, kWalkThreads),
-                 grid_of((const void *)fill_kernel<false>, kFillThreads), (unsigned)std::min(sms, 32)};
+                 grid_of((const void *)fill_kernel<false>, kCsrThreads), (unsigned)std::min(sms, 32),
+                 grid_of((const void *)sym_kernel<false>, kFillThreads)};
 }
 
 // h in tree order (validated) + its checksum
@@ -1469,6 +1517,24 @@ WalkArgs walk_args(TreeDev &t, const Grids &g) {
 
 void read_counters(TreeDev &t, long long *hc) { read_back({{t.counters.p, hc, C_N * sizeof(long long)}}); }
 void zero_counter(TreeDev &t, int c) { BT_CUDA(cudaMemsetAsync(t.counters.p + c, 0, sizeof(int64_t), stream())); }
+
+// Fill-only calls: the caller's offsets must be the scan of the
+// recorded test pass's counts -- compared exactly when the counts are at hand
+// (c1 [+ c2]) and by the checksum of the walk (C_CSUM) otherwise.
+void check_offsets(TreeDev &t, const int64_t *offsets, const int32_t *c1, const int32_t *c2, bool use_sum,
+                   const char *who) {
+    cudaStream_t st = stream();
+    zero_counter(t, C_OSUM);
+    zero_counter(t, C_OBAD);
+    check_offsets_kernel<<<grid_for(t.n, 256, (int64_t)num_sms() * 8), 256, 0, st>>>(offsets, t.n, c1, c2,
+                                                                                     (long long *)t.counters.p);
+    BT_LAUNCH("check_offsets");
+    long long osum = 0, obad = 0;
+    read_back({{t.counters.p + C_OSUM, &osum, sizeof(long long)}, {t.counters.p + C_OBAD, &obad, sizeof(long long)}});
+    if (obad || (use_sum && osum != t.rec_csum))
+        throw Error(BT_ERR_ARG, std::string(who) + ": offsets are not the exclusive scan of this tree's neighbor counts "
+                                "for this h (and partition): call the count pass again");
+}
 
 // A10: candidate-leaf lists of all units; the leaf-list arena is estimated
 // (grown and redone on overflow).  Leaves the counters in hc.
@@ -1534,6 +1600,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     auto zero = [&](int c) { zero_counter(t, c); };
 
     DBuf<int32_t> tmp_counts;
+    const int32_t *cnt_now = nullptr;  // counts of a test pass run by this call
     if (run_test) {
         int32_t *cnt = counts;
         if (!cnt) {
@@ -1557,7 +1624,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             a.mask_cap = (long long)t.arena_masks.n;
             t.scratch.reserve(warps_w * kScratch, 0);
             a.scratch = t.scratch.p;
-            for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero(c);
+            for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT, C_CSUM, C_NZW}) zero(c);
             {
                 Phase ph("search.count");
                 if (cand_tp)
@@ -1570,6 +1637,7 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             const bool fits = hc[C_CAND] <= a.cand_cap && hc[C_MASK] <= a.mask_cap;
             if (!fits) throw Error(BT_ERR_CUDA, "bt_find_neighbors: internal: walk arena bound exceeded");
             t.rec_valid = true;
+            t.rec_csum = hc[C_CSUM];
             t.rec_h = h;
             t.rec_hsum = hsum;
             t.rec_exact = g_exact_only;
@@ -1581,6 +1649,8 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         t.exact_tests = hc[C_EXACT];
         t.mask_words = hc[C_MASK];
         t.cand_slots = hc[C_CAND];
+        t.mask_words_nz = hc[C_NZW];
+        cnt_now = cnt;
         if (count_pass) {
             DBuf<long long> dtot(1);
             Phase ph("search.scan");
@@ -1607,15 +1677,16 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         throw Error(BT_ERR_CAPACITY, "bt_find_neighbors: " + std::to_string(total) + " neighbor pairs exceed capacity " +
                                          std::to_string(capacity));
     if (!t.rec_valid) throw Error(BT_ERR_CUDA, "bt_find_neighbors: internal: no recorded test pass");
+    if (!count_pass) check_offsets(t, offsets, cnt_now, nullptr, true, "bt_fill_neighbors");
     a.masks = t.arena_masks.p;
     a.cands = t.arena_cands.p;
     zero(C_WORK2);
     {
         Phase ph("search.fill");
         if (t.rec_tp)
-            fill_kernel<true><<<g.f, kFillThreads, 0, st>>>(a);
+            fill_kernel<true><<<g.f, kCsrThreads, 0, st>>>(a);
         else
-            fill_kernel<false><<<g.f, kFillThreads, 0, st>>>(a);
+            fill_kernel<false><<<g.f, kCsrThreads, 0, st>>>(a);
         BT_LAUNCH("walk_fill");
     }
     BT_CUDA(cudaStreamSynchronize(st));
@@ -1660,7 +1731,7 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
         zero_counter(t, C_WORK5);
         {
             Phase ph("search.sym_count");
-            sym_kernel<false><<<g.f, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
+            sym_kernel<false><<<g.s, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
             BT_LAUNCH("sym_count");
         }
         t.sym_valid = true;
@@ -1691,6 +1762,7 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
     if (total > capacity)
         throw Error(BT_ERR_CAPACITY, "bt_find_neighbors_sym: " + std::to_string(total) +
                                          " neighbor pairs exceed capacity " + std::to_string(capacity));
+    if (!count_pass) check_offsets(t, offsets, t.sym_g.p, t.sym_x.p, false, "bt_fill_neighbors_sym");
     WalkArgs a = walk_args(t, g);
     a.masks = t.arena_masks.p;
     a.cands = t.arena_cands.p;
@@ -1702,12 +1774,12 @@ void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *o
     BT_CUDA(cudaMemsetAsync(t.sym_x.p, 0, n * sizeof(int32_t), st));  // append cursors
     {
         Phase ph("search.fill");
-        fill_kernel<true><<<g.f, kFillThreads, 0, st>>>(a);  // symmetric pass: tree-position records
+        fill_kernel<true><<<g.f, kCsrThreads, 0, st>>>(a);  // symmetric pass: tree-position records
         BT_LAUNCH("walk_fill");
     }
     {
         Phase ph("search.sym_fill");
-        sym_kernel<true><<<g.f, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
+        sym_kernel<true><<<g.s, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
         BT_LAUNCH("sym_fill");
     }
     t.sym_valid = false;  // the cursors overwrote the extra counts
@@ -1747,7 +1819,7 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
     const long long warps_w = (long long)g.w * (kWalkThreads / 32);
     t.scratch.reserve(warps_w * kScratch, 0);
     a.scratch = t.scratch.p;
-    for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT}) zero_counter(t, c);
+    for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT, C_CSUM, C_NZW}) zero_counter(t, c);
     {
         Phase ph("density.walk");
         walk_kernel<true, false><<<g.w, kWalkThreads, 0, st>>>(a);

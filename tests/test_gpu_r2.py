@@ -1,0 +1,114 @@
+"""GPU tests added in round 2: robustness fixes and the tree-shape
+pins of the oracle (Eq. 4 tie, depth-first ascending-j leaf order) carried to
+the CUDA build.  Run with ``pytest -m gpu`` on a B200."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from paper_1910_02639_b200 import datagen  # noqa: E402
+
+from test_gpu_parity import DEV, assert_same, assert_same_tree, gpu_run  # noqa: E402
+from test_oracle_pins import _tie_set  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1910_02639_b200 as P
+    P.lib()
+    return P
+
+
+def test_big_coincident_leaves(P, oracle):
+    """Clusters of 1500 / 2600 / 4100 identical points (R14: depth-cap leaves
+    above the warp-rank limit, ordered by the segmented sort) in a uniform
+    background: tree and neighbor sets equal the oracle's."""
+    rng = np.random.default_rng(11)
+    parts = [rng.random((20000, 3))]
+    for m, c in ((1500, 0.2), (2600, 0.5), (4100, 0.8)):
+        parts.append(np.tile([[c, c, c]], (m, 1)))
+    pos = np.ascontiguousarray(np.concatenate(parts)[rng.permutation(20000 + 8200)])
+    h = np.full(len(pos), 0.01)
+    for s in (8, 64):
+        t, gpu = gpu_run(P, pos, h, s=s, depth_cap=20)
+        ot = oracle.Tree(pos, s, depth_cap=20)
+        assert_same_tree(t, ot)
+        assert_same(gpu, ot.neighbors(h))
+        assert t.stats()["max_leaf"] == 4100
+
+
+def test_fill_only_rejects_foreign_offsets(P):
+    """A fill-only call whose offsets are not the scan of this tree's counts
+    for this h (another h, another partition) is refused with BT_ERR_ARG
+    instead of writing rows past their ends."""
+    pos, h = datagen.make_config(2, n=40_000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd = torch.from_numpy(h).to(DEV)
+    hd_big = hd * 1.3
+    _, off_small = t.count(hd)
+    c_big, off_big = t.count(hd_big)
+    # offsets of the smaller h with the larger h's record: counts grew
+    with pytest.raises(P.BtreeError) as e:
+        t.fill(hd_big, off_small, out=torch.empty(int(off_big[-1]), dtype=torch.int32, device=DEV))
+    assert e.value.code == 1
+    # after a rerun of the test pass (h changed at the same pointer) as well
+    hd2 = hd.clone()
+    t.count(hd2)
+    hd2.mul_(1.3)
+    with pytest.raises(P.BtreeError) as e:
+        t.fill(hd2, off_small, out=torch.empty(int(off_big[-1]), dtype=torch.int32, device=DEV))
+    assert e.value.code == 1
+    # whole-search offsets on a partitioned tree
+    _, off_all = t.count(hd)
+    t.set_partition(0, 2)
+    with pytest.raises(P.BtreeError) as e:
+        t.fill(hd, off_all)
+    assert e.value.code == 1
+    # the matching offsets still work
+    t.set_partition(0, 1)
+    c, off = t.count(hd)
+    nb = t.fill(hd, off)
+    assert nb.numel() == int(off[-1])
+    # symmetric fill-only with gather offsets (counts differ where h varies)
+    cs, offs = t.count(hd, symmetric=True)
+    assert int(offs[-1]) > int(off[-1])
+    with pytest.raises(P.BtreeError) as e:
+        t.fill(hd, off, out=torch.empty(int(offs[-1]), dtype=torch.int32, device=DEV), symmetric=True)
+    assert e.value.code == 1
+
+
+def test_eq4_tie_and_leaf_order_on_gpu(P, oracle):
+    """The oracle pins' hand-derived trees (test_oracle_pins: Eq. 4 tie r = beta
+    halves; depth-first ascending-j leaf order) built by the CUDA path."""
+    pos = _tie_set()
+    h = np.full(len(pos), 0.3)
+    for beta in (0.5, 0.5 + 2.0 ** -20, 0.5 - 2.0 ** -20):
+        t, gpu = gpu_run(P, pos, h, s=8, beta=beta)
+        ot = oracle.Tree(pos, 8, beta)
+        assert_same_tree(t, ot)
+        assert_same(gpu, ot.neighbors(h))
+    assert P.build(torch.from_numpy(pos).to(DEV), 8, 0.5).stats()["root_b"] == 2
+    assert P.build(torch.from_numpy(pos).to(DEV), 8, 0.5 + 2.0 ** -20).stats()["root_b"] == 4
+
+
+def test_binding_rejects_bad_arguments(P):
+    pos, h = datagen.make_config(1, n=2000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    with pytest.raises(TypeError):
+        t.count(torch.from_numpy(h))                                   # host tensor
+    with pytest.raises(TypeError):
+        t.count(torch.from_numpy(h).to(DEV).float())                   # float32
+    with pytest.raises(ValueError):
+        t.count(torch.from_numpy(h[:-1]).to(DEV))                      # wrong length
+    with pytest.raises(ValueError):
+        t.find_neighbors(torch.from_numpy(h).to(DEV), 4,
+                         nbr_idx=torch.empty(10, dtype=torch.int32, device=DEV))  # below n * ngmax
+    with pytest.raises(TypeError):
+        P.build(torch.from_numpy(pos).to(DEV).reshape(-1))              # not [n, 3]
+    with pytest.raises(ValueError):
+        P.search_host(torch.from_numpy(pos), torch.from_numpy(h), capacity=100,
+                      nbr=torch.empty(10, dtype=torch.int32))          # capacity above the buffer

@@ -466,3 +466,67 @@ def test_k2_trees_same_neighbors(oracle):
     ref = oracle.brute_force(flat, h)
     for pol in ("btree", "btree2d", "quadtree"):
         _assert_same(oracle.Tree(flat, 16, 0.5, policy=pol).neighbors(h), ref)
+
+
+# ---- Eq. 4 tie r = beta (reading R3: the prose "until r < beta", P:254-256,
+# so a ratio equal to beta halves) ---------------------------------------------
+def _tie_set():
+    """A 4^3 lattice of sites (i + 0.5), s = 8 (alpha s = 4): 32 sites carry 5
+    coincident points (over-full), 32 carry 2 (under-full), n = 224.  Eq. 1
+    gives b = 4 (3^3 8 = 216 < 224 <= 512); every site is its own root cell
+    (cell = i), so Eq. 4 gives r = 32 / 64 = 0.5 exactly."""
+    pts = []
+    for k in range(64):
+        i, j, l = k % 4, (k // 4) % 4, k // 16
+        mult = 5 if (i + j + l) % 2 == 0 else 2  # 32 even-parity sites, 32 odd
+        pts += [[i + 0.5, j + 0.5, l + 0.5]] * mult
+    return np.array(pts, dtype=np.float64)
+
+
+def test_eq4_tie_halves(oracle):
+    pos = _tie_set()
+    assert len(pos) == 224 and oracle.branching_factor(224, 8) == 4
+    # r = beta = 0.5: halve (4 -> 2); the root then holds 28 points per cell (r = 0)
+    st = oracle.Tree(pos, 8, 0.5).stats()
+    assert st["root_b"] == 2 and st["halvings"] == 1
+    # beta one ulp-scale step above r: r < beta, b stays 4 and every site is a leaf
+    st = oracle.Tree(pos, 8, 0.5 + 2.0 ** -20).stats()
+    assert st["root_b"] == 4 and st["halvings"] == 0 and st["leaves"] == 64 and st["depth"] == 1
+    # beta below r: halves as well
+    assert oracle.Tree(pos, 8, 0.5 - 2.0 ** -20).stats()["root_b"] == 2
+
+
+# ---- depth-first leaf order, children in ascending j (Sec. IV-E P:491, the
+# reorder along the tree-walk curve; Eq. 3 j = c1 + c2 b + c3 b^2) -------------
+def test_leaf_order_depth_first_ascending_j(oracle):
+    """4^3 lattice at (i + 0.5) without root cell 2's eight sites, plus eight
+    points at (site + 0.1) inside root cell 5: n = 64, s = 8 -> b = 2 (Eq. 1),
+    r = 1/8 (only cell 2 empty).  Root cells 0, 1, 3, 4, 6, 7 are leaves of 8;
+    cell 5 (16 points) splits into 2^3 sub-cells of 2 (a lattice site and its
+    +0.1 partner; sub-cell faces lie at 2.75 / 1.25 / 2.75 of the cell box
+    [2, 3.5] x [0.5, 2] x [2, 3.5]).  The expected order, worked out here from
+    the geometry alone: cells 0, 1, 3, 4, then cell 5's sub-cells in ascending
+    sub-j, then cells 6, 7; inside a leaf ascending input index."""
+    def root_cell(p):
+        c = [int(v - 0.5) // 2 for v in p]   # site index i // 2 on every axis
+        return c[0] + 2 * c[1] + 4 * c[2]
+    sites = [[i + 0.5, j + 0.5, l + 0.5] for l in range(4) for j in range(4) for i in range(4)]
+    sites = [s for s in sites if root_cell(s) != 2]
+    extra = [[s[0] + 0.1, s[1] + 0.1, s[2] + 0.1] for s in sites if root_cell(s) == 5]
+    pos = np.array(sites + extra, dtype=np.float64)
+    assert len(pos) == 64
+    t = oracle.Tree(pos, 8, 0.5)
+    st = t.stats()
+    assert st["root_b"] == 2 and st["halvings"] == 0 and st["depth"] == 2
+    perm, lb, lc, ld = t.order()
+
+    def sub_cell(p):  # cell 5's sub-cells: faces at x 2.75, y 1.25, z 2.75
+        return int(p[0] > 2.75) + 2 * int(p[1] > 1.25) + 4 * int(p[2] > 2.75)
+    in_cell = [root_cell(p) for p in pos]  # (the +0.1 partners stay in their site's cell)
+    expect = [(1, [k for k in range(64) if in_cell[k] == j]) for j in (0, 1, 3, 4)]
+    expect += [(2, [k for k in range(64) if in_cell[k] == 5 and sub_cell(pos[k]) == sj]) for sj in range(8)]
+    expect += [(1, [k for k in range(64) if in_cell[k] == j]) for j in (6, 7)]
+    assert len(lc) == len(expect)
+    for leaf, (depth, members) in enumerate(expect):
+        assert ld[leaf] == depth
+        assert list(perm[lb[leaf]:lb[leaf] + lc[leaf]]) == sorted(members), leaf
