@@ -120,7 +120,9 @@ def weak_value(n_per_rank: int, ws: int, ms: float) -> float:
 
 def config_block(cfg, n, ws, mode="subdomain"):
     nn = n if n is not None else datagen.FULL_N[cfg]
-    par = f"sub-domain x{ws}" if mode == "subdomain" else f"replicated tree, units sharded x{ws} (pos/h broadcast per step)"
+    par = (f"replicas only: {ws} independent sub-domains (one full cfg-size particle set per GPU, no split of one "
+           f"set; --mode replicated splits one set)" if mode == "subdomain"
+           else f"one particle set split over {ws} GPUs: replicated tree, work units sharded (pos/h broadcast per step)")
     return {"workload": (f"BASELINE.json configs[{cfg - 1}] (cfg {cfg}): {WORKLOADS[cfg]}"
                          + ("" if n is None else f" [n overridden to {n}: not a bench line]")),
             ("N_per_gpu" if mode == "subdomain" else "N_total"): nn, "bucket_size": datagen.BUCKET_SIZE,
