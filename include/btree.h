@@ -122,7 +122,10 @@ int bt_find_neighbors(const bt_tree *t, const double *h, int32_t ngmax, int32_t 
  * bt_fill_neighbors -- the fill pass alone, using offsets from a previous
  * bt_find_neighbors call on the same tree and the same h (e.g. count-only,
  * then an exactly sized buffer).  capacity = number of int32 slots of nbr_idx;
- * BT_ERR_CAPACITY if offsets[n] > capacity (nothing written).
+ * BT_ERR_CAPACITY if offsets[n] > capacity (nothing written); BT_ERR_ARG if
+ * offsets are not the exclusive scan of this tree's counts for this h and
+ * partition (checked exactly when the count pass is redone, else by a
+ * checksum of the recorded counts; nothing written).
  */
 int bt_fill_neighbors(const bt_tree *t, const double *h, const int64_t *offsets,
                       int32_t *nbr_idx, int64_t capacity);
@@ -155,14 +158,16 @@ int bt_density(const bt_tree *t, const double *h, const double *mass, double *rh
  * SPEC S:273; reading R22 in DESIGN.md): j != i is a neighbor of i iff
  *   ((dx*dx + dy*dy) + dz*dz) < (2 max(h_i, h_j)) * (2 max(h_i, h_j))
  * in fp64 (no FMA), dx = x_i - x_j.  Equivalently N_sym(i) = N(i) u
- * {j : i in N(j)} with N the gather sets of bt_find_neighbors, which is how it
- * is computed: the gather walk, then a pass over its recorded masks that adds
- * every one-sided pair to the other row.  The relation is symmetric.
- * Arguments, layouts, ownership, synchrony, row order (unspecified), the
- * count-only call (nbr_idx NULL) and the errors are those of
- * bt_find_neighbors (capacity n*ngmax; BT_ERR_CAPACITY leaves counts and
- * offsets valid and nbr_idx untouched).  Uses internal device memory of
- * 2 n int32 + (n+1) int64 besides the gather pass's.
+ * {j : i in N(j)} with N the gather sets of bt_find_neighbors.  It is
+ * searched from the query side in one walk: the descent and culls use
+ * max(R'_i, R'(h_max)) with h_max the largest h of each node / leaf, and
+ * every pair is tested against both thresholds (DESIGN.md lemma L4s).  The
+ * relation is symmetric.  Arguments, layouts, ownership, synchrony, row
+ * order (unspecified), the count-only call (nbr_idx NULL), partitions
+ * (bt_set_partition) and the errors are those of bt_find_neighbors
+ * (capacity n*ngmax; BT_ERR_CAPACITY leaves counts and offsets valid and
+ * nbr_idx untouched).  Uses internal device memory of (leaves + nodes) fp64
+ * besides the gather pass's.
  */
 int bt_find_neighbors_sym(const bt_tree *t, const double *h, int32_t ngmax, int32_t *counts,
                           int64_t *offsets, int32_t *nbr_idx);
@@ -171,7 +176,9 @@ int bt_find_neighbors_sym(const bt_tree *t, const double *h, int32_t ngmax, int3
  * bt_fill_neighbors_sym -- the fill of bt_find_neighbors_sym alone, with the
  * offsets of a previous symmetric count on the same tree and h (the count
  * pass is reused when nothing ran in between, else redone).  capacity =
- * int32 slots of nbr_idx; BT_ERR_CAPACITY if offsets[n] > capacity.
+ * int32 slots of nbr_idx; BT_ERR_CAPACITY if offsets[n] > capacity;
+ * BT_ERR_ARG if offsets are not the scan of this tree's symmetric counts for
+ * this h and partition.
  */
 int bt_fill_neighbors_sym(const bt_tree *t, const double *h, const int64_t *offsets,
                           int32_t *nbr_idx, int64_t capacity);
@@ -186,8 +193,8 @@ int bt_fill_neighbors_sym(const bt_tree *t, const double *h, const int64_t *offs
  * bt_find_neighbors / bt_fill_neighbors return counts[i] = |N(i)| and row i
  * for the particles of the part and counts 0 (empty rows) for all others, so
  * the CSR sizes to the part; bt_density writes rho only for the part's
- * particles.  The symmetric criterion needs the whole tree (BT_ERR_ARG when
- * nparts > 1).  nparts = 1 restores the whole tree.  BT_ERR_ARG for
+ * particles; bt_find_neighbors_sym the part's symmetric rows.  nparts = 1
+ * restores the whole tree.  BT_ERR_ARG for
  * nparts < 1 or part outside [0, nparts).  No device work.
  */
 int bt_set_partition(bt_tree *t, int32_t part, int32_t nparts);

@@ -329,7 +329,7 @@ int bt_find_neighbors_sym(const bt_tree *tc, const double *h, int32_t ngmax, int
         Phase ph("search.total");
         const int64_t cap = t->t.n * (int64_t)ngmax;
         t->t.ngmax = ngmax;
-        find_neighbors_sym(t->t, h, counts, offsets, nbr_idx, cap, true, nbr_idx != nullptr);
+        find_neighbors(t->t, h, counts, offsets, nbr_idx, cap, true, nbr_idx != nullptr, true);
     });
 }
 
@@ -343,7 +343,7 @@ int bt_fill_neighbors_sym(const bt_tree *tc, const double *h, const int64_t *off
     return guarded([&] {
         Phase ph("search.total");
         if (t->t.n == 0) return;
-        find_neighbors_sym(t->t, h, nullptr, const_cast<int64_t *>(offsets), nbr_idx, capacity, false, true);
+        find_neighbors(t->t, h, nullptr, const_cast<int64_t *>(offsets), nbr_idx, capacity, false, true, true);
     });
 }
 
@@ -355,7 +355,6 @@ int bt_set_partition(bt_tree *t, int32_t part, int32_t nparts) {
     t->t.part = part;
     t->t.nparts = nparts;
     t->t.rec_valid = false;  // the recorded masks belong to the previous unit range
-    t->t.sym_valid = false;
     return BT_OK;
 }
 

@@ -823,12 +823,8 @@ void build_tree(TreeDev &t, const double *pos) {
         BT_LAUNCH("pack_bbox");
         root_box_kernel<<<1, 256, 0, st>>>(partials.p, (int)gridN, t.nodes.p, dbox.p);
         BT_LAUNCH("root_box");
-        double hb[8];
-        int hbad = 0;
-        read_back({{dbox.p, hb, 7 * sizeof(double)}, {dflags.p, &hbad, sizeof(int)}});
-        if (hbad) throw Error(BT_ERR_INPUT, "bt_build: non-finite coordinate or |coordinate| > 1e150");
-        for (int l = 0; l < 3; l++) { t.box_lo[l] = hb[l]; t.box_hi[l] = hb[3 + l]; }
-        t.M = hb[6];
+        // (box, M and the input check are read back with the build's last
+        // control read: no host round trip here)
     }
 
     // Root is a leaf when n <= s or the depth cap is 0.
@@ -844,6 +840,8 @@ void build_tree(TreeDev &t, const double *pos) {
         BT_LAUNCH("copy_rec");
         t.n_leaves = 1;
         t.n_nodes = 0;
+        t.level_begin.clear();
+        t.level_cells.clear();
         t.root_is_leaf = true;
     } else {
         t.root_is_leaf = false;
@@ -862,6 +860,8 @@ void build_tree(TreeDev &t, const double *pos) {
             BT_CUDA(cudaMemcpyAsync(ln.p, &r, sizeof(r), cudaMemcpyHostToDevice, st));
         }
         t.n_nodes = 1;
+        t.level_begin.assign(1, 0);
+        t.level_cells.assign(1, 0);
         t.leaf_begin.reserve(1024, 0);
         t.leaf_count.reserve(1024, 0);
         t.leaf_depth.reserve(1024, 0);
@@ -949,7 +949,9 @@ void build_tree(TreeDev &t, const double *pos) {
 
             if (nleaf > 0) t.depth = level + 1;
             t.n_cells += ncells;
+            t.level_cells.push_back(t.n_cells);
             t.n_leaves += nleaf;
+            if (nn_next > 0) t.level_begin.push_back(t.n_nodes);  // the next depth's node ids start here
             t.n_nodes += nn_next;
             std::swap(ln, ln_next);
             nn = nn_next;
@@ -957,9 +959,7 @@ void build_tree(TreeDev &t, const double *pos) {
             cur ^= 1;
             level++;
         }
-        int32_t rb = 0;
-        read_back({{&t.nodes.p[0].b, &rb, sizeof(int32_t)}});
-        t.root_b = rb;
+        t.level_begin.push_back(t.n_nodes);
     }
 
     // Leaves were numbered level by level; renumber them in depth-first order
@@ -993,11 +993,6 @@ void build_tree(TreeDev &t, const double *pos) {
         leaf_finalize_kernel<<<grid_for(t.n_leaves * 32, kThreads, (int64_t)sms * 32), kThreads, 0, st>>>(
             fin.p, t.rec.p, t.rec32.p, t.perm.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_box.p, dstat.p + 1, t.s);
         BT_LAUNCH("leaf_finalize");
-        {
-            unsigned long long ml = 0;
-            read_back({{dstat.p + 1, &ml, sizeof(ml)}});
-            if (ml > (unsigned long long)kBigLeaf) order_big_leaves(t, fin.p, dflags.p + 2);
-        }
         t.leaf_rec.alloc(t.n_leaves);
         leaf_rec_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
             t.leaf_box.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_rec.p);
@@ -1012,7 +1007,10 @@ void build_tree(TreeDev &t, const double *pos) {
         // units: count first (to size the array), then write
         device_scan<long long>(UnitsOfLeaf{t.leaf_count.p, merge.p}, NullOut{}, t.n_leaves, dtot.p);
         long long nu = 0;
-        read_back({{dtot.p, &nu, sizeof(long long)}});
+        unsigned long long ml = 0;
+        read_back({{dtot.p, &nu, sizeof(long long)}, {dstat.p + 1, &ml, sizeof(ml)}});
+        // leaves above kBigLeaf (depth cap): records in canonical order by a segmented sort
+        if (ml > (unsigned long long)kBigLeaf) order_big_leaves(t, fin.p, dflags.p + 2);
         t.units.alloc(nu);
         t.n_units = nu;
         device_scan<long long>(UnitsOfLeaf{t.leaf_count.p, merge.p},
@@ -1031,12 +1029,28 @@ void build_tree(TreeDev &t, const double *pos) {
             BT_LAUNCH("unit_scatter");
             t.units = std::move(sorted);
         }
-        unsigned long long hstat[4];
-        read_back({{dstat.p, hstat, 4 * sizeof(unsigned long long)}});
-        t.halvings = (int64_t)hstat[0];
-        t.max_leaf = (int64_t)hstat[1];
-        t.overfull = (int64_t)hstat[2];
     }
+    // the build's one closing control read: statistics, root box, root b, input check
+    unsigned long long hstat[4];
+    double hb[8];
+    int hbad = 0;
+    int32_t rb = 0;
+    if (t.root_is_leaf)
+        read_back({{dstat.p, hstat, 4 * sizeof(unsigned long long)}, {dbox.p, hb, 7 * sizeof(double)},
+                   {dflags.p, &hbad, sizeof(int)}});
+    else
+        read_back({{dstat.p, hstat, 4 * sizeof(unsigned long long)}, {dbox.p, hb, 7 * sizeof(double)},
+                   {dflags.p, &hbad, sizeof(int)}, {&t.nodes.p[0].b, &rb, sizeof(int32_t)}});
+    if (hbad) throw Error(BT_ERR_INPUT, "bt_build: non-finite coordinate or |coordinate| > 1e150");
+    for (int l = 0; l < 3; l++) {
+        t.box_lo[l] = hb[l];
+        t.box_hi[l] = hb[3 + l];
+    }
+    t.M = hb[6];
+    t.root_b = rb;
+    t.halvings = (int64_t)hstat[0];
+    t.max_leaf = (int64_t)hstat[1];
+    t.overfull = (int64_t)hstat[2];
 }
 
 }  // namespace bt

@@ -135,6 +135,7 @@ struct UnitRun {             // per walk unit, written by the walk kernels
     int loaded;             // particle records of the candidate leaves (arena bound)
     int nstaged;            // candidates kept by the per-particle cull
     int ok;                 // the unit's masks and candidate indices were recorded
+    double rmax;            // symmetric criterion: largest cull radius max(R'_u, R'(h_max of a kept leaf))
 };
 
 struct TreeDev {
@@ -151,6 +152,8 @@ struct TreeDev {
     DBuf<int32_t> perm;        // caller index of each tree position (as rec / rec32 .w)
     DBuf<NodeRec> nodes;       // internal nodes, all levels
     int64_t n_nodes = 0;
+    std::vector<int64_t> level_begin;  // node ids of depth d: [level_begin[d], level_begin[d + 1])
+    std::vector<int64_t> level_cells;  // their cells: [level_cells[d], level_cells[d + 1]) of the cell table
     DBuf<int32_t> cells;       // cell table, all levels
     int64_t n_cells = 0;
     DBuf<int32_t> leaf_begin;  // tree-order position of each leaf (depth-first order)
@@ -170,6 +173,7 @@ struct TreeDev {
     bool root_is_leaf = true;
     // search scratch
     DBuf<double> h_tree;       // h in tree order
+    DBuf<double> leaf_hmax, node_hmax;  // symmetric criterion: max h per leaf / per node subtree
     DBuf<double> m_tree;       // masses in tree order (density consumer)
     DBuf<UnitRun> urun;                    // per-unit walk record
     DBuf<int32_t> ulist;                   // candidate leaf lists of all units
@@ -181,13 +185,9 @@ struct TreeDev {
     long long rec_hsum = 0;
     long long rec_csum = 0;    // checksum of the recorded pass's counts (fill-only offsets validation)
     int rec_exact = 0;
-    bool rec_tp = false;       // the candidate records hold tree positions (symmetric pass)
+    bool rec_sym = false;      // the recorded pass is the symmetric criterion's
     DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
     DBuf<int32_t> front;       // descent frontier scratch of the big-unit pass (per warp)
-    // symmetric criterion (R22): gather counts, one-sided extras / append cursors, gather offsets
-    DBuf<int32_t> sym_g, sym_x;
-    DBuf<int64_t> sym_off;
-    bool sym_valid = false;    // sym_g / sym_x hold the pass of the current recorded masks
 
     int64_t total_pairs = 0, max_count = 0, staged = 0, loaded = 0, tests = 0, exact_tests = 0;
     int64_t ngmax = 512, rows_over_ngmax = 0;  // the last count's ngmax and its rows above it
@@ -196,11 +196,9 @@ struct TreeDev {
 
 // Build (build.cu) and search (walk.cu) entry points.
 void build_tree(TreeDev &t, const double *pos);
+// sym: the symmetric max(h_i, h_j) criterion (R22) instead of the gather one
 void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets,
-                    int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass, bool cand_tp = false);
-
-void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
-                        int64_t capacity, bool count_pass, bool fill_pass);
+                    int32_t *nbr_idx, int64_t capacity, bool count_pass, bool fill_pass, bool sym = false);
 
 void density(TreeDev &t, const double *h, const double *mass, double *rho);
 

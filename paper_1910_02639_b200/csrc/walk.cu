@@ -112,6 +112,9 @@ struct WalkArgs {
     int desc_batch;           // units claimed per atomic by the descent warps
     const double *m_tree;     // density mode: masses in tree order
     double *rho;              // density mode: output, caller order
+    float *scrk;              // symmetric mode: per walk warp, kScratch staged -k Mid_j (candidate thresholds)
+    const double *leaf_hmax;  // symmetric mode: max h per leaf
+    const double *node_hmax;  // symmetric mode: max h per internal node subtree
 };
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -208,6 +211,37 @@ __device__ __forceinline__ void l4_band(double T, double E, double eps, bool exa
     Mid = M;
 }
 
+// Lemma L4 for the symmetric criterion (L4s): the hot
+// loop evaluates u = fl(cx Qx + fl(cy Qy + fl(cz Qz + fl(Ac + B''q)))) with
+// B''q = fl32(k |q|^2) (no Mid), then v_i = fl(u - k Mid_i) (query threshold)
+// and v_j = fl(u - k Mid_j) (candidate threshold), Mid = fl32(T).  u errs by
+// at most k G'', G'' = w 60.1 E'^2 (as G without the Mid terms); the final
+// subtraction adds at most w |u - k Mid|, which moves the +-1 decision
+// thresholds by < 2w.  So for every T <= Tmax of the unit,
+//   HW(T) = w T + 8 u64 T + Err(T+) + G'' <= HW(Tmax)   (increasing in T)
+// with Err(S) = 4 sqrt3 eps sqrt(S) + 12 eps^2 and sqrt(Tmax+) <= rmax (Tmax
+// <= rmax^2: every threshold of the unit comes from an h whose R' <= rmax),
+// and k = the largest power of two <= (1 - 2^-22) / HW(Tmax) makes v < -1 a
+// certain neighbor, v > 1 a certain non-neighbor, |v| <= 1 the fp64 band.
+// S - Err(S) must increase on [T-, inf) for the smallest threshold that can
+// decide a pair: the smallest query threshold Tqmin (a candidate threshold
+// Tj <= Tqmin is redundant, d2 < Tj implying d2 < Ti: such candidates carry
+// +inf, never deciding).  k = 0: force (every pair to the fp64 predicate).
+__device__ __forceinline__ float l4_band_sym(double Tqmin, double rmax, double E, double eps, bool exact_only) {
+    if (exact_only || !(E < 1e15) || !(rmax < 1e15)) return 0.0f;
+    const double u = 0x1p-24, u64 = 0x1p-53, s3 = 1.7320508075688775;
+    const double Ep = E * (1.0 + 1e-6) + 5.0 * eps;
+    const double Tmax = rmax * rmax * (1.0 + 0x1p-40);
+    if (!(2.0 * s3 * eps * 1.0001 <= 0.5 * sqrt(Tqmin * (1.0 - 8.0 * u64)))) return 0.0f;
+    const double err = (4.0 * s3 * eps * rmax * (1.0 + 0x1p-40) + 12.0 * eps * eps) * 1.0001;
+    const double hw = (u * Tmax + 8.0 * u64 * Tmax + err + u * 60.1 * Ep * Ep) * (1.0 + 0x1p-30);
+    int e;
+    frexp((1.0 - 0x1p-22) / hw, &e);          // = f 2^e, f in [0.5, 1)
+    const double kd = ldexp(1.0, e - 1);      // largest power of two <= (1 - 2^-22) / hw
+    if (!(kd * (12.0 * Ep * Ep + 2.0 * Tmax) < 1e36) || !(2.0 * kd * Ep < 1e36)) return 0.0f;
+    return (float)kd;
+}
+
 // ---------------------------------------------------------------------------
 // Unit geometry: identical code in the descent and the walk kernels, so both
 // derive bit-identical c, E and R'_u.
@@ -215,13 +249,15 @@ __device__ __forceinline__ void l4_band(double T, double E, double eps, bool exa
 struct UnitGeom {
     int q0, nq, leaf;
     double lo[3], hi[3], c[3];
-    double Ru, Ru2, E;
+    double Ru, Ru2, Rx, E;  // R'_u, its square, the largest cull radius, the coordinate bound
     // this lane's queries (lane, lane + 32): fp64 coordinates, (2h)^2, caller index
     double qx[2], qy[2], qz[2], qT[2];
     int32_t qo[2];
 };
 
-__device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, int lane, UnitGeom &G) {
+// rext: the largest cull radius of the unit's candidates (the gather walk:
+// R'_u itself; the symmetric walk: the descent's rmax >= R'_u)
+__device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, int lane, UnitGeom &G, double rext) {
     G.leaf = UU.x;
     G.q0 = UU.y;
     G.nq = UU.z;
@@ -259,8 +295,9 @@ __device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, in
     }
     G.Ru = warp_max(Ru);
     G.Ru2 = __dmul_rn(G.Ru, G.Ru);
+    G.Rx = fmax(G.Ru, rext);
     // a-priori bound |x - c| <= E per axis for queries and kept candidates (L4)
-    G.E = (E + G.Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;
+    G.E = (E + G.Rx) * 1.0001 + 4.0 * 0x1p-53 * Mu;
 }
 
 // The unit's query box and R'_u only (the descent): the same operations as
@@ -350,16 +387,52 @@ struct DescOut {
     int nleaf;
     long long loaded;
     bool overflow;  // a level frontier exceeded the frontier capacity
+    double rmax;    // symmetric criterion: largest cull radius of a kept leaf
 };
+
+// R' of a particle (or of a subtree's largest h): 2h (1 + 2^-40) + 2^-50 M
+// (lemma L1/L2); the same operations as the queries' R' in unit_box
+__device__ __forceinline__ double rprime(double hh, double M) {
+    return __dadd_rn(__dmul_rn(__dmul_rn(2.0, hh), 1.0 + 0x1p-40), __dmul_rn(0x1p-50, M));
+}
 
 // Breadth-first descent of one unit; appends the kept leaves to out[0, lim)
 // (when out != nullptr) and returns how many there are.
+// Internal-node cull (L3 for a whole subtree; the symmetric walk, where a
+// far subtree of small h can be skipped -- for the gather walk the Eq. 5
+// ranges prune as well and the extra loads did not pay): the child's equal-slice box
+// [lo, lo + ext] contains its particles up to the rounding of the parent's
+// Eq. 2 (a few ulps of |x - lo|), covered by the widening delta; the node is
+// skipped only if that box is farther than R (1 + 2^-40) + delta from the
+// query box, R = R'_u (gather) or max(R'_u, R'(h_max of the subtree))
+// (symmetric).  Exact fp64 min / max, rounded products on a 2^-40 margin.
+template <bool kSym>
+__device__ __forceinline__ bool node_near(const WalkArgs &a, int32_t node, const double (&qlo)[3],
+                                          const double (&qhi)[3], double Ru) {
+    const NodeRec &nd = a.nodes[node];
+    const double R = kSym ? fmax(Ru, rprime(a.node_hmax[node], a.M)) : Ru;
+    double g2 = 0.0;
+    for (int l = 0; l < 3; l++) {
+        const double lo = nd.lo[l], hi = __dadd_rn(nd.lo[l], nd.ext[l]);
+        const double d = (fabs(lo) + fabs(hi)) * 0x1p-40 + 0x1p-1000;
+        const double g = fmax(0.0, fmax(__dsub_rn(__dsub_rn(lo, d), qhi[l]), __dsub_rn(qlo[l], __dadd_rn(hi, d))));
+        g2 = __dadd_rn(g2, __dmul_rn(g, g));
+    }
+    const double Rc = __dadd_rn(__dmul_rn(R, 1.0 + 0x1p-40), 0x1p-1000);
+    return g2 < __dmul_rn(Rc, Rc);
+}
+
+// kSym (symmetric criterion, R22): a node's Eq. 5 ranges use max(R'_u,
+// R'(h_max of the node)) and a leaf is kept when its box is within max(R'_u,
+// R'(h_max of the leaf)) of the query box: every j with d(i, j) below
+// 2 max(h_i, h_j) (lemma L1) lies in a kept leaf.
+template <bool kSym>
 __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo)[3], const double (&qhi)[3],
                                            double Ru, int lane, int32_t *fcur, int32_t *fnext, long long fcap,
                                            int32_t *out, long long lim) {
     const double Ru2 = __dmul_rn(Ru, Ru);
     const unsigned lt = lanemask_lt();
-    DescOut r{0, 0, false};
+    DescOut r{0, 0, false, Ru};
     long long loaded = 0;
     // leaf cell found by this lane: keep it if its tight box is within R'_u of
     // the query box (L3, exact fp64 box distance)
@@ -372,7 +445,13 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
             double gy = fmax(0.0, fmax(__dsub_rn(b0.y, qhi[1]), __dsub_rn(qlo[1], b2.x)));
             double gz = fmax(0.0, fmax(__dsub_rn(b1.x, qhi[2]), __dsub_rn(qlo[2], b2.y)));
             double g2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
-            keep = g2 < Ru2;
+            if (kSym) {
+                const double RL = fmax(Ru, rprime(a.leaf_hmax[leaf], a.M));
+                keep = g2 < __dmul_rn(RL, RL);
+                if (keep) r.rmax = fmax(r.rmax, RL);
+            } else {
+                keep = g2 < Ru2;
+            }
         }
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
@@ -398,11 +477,12 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
                     const NodeRec &nd = a.nodes[fcur[fi]];
                     b = nd.b;
                     cb = nd.cell_base;
+                    const double Rn = kSym ? fmax(Ru, rprime(a.node_hmax[fcur[fi]], a.M)) : Ru;
                     int r0[3], r1[3];
                     for (int l = 0; l < 3; l++) {  // Eq. 5 with R'_u (lemma L2); b_z = nd.bz
                         const int bl = l == 2 ? nd.bz : b;
-                        r0[l] = cell_coord_fast(__dsub_rn(qlo[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], bl);
-                        r1[l] = cell_coord_fast(__dadd_rn(qhi[l], Ru), nd.lo[l], nd.ext[l], nd.bx[l], bl);
+                        r0[l] = cell_coord_fast(__dsub_rn(qlo[l], Rn), nd.lo[l], nd.ext[l], nd.bx[l], bl);
+                        r1[l] = cell_coord_fast(__dadd_rn(qhi[l], Rn), nd.lo[l], nd.ext[l], nd.bx[l], bl);
                     }
                     r0x = r0[0];
                     r0y = r0[1];
@@ -449,6 +529,7 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
                         code = a.cells[ocb + j];
                         is_leaf = code >= 0;
                         is_node = code <= -2;
+                        if (kSym && is_node) is_node = node_near<kSym>(a, code_node(code), qlo, qhi, Ru);
                         BT_DEV_CHECK(ocb + j < a.n_cells && code < a.n_leaves);
                     }
                     const unsigned nm = __ballot_sync(0xffffffffu, is_node);
@@ -471,6 +552,7 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
     }
     for (int d = 16; d; d >>= 1) loaded += __shfl_xor_sync(0xffffffffu, loaded, d);
     r.loaded = loaded;
+    if (kSym) r.rmax = warp_max(r.rmax);
     return r;
 }
 
@@ -485,7 +567,10 @@ __device__ __forceinline__ void add_need(const WalkArgs &a, long long loaded, in
 //   (nleaf = -1) for the big pass.
 // kBig = true: only marked units; frontier in global scratch (front_cap =
 //   all nodes), the list counted first and allocated exactly.
-template <bool kBig>
+// (A batched variant -- one descent with the union box of 8 Morton-adjacent
+// units, each unit filtering the union list -- measured slower in round 2:
+// cfg 5 descent 2.9 -> 5.5 ms, the union lists being far larger than a unit's.)
+template <bool kBig, bool kSym>
 __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
     __shared__ int32_t sfront[kBig ? 1 : kDescThreads / 32][2][kBig ? 1 : kFrontCap];
     const int lane = threadIdx.x & 31;
@@ -514,27 +599,29 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
         if (!kBig) {
             const bool ok = slab_reserve(ls, kListReserve, kListSlab, a.list_cap, &a.ctr[C_LIST], lane);
             const long long lim = ls.end - ls.cur;
-            DescOut d = descend(a, qlo, qhi, Ru, lane, f0, f1, fcap, ok ? a.ulist + ls.cur : nullptr, lim);
+            DescOut d = descend<kSym>(a, qlo, qhi, Ru, lane, f0, f1, fcap, ok ? a.ulist + ls.cur : nullptr, lim);
             const bool fits = ok && !d.overflow && d.nleaf <= lim;
             if (lane == 0) {
                 R.list_off = ls.cur;
                 R.nleaf = fits ? d.nleaf : -1;
                 R.loaded = (int)d.loaded;
+                R.rmax = d.rmax;
                 if (!fits) atomicAdd((unsigned long long *)&a.ctr[C_BIG], 1ull);
                 else add_need(a, d.loaded, U.z);
             }
             if (fits) ls.cur += d.nleaf;
         } else {
-            DescOut d = descend(a, qlo, qhi, Ru, lane, f0, f1, fcap, nullptr, 0);
+            DescOut d = descend<kSym>(a, qlo, qhi, Ru, lane, f0, f1, fcap, nullptr, 0);
             long long base = 0;
             if (lane == 0) base = (long long)atomicAdd((unsigned long long *)&a.ctr[C_LIST], (unsigned long long)d.nleaf);
             base = __shfl_sync(0xffffffffu, base, 0);
             const bool ok = !d.overflow && base + d.nleaf <= a.list_cap;
-            if (ok) descend(a, qlo, qhi, Ru, lane, f0, f1, fcap, a.ulist + base, d.nleaf);
+            if (ok) descend<kSym>(a, qlo, qhi, Ru, lane, f0, f1, fcap, a.ulist + base, d.nleaf);
             if (lane == 0) {
                 R.list_off = base;
                 R.nleaf = ok ? d.nleaf : -2;  // -2: list arena too small (host grows it and redoes the pass)
                 R.loaded = (int)d.loaded;
+                R.rmax = d.rmax;
                 add_need(a, d.loaded, U.z);
             }
         }
@@ -552,6 +639,8 @@ struct UnitSm {                     // per-warp unit state (shared memory)
     float4 *scr;                     // the warp's staging scratch (read from here: not rematerialised)
     int32_t *cand_ptr;               // the unit's candidate-index records (a.cands + cand_base)
     double c[3], E;                  // unit centre, coordinate bound (L4)
+    double Ru, eps, tqmin;           // symmetric: R'_u, l4_eps(E), smallest query threshold
+    float *scrk;                     // symmetric: the staged candidates' -k Mid_j
     float4 box0, box1;               // fp32 query box relative to c: (lo xyz, cull2), (hi xyz, -)
     int q0, nq;                      // (8-byte aligned: read as one int2)
     float k;                         // band scale of the unit (power of two; 0: force)
@@ -567,6 +656,8 @@ struct WalkSmem {
     unsigned lstart[kGroupPos / 32];       // group positions: bit p set where a leaf starts (p = 32 w + bit)
     unsigned char lwpre[kGroupPos / 32];   // leaves starting before word w
     float4 loff[kGroup];            // group leaves: fl32(c_leaf - c), w = 1 compact / 0 fp64 records
+    float lcull[kGroup];            // symmetric: group leaves' fp32 cull radius^2 (max(R'_u, R'(h_max)))
+    float2 qm[kQ + 1];              // symmetric: -k Mid_i per query (packed pair); [kQ]: look-ahead pad
     UnitSm u;
 };
 
@@ -604,6 +695,7 @@ __device__ __forceinline__ float w_m4f(float q) {
 // hot loop's fp32 operations and let the fp64 predicate decide every pair
 // with |d'| <= 1 (all pairs when `force`; padding slots >= n are never
 // neighbors).  blk: the block's staged candidates (ax, ay, az, tree position).
+template <bool kSym>
 __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int lane, const float4 *blk, int n,
                                           long long &exact) {
     const int nch = (n + 63) >> 6;
@@ -611,9 +703,11 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
     const float ku = S.u.k;
     const bool force = S.u.force != 0;  // (inf used for padding Ac)
     const int q0 = S.u.q0, nq = S.u.nq;
+    // symmetric: the block's -k Mid_j (scratch slots blk - scr)
+    const float *blkk = kSym ? S.u.scrk + (blk - S.u.scr) : nullptr;
     for (int k = 0; k < nch; k++) {
         float4 c[2];
-        float ac[2];
+        float ac[2], nk[2] = {0.f, 0.f};
         bool real[2];
 #pragma unroll
         for (int h = 0; h < 2; h++) {
@@ -622,6 +716,7 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
             c[h] = real[h] ? __ldcg(&blk[s]) : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
             const float nc = __fmaf_rn(c[h].z, c[h].z, __fmaf_rn(c[h].y, c[h].y, __fmul_rn(c[h].x, c[h].x)));
             ac[h] = real[h] ? __fmul_rn(ku, nc) : inf;  // identical to test_block
+            if (kSym) nk[h] = real[h] ? __ldcg(&blkk[s]) : 0.f;
         }
         for (int q = 0; q < nq; q++) {
             const float4 Q0 = S.q0[q], Q1 = S.q1[q];
@@ -630,7 +725,12 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
             for (int h = 0; h < 2; h++) {
                 // the hot loop's v, operation for operation
                 const float v = __fmaf_rn(c[h].x, Q0.x, __fmaf_rn(c[h].y, Q0.z, __fmaf_rn(c[h].z, Q1.x, __fadd_rn(ac[h], Q1.z))));
-                flag[h] = real[h] && (force || fabsf(v) <= 1.0f);
+                if (kSym) {
+                    const float vi = __fadd_rn(v, S.qm[q].x), vj = __fadd_rn(v, nk[h]);
+                    flag[h] = real[h] && (force || fabsf(vi) <= 1.0f || fabsf(vj) <= 1.0f);
+                } else {
+                    flag[h] = real[h] && (force || fabsf(v) <= 1.0f);
+                }
             }
             const unsigned f0 = __ballot_sync(0xffffffffu, flag[0]), f1 = __ballot_sync(0xffffffffu, flag[1]);
             if (!(f0 | f1)) continue;
@@ -638,11 +738,20 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
             const double4 Qr = a.rec[qp];
             const double t = __dmul_rn(2.0, a.h_tree[qp]);
             const double T = __dmul_rn(t, t);
-            bool e0 = false, e1 = false;
-            const int tp0 = __float_as_int(c[0].w), tp1 = __float_as_int(c[1].w);
-            if (flag[0]) e0 = tp0 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp0]);
-            if (flag[1]) e1 = tp1 != qp && exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp1]);
-            const unsigned m0 = __ballot_sync(0xffffffffu, e0), m1 = __ballot_sync(0xffffffffu, e1);
+            bool e[2] = {false, false};
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int tp = __float_as_int(c[h].w);
+                if (flag[h] && tp != qp) {
+                    double Tp = T;
+                    if (kSym) {  // the pair's threshold: fl((2 max(h_i, h_j))^2) = max(T_i, T_j)
+                        const double tj = __dmul_rn(2.0, a.h_tree[tp]);
+                        Tp = fmax(T, __dmul_rn(tj, tj));
+                    }
+                    e[h] = exact_pair(Qr.x, Qr.y, Qr.z, Tp, a.rec[tp]);
+                }
+            }
+            const unsigned m0 = __ballot_sync(0xffffffffu, e[0]), m1 = __ballot_sync(0xffffffffu, e[1]);
             if (lane == 0) {
                 const unsigned long long fm = ((unsigned long long)f1 << 32) | f0;
                 const unsigned long long em = ((unsigned long long)m1 << 32) | m0;
@@ -658,9 +767,9 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
 // Test n (<= kBlk) staged candidates (blk, unit slots us0 .. us0 + n) against
 // the unit's queries and record the block's masks; returns this lane's count
 // increments for queries (lane, lane + 32).
-template <bool kDensity>
+template <bool kDensity, bool kSym>
 __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArgs &a, int lane, const float4 *blk,
-                                           int n, int us0, double (&dacc)[2]) {
+                                           int n, int us0, int b0, double (&dacc)[2]) {
     const float inf = __int_as_float(0x7f800000);
     const int nch = (n + 63) >> 6;  // 1 or 2 chunks of 64
     const int nq = S.u.nq;
@@ -694,7 +803,47 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     };
     float4 N0, N1;
     ldq(0, N0, N1);
-    if (nch == 2) {
+    if constexpr (kSym) {
+        // symmetric criterion (lemma L4s): u = k |c - q|^2 without Mid, then
+        // v_i = u - k Mid_i (query threshold) and v_j = u - k Mid_j (candidate
+        // threshold, +inf when it cannot decide); the bit is min(v_i, v_j) < 0
+        float nk[4];
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int sl = 32 * j + lane;
+            nk[j] = (sl < n) ? __ldcg(&S.u.scrk[b0 + sl]) : 0.f;
+        }
+        const unsigned long long ka = pk(nk[0], nk[1]), kb = pk(nk[2], nk[3]);
+        const unsigned aqm = (unsigned)__cvta_generic_to_shared(&S.qm[0]);
+        unsigned long long NM;
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm));
+#pragma unroll 2
+        for (int q = 0; q < nqp; q++) {
+            const float4 Q0 = N0, Q1 = N1;
+            const unsigned long long qm = NM;
+            ldq(q + 1, N0, N1);
+            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm + 8 * (q + 1)));
+            const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
+                                     bq = pk(Q1.z, Q1.w);
+            const unsigned long long ua = f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq))));
+            const unsigned long long via = f2_add(ua, qm), vja = f2_add(ua, ka);
+            bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(via)), fabsf(hi_f(via))), fminf(fabsf(lo_f(vja)), fabsf(hi_f(vja)))));
+            const unsigned m0 = __ballot_sync(0xffffffffu, fminf(lo_f(via), lo_f(vja)) < 0.0f);
+            const unsigned m1 = __ballot_sync(0xffffffffu, fminf(hi_f(via), hi_f(vja)) < 0.0f);
+            unsigned m2 = 0u, m3 = 0u;
+            if (nch == 2) {  // (warp-uniform)
+                const unsigned long long ub = f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq))));
+                const unsigned long long vib = f2_add(ub, qm), vjb = f2_add(ub, kb);
+                bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))), fminf(fabsf(lo_f(vjb)), fabsf(hi_f(vjb)))));
+                m2 = __ballot_sync(0xffffffffu, fminf(lo_f(vib), lo_f(vjb)) < 0.0f);
+                m3 = __ballot_sync(0xffffffffu, fminf(hi_f(vib), hi_f(vjb)) < 0.0f);
+            }
+            if (lane == 0) {
+                S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
+                S.mask[1][q] = ((unsigned long long)m3 << 32) | m2;
+            }
+        }
+    } else if (nch == 2) {
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
             const float4 Q0 = N0, Q1 = N1;
@@ -731,7 +880,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     const bool band = S.u.force != 0 || bmin <= 1.0f;
     __syncwarp();
     long long exact = 0;
-    if (__any_sync(0xffffffffu, band)) resolve_band(S, a, lane, blk, n, exact);
+    if (__any_sync(0xffffffffu, band)) resolve_band<kSym>(S, a, lane, blk, n, exact);
     // self is never its own neighbor (R12); counts; the final masks recorded
     // for the fill pass (chunk kk = us0 / 64 + k of the unit) straight from
     // the lanes that own the queries
@@ -823,7 +972,7 @@ __device__ __forceinline__ void locate(const WalkSmem &S, int total, bool single
 // cull) into the warp's scratch at nst, until the group is done or the
 // scratch cannot take another window.  kMixed: some leaf of the group is
 // staged from the fp64 records (a = fl32(fl64(x - c))).
-template <bool kMixed, bool kTP>
+template <bool kMixed, bool kSym, bool kD>
 __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int total, bool single,
                                             int &w0, int &nst, int slot0) {
     const unsigned lt = lanemask_lt(), le = lt | (1u << lane);
@@ -881,14 +1030,20 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         const float gy = fmaxf(0.0f, fmaxf(-hi_f(lxy), hi_f(hxy)));
         const float gz = fmaxf(0.0f, fmaxf(__fsub_rn(B0.z, az), __fsub_rn(az, B1.z)));
         const float g2 = __fmaf_rn(gz, gz, __fmaf_rn(gy, gy, __fmul_rn(gx, gx)));
-        const bool keep = pos >= 0 && g2 < B0.w;
+        const bool keep = pos >= 0 && g2 < (kSym ? S.lcull[mine] : B0.w);
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             const int slot = nst + __popc(km & lt);
             BT_DEV_CHECK(slot < kScratch && pos >= 0 && pos < a.n_rec);
             BT_DEV_CHECK(!rec_ok || S.u.cand_base + slot0 + slot < a.cand_cap);
             __stcg(&scr[(unsigned)slot], make_float4(ax, ay, az, __int_as_float(pos)));  // L2-resident scratch
-            if (rec_ok) __stcs(&cands[(unsigned)slot], kTP ? pos : __float_as_int(r.w));
+            if (kSym) {  // -k Mid_j of the candidate threshold; +inf when it cannot decide (Tj <= Tqmin, L4s)
+                const double tj = __dmul_rn(2.0, a.h_tree[pos]);
+                const double Tj = __dmul_rn(tj, tj);
+                __stcg(&S.u.scrk[(unsigned)slot],
+                       Tj > S.u.tqmin ? -S.u.k * __double2float_rn(Tj) : __int_as_float(0x7f800000));
+            }
+            if (rec_ok) __stcs(&cands[(unsigned)slot], __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
         }
         nst += __popc(km);
@@ -902,9 +1057,9 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
 #ifndef BT_WALK_MIN_BLOCKS
 #define BT_WALK_MIN_BLOCKS 7
 #endif
-// kTP: record each candidate's tree position instead of its caller index
-// (the symmetric pass reads the records; the fill maps them through perm)
-template <bool kDensity, bool kTP>
+// kSym: the symmetric criterion (R22): candidates culled with their leaf's
+// radius, each pair tested against both thresholds (lemma L4s)
+template <bool kDensity, bool kSym>
 __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(WalkArgs a) {
     __shared__ WalkSmemT<kDensity> smem[kWalkThreads / 32];
     const int lane = threadIdx.x & 31;
@@ -913,6 +1068,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (lane == 0) {
         S.u.scr = a.scratch + gwarp * kScratch;
+        if (kSym) S.u.scrk = a.scrk + gwarp * kScratch;
         S.u.cs = Slab();
         S.u.ms = Slab();
         S.u.tests = S.u.exact = S.u.staged = S.u.loaded = S.u.nzw = 0;
@@ -928,19 +1084,32 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         int nq, q0;
         {
             UnitGeom G;
-            unit_setup(a, a.units[uid], lane, G);
+            unit_setup(a, a.units[uid], lane, G, kSym ? R.rmax : 0.0);
             nq = G.nq;
             q0 = G.q0;
             qo[0] = G.qo[0];
             qo[1] = G.qo[1];
             const double eps = l4_eps(G.E);
             float kq[2] = {INFINITY, INFINITY}, mid[2] = {0.0f, 0.0f};
+            float ku;
+            double tqmin = INFINITY;  // symmetric: the smallest query threshold of the unit
+            if (kSym) {
 #pragma unroll
-            for (int h = 0; h < 2; h++)
-                if (lane + 32 * h < G.nq) l4_band(G.qT[h], G.E, eps, a.exact_only != 0, kq[h], mid[h]);
-            // unit band scale: the minimum power of two (0 = force)
-            float ku = fminf(kq[0], kq[1]);
-            for (int d = 16; d; d >>= 1) ku = fminf(ku, __shfl_xor_sync(0xffffffffu, ku, d));
+                for (int h = 0; h < 2; h++)
+                    if (lane + 32 * h < G.nq) {
+                        tqmin = fmin(tqmin, G.qT[h]);
+                        mid[h] = __double2float_rn(G.qT[h]);  // Mid_i = fl32(T_i)
+                    }
+                tqmin = warp_min(tqmin);
+                ku = l4_band_sym(tqmin, G.Rx, G.E, eps, a.exact_only != 0);
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; h++)
+                    if (lane + 32 * h < G.nq) l4_band(G.qT[h], G.E, eps, a.exact_only != 0, kq[h], mid[h]);
+                // unit band scale: the minimum power of two (0 = force)
+                ku = fminf(kq[0], kq[1]);
+                for (int d = 16; d; d >>= 1) ku = fminf(ku, __shfl_xor_sync(0xffffffffu, ku, d));
+            }
             const bool force = ku == 0.0f;
 #pragma unroll
             for (int h = 0; h < 2; h++) {
@@ -950,18 +1119,22 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     const float ay = __double2float_rn(__dsub_rn(G.qy[h], G.c[1]));
                     const float az = __double2float_rn(__dsub_rn(G.qz[h], G.c[2]));
                     // Q = -2 k q (exact), Bq = fl32(k (|q|^2 - Mid)), |q|^2 in fp64 from the fp32 q
+                    // (symmetric: B''q = fl32(k |q|^2), -k Mid_i apart)
                     const float m2k = -2.0f * ku;
                     const double qq = (double)ax * ax + (double)ay * ay + (double)az * az;
-                    const float bq = force ? 0.0f : __double2float_rn((double)ku * (qq - (double)mid[h]));
+                    const float bq = force ? 0.0f
+                                           : __double2float_rn((double)ku * (qq - (kSym ? 0.0 : (double)mid[h])));
                     S.q0[k] = make_float4(m2k * ax, m2k * ax, m2k * ay, m2k * ay);
                     S.q1[k] = make_float4(m2k * az, m2k * az, bq, bq);
+                    if (kSym) S.qm[k] = make_float2(-ku * mid[h], -ku * mid[h]);
                     if constexpr (kDensity) {
                         S.d.hinv[k] = (float)(1.0 / a.h_tree[G.q0 + k]);
                         S.d.qraw[k] = make_float4(ax, ay, az, 0.f);
                     }
-                } else {  // padding query: v = Ac + 2 >= 2 (never a neighbor, never banded)
+                } else {  // padding query: v = Ac + 2 >= 2 (never a neighbor, never banded; symmetric: +inf)
                     S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    S.q1[k] = make_float4(0.f, 0.f, 2.f, 2.f);
+                    S.q1[k] = kSym ? make_float4(0.f, 0.f, inf, inf) : make_float4(0.f, 0.f, 2.f, 2.f);
+                    if (kSym) S.qm[k] = make_float2(0.f, 0.f);
                 }
                 S.self[k] = -1;
             }
@@ -1001,6 +1174,11 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                 S.u.k = ku;
                 S.u.box0 = make_float4(blo[0], blo[1], blo[2], cull2);
                 S.u.box1 = make_float4(bhi[0], bhi[1], bhi[2], 0.0f);
+                if (kSym) {
+                    S.u.Ru = G.Ru;
+                    S.u.eps = eps;
+                    S.u.tqmin = tqmin;
+                }
             }
         }
         __syncwarp();
@@ -1019,6 +1197,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     // the group's leaves: first position, count, offset of the centre
                     const int gi = g0 + lane;
                     int cnt = 0, beg = 0;
+                    float lcull = 0.0f;
                     float4 off = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (gi < nleaf) {
                         const LeafRec *lr = a.leaf_rec + a.ulist[list_off + gi];
@@ -1033,6 +1212,12 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                                           __double2float_rn(__dsub_rn(cxy.y, S.u.c[1])),
                                           __double2float_rn(__dsub_rn(czH.x, S.u.c[2])),
                                           (czH.y <= 7.0 * S.u.E) ? 1.0f : 0.0f);
+                        if (kSym) {  // the leaf's cull radius: max(R'_u, R'(h_max)), fp32 image as the unit's (L3 / L4)
+                            const double RL = fmax(S.u.Ru, rprime(a.leaf_hmax[a.ulist[list_off + gi]], a.M));
+                            const double rc = (RL + 4.0 * S.u.eps) * (1.0 + 0x1p-20);
+                            const double rc2 = rc * rc * (1.0 + 0x1p-40);
+                            lcull = (rc2 < 3.0e38) ? __double2float_ru(rc2) : __int_as_float(0x7f800000);
+                        }
                     }
                     int inc = cnt;
                     for (int d = 1; d < 32; d <<= 1) {
@@ -1044,6 +1229,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     total = __shfl_sync(0xffffffffu, inc, nl - 1);
                     S.ldel[lane] = beg - (inc - cnt);
                     S.loff[lane] = off;
+                    if (kSym) S.lcull[lane] = lcull;
                     // start bitmap of the group's positions and the starts before each word
                     const int nw = nl > 1 ? (total + 31) >> 5 : 0;  // <= kGroupPos / 32
                     for (int w = lane; w < nw; w += 32) S.lstart[w] = 0u;
@@ -1071,9 +1257,9 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     have_group = true;
                 }
                 if (mixed)
-                    stage_group<true, kTP>(S, a, lane, total, nl == 1, w0, nst, slot0);
+                    stage_group<true, kSym, kDensity>(S, a, lane, total, nl == 1, w0, nst, slot0);
                 else
-                    stage_group<false, kTP>(S, a, lane, total, nl == 1, w0, nst, slot0);
+                    stage_group<false, kSym, kDensity>(S, a, lane, total, nl == 1, w0, nst, slot0);
                 if (w0 < total) break;  // scratch full
                 loaded += total;
                 g0 += nl;
@@ -1084,7 +1270,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             // ---- test phase: the staged blocks (all but a partial last one unless done)
             const int ntest = done ? nst : nst - nst % kBlk;
             for (int b0 = 0; b0 < ntest; b0 += kBlk) {
-                const int2 inc = test_block<kDensity>(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0), slot0 + b0, dacc);
+                const int2 inc = test_block<kDensity, kSym>(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0), slot0 + b0, b0, dacc);
                 cnt0 += inc.x;
                 cnt1 += inc.y;
             }
@@ -1096,6 +1282,8 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             const int rest = nst - ntest;
             float4 *const scr = S.u.scr;
             for (int i = lane; i < rest; i += 32) __stcg(&scr[i], __ldcg(&scr[ntest + i]));
+            if constexpr (kSym)
+                for (int i = lane; i < rest; i += 32) __stcg(&S.u.scrk[i], __ldcg(&S.u.scrk[ntest + i]));
             slot0 += ntest;
             nst = rest;
             __syncwarp();
@@ -1166,7 +1354,6 @@ struct FillSmem {
     unsigned long long mask[kFillChunks * kQ];   // the round's masks, [k][q]
 };
 
-template <bool kTP>
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     __shared__ FillSmem fsm[kFillWarps];
     const int lane = threadIdx.x & 31;
@@ -1192,10 +1379,6 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
                 const int s0 = 64 * (kk0 + k) + lane, s1 = s0 + 32;
                 c0[k] = (k < nk && s0 < R.nstaged) ? __ldcs(&cands[R.cand_base + s0]) : -1;
                 c1[k] = (k < nk && s1 < R.nstaged) ? __ldcs(&cands[R.cand_base + s1]) : -1;
-                if (kTP) {  // tree positions -> caller indices
-                    if (c0[k] >= 0) c0[k] = a.perm[c0[k]];
-                    if (c1[k] >= 0) c1[k] = a.perm[c1[k]];
-                }
             }
             __syncwarp();
             const unsigned long long *src = masks + R.mask_base + (long long)kk0 * nq;
@@ -1228,118 +1411,44 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
 
 // ---------------------------------------------------------------------------
 // Symmetric criterion (reading R22): j is a neighbor of i
-// iff d2 < (2 max(h_i, h_j))^2.  fl(t^2) is monotone in t and d2 is the same
-// bits for (i, j) and (j, i), so N_sym(i) = N(i) u {j : i in N(j)}: the gather
-// sets plus their transpose.  The pass replays the recorded gather masks
-// (query i = unit query, candidate j = lane's slot): a pair (i, j) of N(i)
-// with NOT d2 < T_j is one-sided, and i is added to row j.  Lanes = candidates,
-// so a lane collects its candidate's one-sided queries in a 64-bit mask and
-// touches j's counter once per (unit, chunk).
+// iff d2 < (2 max(h_i, h_j))^2.  The walk finds these pairs from the query
+// side: every radius of the descent, the culls and the staging becomes
+// max(R'_u, R'(h_max)) with h_max the largest h of the node / leaf tested,
+// and the pair test checks both thresholds (walk_kernel<.., kSym>).  These
+// kernels give every leaf and internal node its h_max per search.
 // ---------------------------------------------------------------------------
-__global__ void add_counts_kernel(const int32_t *__restrict__ g, const int32_t *__restrict__ x, int64_t n,
-                                  int32_t *__restrict__ out) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = g[i] + x[i];
-}
-
-// kFill = false: extra[j] += one-sided pairs (i, j).  kFill = true: append i
-// to row j at offsets[j] + gcnt[j] + (cursor extra[j], zeroed by the caller).
-template <bool kFill>
-__global__ void __launch_bounds__(kFillThreads) sym_kernel(WalkArgs a, const int32_t *__restrict__ gcnt,
-                                                           int32_t *__restrict__ extra) {
-    __shared__ double4 qs[kFillWarps][kQ];
-    __shared__ double qT[kFillWarps][kQ];
+__global__ void leaf_hmax_kernel(const double *__restrict__ h_tree, const int32_t *__restrict__ begin,
+                                 const int32_t *__restrict__ count, int64_t n_leaves, double *__restrict__ hmax) {
     const int lane = threadIdx.x & 31;
-    double4 *Q = qs[threadIdx.x >> 5];
-    double *TQ = qT[threadIdx.x >> 5];
-    WorkBatch wb;
-    for (;;) {
-        const long long u = next_unit(wb, &a.ctr[C_WORK5], a.n_units, 1, lane);
-        if (u >= a.n_units) break;
-        const int4 U = a.units[u];
-        const UnitRun R = a.urun[u];
-        const int nq = U.z;
-        __syncwarp();
-        // the queries' exact records and T_i = fl((2 h_i)^2); a pair can only be
-        // one-sided when T_j < T_i, so candidates with T_j >= max_i T_i are idle
-        double tmax = 0.0;
-        for (int q = lane; q < nq; q += 32) {
-            Q[q] = a.rec[U.y + q];
-            const double t = __dmul_rn(2.0, a.h_tree[U.y + q]);
-            TQ[q] = __dmul_rn(t, t);
-            tmax = fmax(tmax, TQ[q]);
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t L = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; L < n_leaves; L += nw) {
+        const int32_t b = begin[L], c = count[L];
+        double m = 0.0;
+        for (int32_t k = lane; k < c; k += 32) m = fmax(m, h_tree[b + k]);
+        m = warp_max(m);
+        if (lane == 0) hmax[L] = m;
+    }
+}
+// internal nodes of one depth [n0, n1): every cell of the depth (one
+// contiguous range of the cell table) raises its node's h_max (atomic max on
+// the bit patterns: h > 0, so they order like the values); children one
+// depth deeper and leaves are done
+__global__ void node_hmax_kernel(const NodeRec *__restrict__ nodes, const int32_t *__restrict__ cells, int64_t n0,
+                                 int64_t n1, int64_t c0, int64_t c1, const double *__restrict__ leaf_hmax,
+                                 double *__restrict__ node_hmax) {
+    for (int64_t g = c0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < c1; g += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t code = cells[g];
+        double v = 0.0;
+        if (code >= 0) v = leaf_hmax[code];
+        else if (code <= -2) v = node_hmax[code_node(code)];
+        if (!(v > 0.0)) continue;
+        int64_t lo = n0, hi = n1 - 1;  // the node of cell g: largest i with cell_base <= g
+        while (lo < hi) {
+            const int64_t m = (lo + hi + 1) >> 1;
+            if (nodes[m].cell_base <= g) lo = m;
+            else hi = m - 1;
         }
-        tmax = warp_max(tmax);
-        __syncwarp();
-        const int nchk = (R.nstaged + 63) >> 6;
-        for (int k = 0; k < nchk; k++) {
-            const unsigned long long *mw = a.masks + R.mask_base + (long long)k * nq;
-            const unsigned long long w0 = lane < nq ? mw[lane] : 0ull, w1 = lane + 32 < nq ? mw[lane + 32] : 0ull;
-            if (!__any_sync(0xffffffffu, (w0 | w1) != 0ull)) continue;
-            int32_t j[2];
-            double4 c[2];
-            double T[2];
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int slot = 64 * k + 32 * h + lane;
-                const int32_t tp = slot < R.nstaged ? a.cands[R.cand_base + slot] : -1;  // tree position (kTP records)
-                j[h] = tp >= 0 ? a.perm[tp] : -1;
-                if (tp >= 0) {
-                    c[h] = a.rec[tp];
-                    const double t = __dmul_rn(2.0, a.h_tree[tp]);  // 2 h_j (exact)
-                    T[h] = __dmul_rn(t, t);
-                } else {
-                    c[h] = make_double4(0.0, 0.0, 0.0, 0.0);
-                    T[h] = 0.0;
-                }
-            }
-            const bool act0 = j[0] >= 0 && T[0] < tmax, act1 = j[1] >= 0 && T[1] < tmax;
-            if (!__any_sync(0xffffffffu, act0 || act1)) continue;
-            // queries worth a visit: a non-empty mask word and T_i above the
-            // smallest T_j of an active candidate (lanes = queries here)
-            const double tlo = warp_min(fmin(act0 ? T[0] : INFINITY, act1 ? T[1] : INFINITY));
-            const unsigned long long qv =
-                (unsigned long long)__ballot_sync(0xffffffffu, w0 != 0ull && TQ[lane] > tlo) |
-                ((unsigned long long)__ballot_sync(0xffffffffu, w1 != 0ull && TQ[lane + 32] > tlo) << 32);
-            unsigned long long os[2] = {0ull, 0ull};  // bit q: (query q, this lane's candidate) one-sided
-            for (unsigned long long qq = qv; qq; qq &= qq - 1ull) {
-                const int q = __ffsll((long long)qq) - 1;
-                const unsigned long long m = __shfl_sync(0xffffffffu, q < 32 ? w0 : w1, q & 31);
-                const double Ti = TQ[q];
-                const bool b0 = act0 && ((m >> lane) & 1ull) && T[0] < Ti;
-                const bool b1 = act1 && ((m >> (32 + lane)) & 1ull) && T[1] < Ti;
-                if (b0 || b1) {
-                    const double4 qr = Q[q];
-#pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        if (h == 0 ? b0 : b1) {
-                            // the predicate's d2, bit for bit (no contraction)
-                            const double dx = __dsub_rn(qr.x, c[h].x), dy = __dsub_rn(qr.y, c[h].y),
-                                         dz = __dsub_rn(qr.z, c[h].z);
-                            const double d2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
-                            if (!(d2 < T[h])) os[h] |= 1ull << q;
-                        }
-                    }
-                }
-            }
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                if (!os[h]) continue;
-                const int cnt = __popcll(os[h]);
-                if constexpr (!kFill) {
-                    atomicAdd(&extra[j[h]], cnt);
-                } else {
-                    int32_t *dst = a.nbr + a.offsets[j[h]] + gcnt[j[h]] + atomicAdd(&extra[j[h]], cnt);
-                    unsigned long long m = os[h];
-                    BT_DEV_CHECK(dst - a.nbr + cnt <= a.nbr_cap);
-                    while (m) {
-                        const int q = __ffsll((long long)m) - 1;
-                        m &= m - 1ull;
-                        *dst++ = (int32_t)__double_as_longlong(Q[q].w);  // caller index of query q
-                    }
-                }
-            }
-        }
+        atomicMax((unsigned long long *)&node_hmax[lo], (unsigned long long)__double_as_longlong(v));
     }
 }
 
@@ -1443,10 +1552,10 @@ __global__ void gather_m_kernel(const int32_t *__restrict__ perm, const double *
 }
 
 struct Grids {
-    unsigned d, w, f, big, s;
+    unsigned d, w, f, big;
 };
 
-template <bool kDensity>
+template <bool kDensity, bool kSym = false>
 Grids walk_grids() {
     const int sms = num_sms();
     auto grid_of = [&](const void *fn, int threads) {
@@ -1454,10 +1563,9 @@ Grids walk_grids() {
         BT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0));
         return (unsigned)(sms * std::max(per_sm, 1));
     };
-    return Grids{grid_of((const void *)desc_kernel<false>, kDescThreads),
-                 grid_of((const void *)walk_kernel<kDensity, false>, kWalkThreads),
-                 grid_of((const void *)fill_kernel<false>, kCsrThreads), (unsigned)std::min(sms, 32),
-                 grid_of((const void *)sym_kernel<false>, kFillThreads)};
+    return Grids{grid_of((const void *)desc_kernel<false, kSym>, kDescThreads),
+                 grid_of((const void *)walk_kernel<kDensity, kSym>, kWalkThreads),
+                 grid_of((const void *)fill_kernel, kCsrThreads), (unsigned)std::min(sms, 32)};
 }
 
 // h in tree order (validated) + its checksum
@@ -1538,6 +1646,7 @@ void check_offsets(TreeDev &t, const int64_t *offsets, const int32_t *c1, const 
 
 // A10: candidate-leaf lists of all units; the leaf-list arena is estimated
 // (grown and redone on overflow).  Leaves the counters in hc.
+template <bool kSym>
 void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
     cudaStream_t st = stream();
     double list_per_unit = 96.0;
@@ -1549,7 +1658,7 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
         for (int c : {C_WORK, C_LIST, C_BIG, C_WORK4, C_NEEDC, C_NEEDM}) zero_counter(t, c);
         {
             Phase ph("search.desc");
-            desc_kernel<false><<<g.d, kDescThreads, 0, st>>>(a);
+            desc_kernel<false, kSym><<<g.d, kDescThreads, 0, st>>>(a);
             BT_LAUNCH("walk_desc");
         }
         read_counters(t, hc);
@@ -1560,7 +1669,7 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
             a.front = t.front.p;
             a.front_cap = std::max<int64_t>(t.n_nodes, 1);
             Phase ph("search.desc_big");
-            desc_kernel<true><<<g.big, kDescThreads, 0, st>>>(a);
+            desc_kernel<true, kSym><<<g.big, kDescThreads, 0, st>>>(a);
             BT_LAUNCH("walk_desc_big");
             read_counters(t, hc);
         }
@@ -1573,10 +1682,35 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
 
 }  // namespace
 
-void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
-                    int64_t capacity, bool count_pass, bool fill_pass, bool cand_tp) {
+namespace {
+
+// h_max of every leaf and internal node (symmetric criterion): leaves from
+// h_tree, internal nodes bottom-up, one launch per depth
+void compute_hmax(TreeDev &t) {
+    cudaStream_t st = stream();
+    const int sms = num_sms();
+    t.leaf_hmax.reserve(std::max<int64_t>(t.n_leaves, 1), 0);
+    t.node_hmax.reserve(std::max<int64_t>(t.n_nodes, 1), 0);
+    leaf_hmax_kernel<<<grid_for(t.n_leaves * 32, 256, (int64_t)sms * 16), 256, 0, st>>>(
+        t.h_tree.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_hmax.p);
+    BT_LAUNCH("leaf_hmax");
+    if (t.n_nodes > 0) BT_CUDA(cudaMemsetAsync(t.node_hmax.p, 0, t.n_nodes * sizeof(double), st));
+    for (int64_t d = (int64_t)t.level_begin.size() - 2; d >= 0; d--) {
+        const int64_t n0 = t.level_begin[d], n1 = t.level_begin[d + 1];
+        if (n1 <= n0) continue;
+        const int64_t c0 = t.level_cells[d], c1 = t.level_cells[d + 1];
+        node_hmax_kernel<<<grid_for(c1 - c0, 256, (int64_t)sms * 16), 256, 0, st>>>(
+            t.nodes.p, t.cells.p, n0, n1, c0, c1, t.leaf_hmax.p, t.node_hmax.p);
+        BT_LAUNCH("node_hmax");
+    }
+}
+
+template <bool kSym>
+void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx, int64_t capacity,
+            bool count_pass, bool fill_pass) {
     cudaStream_t st = stream();
     const int64_t n = t.n;
+    const char *who = kSym ? "bt_find_neighbors_sym" : "bt_find_neighbors";
     if (n == 0) {
         if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
         t.total_pairs = t.max_count = t.staged = t.loaded = t.tests = t.exact_tests = t.rows_over_ngmax = 0;
@@ -1584,13 +1718,13 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         return;
     }
     const int sms = num_sms();
-    const long long hsum = gather_h(t, h, "bt_find_neighbors");
-    const Grids g = walk_grids<false>();
+    const long long hsum = gather_h(t, h, who);
+    const Grids g = walk_grids<false, kSym>();
 
     // the recorded masks of a previous test pass are reused by a fill-only
-    // call when the tree, h pointer, exactness mode and h checksum all match
+    // call when the tree, h pointer, exactness mode, criterion and h checksum all match
     const bool have_record = t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only &&
-                             t.rec_tp == cand_tp;
+                             t.rec_sym == kSym;
     const bool run_test = count_pass || !have_record;
 
     WalkArgs a = walk_args(t, g);
@@ -1610,10 +1744,15 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
         // partitioned tree: particles of other parts keep count 0 (empty rows)
         if (t.nparts > 1) BT_CUDA(cudaMemsetAsync(cnt, 0, n * sizeof(int32_t), st));
         a.counts = cnt;
+        if (kSym) {
+            Phase ph("search.hmax");
+            compute_hmax(t);
+            a.leaf_hmax = t.leaf_hmax.p;
+            a.node_hmax = t.node_hmax.p;
+        }
         long long hc[C_N];
         t.rec_valid = false;
-        t.sym_valid = false;
-        run_descent(t, a, g, hc);
+        run_descent<kSym>(t, a, g, hc);
         const long long warps_w = (long long)g.w * (kWalkThreads / 32);
         {  // A10 staging + A11 pair tests, counts, masks; candidate and mask arenas: exact bounds from the descent
             t.arena_cands.reserve(hc[C_NEEDC] + warps_w * kCandSlab, 0);
@@ -1624,24 +1763,26 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
             a.mask_cap = (long long)t.arena_masks.n;
             t.scratch.reserve(warps_w * kScratch, 0);
             a.scratch = t.scratch.p;
+            DBuf<float> scrk;
+            if (kSym) {
+                scrk.alloc(warps_w * kScratch);
+                a.scrk = scrk.p;
+            }
             for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT, C_CSUM, C_NZW}) zero(c);
             {
                 Phase ph("search.count");
-                if (cand_tp)
-                    walk_kernel<false, true><<<g.w, kWalkThreads, 0, st>>>(a);
-                else
-                    walk_kernel<false, false><<<g.w, kWalkThreads, 0, st>>>(a);
-                BT_LAUNCH("walk_test");
+                walk_kernel<false, kSym><<<g.w, kWalkThreads, 0, st>>>(a);
+                BT_LAUNCH(kSym ? "walk_test_sym" : "walk_test");
             }
             read_counters(t, hc);
             const bool fits = hc[C_CAND] <= a.cand_cap && hc[C_MASK] <= a.mask_cap;
-            if (!fits) throw Error(BT_ERR_CUDA, "bt_find_neighbors: internal: walk arena bound exceeded");
+            if (!fits) throw Error(BT_ERR_CUDA, std::string(who) + ": internal: walk arena bound exceeded");
             t.rec_valid = true;
             t.rec_csum = hc[C_CSUM];
             t.rec_h = h;
             t.rec_hsum = hsum;
             t.rec_exact = g_exact_only;
-            t.rec_tp = cand_tp;
+            t.rec_sym = kSym;
         }
         t.staged = hc[C_STAGED];
         t.loaded = hc[C_LOADED];
@@ -1674,118 +1815,28 @@ void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offse
     t.total_pairs = total;
     if (!fill_pass || nbr_idx == nullptr) return;
     if (total > capacity)
-        throw Error(BT_ERR_CAPACITY, "bt_find_neighbors: " + std::to_string(total) + " neighbor pairs exceed capacity " +
+        throw Error(BT_ERR_CAPACITY, std::string(who) + ": " + std::to_string(total) + " neighbor pairs exceed capacity " +
                                          std::to_string(capacity));
-    if (!t.rec_valid) throw Error(BT_ERR_CUDA, "bt_find_neighbors: internal: no recorded test pass");
-    if (!count_pass) check_offsets(t, offsets, cnt_now, nullptr, true, "bt_fill_neighbors");
+    if (!t.rec_valid) throw Error(BT_ERR_CUDA, std::string(who) + ": internal: no recorded test pass");
+    if (!count_pass) check_offsets(t, offsets, cnt_now, nullptr, true, kSym ? "bt_fill_neighbors_sym" : "bt_fill_neighbors");
     a.masks = t.arena_masks.p;
     a.cands = t.arena_cands.p;
     zero(C_WORK2);
     {
         Phase ph("search.fill");
-        if (t.rec_tp)
-            fill_kernel<true><<<g.f, kCsrThreads, 0, st>>>(a);
-        else
-            fill_kernel<false><<<g.f, kCsrThreads, 0, st>>>(a);
+        fill_kernel<<<g.f, kCsrThreads, 0, st>>>(a);
         BT_LAUNCH("walk_fill");
     }
     BT_CUDA(cudaStreamSynchronize(st));
 }
 
+}  // namespace
 
-// Symmetric criterion (reading R22): the gather test pass (recorded masks,
-// gather counts in t.sym_g), then sym_kernel<false> counts the one-sided pairs
-// per row (t.sym_x); counts = gather + extra.  The fill writes each row's
-// gather part with fill_kernel at the symmetric offsets and appends the
-// transposed one-sided pairs with sym_kernel<true>.
-void find_neighbors_sym(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
-                        int64_t capacity, bool count_pass, bool fill_pass) {
-    cudaStream_t st = stream();
-    const int64_t n = t.n;
-    if (n == 0) {
-        if (offsets && count_pass) BT_CUDA(cudaMemsetAsync(offsets, 0, sizeof(int64_t), st));
-        t.total_pairs = t.max_count = t.rows_over_ngmax = 0;
-        BT_CUDA(cudaStreamSynchronize(st));
-        return;
-    }
-    if (t.nparts > 1)
-        throw Error(BT_ERR_ARG, "bt_find_neighbors_sym: the symmetric criterion needs the whole tree (bt_set_partition 0, 1)");
-    const int sms = num_sms();
-    const Grids g = walk_grids<false>();
-    t.sym_g.reserve(n, 0);
-    t.sym_x.reserve(n, 0);
-    t.sym_off.reserve(n + 1, 0);
-    bool have = false;
-    if (!count_pass) {
-        const long long hsum = gather_h(t, h, "bt_fill_neighbors_sym");
-        have = t.sym_valid && t.rec_valid && t.rec_tp && t.rec_h == h && t.rec_hsum == hsum &&
-               t.rec_exact == g_exact_only;
-    }
-    if (!have) {
-        // gather counts + recorded masks, candidates recorded as tree positions
-        find_neighbors(t, h, t.sym_g.p, t.sym_off.p, nullptr, 0, true, false, true);
-        WalkArgs a = walk_args(t, g);
-        a.masks = t.arena_masks.p;
-        a.cands = t.arena_cands.p;
-        BT_CUDA(cudaMemsetAsync(t.sym_x.p, 0, n * sizeof(int32_t), st));
-        zero_counter(t, C_WORK5);
-        {
-            Phase ph("search.sym_count");
-            sym_kernel<false><<<g.s, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
-            BT_LAUNCH("sym_count");
-        }
-        t.sym_valid = true;
-    }
-    if (count_pass) {
-        add_counts_kernel<<<grid_for(n, 256, (int64_t)sms * 16), 256, 0, st>>>(t.sym_g.p, t.sym_x.p, n, counts);
-        BT_LAUNCH("sym_add_counts");
-        DBuf<long long> dtot(1);
-        Phase ph("search.scan");
-        device_scan<long long>(CountIn{counts}, OffsetOut{offsets}, n, dtot.p);
-        write_total_kernel<<<1, 1, 0, st>>>(offsets, n, dtot.p);
-        BT_LAUNCH("write_total");
-        zero_counter(t, C_MAXC);
-        zero_counter(t, C_OVER);
-        max_count_kernel<<<grid_for(n, 256, (int64_t)sms * 8), 256, 0, st>>>(counts, n, t.ngmax,
-                                                                              (long long *)t.counters.p + C_MAXC);
-        BT_LAUNCH("max_count");
-    }
-    int64_t total = 0, maxc = 0, over = 0;
-    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)},
-               {t.counters.p + C_OVER, &over, sizeof(int64_t)}});
-    if (count_pass) {
-        t.max_count = maxc;
-        t.rows_over_ngmax = over;
-    }
-    t.total_pairs = total;
-    if (!fill_pass || nbr_idx == nullptr) return;
-    if (total > capacity)
-        throw Error(BT_ERR_CAPACITY, "bt_find_neighbors_sym: " + std::to_string(total) +
-                                         " neighbor pairs exceed capacity " + std::to_string(capacity));
-    if (!count_pass) check_offsets(t, offsets, t.sym_g.p, t.sym_x.p, false, "bt_fill_neighbors_sym");
-    WalkArgs a = walk_args(t, g);
-    a.masks = t.arena_masks.p;
-    a.cands = t.arena_cands.p;
-    a.offsets = offsets;
-    a.nbr = nbr_idx;
-    a.nbr_cap = capacity;
-    zero_counter(t, C_WORK2);
-    zero_counter(t, C_WORK5);
-    BT_CUDA(cudaMemsetAsync(t.sym_x.p, 0, n * sizeof(int32_t), st));  // append cursors
-    {
-        Phase ph("search.fill");
-        fill_kernel<true><<<g.f, kCsrThreads, 0, st>>>(a);  // symmetric pass: tree-position records
-        BT_LAUNCH("walk_fill");
-    }
-    {
-        Phase ph("search.sym_fill");
-        sym_kernel<true><<<g.s, kFillThreads, 0, st>>>(a, t.sym_g.p, t.sym_x.p);
-        BT_LAUNCH("sym_fill");
-    }
-    t.sym_valid = false;  // the cursors overwrote the extra counts
-    BT_CUDA(cudaStreamSynchronize(st));
+void find_neighbors(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int32_t *nbr_idx,
+                    int64_t capacity, bool count_pass, bool fill_pass, bool sym) {
+    if (sym) search<true>(t, h, counts, offsets, nbr_idx, capacity, count_pass, fill_pass);
+    else search<false>(t, h, counts, offsets, nbr_idx, capacity, count_pass, fill_pass);
 }
-
 
 // SPH density with the neighbor search fused in: the
 // descent and the walk as in find_neighbors, the walk in density mode (no
@@ -1814,8 +1865,7 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
     a.rho = rho;
     long long hc[C_N];
     t.rec_valid = false;  // the density walk records no masks
-    t.sym_valid = false;
-    run_descent(t, a, g, hc);
+    run_descent<false>(t, a, g, hc);
     const long long warps_w = (long long)g.w * (kWalkThreads / 32);
     t.scratch.reserve(warps_w * kScratch, 0);
     a.scratch = t.scratch.p;

@@ -37,6 +37,6 @@ def test_value_helpers():
     assert bench.weak_value(1000, 4, 2.0) == pytest.approx(4000 / 2e-3)
     assert bench.strong_value(1000, 2.0) == pytest.approx(1000 / 2e-3)
     c = bench.config_block(5, None, 2)
-    assert c["N_per_gpu"] == 2 ** 25 and "sub-domain x2" in c["parallelism"]
+    assert c["N_per_gpu"] == 2 ** 25 and "replicas only: 2 independent sub-domains" in c["parallelism"]
     r = bench.config_block(5, None, 8, "replicated")
     assert r["N_total"] == 2 ** 25 and "replicated" in r["parallelism"]

@@ -1,4 +1,4 @@
-# time the walk at cfg 5 for each library variant paper_1910_02639_b200/libbtree_*.so
+# time the search at config $1 (default 5) for each library variant paper_1910_02639_b200/libbtree_*.so ($2: extra run_case flags)
 mkdir -p gpurun_out
 for f in paper_1910_02639_b200/libbtree_*.so; do
   v=$(basename $f .so)
