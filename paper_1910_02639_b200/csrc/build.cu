@@ -32,6 +32,9 @@ namespace bt {
 namespace {
 
 constexpr int kThreads = 256;
+#ifndef BT_SCATTER_UNROLL
+#define BT_SCATTER_UNROLL 4  // particles per thread in flight in key_hist / scatter
+#endif
 
 struct LevelNode {
     int32_t act_begin;   // first active particle of this node (level array)
@@ -185,20 +188,33 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__res
                                                             int64_t n_act, const LevelNode *__restrict__ ln,
                                                             const NodeRec *__restrict__ nodes, uint32_t *__restrict__ keys,
                                                             int32_t *__restrict__ hist, int round) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_act; p += (int64_t)gridDim.x * blockDim.x) {
-        int32_t node = act_node[p];
-        const LevelNode &L = ln[node];
-        if (round > 0 && !L.flag) continue;
-        const NodeRec &nr = nodes[L.gid];
-        double4 r = act[p];
-        int b = L.b;
-        // Eq. 2 (cell_coord_fast: identical results, division only near cell faces)
-        int c1 = cell_coord_fast(r.x, nr.lo[0], nr.ext[0], L.bx[0], b);
-        int c2 = cell_coord_fast(r.y, nr.lo[1], nr.ext[1], L.bx[1], b);
-        int c3 = cell_coord_fast(r.z, nr.lo[2], nr.ext[2], L.bx[2], bz_of(b, L.kz));
-        uint32_t j = (uint32_t)c1 + (uint32_t)c2 * (uint32_t)b + (uint32_t)c3 * (uint32_t)b * (uint32_t)b;
-        keys[p] = j;
-        atomicAdd(&hist[L.cell_base + j], 1);
+    // (BT_SCATTER_UNROLL particles per thread: independent load chains in flight)
+    constexpr int U = BT_SCATTER_UNROLL;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n_act; p0 += U * stride) {
+        int32_t node[U];
+        double4 r[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t p = p0 + u * stride;
+            node[u] = p < n_act ? act_node[p] : -1;
+            if (node[u] >= 0) r[u] = act[p];
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (node[u] < 0) continue;
+            const LevelNode &L = ln[node[u]];
+            if (round > 0 && !L.flag) continue;
+            const NodeRec &nr = nodes[L.gid];
+            const int b = L.b;
+            // Eq. 2 (cell_coord_fast: identical results, division only near cell faces)
+            const int c1 = cell_coord_fast(r[u].x, nr.lo[0], nr.ext[0], L.bx[0], b);
+            const int c2 = cell_coord_fast(r[u].y, nr.lo[1], nr.ext[1], L.bx[1], b);
+            const int c3 = cell_coord_fast(r[u].z, nr.lo[2], nr.ext[2], L.bx[2], bz_of(b, L.kz));
+            const uint32_t j = (uint32_t)c1 + (uint32_t)c2 * (uint32_t)b + (uint32_t)c3 * (uint32_t)b * (uint32_t)b;
+            keys[p0 + u * stride] = (uint32_t)(L.cell_base + j);  // the level's cell index (< 2^32)
+            atomicAdd(&hist[L.cell_base + j], 1);
+        }
     }
 }
 
@@ -290,13 +306,13 @@ struct CellBaseOut {
 };
 
 // ---- A8: children, leaves, cell table --------------------------------------
-__global__ void __launch_bounds__(kThreads) emit_kernel(const LevelNode *__restrict__ ln, int64_t nn, const int32_t *__restrict__ hist,
+__global__ void __launch_bounds__(kThreads) emit_kernel(const LevelNode *__restrict__ ln, int64_t nn, int32_t *hist,
                                                         int64_t ncells, const int64_t *__restrict__ cpre,
                                                         const int32_t *__restrict__ cid, const int32_t *__restrict__ cact,
                                                         NodeRec *nodes, int32_t *cells, int64_t cells_base,
                                                         LevelNode *ln_next, int32_t next_gid_base, int32_t *leaf_begin,
                                                         int32_t *leaf_count, int32_t *leaf_depth, int64_t leaf_base,
-                                                        int32_t child_depth, int2 *cmove, int32_t s) {
+                                                        int32_t child_depth, int32_t s) {
     for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ncells; g += (int64_t)gridDim.x * blockDim.x) {
         int64_t node = find_node(ln, nn, g);
         const LevelNode &L = ln[node];
@@ -331,14 +347,15 @@ __global__ void __launch_bounds__(kThreads) emit_kernel(const LevelNode *__restr
                 R.b = 0;
                 R.cell_base = 0;
                 code = node_code(gid);
-                cmove[g] = make_int2(cact[g], id);  // next-level position, child node (level-local)
+                // the scatter's cursor: next-level position, bit 31 = child node
+                hist[g] = (int32_t)((unsigned)cact[g] | 0x80000000u);
             } else {
                 int64_t leaf = leaf_base + id;
                 leaf_begin[leaf] = final_pos;
                 leaf_count[leaf] = c;
                 leaf_depth[leaf] = child_depth;
                 code = (int32_t)leaf;
-                cmove[g] = make_int2(final_pos, -1);  // final tree position, leaf
+                hist[g] = final_pos;  // the scatter's cursor: final tree position (leaf)
             }
         }
         cells[cells_base + g] = code;
@@ -359,20 +376,35 @@ __global__ void finalize_level_nodes_kernel(const LevelNode *ln, int64_t nn, Nod
 }
 
 // ---- A7: counting-sort scatter ------------------------------------------------
-__global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__restrict__ act, const int32_t *__restrict__ act_node,
-                                                           int64_t n_act, const LevelNode *__restrict__ ln,
-                                                           const uint32_t *__restrict__ keys, int32_t *__restrict__ cursor,
-                                                           const int2 *__restrict__ cmove,
+// Latency-bound per particle (node record -> cell -> returning atomic on the
+// cell cursor -> destination): kUnroll particles per thread keep that many
+// independent chains in flight.
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__restrict__ act, int64_t n_act,
+                                                           const uint32_t *__restrict__ keys, int32_t *cursor,
                                                            double4 *__restrict__ out_final, double4 *__restrict__ act_next) {
-    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < n_act; p += (int64_t)gridDim.x * blockDim.x) {
-        int32_t node = act_node[p];
-        int64_t g = ln[node].cell_base + keys[p];
-        int32_t r = atomicAdd(&cursor[g], 1);
-        const int2 mv = cmove[g];  // one random 8-byte load per particle
-        double4 v = act[p];
-        int32_t dst = mv.x + r;
-        if (mv.y < 0) out_final[dst] = v;
-        else act_next[dst] = v;  // (its node id: node_ids_kernel, coalesced)
+    // cursor[g] (written by emit): the cell's next destination, bit 31 set
+    // for a child-node cell (next level's active array) -- one returning
+    // atomic per particle gives both its slot and its destination array
+    constexpr int U = BT_SCATTER_UNROLL;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n_act; p0 += U * stride) {
+        int32_t d[U];
+        double4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t p = p0 + u * stride;
+            if (p < n_act) {
+                d[u] = atomicAdd(&cursor[keys[p]], 1);
+                v[u] = act[p];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            if (p0 + u * stride >= n_act) continue;
+            const int32_t dst = (int32_t)((unsigned)d[u] & 0x7fffffffu);
+            if (d[u] < 0) act_next[dst] = v[u];  // (its node id: node_ids_kernel, coalesced)
+            else out_final[dst] = v[u];
+        }
     }
 }
 
@@ -871,7 +903,6 @@ void build_tree(TreeDev &t, const double *pos) {
         DBuf<int32_t> hist;
         DBuf<int64_t> cpre;
         DBuf<int32_t> cid, cact;
-        DBuf<int2> cmove;
         DBuf<long long> dtotal(1);
         DBuf<CellScan> dcs(1);
         while (nn > 0) {
@@ -884,11 +915,12 @@ void build_tree(TreeDev &t, const double *pos) {
             long long ncells_h = 0;
             read_back({{dtotal.p, &ncells_h, sizeof(long long)}});
             const int64_t ncells = ncells_h;
+            if (ncells > (int64_t)0xffffffffLL)  // (keys hold a level's cell index in 32 bits)
+                throw Error(BT_ERR_OOM, "bt_build: more than 2^32 sub-cells in one level (bucket_size too small for n)");
             hist.reserve(ncells, 0);
             cpre.reserve(ncells, 0);
             cid.reserve(ncells, 0);
             cact.reserve(ncells, 0);
-            cmove.reserve(ncells, 0);
             t.cells.reserve(t.n_cells + ncells, t.n_cells);
             BT_CUDA(cudaMemsetAsync(hist.p, 0, ncells * sizeof(int32_t), st));
             const unsigned gridC = grid_for(ncells, kThreads, (int64_t)sms * 16);
@@ -933,13 +965,14 @@ void build_tree(TreeDev &t, const double *pos) {
             emit_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, cpre.p, cid.p, cact.p, t.nodes.p, t.cells.p,
                                                     t.n_cells, child_ok ? ln_next.p : nullptr, (int32_t)t.n_nodes,
                                                     t.leaf_begin.p, t.leaf_count.p, t.leaf_depth.p, t.n_leaves,
-                                                    level + 1, cmove.p, t.s);
+                                                    level + 1, t.s);
             BT_LAUNCH("emit");
 
-            // A7: scatter (cursor = zeroed histogram)
-            BT_CUDA(cudaMemsetAsync(hist.p, 0, ncells * sizeof(int32_t), st));
-            scatter_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, keys.p, hist.p, cmove.p,
-                                                       fin.p, act[cur ^ 1].p);
+            // A7: scatter (cursors initialised by emit in the histogram).  (A two-pass variant --
+            // particles first grouped by coarse cell range so the scatter's
+            // destination window stays L2-resident -- measured slower in round 2:
+            // cfg 5 levels 3.9 -> 5.1 ms.)
+            scatter_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, n_act, keys.p, hist.p, fin.p, act[cur ^ 1].p);
             BT_LAUNCH("scatter");
             if (nn_next > 0) {
                 node_ids_kernel<<<grid_for(nn_next * 32, kThreads, (int64_t)sms * 16), kThreads, 0, st>>>(

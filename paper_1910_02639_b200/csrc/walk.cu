@@ -188,7 +188,11 @@ __device__ __forceinline__ double l4_eps(double E) { return 16.02 * 0x1p-24 * E 
 // k = 0 ("force": exact-only, E >= 1e15, or a bound that fails) sends every
 // pair to the fp64 predicate.  A unit uses the minimum k over its queries
 // (1/k only grows, the band only widens).
-__device__ __forceinline__ void l4_band(double T, double E, double eps, bool exact_only, float &k, float &Mid) {
+// (t = 2h exactly, T = fl(t t): sqrt(T-) < t and sqrt(T+) <= t (1 + 2^-48)
+// stand in for the square roots, and the power of two comes from hw's
+// exponent -- no fp64 sqrt or division per query.)
+__device__ __forceinline__ void l4_band(double T, double t, double E, double eps, bool exact_only, float &k,
+                                        float &Mid) {
     k = 0.0f;
     Mid = 0.0f;
     if (exact_only || !(E < 1e15)) return;
@@ -196,15 +200,16 @@ __device__ __forceinline__ void l4_band(double T, double E, double eps, bool exa
     const double Ep = E * (1.0 + 1e-6) + 5.0 * eps;
     const double Tm = T * (1.0 - 8.0 * u64), Tp = T * (1.0 + 8.0 * u64);
     const double G = u * (60.1 * Ep * Ep + 5.01 * (2.0 * Tp));  // Mid <= B <= 2 T+ (checked below)
-    auto err = [&](double S) { return (4.0 * s3 * eps * sqrt(S) + 12.0 * eps * eps + G) * 1.0001; };
-    if (!(2.0 * s3 * eps * 1.0001 <= 0.5 * sqrt(Tm))) return;  // S - Err(S) increasing on [T-, inf)
-    const double A = Tm - err(Tm), B = Tp + err(Tp);
+    // S - Err(S) increasing on [T-, inf): 2 sqrt3 eps <= sqrt(T-) / 2, sqrt(T-) >= t (1 - 2^-48)
+    if (!(2.0 * s3 * eps * 1.0001 <= 0.5 * t * (1.0 - 0x1p-48))) return;
+    const double A = Tm - (4.0 * s3 * eps * t + 12.0 * eps * eps + G) * 1.0001;                       // sqrt(T-) < t
+    const double B = Tp + (4.0 * s3 * eps * t * (1.0 + 0x1p-48) + 12.0 * eps * eps + G) * 1.0001;  // sqrt(T+) bound
     if (!(A > 0.0) || !(B <= 2.0 * Tp)) return;
     const float M = __double2float_rn(0.5 * (A + B));
     double hw = fmax(fmax((double)M - A, B - (double)M), (double)M * 0x1p-23) * (1.0 + 0x1p-40);
     int e;
-    frexp(1.0 / hw, &e);                       // 1/hw = f 2^e, f in [0.5, 1)
-    const double kd = ldexp(1.0, e - 1);       // largest power of two <= 1/hw
+    const double f = frexp(hw, &e);                      // hw = f 2^e, f in [0.5, 1): 1/hw in (2^-e, 2^(1-e)]
+    const double kd = ldexp(1.0, f == 0.5 ? 1 - e : -e); // largest power of two <= 1/hw
     // the expanded form's magnitudes stay far below fp32 overflow
     if (!(kd * (12.0 * Ep * Ep + (double)M) < 1e36) || !(2.0 * kd * Ep < 1e36)) return;
     k = (float)kd;
@@ -251,7 +256,7 @@ struct UnitGeom {
     double lo[3], hi[3], c[3];
     double Ru, Ru2, Rx, E;  // R'_u, its square, the largest cull radius, the coordinate bound
     // this lane's queries (lane, lane + 32): fp64 coordinates, (2h)^2, caller index
-    double qx[2], qy[2], qz[2], qT[2];
+    double qx[2], qy[2], qz[2], qT[2], qt[2];
     int32_t qo[2];
 };
 
@@ -266,7 +271,7 @@ __device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, in
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         const int k = lane + 32 * h;
-        G.qx[h] = G.qy[h] = G.qz[h] = G.qT[h] = 0.0;
+        G.qx[h] = G.qy[h] = G.qz[h] = G.qT[h] = G.qt[h] = 0.0;
         G.qo[h] = 0;
         if (k < G.nq) {
             const double4 r = a.rec[G.q0 + k];
@@ -275,6 +280,7 @@ __device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, in
             G.qy[h] = r.y;
             G.qz[h] = r.z;
             G.qT[h] = __dmul_rn(t, t);
+            G.qt[h] = t;
             G.qo[h] = (int32_t)__double_as_longlong(r.w);
             // R' = 2h (1 + 2^-40) + 2^-50 M   (lemma L1/L2)
             Ru = fmax(Ru, __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M)));
@@ -651,7 +657,7 @@ struct WalkSmem {
     float4 q0[kQ + 1];              // ax, ax, ay, ay  (fp32, relative to the unit centre)
     float4 q1[kQ + 1];              // az, az, c, c   (band map d' = s k + c); [kQ]: look-ahead pad
     int self[kQ];                   // unit slot of each query's own record (-1: none)
-    unsigned long long mask[2][kQ]; // the block's neighbor masks [chunk][query]
+    unsigned long long mask[kQ][2]; // the block's neighbor masks [query][chunk] (one 16-B store per query)
     int ldel[kGroup];               // group leaves: first tree position - exclusive prefix of counts
     unsigned lstart[kGroupPos / 32];       // group positions: bit p set where a leaf starts (p = 32 w + bit)
     unsigned char lwpre[kGroupPos / 32];   // leaves starting before word w
@@ -755,7 +761,7 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
             if (lane == 0) {
                 const unsigned long long fm = ((unsigned long long)f1 << 32) | f0;
                 const unsigned long long em = ((unsigned long long)m1 << 32) | m0;
-                S.mask[k][q] = (S.mask[k][q] & ~fm) | em;
+                S.mask[q][k] = (S.mask[q][k] & ~fm) | em;
             }
             exact += __popc(f0) + __popc(f1);
             __syncwarp();
@@ -839,8 +845,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
                 m3 = __ballot_sync(0xffffffffu, fminf(hi_f(vib), hi_f(vjb)) < 0.0f);
             }
             if (lane == 0) {
-                S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
-                S.mask[1][q] = ((unsigned long long)m3 << 32) | m2;
+                *reinterpret_cast<ulonglong2 *>(S.mask[q]) =
+                    make_ulonglong2(((unsigned long long)m1 << 32) | m0, ((unsigned long long)m3 << 32) | m2);
             }
         }
     } else if (nch == 2) {
@@ -859,8 +865,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             const unsigned m2 = __ballot_sync(0xffffffffu, lo_f(db) < 0.0f);
             const unsigned m3 = __ballot_sync(0xffffffffu, hi_f(db) < 0.0f);
             if (lane == 0) {
-                S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
-                S.mask[1][q] = ((unsigned long long)m3 << 32) | m2;
+                *reinterpret_cast<ulonglong2 *>(S.mask[q]) =
+                    make_ulonglong2(((unsigned long long)m1 << 32) | m0, ((unsigned long long)m3 << 32) | m2);
             }
         }
     } else {
@@ -874,7 +880,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             bmin = fminf(bmin, fminf(fabsf(lo_f(da)), fabsf(hi_f(da))));
             const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(da) < 0.0f);
             const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(da) < 0.0f);
-            if (lane == 0) S.mask[0][q] = ((unsigned long long)m1 << 32) | m0;
+            if (lane == 0) S.mask[q][0] = ((unsigned long long)m1 << 32) | m0;
         }
     }
     const bool band = S.u.force != 0 || bmin <= 1.0f;
@@ -893,7 +899,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
         const int q = lane + 32 * h;
         if (q < nq) {
             const int sl = S.self[q] - us0;
-            unsigned long long m0 = S.mask[0][q], m1 = nch > 1 ? S.mask[1][q] : 0ull;
+            unsigned long long m0 = S.mask[q][0], m1 = nch > 1 ? S.mask[q][1] : 0ull;
             if (sl >= 0 && sl < n) {
                 if (sl < 64) m0 &= ~(1ull << sl);
                 else m1 &= ~(1ull << (sl - 64));
@@ -901,8 +907,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             inc[h] = __popcll(m0) + __popcll(m1);
             nzw += (m0 != 0ull) + (m1 != 0ull);
             if constexpr (kDensity) {
-                S.mask[0][q] = m0;
-                S.mask[1][q] = m1;
+                S.mask[q][0] = m0;
+                S.mask[q][1] = m1;
             } else if (dst) {
                 BT_DEV_CHECK(S.u.mask_base + (long long)(us0 >> 6) * nq + (nch > 1 ? nq : 0) + q < a.mask_cap);
                 __stcs(&dst[q], m0);
@@ -928,7 +934,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
                 const float qx = qr.x, qy = qr.y, qz = qr.z, hinv = S.d.hinv[q];
                 float acc = 0.0f;
                 for (int k = 0; k < 2 * nch; k++) {  // 32-bit halves of the chunk masks
-                    unsigned m = (unsigned)(S.mask[k >> 1][q] >> (32 * (k & 1)));
+                    unsigned m = (unsigned)(S.mask[q][k >> 1] >> (32 * (k & 1)));
                     while (m) {
                         const int sl = 32 * k + __ffs(m) - 1;
                         m &= m - 1u;
@@ -1105,7 +1111,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             } else {
 #pragma unroll
                 for (int h = 0; h < 2; h++)
-                    if (lane + 32 * h < G.nq) l4_band(G.qT[h], G.E, eps, a.exact_only != 0, kq[h], mid[h]);
+                    if (lane + 32 * h < G.nq) l4_band(G.qT[h], G.qt[h], G.E, eps, a.exact_only != 0, kq[h], mid[h]);
                 // unit band scale: the minimum power of two (0 = force)
                 ku = fminf(kq[0], kq[1]);
                 for (int d = 16; d; d >>= 1) ku = fminf(ku, __shfl_xor_sync(0xffffffffu, ku, d));
