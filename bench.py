@@ -243,19 +243,26 @@ def run_reference(args):
         return 0
     pos, h = datagen.make_config(args.config, n=args.n)
     n = pos.shape[0]
-    steps = []
+    steps, walls = [], []
     desc = cores = None
+    k = min(args.cpu_sample or default_sample(n), 200_000) if n > 4_200_000 else default_sample(n)
     for s in range(args.warmup + args.steps):
-        step_s, desc, cores, b, srch = oracle_sample(pos, h, min(args.cpu_sample or default_sample(n), 200_000)
-                                                     if n > 4_200_000 else default_sample(n))
+        w0 = time.perf_counter()
+        step_s, desc, cores, b, srch = oracle_sample(pos, h, k)
         if s >= args.warmup:
             steps.append(step_s)
+            walls.append(time.perf_counter() - w0)
     t = float(np.mean(steps))
     v = n / t
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded numpy PCG64, SURVEY 8(d) recipe)",
             "config": config_block(args.config, args.n, 1),
+            # a step times BuildTree on all N and the search of the whole workload (N <= 4.2M) or of k
+            # sampled queries; ms_per_step / value scale the sampled search to all N queries
+            "sampled": k < n, "ms_per_step_measured_wall": float(np.mean(walls)) * 1e3,
+            "full_measured_runs": "profiles/r02_oracle_baseline.jsonl (tools/oracle_baseline.py: every query, "
+                                  "1 thread and all cores)",
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -685,7 +685,7 @@ struct WalkSmemT : WalkSmem {
 // fp32 square root on the SFU (sqrt.approx: relative error ~2^-22, sqrt(0) = 0)
 __device__ __forceinline__ float sqrt_approx(float x) {
     float r;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));  // (flushing a subnormal r^2 gives r = 0: w(0), the limit)
     return r;
 }
 
@@ -766,6 +766,72 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
             exact += __popc(f0) + __popc(f1);
             __syncwarp();
         }
+    }
+    __syncwarp();
+}
+
+// Density mode (reading R21), round 2: the SPH sum needs
+// no neighbor masks.  The M4 shape vanishes at the support's edge (w(2) = 0,
+// w(2 - d) = d^3 / 4), so a pair decided differently by fp32 near r = 2h
+// changes rho by ~(its distance to the edge)^3 -- nothing at fp32 precision;
+// w(q) = max(0, 2 - q)^3 / 4 - max(0, 1 - q)^3 is the spline on both
+// pieces and 0 beyond, branch-free.  So every staged candidate is summed
+// against every query of the unit: lanes = queries (balanced: each lane owns
+// one query's sum; the self pair gives w(0) = 1, the m_i W(0, h_i) term),
+// candidates broadcast from shared memory in packed pairs, the arithmetic in
+// packed f32x2.
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ void density_block(WalkSmemT<true> &S, const WalkArgs &a, int lane, const float4 *blk, int n,
+                                              double (&dacc)[2]) {
+    float4 *P = S.d.dc;       // pair p: (x_2p, x_2p+1, y_2p, y_2p+1)
+    float4 *Qz = S.d.dc + kBlk / 2;  // pair p: (z_2p, z_2p+1, m_2p, m_2p+1)
+    float *Pf = reinterpret_cast<float *>(P), *Qf = reinterpret_cast<float *>(Qz);
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int sl = 32 * j + lane;
+        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
+        float m = 0.f;  // padding: m = 0 (no contribution)
+        if (sl < n) {
+            c = __ldcg(&blk[sl]);
+            m = (float)a.m_tree[__float_as_int(c.w)];
+        }
+        const int p = sl >> 1, o = sl & 1;
+        Pf[4 * p + o] = c.x;
+        Pf[4 * p + 2 + o] = c.y;
+        Qf[4 * p + o] = c.z;
+        Qf[4 * p + 2 + o] = m;
+    }
+    __syncwarp();
+    const int nq = S.u.nq, np = (n + 1) >> 1;
+    const unsigned long long two = pk(2.0f, 2.0f), mone = pk(-1.0f, -1.0f), mfour = pk(-4.0f, -4.0f);
+#pragma unroll 1
+    for (int h = 0; h < 2; h++) {
+        if (32 * h >= nq) break;  // (warp-uniform)
+        const int q = lane + 32 * h;
+        const float4 qr = S.d.qraw[q < nq ? q : 0];
+        const float hv = S.d.hinv[q < nq ? q : 0];
+        const unsigned long long nqx = pk(-qr.x, -qr.x), nqy = pk(-qr.y, -qr.y), nqz = pk(-qr.z, -qr.z);
+        const unsigned long long nhinv = pk(-hv, -hv);
+        unsigned long long acc = 0ull;  // (+0, +0): sum of m_j (4 w(q_ij))
+#pragma unroll 4
+        for (int p = 0; p < np; p++) {
+            const float4 A = P[p], B = Qz[p];
+            const unsigned long long dx = f2_add(pk(A.x, A.y), nqx), dy = f2_add(pk(A.z, A.w), nqy),
+                                     dz = f2_add(pk(B.x, B.y), nqz);
+            const unsigned long long r2 = f2_fma(dz, dz, f2_fma(dy, dy, f2_mul(dx, dx)));
+            const unsigned long long nq2 = f2_mul(pk(sqrt_approx(lo_f(r2)), sqrt_approx(hi_f(r2))), nhinv);  // -r / h
+            const unsigned long long t2 = f2_add(two, nq2);   // 2 - q
+            const unsigned long long t1 = f2_add(t2, mone);   // 1 - q
+            const unsigned long long u2 = pk(fmaxf(lo_f(t2), 0.f), fmaxf(hi_f(t2), 0.f));
+            const unsigned long long u1 = pk(fmaxf(lo_f(t1), 0.f), fmaxf(hi_f(t1), 0.f));
+            const unsigned long long c2 = f2_mul(f2_mul(u2, u2), u2), c1 = f2_mul(f2_mul(u1, u1), u1);
+            acc = f2_fma(pk(B.z, B.w), f2_fma(c1, mfour, c2), acc);  // m (max(0,2-q)^3 - 4 max(0,1-q)^3)
+        }
+        if (q < nq) dacc[h] += 0.25 * ((double)lo_f(acc) + (double)hi_f(acc));  // w = (...) / 4
     }
     __syncwarp();
 }
@@ -906,10 +972,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             }
             inc[h] = __popcll(m0) + __popcll(m1);
             nzw += (m0 != 0ull) + (m1 != 0ull);
-            if constexpr (kDensity) {
-                S.mask[q][0] = m0;
-                S.mask[q][1] = m1;
-            } else if (dst) {
+            if (dst) {
                 BT_DEV_CHECK(S.u.mask_base + (long long)(us0 >> 6) * nq + (nch > 1 ? nq : 0) + q < a.mask_cap);
                 __stcs(&dst[q], m0);
                 if (nch > 1) __stcs(&dst[nq + q], m1);
@@ -917,40 +980,6 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
         }
     }
     __syncwarp();
-    if constexpr (kDensity) {
-        // consumer fusion: the block's candidates (coordinates, masses) to shared
-        // memory, then lanes = queries sum m_j w(r_ij / h_i) over their set bits
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int sl = 32 * j + lane;
-            if (sl < n) S.d.dc[sl] = make_float4(c[j].x, c[j].y, c[j].z, (float)a.m_tree[__float_as_int(c[j].w)]);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int q = lane + 32 * h;
-            if (q < nq) {
-                const float4 qr = S.d.qraw[q];
-                const float qx = qr.x, qy = qr.y, qz = qr.z, hinv = S.d.hinv[q];
-                float acc = 0.0f;
-                for (int k = 0; k < 2 * nch; k++) {  // 32-bit halves of the chunk masks
-                    unsigned m = (unsigned)(S.mask[q][k >> 1] >> (32 * (k & 1)));
-                    while (m) {
-                        const int sl = 32 * k + __ffs(m) - 1;
-                        m &= m - 1u;
-                        const float4 cd = S.d.dc[sl];
-                        const float dx = cd.x - qx, dy = cd.y - qy, dz = cd.z - qz;
-                        const float r2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-                        const float qq = sqrt_approx(r2) * hinv;  // r / h (MUFU.SQRT; coincident: 0)
-                        acc = __fmaf_rn(cd.w, w_m4f(qq), acc);
-                    }
-                }
-                dacc[h] += (double)acc;
-            }
-        }
-        __syncwarp();
-    }
-    nzw = (int)__reduce_add_sync(0xffffffffu, (unsigned)nzw);
     if (lane == 0) {
         S.u.tests += (long long)n * nq;
         S.u.exact += exact;
@@ -1276,9 +1305,15 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             // ---- test phase: the staged blocks (all but a partial last one unless done)
             const int ntest = done ? nst : nst - nst % kBlk;
             for (int b0 = 0; b0 < ntest; b0 += kBlk) {
-                const int2 inc = test_block<kDensity, kSym>(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0), slot0 + b0, b0, dacc);
-                cnt0 += inc.x;
-                cnt1 += inc.y;
+                if constexpr (kDensity) {
+                    density_block(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0), dacc);
+                    if (lane == 0) S.u.tests += (long long)min(kBlk, ntest - b0) * S.u.nq;
+                } else {
+                    const int2 inc = test_block<kDensity, kSym>(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0),
+                                                                slot0 + b0, b0, dacc);
+                    cnt0 += inc.x;
+                    cnt1 += inc.y;
+                }
             }
             if (done) {
                 slot0 += nst;
@@ -1296,13 +1331,13 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         }
         const int nstaged = slot0;
         if constexpr (kDensity) {
-            // rho_i = (m_i w(0) + sum_j m_j w(r_ij / h_i)) / (pi h_i^3)   (R21)
+            // rho_i = (m_i w(0) + sum_j m_j w(r_ij / h_i)) / (pi h_i^3)   (R21; the dense sum holds the self term)
 #pragma unroll
             for (int h = 0; h < 2; h++) {
                 const int k = lane + 32 * h;
                 if (k < nq) {
                     const double hi = a.h_tree[q0 + k];
-                    a.rho[qo[h]] = (a.m_tree[q0 + k] + dacc[h]) / (3.14159265358979323846 * hi * hi * hi);
+                    a.rho[qo[h]] = dacc[h] / (3.14159265358979323846 * hi * hi * hi);  // (self: w(0) in the sum)
                 }
             }
         } else {
