@@ -112,3 +112,51 @@ def test_binding_rejects_bad_arguments(P):
     with pytest.raises(ValueError):
         P.search_host(torch.from_numpy(pos), torch.from_numpy(h), capacity=100,
                       nbr=torch.empty(10, dtype=torch.int32))          # capacity above the buffer
+
+
+def _sym_rows(P, pos, h, **kw):
+    from test_gpu_parity import sort_rows
+    t = P.build(torch.from_numpy(pos).to(DEV), kw.get("s", 64), 0.5)
+    c, o, nb = t.find_neighbors(torch.from_numpy(h).to(DEV), symmetric=True)
+    torch.cuda.synchronize()
+    return t, (c.cpu().numpy(), o.cpu().numpy(), sort_rows(c, o, nb))
+
+
+@pytest.mark.parametrize("case", ["boundary", "cfg5", "far_origin", "tiny_h", "h_spread"])
+def test_symmetric_exact_only_identical(P, oracle, case):
+    """Lemma L4s: the symmetric walk's fp32 decisions (two thresholds, one k
+    per unit, candidate thresholds that cannot decide set to +inf) give the
+    max(h_i, h_j) definition's sets, as the fp64 predicate alone does."""
+    rng = np.random.default_rng(41)
+    if case == "boundary":
+        pos, h = datagen.near_boundary(2048, 64, 43)
+        h = h * (1.0 + rng.integers(-2, 3, h.size) * 2.0 ** -50)  # thresholds within ulps of each other
+    elif case == "cfg5":
+        pos, h = datagen.make_config(5, n=200_000)
+    elif case == "far_origin":
+        pos, h = datagen.uniform(30_000, 47, 0.01, 0.03)
+        pos = np.ascontiguousarray(pos + 1.0e4)
+    elif case == "tiny_h":
+        pos, h = datagen.uniform(20_000, 53, 1e-5, 3e-5)
+        pos = np.ascontiguousarray(pos * 1e-3)
+    else:  # a few huge-h particles among small ones: node h_max radii far above the unit's own
+        pos, h = datagen.uniform(40_000, 59, 0.005, 0.01)
+        h[rng.choice(h.size, 40, replace=False)] = 0.2
+    h = np.ascontiguousarray(h)
+    ref = oracle.brute_force(pos, h, symmetric=True) if pos.shape[0] <= 50_000 else None
+    try:
+        P.set_exact_only(True)
+        _, g_exact = _sym_rows(P, pos, h)
+    finally:
+        P.set_exact_only(False)
+    _, g_fast = _sym_rows(P, pos, h)
+    assert_same(g_fast, g_exact)
+    if ref is not None:
+        assert_same(g_fast, ref)
+    else:  # sampled rows against the symmetric brute force
+        q = np.sort(rng.choice(pos.shape[0], 1500, replace=False)).astype(np.int64)
+        rc, ro, ri = oracle.brute_force(pos, h, queries=q, symmetric=True)
+        gc, go, gi = g_fast
+        assert np.array_equal(gc[q], rc)
+        for k, i in enumerate(q):
+            assert np.array_equal(gi[go[i]:go[i + 1]], ri[ro[k]:ro[k + 1]])
