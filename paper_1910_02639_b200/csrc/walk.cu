@@ -689,14 +689,6 @@ __device__ __forceinline__ float sqrt_approx(float x) {
     return r;
 }
 
-// M4 cubic spline shape (reading R21), fp32
-__device__ __forceinline__ float w_m4f(float q) {
-    const float t = 2.0f - q;
-    const float far = 0.25f * t * t * t;
-    const float near = __fmaf_rn(q * q, __fmaf_rn(0.75f, q, -1.5f), 1.0f);
-    return q < 1.0f ? near : (q < 2.0f ? far : 0.0f);
-}
-
 // The exact band of lemma L4 (rare): recompute the block's pairs with the
 // hot loop's fp32 operations and let the fp64 predicate decide every pair
 // with |d'| <= 1 (all pairs when `force`; padding slots >= n are never
@@ -883,12 +875,43 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const int sl = 32 * j + lane;
-            nk[j] = (sl < n) ? __ldcg(&S.u.scrk[b0 + sl]) : 0.f;
+            nk[j] = (sl < n) ? __ldcg(&S.u.scrk[b0 + sl]) : inf;  // (padding: u = +inf anyway)
         }
         const unsigned long long ka = pk(nk[0], nk[1]), kb = pk(nk[2], nk[3]);
         const unsigned aqm = (unsigned)__cvta_generic_to_shared(&S.qm[0]);
         unsigned long long NM;
         asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm));
+        // a block whose every candidate threshold cannot decide (all +inf: the
+        // common case inside a region of one h) tests the query thresholds alone
+        const bool red = __all_sync(0xffffffffu, nk[0] == inf && nk[1] == inf && nk[2] == inf && nk[3] == inf);
+        if (red) {
+#pragma unroll 2
+            for (int q = 0; q < nqp; q++) {
+                const float4 Q0 = N0, Q1 = N1;
+                const unsigned long long qm = NM;
+                ldq(q + 1, N0, N1);
+                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm + 8 * (q + 1)));
+                const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
+                                         bq = pk(Q1.z, Q1.w);
+                const unsigned long long via =
+                    f2_add(f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq)))), qm);
+                bmin = fminf(bmin, fminf(fabsf(lo_f(via)), fabsf(hi_f(via))));
+                const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(via) < 0.0f);
+                const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(via) < 0.0f);
+                unsigned m2 = 0u, m3 = 0u;
+                if (nch == 2) {  // (warp-uniform)
+                    const unsigned long long vib =
+                        f2_add(f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq)))), qm);
+                    bmin = fminf(bmin, fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))));
+                    m2 = __ballot_sync(0xffffffffu, lo_f(vib) < 0.0f);
+                    m3 = __ballot_sync(0xffffffffu, hi_f(vib) < 0.0f);
+                }
+                if (lane == 0) {
+                    *reinterpret_cast<ulonglong2 *>(S.mask[q]) =
+                        make_ulonglong2(((unsigned long long)m1 << 32) | m0, ((unsigned long long)m3 << 32) | m2);
+                }
+            }
+        } else
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
             const float4 Q0 = N0, Q1 = N1;
