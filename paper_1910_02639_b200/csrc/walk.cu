@@ -884,60 +884,65 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
         // a block whose every candidate threshold cannot decide (all +inf: the
         // common case inside a region of one h) tests the query thresholds alone
         const bool red = __all_sync(0xffffffffu, nk[0] == inf && nk[1] == inf && nk[2] == inf && nk[3] == inf);
-        if (red) {
+        // (four loop variants -- all thresholds or query thresholds only, two
+        // chunks or one -- so no branch sits inside a loop with ballots)
+#define BT_SYM_LOOP(TWO, RED)                                                                                    \
+    for (int q = 0; q < nqp; q++) {                                                                              \
+        const float4 Q0 = N0, Q1 = N1;                                                                           \
+        const unsigned long long qm = NM;                                                                        \
+        ldq(q + 1, N0, N1);                                                                                      \
+        asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm + 8 * (q + 1)));                          \
+        const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),                 \
+                                 bq = pk(Q1.z, Q1.w);                                                            \
+        const unsigned long long ua = f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq))));           \
+        const unsigned long long via = f2_add(ua, qm);                                                           \
+        unsigned m0, m1, m2 = 0u, m3 = 0u;                                                                       \
+        if (RED) {                                                                                               \
+            bmin = fminf(bmin, fminf(fabsf(lo_f(via)), fabsf(hi_f(via))));                                       \
+            m0 = __ballot_sync(0xffffffffu, lo_f(via) < 0.0f);                                                   \
+            m1 = __ballot_sync(0xffffffffu, hi_f(via) < 0.0f);                                                   \
+        } else {                                                                                                 \
+            const unsigned long long vja = f2_add(ua, ka);                                                       \
+            bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(via)), fabsf(hi_f(via))), fminf(fabsf(lo_f(vja)), fabsf(hi_f(vja))))); \
+            m0 = __ballot_sync(0xffffffffu, fminf(lo_f(via), lo_f(vja)) < 0.0f);                                 \
+            m1 = __ballot_sync(0xffffffffu, fminf(hi_f(via), hi_f(vja)) < 0.0f);                                 \
+        }                                                                                                        \
+        if (TWO) {                                                                                               \
+            const unsigned long long ub = f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq))));       \
+            const unsigned long long vib = f2_add(ub, qm);                                                       \
+            if (RED) {                                                                                           \
+                bmin = fminf(bmin, fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))));                                   \
+                m2 = __ballot_sync(0xffffffffu, lo_f(vib) < 0.0f);                                               \
+                m3 = __ballot_sync(0xffffffffu, hi_f(vib) < 0.0f);                                               \
+            } else {                                                                                             \
+                const unsigned long long vjb = f2_add(ub, kb);                                                   \
+                bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))), fminf(fabsf(lo_f(vjb)), fabsf(hi_f(vjb))))); \
+                m2 = __ballot_sync(0xffffffffu, fminf(lo_f(vib), lo_f(vjb)) < 0.0f);                             \
+                m3 = __ballot_sync(0xffffffffu, fminf(hi_f(vib), hi_f(vjb)) < 0.0f);                             \
+            }                                                                                                    \
+        }                                                                                                        \
+        if (lane == 0)                                                                                           \
+            *reinterpret_cast<ulonglong2 *>(S.mask[q]) =                                                         \
+                make_ulonglong2(((unsigned long long)m1 << 32) | m0, ((unsigned long long)m3 << 32) | m2);      \
+    }
+        if (nch == 2) {
+            if (red) {
 #pragma unroll 2
-            for (int q = 0; q < nqp; q++) {
-                const float4 Q0 = N0, Q1 = N1;
-                const unsigned long long qm = NM;
-                ldq(q + 1, N0, N1);
-                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm + 8 * (q + 1)));
-                const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
-                                         bq = pk(Q1.z, Q1.w);
-                const unsigned long long via =
-                    f2_add(f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq)))), qm);
-                bmin = fminf(bmin, fminf(fabsf(lo_f(via)), fabsf(hi_f(via))));
-                const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(via) < 0.0f);
-                const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(via) < 0.0f);
-                unsigned m2 = 0u, m3 = 0u;
-                if (nch == 2) {  // (warp-uniform)
-                    const unsigned long long vib =
-                        f2_add(f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq)))), qm);
-                    bmin = fminf(bmin, fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))));
-                    m2 = __ballot_sync(0xffffffffu, lo_f(vib) < 0.0f);
-                    m3 = __ballot_sync(0xffffffffu, hi_f(vib) < 0.0f);
-                }
-                if (lane == 0) {
-                    *reinterpret_cast<ulonglong2 *>(S.mask[q]) =
-                        make_ulonglong2(((unsigned long long)m1 << 32) | m0, ((unsigned long long)m3 << 32) | m2);
-                }
-            }
-        } else
+                BT_SYM_LOOP(true, true)
+            } else {
 #pragma unroll 2
-        for (int q = 0; q < nqp; q++) {
-            const float4 Q0 = N0, Q1 = N1;
-            const unsigned long long qm = NM;
-            ldq(q + 1, N0, N1);
-            asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm + 8 * (q + 1)));
-            const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
-                                     bq = pk(Q1.z, Q1.w);
-            const unsigned long long ua = f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq))));
-            const unsigned long long via = f2_add(ua, qm), vja = f2_add(ua, ka);
-            bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(via)), fabsf(hi_f(via))), fminf(fabsf(lo_f(vja)), fabsf(hi_f(vja)))));
-            const unsigned m0 = __ballot_sync(0xffffffffu, fminf(lo_f(via), lo_f(vja)) < 0.0f);
-            const unsigned m1 = __ballot_sync(0xffffffffu, fminf(hi_f(via), hi_f(vja)) < 0.0f);
-            unsigned m2 = 0u, m3 = 0u;
-            if (nch == 2) {  // (warp-uniform)
-                const unsigned long long ub = f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq))));
-                const unsigned long long vib = f2_add(ub, qm), vjb = f2_add(ub, kb);
-                bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))), fminf(fabsf(lo_f(vjb)), fabsf(hi_f(vjb)))));
-                m2 = __ballot_sync(0xffffffffu, fminf(lo_f(vib), lo_f(vjb)) < 0.0f);
-                m3 = __ballot_sync(0xffffffffu, fminf(hi_f(vib), hi_f(vjb)) < 0.0f);
+                BT_SYM_LOOP(true, false)
             }
-            if (lane == 0) {
-                *reinterpret_cast<ulonglong2 *>(S.mask[q]) =
-                    make_ulonglong2(((unsigned long long)m1 << 32) | m0, ((unsigned long long)m3 << 32) | m2);
+        } else {
+            if (red) {
+#pragma unroll 2
+                BT_SYM_LOOP(false, true)
+            } else {
+#pragma unroll 2
+                BT_SYM_LOOP(false, false)
             }
         }
+#undef BT_SYM_LOOP
     } else if (nch == 2) {
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
