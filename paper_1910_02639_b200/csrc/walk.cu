@@ -73,7 +73,8 @@ enum {
     C_OSUM = 19,     // the same checksum of a fill-only call's offsets differences
     C_OBAD = 20,     // a fill-only call's offsets are not a valid scan of the counts
     C_NZW = 21,      // recorded mask words with at least one neighbor
-    C_N = 22
+    C_HBAD = 22,     // the descent's fused gather met an h outside (0, 1e150]
+    C_N = 23
 };
 
 struct WalkArgs {
@@ -81,6 +82,8 @@ struct WalkArgs {
     const float4 *rec32;
     const int32_t *perm;      // caller index of each tree position
     const double *h_tree;
+    const double *h_src;      // non-null: the descent gathers h (caller order) into h_out itself
+    double *h_out;            // (= h_tree)
     const NodeRec *nodes;
     const int32_t *cells;
     const int32_t *leaf_begin;
@@ -310,7 +313,7 @@ __device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, in
 // unit_setup (min / max are exact and order independent), so both kernels
 // see bit-identical boxes.  A whole-leaf unit needs only its queries' h.
 __device__ __forceinline__ void unit_box(const WalkArgs &a, const int4 &UU, int lane, double (&lo)[3], double (&hi)[3],
-                                         double &Ru) {
+                                         double &Ru, long long &hsum, bool &hbad) {
     const int q0 = UU.y, nq = UU.z;
     const bool whole = nq == a.leaf_count[UU.x];
     double r = 0.0;
@@ -322,7 +325,17 @@ __device__ __forceinline__ void unit_box(const WalkArgs &a, const int4 &UU, int 
     for (int h = 0; h < 2; h++) {
         const int k = lane + 32 * h;
         if (k < nq) {
-            const double t = __dmul_rn(2.0, a.h_tree[q0 + k]);  // 2h (exact)
+            double hv;
+            if (a.h_src) {  // fused gather of h into tree order (+ validation, checksum: gather_h_kernel's)
+                const int32_t i = a.perm[q0 + k];
+                hv = a.h_src[i];
+                a.h_out[q0 + k] = hv;
+                hbad = hbad || !(hv > 0.0 && hv <= 1e150);
+                hsum += __double_as_longlong(hv) * (2 * (long long)i + 1);
+            } else {
+                hv = a.h_tree[q0 + k];
+            }
+            const double t = __dmul_rn(2.0, hv);  // 2h (exact)
             r = fmax(r, __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M)));
             if (!whole) {
                 const double4 p = a.rec[q0 + k];
@@ -594,13 +607,15 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
     }
     Slab ls;
     WorkBatch wb;
+    long long hsum = 0;  // fused gather of h (first pass only): checksum and validity of this lane's values
+    bool hbad = false;
     for (;;) {
         const long long uid = next_unit(wb, &a.ctr[kBig ? C_WORK4 : C_WORK], a.n_units, kBig ? 1 : a.desc_batch, lane);
         if (uid >= a.n_units) break;
         if (kBig && a.urun[uid].nleaf >= 0) continue;
         const int4 U = a.units[uid];
         double qlo[3], qhi[3], Ru;
-        unit_box(a, U, lane, qlo, qhi, Ru);
+        unit_box(a, U, lane, qlo, qhi, Ru, hsum, hbad);
         UnitRun &R = a.urun[uid];
         if (!kBig) {
             const bool ok = slab_reserve(ls, kListReserve, kListSlab, a.list_cap, &a.ctr[C_LIST], lane);
@@ -632,6 +647,14 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
             }
         }
         __syncwarp();
+    }
+    if (a.h_src) {
+        for (int d = 16; d; d >>= 1) hsum += __shfl_xor_sync(0xffffffffu, hsum, d);
+        const bool bad = __any_sync(0xffffffffu, hbad);
+        if (lane == 0) {
+            atomicAdd((unsigned long long *)&a.ctr[C_HSUM], (unsigned long long)hsum);
+            if (bad) atomicOr((unsigned long long *)&a.ctr[C_HBAD], 1ull);
+        }
     }
 }
 
@@ -1720,23 +1743,31 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
     cudaStream_t st = stream();
     double list_per_unit = 96.0;
     const long long warps_d = (long long)g.d * (kDescThreads / 32);
+    const double *h_src = a.h_src;  // fused gather of h (first pass only)
     for (int attempt = 0;; attempt++) {
         t.ulist.reserve((long long)(list_per_unit * a.n_units) + warps_d * kListSlab, 0);
         a.ulist = t.ulist.p;
         a.list_cap = (long long)t.ulist.n;
+        a.h_src = h_src;
         for (int c : {C_WORK, C_LIST, C_BIG, C_WORK4, C_NEEDC, C_NEEDM}) zero_counter(t, c);
+        if (h_src) {
+            zero_counter(t, C_HSUM);
+            zero_counter(t, C_HBAD);
+        }
         {
             Phase ph("search.desc");
             desc_kernel<false, kSym><<<g.d, kDescThreads, 0, st>>>(a);
             BT_LAUNCH("walk_desc");
         }
         read_counters(t, hc);
+        if (h_src && hc[C_HBAD]) return;  // invalid h: the caller reports it (no arena growth for r = inf)
         t.big_units = hc[C_BIG];
         if (hc[C_BIG] > 0 && hc[C_LIST] <= a.list_cap) {
             // units beyond the shared-memory frontier / list reserve
             t.front.reserve((long long)g.big * (kDescThreads / 32) * 2 * std::max<int64_t>(t.n_nodes, 1), 0);
             a.front = t.front.p;
             a.front_cap = std::max<int64_t>(t.n_nodes, 1);
+            a.h_src = nullptr;  // (h_tree is complete after the first pass)
             Phase ph("search.desc_big");
             desc_kernel<true, kSym><<<g.big, kDescThreads, 0, st>>>(a);
             BT_LAUNCH("walk_desc_big");
@@ -1747,6 +1778,7 @@ void run_descent(TreeDev &t, WalkArgs &a, const Grids &g, long long *hc) {
         if (attempt > 2) throw Error(BT_ERR_OOM, "bt_find_neighbors: leaf-list arena does not converge");
     }
     t.list_entries = hc[C_LIST];
+    a.h_src = nullptr;
 }
 
 }  // namespace
@@ -1787,7 +1819,18 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
         return;
     }
     const int sms = num_sms();
-    const long long hsum = gather_h(t, h, who);
+    // the gather walk of a count call gathers h in its descent (each unit's
+    // queries; validation and checksum as gather_h_kernel's); fill-only calls
+    // (the record check needs the checksum first), partitioned trees and the
+    // symmetric walk (its staging reads every candidate's h) gather first
+    const bool fuse = !kSym && count_pass && t.nparts == 1;
+    long long hsum = 0;
+    if (fuse) {
+        t.h_tree.reserve(n, 0);
+        t.counters.reserve(C_N, 0);
+    } else {
+        hsum = gather_h(t, h, who);
+    }
     const Grids g = walk_grids<false, kSym>();
 
     // the recorded masks of a previous test pass are reused by a fill-only
@@ -1821,7 +1864,15 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
         }
         long long hc[C_N];
         t.rec_valid = false;
+        if (fuse) {
+            a.h_src = h;
+            a.h_out = t.h_tree.p;
+        }
         run_descent<kSym>(t, a, g, hc);
+        if (fuse) {
+            if (hc[C_HBAD]) throw Error(BT_ERR_INPUT, std::string(who) + ": h must be finite, > 0 and <= 1e150");
+            hsum = hc[C_HSUM];
+        }
         const long long warps_w = (long long)g.w * (kWalkThreads / 32);
         {  // A10 staging + A11 pair tests, counts, masks; candidate and mask arenas: exact bounds from the descent
             t.arena_cands.reserve(hc[C_NEEDC] + warps_w * kCandSlab, 0);

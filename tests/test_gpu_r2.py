@@ -8,7 +8,7 @@ torch = pytest.importorskip("torch")
 
 from paper_1910_02639_b200 import datagen  # noqa: E402
 
-from test_gpu_parity import DEV, assert_same, assert_same_tree, gpu_run  # noqa: E402
+from test_gpu_parity import DEV, assert_same, assert_same_tree, gpu_run, sort_rows  # noqa: E402
 from test_oracle_pins import _tie_set  # noqa: E402
 
 pytestmark = pytest.mark.gpu
@@ -160,3 +160,45 @@ def test_symmetric_exact_only_identical(P, oracle, case):
         assert np.array_equal(gc[q], rc)
         for k, i in enumerate(q):
             assert np.array_equal(gi[go[i]:go[i + 1]], ri[ro[k]:ro[k + 1]])
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), 0.0, -1.0, 1e200])
+def test_count_rejects_bad_h(P, oracle, bad):
+    """The count walk gathers h into tree order inside its descent (no
+    separate gather launch): an h outside (0, 1e150] anywhere is still
+    BT_ERR_INPUT before any arena grows for r = inf, and the tree stays
+    usable (the next call with a valid h equals the oracle)."""
+    pos, h = datagen.make_config(2, n=30_000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hb = h.copy()
+    hb[12345] = bad
+    with pytest.raises(P.BtreeError) as e:
+        t.count(torch.from_numpy(hb).to(DEV))
+    assert e.value.code == 2
+    with pytest.raises(P.BtreeError) as e:
+        t.find_neighbors(torch.from_numpy(hb).to(DEV), ngmax=512)
+    assert e.value.code == 2
+    c, o, nb = t.find_neighbors(torch.from_numpy(h).to(DEV), ngmax=512)
+    assert_same((c.cpu().numpy(), o.cpu().numpy(), sort_rows(c, o, nb)), oracle.Tree(pos, 64).neighbors(h))
+
+
+def test_fill_after_count_replays_record(P, oracle):
+    """A count call (h gathered in the descent) followed by a fill-only call
+    with the same h: the fill replays the recorded masks (no second descent
+    or test pass), i.e. the fused checksum equals the gather kernel's."""
+    pos, h = datagen.make_config(2, n=40_000)
+    t = P.build(torch.from_numpy(pos).to(DEV))
+    hd = torch.from_numpy(h).to(DEV)
+    c, off = t.count(hd)
+    P.profile_enable(True)
+    try:
+        P.profile_reset()
+        nb = t.fill(hd, off)
+        prof = P.profile()
+    finally:
+        P.profile_enable(False)
+    assert "search.fill" in prof
+    assert "search.desc" not in prof and "search.count" not in prof
+    oc, ooff, oidx = oracle.Tree(pos, 64).neighbors(h)
+    assert np.array_equal(off.cpu().numpy(), ooff)
+    assert np.array_equal(sort_rows(c, off, nb), oidx)
