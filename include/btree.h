@@ -199,6 +199,38 @@ int bt_fill_neighbors_sym(const bt_tree *t, const double *h, const int64_t *offs
  */
 int bt_set_partition(bt_tree *t, int32_t part, int32_t nparts);
 
+/*
+ * bt_set_tree_order -- the index space of this tree's later searches.  The
+ * paper's first walk optimisation is that "particles are reordered in memory
+ * along this curve" (the depth-first leaf order of the tree walk); a
+ * caller that keeps its particles in that order works in tree positions
+ * k = 0 .. n-1 (particle perm[k] of bt_tree_order).  With on != 0, every
+ * per-particle array of bt_find_neighbors(_sym), bt_fill_neighbors(_sym) and
+ * bt_density is indexed by tree position: h[k], mass[k], counts[k], row k of
+ * offsets / nbr_idx and rho[k] belong to particle perm[k], and the neighbor
+ * indices written to nbr_idx are tree positions.  The neighbor sets are
+ * those of the default (caller-order) space mapped through perm: row k holds
+ * {perm^-1(j) : j in N(perm[k])}.  Equivalently, the result equals the
+ * default-space search of the reordered particle set pos[perm] (whose tree
+ * has the identity permutation).  on = 0 restores caller order (the
+ * default).  Rows of consecutive tree positions are adjacent in nbr_idx, so
+ * the fill pass writes each work unit's rows as one contiguous range.
+ * Invalidates the recorded count pass.  No device work.  BT_ERR_ARG for a
+ * NULL tree.
+ */
+int bt_set_tree_order(bt_tree *t, int on);
+
+/*
+ * bt_reorder -- gather a caller-order array into tree order:
+ *   dst[k * ncomp + c] = src[perm[k] * ncomp + c],  k < n, c < ncomp,
+ * perm = bt_tree_order's (e.g. h or masses for bt_set_tree_order, or
+ * positions with ncomp = 3).  src, dst: DEVICE fp64, n * ncomp each, caller
+ * owned, must not overlap.  ncomp in [1, 16].  Values are copied bit for bit
+ * (no validation).  BT_ERR_ARG for a NULL tree / pointers or ncomp outside
+ * [1, 16].  Enqueued on the thread's stream; returns after completion.
+ */
+int bt_reorder(const bt_tree *t, const double *src, int32_t ncomp, double *dst);
+
 /* Frees all tree-owned device memory (into this thread's block cache).  NULL-safe. */
 void bt_free(bt_tree *t);
 

@@ -21,7 +21,8 @@ _NAMES = {0: "BT_OK", 1: "BT_ERR_ARG", 2: "BT_ERR_INPUT", 3: "BT_ERR_CAPACITY", 
 
 # every symbol include/btree.h declares
 EXPORTS = ["bt_build", "bt_build_ex", "bt_build_policy", "bt_find_neighbors", "bt_fill_neighbors",
-           "bt_find_neighbors_sym", "bt_fill_neighbors_sym", "bt_density", "bt_set_partition", "bt_free",
+           "bt_find_neighbors_sym", "bt_fill_neighbors_sym", "bt_density", "bt_set_partition", "bt_set_tree_order",
+           "bt_reorder", "bt_free",
            "bt_search_host", "bt_set_stream", "bt_set_exact_only", "bt_release_cache", "bt_last_error", "bt_last_status", "bt_tree_stats",
            "bt_tree_order", "bt_profile_enable", "bt_profile_reset", "bt_profile_get"]
 
@@ -83,6 +84,10 @@ def lib():
         L.bt_fill_neighbors_sym.restype = C.c_int
         L.bt_set_partition.argtypes = [_P, C.c_int32, C.c_int32]
         L.bt_set_partition.restype = C.c_int
+        L.bt_set_tree_order.argtypes = [_P, C.c_int]
+        L.bt_set_tree_order.restype = C.c_int
+        L.bt_reorder.argtypes = [_P, _P, C.c_int32, _P]
+        L.bt_reorder.restype = C.c_int
         L.bt_density.argtypes = [_P, _P, _P, _P]
         L.bt_density.restype = C.c_int
         L.bt_free.argtypes = [_P]
@@ -277,6 +282,31 @@ class Tree:
         rows of other parts' particles come back empty."""
         _check(lib().bt_set_partition(self._handle(), int(part), int(nparts)))
         return self
+
+    def set_tree_order(self, on: bool = True):
+        """Index space of later searches (bt_set_tree_order): with on, h, mass,
+        counts, offsets rows, rho and neighbor indices are tree positions
+        (particles reordered along the walk's curve)."""
+        _check(lib().bt_set_tree_order(self._handle(), 1 if on else 0))
+        return self
+
+    def reorder(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """x (caller order, fp64 [n] or [n, c]) gathered into tree order by
+        bt_reorder: out[k] = x[perm[k]]."""
+        if not isinstance(x, torch.Tensor) or x.dtype != torch.float64 or x.device != self.device:
+            raise ValueError(f"x: expected a float64 tensor on {self.device}")
+        if x.shape[0] != self.n or x.dim() > 2 or not x.is_contiguous():
+            raise ValueError(f"x: expected a contiguous [{self.n}] or [{self.n}, c] tensor")
+        ncomp = 1 if x.dim() == 1 else x.shape[1]
+        if out is None:
+            out = torch.empty_like(x)
+        _dev_out(out, torch.float64, x.numel(), self.device, "out")
+        if out.data_ptr() == x.data_ptr():
+            raise ValueError("out: must not alias x")
+        with torch.cuda.device(self.device):
+            _use_current_stream(self.device)
+            _check(lib().bt_reorder(self._handle(), _ptr(x), int(ncomp), _ptr(out)))
+        return out
 
     def stats(self) -> dict:
         s = Stats()

@@ -358,6 +358,48 @@ int bt_set_partition(bt_tree *t, int32_t part, int32_t nparts) {
     return BT_OK;
 }
 
+int bt_set_tree_order(bt_tree *t, int on) {
+    if (!t) {
+        set_error(BT_ERR_ARG, "bt_set_tree_order: NULL tree");
+        return BT_ERR_ARG;
+    }
+    t->t.tree_order = on != 0;
+    t->t.rec_valid = false;  // the recorded candidates hold the other space's indices
+    return BT_OK;
+}
+
+namespace bt_export {
+__global__ void reorder_kernel(const double4 *rec, const double *src, int ncomp, int64_t n, double *dst) {
+    const int64_t total = n * ncomp;
+    if (ncomp == 1) {
+        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+            dst[k] = src[__double_as_longlong(rec[k].w)];
+        return;
+    }
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e / ncomp, c = e - k * ncomp;
+        dst[e] = src[__double_as_longlong(rec[k].w) * ncomp + c];
+    }
+}
+}  // namespace bt_export
+
+int bt_reorder(const bt_tree *t, const double *src, int32_t ncomp, double *dst) {
+    if (!t || ncomp < 1 || ncomp > 16 || (t->t.n > 0 && (!src || !dst))) {
+        set_error(BT_ERR_ARG, "bt_reorder: need a tree, src, dst and 1 <= ncomp <= 16");
+        return BT_ERR_ARG;
+    }
+    return guarded([&] {
+        const TreeDev &d = t->t;
+        cudaStream_t st = stream();
+        if (d.n) {
+            bt_export::reorder_kernel<<<grid_for(d.n * ncomp, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
+                d.rec.p, src, ncomp, d.n, dst);
+            BT_LAUNCH("reorder");
+        }
+        BT_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 int bt_density(const bt_tree *tc, const double *h, const double *mass, double *rho) {
     bt_tree *t = const_cast<bt_tree *>(tc);
     if (!t || (t->t.n > 0 && (!h || !mass || !rho))) {

@@ -186,6 +186,8 @@ struct TreeDev {
     long long rec_csum = 0;    // checksum of the recorded pass's counts (fill-only offsets validation)
     int rec_exact = 0;
     bool rec_sym = false;      // the recorded pass is the symmetric criterion's
+    bool rec_tree_order = false;  // ... and in the tree-order index space
+    bool tree_order = false;   // bt_set_tree_order: h, mass, counts, offsets, rho and neighbor indices by tree position
     DBuf<int64_t> counters;    // [8] device counters (staged, tests, exact, max_count, ...)
     DBuf<int32_t> front;       // descent frontier scratch of the big-unit pass (per warp)
 

@@ -95,6 +95,7 @@ struct WalkArgs {
     double M;
     int root_is_leaf;
     int exact_only;
+    int tree_order;           // bt_set_tree_order: per-particle arrays and neighbor indices in tree positions
     int32_t *front;           // big-unit pass: per-warp frontier scratch, 2 x front_cap node ids
     int64_t front_cap;
     UnitRun *urun;
@@ -284,7 +285,7 @@ __device__ __forceinline__ void unit_setup(const WalkArgs &a, const int4 &UU, in
             G.qz[h] = r.z;
             G.qT[h] = __dmul_rn(t, t);
             G.qt[h] = t;
-            G.qo[h] = (int32_t)__double_as_longlong(r.w);
+            G.qo[h] = a.tree_order ? G.q0 + k : (int32_t)__double_as_longlong(r.w);
             // R' = 2h (1 + 2^-40) + 2^-50 M   (lemma L1/L2)
             Ru = fmax(Ru, __dadd_rn(__dmul_rn(t, 1.0 + 0x1p-40), __dmul_rn(0x1p-50, a.M)));
             lo[0] = fmin(lo[0], r.x); lo[1] = fmin(lo[1], r.y); lo[2] = fmin(lo[2], r.z);
@@ -327,7 +328,7 @@ __device__ __forceinline__ void unit_box(const WalkArgs &a, const int4 &UU, int 
         if (k < nq) {
             double hv;
             if (a.h_src) {  // fused gather of h into tree order (+ validation, checksum: gather_h_kernel's)
-                const int32_t i = a.perm[q0 + k];
+                const int32_t i = a.tree_order ? q0 + k : a.perm[q0 + k];
                 hv = a.h_src[i];
                 a.h_out[q0 + k] = hv;
                 hbad = hbad || !(hv > 0.0 && hv <= 1e150);
@@ -1030,7 +1031,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
             }
         }
     }
-    __syncwarp();
+    nzw = __reduce_add_sync(0xffffffffu, nzw);
     if (lane == 0) {
         S.u.tests += (long long)n * nq;
         S.u.exact += exact;
@@ -1129,7 +1130,7 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
                 __stcg(&S.u.scrk[(unsigned)slot],
                        Tj > S.u.tqmin ? -S.u.k * __double2float_rn(Tj) : __int_as_float(0x7f800000));
             }
-            if (rec_ok) __stcs(&cands[(unsigned)slot], __float_as_int(r.w));
+            if (rec_ok) __stcs(&cands[(unsigned)slot], a.tree_order ? pos : __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
         }
         nst += __popc(km);
@@ -1462,7 +1463,7 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
         const int nq = U.z;
         const int nchk = (R.nstaged + 63) >> 6;
         for (int q = lane; q < nq; q += 32)
-            F.row[q] = a.nbr + a.offsets[a.perm[U.y + q]];
+            F.row[q] = a.nbr + a.offsets[a.tree_order ? U.y + q : a.perm[U.y + q]];
         for (int kk0 = 0; kk0 < nchk; kk0 += kFillChunks) {
             const int nk = min(kFillChunks, nchk - kk0);
             int32_t c0[kFillChunks], c1[kFillChunks];
@@ -1556,7 +1557,7 @@ __global__ void gather_h_kernel(const int32_t *__restrict__ perm, const double *
         long long i[4];
         double v[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) i[u] = perm[k + u * stride];
+        for (int u = 0; u < 4; u++) i[u] = perm ? perm[k + u * stride] : k + u * stride;
 #pragma unroll
         for (int u = 0; u < 4; u++) v[u] = h[i[u]];
 #pragma unroll
@@ -1567,7 +1568,7 @@ __global__ void gather_h_kernel(const int32_t *__restrict__ perm, const double *
         }
     }
     for (; k < n; k += stride) {
-        const long long i = perm[k];
+        const long long i = perm ? perm[k] : k;
         const double v = h[i];
         ok = ok && (v > 0.0 && v <= 1e150);
         h_tree[k] = v;
@@ -1637,7 +1638,7 @@ namespace {
 __global__ void gather_m_kernel(const int32_t *__restrict__ perm, const double *__restrict__ m, int64_t n,
                                 double *__restrict__ m_tree, int *bad) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const double v = m[perm[k]];
+        const double v = m[perm ? perm[k] : k];
         if (!(fabs(v) <= 1e150)) atomicOr(bad, 1);
         m_tree[k] = v;
     }
@@ -1671,8 +1672,8 @@ long long gather_h(TreeDev &t, const double *h, const char *who) {
     BT_CUDA(cudaMemsetAsync(t.counters.p + C_HSUM, 0, sizeof(int64_t), st));
     {
         Phase ph("search.gather_h");
-        gather_h_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.perm.p, h, n, t.h_tree.p, dbad.p,
-                                                                                  (long long *)t.counters.p + C_HSUM);
+        gather_h_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
+            t.tree_order ? nullptr : t.perm.p, h, n, t.h_tree.p, dbad.p, (long long *)t.counters.p + C_HSUM);
         BT_LAUNCH("gather_h");
     }
     int hbad = 0;
@@ -1691,6 +1692,7 @@ WalkArgs walk_args(TreeDev &t, const Grids &g) {
     a.rec = t.rec.p;
     a.rec32 = t.rec32.p;
     a.perm = t.perm.p;
+    a.tree_order = t.tree_order ? 1 : 0;
     a.n_rec = t.n;
     a.n_cells = t.n_cells;
     a.n_leaves = t.n_leaves;
@@ -1836,7 +1838,7 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
     // the recorded masks of a previous test pass are reused by a fill-only
     // call when the tree, h pointer, exactness mode, criterion and h checksum all match
     const bool have_record = t.rec_valid && t.rec_h == h && t.rec_hsum == hsum && t.rec_exact == g_exact_only &&
-                             t.rec_sym == kSym;
+                             t.rec_sym == kSym && t.rec_tree_order == t.tree_order;
     const bool run_test = count_pass || !have_record;
 
     WalkArgs a = walk_args(t, g);
@@ -1903,6 +1905,7 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
             t.rec_hsum = hsum;
             t.rec_exact = g_exact_only;
             t.rec_sym = kSym;
+            t.rec_tree_order = t.tree_order;
         }
         t.staged = hc[C_STAGED];
         t.loaded = hc[C_LOADED];
@@ -1973,7 +1976,8 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
         DBuf<int> dbad(1);
         BT_CUDA(cudaMemsetAsync(dbad.p, 0, sizeof(int), st));
         t.m_tree.reserve(n, 0);
-        gather_m_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.perm.p, mass, n, t.m_tree.p, dbad.p);
+        gather_m_kernel<<<grid_for(n, 256, (int64_t)num_sms() * 16), 256, 0, st>>>(t.tree_order ? nullptr : t.perm.p, mass,
+                                                                                  n, t.m_tree.p, dbad.p);
         BT_LAUNCH("gather_m");
         int mbad = 0;
         read_back({{dbad.p, &mbad, sizeof(int)}});

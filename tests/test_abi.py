@@ -49,6 +49,8 @@ def test_argument_errors_without_device():
     assert L.bt_fill_neighbors_sym(None, None, None, None, 0) == btree.BT_ERR_ARG
     assert L.bt_density(None, None, None, None) == btree.BT_ERR_ARG
     assert L.bt_set_partition(None, 0, 1) == btree.BT_ERR_ARG
+    assert L.bt_set_tree_order(None, 1) == btree.BT_ERR_ARG
+    assert L.bt_reorder(None, None, 1, None) == btree.BT_ERR_ARG
     for bad_policy in (-1, 4):  # BT_POLICY_BTREE .. BT_POLICY_QUADTREE
         assert not L.bt_build_policy(None, 0, 8, 0.5, 0.5, 64, bad_policy)
         assert L.bt_last_status() == btree.BT_ERR_ARG

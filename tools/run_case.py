@@ -22,6 +22,7 @@ ap.add_argument("--exact", action="store_true")
 ap.add_argument("--ngmax", type=int, default=512)
 ap.add_argument("--count-only", action="store_true")
 ap.add_argument("--symmetric", action="store_true", help="max(h_i, h_j) criterion (bt_find_neighbors_sym)")
+ap.add_argument("--tree-order", action="store_true", help="bt_set_tree_order: h by tree position (bt_reorder)")
 args = ap.parse_args()
 
 pos_np, h_np = datagen.make_config(args.config, n=args.n)
@@ -40,10 +41,14 @@ for r in range(args.reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     t = P.Tree(pos, 64, 0.5)
+    hq = h
+    if args.tree_order:
+        t.set_tree_order(True)
+        hq = t.reorder(h)
     if args.count_only:
-        t.count(h, symmetric=args.symmetric)
+        t.count(hq, symmetric=args.symmetric)
     else:
-        t.find_neighbors(h, args.ngmax, counts=counts, offsets=offsets, nbr_idx=nbr, symmetric=args.symmetric)
+        t.find_neighbors(hq, args.ngmax, counts=counts, offsets=offsets, nbr_idx=nbr, symmetric=args.symmetric)
     st = t.stats()
     t.free()
     torch.cuda.synchronize()
