@@ -748,8 +748,8 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
                 // the hot loop's v, operation for operation
                 const float v = __fmaf_rn(c[h].x, Q0.x, __fmaf_rn(c[h].y, Q0.z, __fmaf_rn(c[h].z, Q1.x, __fadd_rn(ac[h], Q1.z))));
                 if (kSym) {
-                    const float vi = __fadd_rn(v, S.qm[q].x), vj = __fadd_rn(v, nk[h]);
-                    flag[h] = real[h] && (force || fabsf(vi) <= 1.0f || fabsf(vj) <= 1.0f);
+                    const float w = __fadd_rn(v, fminf(S.qm[q].x, nk[h]));  // the hot loop's min(v_i, v_j)
+                    flag[h] = real[h] && (force || fabsf(w) <= 1.0f);
                 } else {
                     flag[h] = real[h] && (force || fabsf(v) <= 1.0f);
                 }
@@ -894,14 +894,15 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     if constexpr (kSym) {
         // symmetric criterion (lemma L4s): u = k |c - q|^2 without Mid, then
         // v_i = u - k Mid_i (query threshold) and v_j = u - k Mid_j (candidate
-        // threshold, +inf when it cannot decide); the bit is min(v_i, v_j) < 0
+        // threshold, +inf when it cannot decide); the bit is w < 0 for
+        // w = min(v_i, v_j) = u + min(-k Mid_i, -k Mid_j), and only |w| <= 1
+        // is uncertain (w < -1: one threshold certainly holds; w > 1: neither)
         float nk[4];
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const int sl = 32 * j + lane;
             nk[j] = (sl < n) ? __ldcg(&S.u.scrk[b0 + sl]) : inf;  // (padding: u = +inf anyway)
         }
-        const unsigned long long ka = pk(nk[0], nk[1]), kb = pk(nk[2], nk[3]);
         const unsigned aqm = (unsigned)__cvta_generic_to_shared(&S.qm[0]);
         unsigned long long NM;
         asm volatile("ld.shared.b64 %0, [%1];" : "=l"(NM) : "r"(aqm));
@@ -919,31 +920,19 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
         const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),                 \
                                  bq = pk(Q1.z, Q1.w);                                                            \
         const unsigned long long ua = f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq))));           \
-        const unsigned long long via = f2_add(ua, qm);                                                           \
-        unsigned m0, m1, m2 = 0u, m3 = 0u;                                                                       \
-        if (RED) {                                                                                               \
-            bmin = fminf(bmin, fminf(fabsf(lo_f(via)), fabsf(hi_f(via))));                                       \
-            m0 = __ballot_sync(0xffffffffu, lo_f(via) < 0.0f);                                                   \
-            m1 = __ballot_sync(0xffffffffu, hi_f(via) < 0.0f);                                                   \
-        } else {                                                                                                 \
-            const unsigned long long vja = f2_add(ua, ka);                                                       \
-            bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(via)), fabsf(hi_f(via))), fminf(fabsf(lo_f(vja)), fabsf(hi_f(vja))))); \
-            m0 = __ballot_sync(0xffffffffu, fminf(lo_f(via), lo_f(vja)) < 0.0f);                                 \
-            m1 = __ballot_sync(0xffffffffu, fminf(hi_f(via), hi_f(vja)) < 0.0f);                                 \
-        }                                                                                                        \
+        /* w = u + min(-k Mid_i, -k Mid_j) = min(v_i, v_j) (fl(u + .) is monotone) */                            \
+        const unsigned long long wa = f2_add(ua, RED ? qm : pk(fminf(lo_f(qm), nk[0]), fminf(lo_f(qm), nk[1])));  \
+        bmin = fminf(bmin, fminf(fabsf(lo_f(wa)), fabsf(hi_f(wa))));                                             \
+        unsigned m2 = 0u, m3 = 0u;                                                                               \
+        const unsigned m0 = __ballot_sync(0xffffffffu, lo_f(wa) < 0.0f);                                         \
+        const unsigned m1 = __ballot_sync(0xffffffffu, hi_f(wa) < 0.0f);                                         \
         if (TWO) {                                                                                               \
             const unsigned long long ub = f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq))));       \
-            const unsigned long long vib = f2_add(ub, qm);                                                       \
-            if (RED) {                                                                                           \
-                bmin = fminf(bmin, fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))));                                   \
-                m2 = __ballot_sync(0xffffffffu, lo_f(vib) < 0.0f);                                               \
-                m3 = __ballot_sync(0xffffffffu, hi_f(vib) < 0.0f);                                               \
-            } else {                                                                                             \
-                const unsigned long long vjb = f2_add(ub, kb);                                                   \
-                bmin = fminf(bmin, fminf(fminf(fabsf(lo_f(vib)), fabsf(hi_f(vib))), fminf(fabsf(lo_f(vjb)), fabsf(hi_f(vjb))))); \
-                m2 = __ballot_sync(0xffffffffu, fminf(lo_f(vib), lo_f(vjb)) < 0.0f);                             \
-                m3 = __ballot_sync(0xffffffffu, fminf(hi_f(vib), hi_f(vjb)) < 0.0f);                             \
-            }                                                                                                    \
+            const unsigned long long wb =                                                                        \
+                f2_add(ub, RED ? qm : pk(fminf(lo_f(qm), nk[2]), fminf(lo_f(qm), nk[3])));                       \
+            bmin = fminf(bmin, fminf(fabsf(lo_f(wb)), fabsf(hi_f(wb))));                                         \
+            m2 = __ballot_sync(0xffffffffu, lo_f(wb) < 0.0f);                                                    \
+            m3 = __ballot_sync(0xffffffffu, hi_f(wb) < 0.0f);                                                    \
         }                                                                                                        \
         if (lane == 0)                                                                                           \
             *reinterpret_cast<ulonglong2 *>(S.mask[q]) =                                                         \
