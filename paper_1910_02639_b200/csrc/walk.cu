@@ -1468,23 +1468,21 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
             for (int w = lane; w < nk * nq; w += 32) F.mask[w] = __ldcs(&src[w]);
             __syncwarp();
             for (int q = 0; q < nq; q++) {
-                int32_t *dst = F.row[q];
-                int wrote = 0;
+                int32_t *const dst = F.row[q];
+                int o = 0;  // entries of this round written to the row
 #pragma unroll
                 for (int k = 0; k < kFillChunks; k++) {
                     if (k >= nk) break;
                     const unsigned long long m = F.mask[k * nq + q];
-                    if (m == 0ull) continue;
                     const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+                    if (!(lo | hi)) continue;
                     const int plo = __popc(lo);
-                    BT_DEV_CHECK(dst - a.nbr + plo + __popc(hi) <= a.nbr_cap);
-                    if (lo & lanebit) __stcs(&dst[__popc(lo & lt)], c0[k]);
-                    if (hi & lanebit) __stcs(&dst[plo + __popc(hi & lt)], c1[k]);
-                    const int n = plo + __popc(hi);
-                    dst += n;
-                    wrote += n;
+                    BT_DEV_CHECK(dst - a.nbr + o + plo + __popc(hi) <= a.nbr_cap);
+                    if (lo & lanebit) __stcs(&dst[o + __popc(lo & lt)], c0[k]);
+                    if (hi & lanebit) __stcs(&dst[o + plo + __popc(hi & lt)], c1[k]);
+                    o += plo + __popc(hi);
                 }
-                if (lane == 0 && wrote) F.row[q] = dst;
+                if (lane == 0 && o) F.row[q] = dst + o;
             }
             __syncwarp();
         }
