@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-tree-order", action="store_true",
+                    help="skip the secondary tree-order measurement (bt_set_tree_order, P:491)")
     ap.add_argument("--cpu-sample", type=int, default=None,
                     help="oracle queries timed for cpu_baseline (default: every query up to N = 4.2M, else 1M)")
     return ap.parse_args()
@@ -345,7 +347,9 @@ def run_b200(args):
     launches = sum(v[1] for k, v in prof.items() if k.startswith("kernel.")) // args.steps
     kern = {"build": ph("build.total"), "walk_desc": ph("search.desc") + ph("search.desc_big"),
             "walk_test": ph("search.count"), "scan": ph("search.scan"), "walk_fill": ph("search.fill"),
-            "gather_h": ph("search.gather_h"), "search_total": ph("search.total")}
+            "search_total": ph("search.total")}
+    if ph("search.gather_h") > 0:  # (the count call gathers h inside its descent; separate only when partitioned)
+        kern["gather_h"] = ph("search.gather_h")
 
     # ---- roofline of the dominant kernel -----------------
     peaks = {}
@@ -409,6 +413,52 @@ def run_b200(args):
                "definition": "16 B x compact records loaded by the walk staging / whole bt_find_neighbors time / "
                              "measured HBM peak"}
 
+    # ---- secondary: the same step in the tree-order index space ---------------
+    # (bt_set_tree_order: particles reordered along the walk's curve; the
+    # step gathers h into tree order with bt_reorder, then count + fill write
+    # rows and neighbor indices by tree position -- the rows of one work unit
+    # are one contiguous range of the CSR)
+    tree_order = None
+    if not replicated and not args.no_tree_order and args.steps > 0:
+        h_t = torch.empty_like(h)
+
+        def step_to():
+            t = P.Tree(pos, datagen.BUCKET_SIZE, datagen.MAX_EMPTY)
+            t.set_tree_order(True)
+            t.reorder(h, out=h_t)
+            t.find_neighbors(h_t, ngmax, counts=counts, offsets=offsets, nbr_idx=nbr)
+            s2 = t.stats()
+            t.free()
+            return s2
+
+        step_to()
+        P.profile_reset()
+        P.profile_enable(True)
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        g0 = torch.cuda.Event(enable_timing=True)
+        g1 = torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            s2 = step_to()
+        g1.record(stream)
+        torch.cuda.synchronize()
+        P.profile_enable(False)
+        prof2 = P.profile()
+        tms = max_over_ranks(g0.elapsed_time(g1) / args.steps, dev)
+
+        def ph2(name):
+            return prof2.get(name, (0.0, 0))[0] / args.steps
+
+        assert int(s2["total_pairs"]) == total_pairs
+        tree_order = {"value": weak_value(n, ws, tms), "unit": UNIT, "ms_per_step": tms,
+                      "kernel_ms": {"build": ph2("build.total"), "walk_desc": ph2("search.desc"),
+                                    "walk_test": ph2("search.count"), "walk_fill": ph2("search.fill"),
+                                    "search_total": ph2("search.total")},
+                      "api": "bt_set_tree_order + bt_reorder(h) + bt_find_neighbors (rows and indices by tree "
+                             "position; same pairs)"}
+
     # ---- end to end through the public API on host buffers --------------------
     e2e = None
     if replicated:
@@ -457,7 +507,7 @@ def run_b200(args):
                 "tree": {k: st[k] for k in ("depth", "root_b", "nodes", "leaves", "halvings", "units")},
                 "walk_counters": {k: st.get(k) for k in ("loaded", "staged", "tests", "exact_tests", "mask_words",
                                                          "cand_slots", "list_entries", "big_units", "mask_words_nonzero")},
-                "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
+                "tree_order": tree_order, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
