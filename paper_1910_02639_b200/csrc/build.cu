@@ -55,10 +55,14 @@ struct LevelNode {
 struct CellScan {  // per-cell values scanned in one pass (A6)
     long long pre;     // particles before this cell (level-wide)
     long long actoff;  // particles of child-node cells before this cell
+    long long ncnext;  // sub-cells (Eq. 1 b0^k) of the child nodes before this cell: the next level's cell count
     int nnode;         // child-node cells before this cell
     int nleaf;         // leaf cells before this cell
+    int maxleaf;       // largest leaf cell (max, not sum: the combine is still associative)
+    int pad_;
     __host__ __device__ CellScan operator+(const CellScan &o) const {
-        return CellScan{pre + o.pre, actoff + o.actoff, nnode + o.nnode, nleaf + o.nleaf};
+        return CellScan{pre + o.pre, actoff + o.actoff, ncnext + o.ncnext, nnode + o.nnode, nleaf + o.nleaf,
+                        maxleaf > o.maxleaf ? maxleaf : o.maxleaf, 0};
     }
 };
 
@@ -143,10 +147,10 @@ __global__ void copy_rec_kernel(const double4 *__restrict__ src, double4 *__rest
 }
 
 // ---- A2: Eq. 1 --------------------------------------------------------------
-__device__ __forceinline__ int64_t ipow_k(int64_t b, int k) { return k == 3 ? b * b * b : b * b; }
+__host__ __device__ __forceinline__ int64_t ipow_k(int64_t b, int k) { return k == 3 ? b * b * b : b * b; }
 
 // smallest integer b >= 2 with b^k s >= n (R6; k = 2: R23)
-__device__ __forceinline__ int eq1_branching(int64_t n, int64_t s, int k) {
+__host__ __device__ __forceinline__ int eq1_branching(int64_t n, int64_t s, int k) {
     int64_t m = (n + s - 1) / s;  // b^k s >= n  <=>  b^k >= ceil(n/s)
     int64_t b = (int64_t)(k == 3 ? cbrt((double)m) : sqrt((double)m));
     if (b < 2) b = 2;
@@ -156,7 +160,13 @@ __device__ __forceinline__ int eq1_branching(int64_t n, int64_t s, int k) {
 }
 
 // sub-cells along z: b (k = 3) or 1 (k = 2: the z axis is one slab)
-__device__ __forceinline__ int bz_of(int b, int kz) { return kz ? b : 1; }
+__host__ __device__ __forceinline__ int bz_of(int b, int kz) { return kz ? b : 1; }
+
+// sub-cells of a node of `count` particles (Eq. 1 b0, before any halving)
+__host__ __device__ __forceinline__ long long node_cells(int64_t count, int64_t s, int octree, int dims) {
+    const int b = octree ? 2 : eq1_branching(count, s, dims);
+    return (long long)b * b * bz_of(b, dims == 3 ? 1 : 0);
+}
 
 __global__ void level_b_kernel(LevelNode *ln, int64_t nn, int64_t s, int octree, int dims, const NodeRec *nodes) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -277,11 +287,13 @@ struct CellIn {
     const int32_t *hist;
     int32_t s;
     bool child_ok;  // depth + 1 < depth_cap
+    int octree, dims;
     __device__ CellScan operator()(int64_t g) const {
         long long c = hist[g];
         bool is_node = child_ok && c > s;
         bool is_leaf = c > 0 && !is_node;
-        return CellScan{c, is_node ? c : 0, is_node ? 1 : 0, is_leaf ? 1 : 0};
+        return CellScan{c, is_node ? c : 0, is_node ? node_cells(c, s, octree, dims) : 0, is_node ? 1 : 0,
+                        is_leaf ? 1 : 0, is_leaf ? (int)c : 0, 0};
     }
 };
 struct CellOut {
@@ -671,8 +683,10 @@ __global__ void leaf_rec_kernel(const double *__restrict__ box, const int32_t *_
     }
 }
 
-__global__ void unit_key_kernel(const int4 *__restrict__ units, int64_t nu, const double *__restrict__ leaf_box,
-                                const double *__restrict__ box, unsigned *__restrict__ key, int32_t *__restrict__ hist) {
+__global__ void unit_key_kernel(const int4 *__restrict__ units, const long long *__restrict__ dnu,
+                                const double *__restrict__ leaf_box, const double *__restrict__ box,
+                                unsigned *__restrict__ key, int32_t *__restrict__ hist) {
+    const int64_t nu = *dnu;  // (the unit count stays on the device: grids sized by its bound)
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
         const double *lb = leaf_box + 6 * (int64_t)units[u].x;
         unsigned q[3];
@@ -697,8 +711,10 @@ struct HistOut {
     __device__ void operator()(int64_t i, long long exc, long long) const { start[i] = (int32_t)exc; }
 };
 
-__global__ void unit_scatter_kernel(const int4 *__restrict__ units, int64_t nu, const unsigned *__restrict__ key,
-                                    int32_t *__restrict__ cursor, int4 *__restrict__ out) {
+__global__ void unit_scatter_kernel(const int4 *__restrict__ units, const long long *__restrict__ dnu,
+                                    const unsigned *__restrict__ key, int32_t *__restrict__ cursor,
+                                    int4 *__restrict__ out) {
+    const int64_t nu = *dnu;
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x)
         out[atomicAdd(&cursor[key[u]], 1)] = units[u];
 }
@@ -834,6 +850,8 @@ void build_tree(TreeDev &t, const double *pos) {
     DBuf<int> dflags;
     DBuf<unsigned long long> dstat;  // halvings, max_leaf, overfull
     DBuf<double> partials, dbox;
+    DBuf<long long> dnu(1);  // work units (A9), read with the build's closing read
+    int64_t max_leaf_h = n;  // largest leaf (the root leaf: n; else from the levels' cell scans)
     {
         Phase ph("build.setup");
         fin.alloc(n);
@@ -877,6 +895,7 @@ void build_tree(TreeDev &t, const double *pos) {
         t.root_is_leaf = true;
     } else {
         t.root_is_leaf = false;
+        max_leaf_h = 0;
         act_node[0].alloc(n);
         BT_CUDA(cudaMemsetAsync(act_node[0].p, 0, n * sizeof(int32_t), st));
         act[1].alloc(n);
@@ -903,18 +922,19 @@ void build_tree(TreeDev &t, const double *pos) {
         DBuf<int32_t> hist;
         DBuf<int64_t> cpre;
         DBuf<int32_t> cid, cact;
-        DBuf<long long> dtotal(1);
         DBuf<CellScan> dcs(1);
+        // the level's cell count: the root's from Eq. 1 on the host, every
+        // later level's from the previous level's cell scan (ncnext) -- one
+        // host read per level (its cell scan + the halving flag of round 0)
+        int64_t ncells_next = node_cells(n, t.s, t.octree ? 1 : 0, t.dims);
         while (nn > 0) {
             Phase ph("build.level");
             // A2: Eq. 1 and the level's cell layout
             level_b_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.s, t.octree ? 1 : 0, t.dims,
                                                                         t.nodes.p);
             BT_LAUNCH("level_b");
-            device_scan<long long>(CellsOfNode{ln.p}, CellBaseOut{ln.p}, nn, dtotal.p);
-            long long ncells_h = 0;
-            read_back({{dtotal.p, &ncells_h, sizeof(long long)}});
-            const int64_t ncells = ncells_h;
+            device_scan<long long>(CellsOfNode{ln.p}, CellBaseOut{ln.p}, nn, (long long *)nullptr);
+            const int64_t ncells = ncells_next;
             if (ncells > (int64_t)0xffffffffLL)  // (keys hold a level's cell index in 32 bits)
                 throw Error(BT_ERR_OOM, "bt_build: more than 2^32 sub-cells in one level (bucket_size too small for n)");
             hist.reserve(ncells, 0);
@@ -926,7 +946,14 @@ void build_tree(TreeDev &t, const double *pos) {
             const unsigned gridC = grid_for(ncells, kThreads, (int64_t)sms * 16);
             const unsigned gridA = grid_for(n_act, kThreads, (int64_t)sms * 16);
 
-            // A3-A5: distribute, ratio, halving rounds (at most log2 b0 rounds)
+            // A3-A5: distribute, ratio, halving rounds (at most log2 b0 rounds).
+            // Round 0 is followed by the level's cell scan (A6) before the
+            // host looks at its halving flag: when no node halves (the common
+            // case) that scan is the level's and one read returns both.
+            const bool child_ok = (level + 1) < t.depth_cap;
+            const CellIn cin{hist.p, (int32_t)t.s, child_ok, t.octree ? 1 : 0, t.dims};
+            CellScan tot{};
+            bool scanned = false;
             for (int round = 0;; round++) {
                 if (round > 0) {
                     zero_flagged_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells);
@@ -942,19 +969,27 @@ void build_tree(TreeDev &t, const double *pos) {
                 ratio_decide_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.beta, dflags.p + 1, t.nodes.p);
                 BT_LAUNCH("ratio_decide");
                 int any = 0;
-                read_back({{dflags.p + 1, &any, sizeof(int)}});
+                if (round == 0) {
+                    device_scan<CellScan>(cin, CellOut{cpre.p, cid.p, cact.p}, ncells, dcs.p);
+                    read_back({{dflags.p + 1, &any, sizeof(int)}, {dcs.p, &tot, sizeof(CellScan)}});
+                    scanned = !any;
+                } else {
+                    read_back({{dflags.p + 1, &any, sizeof(int)}});
+                }
                 if (!any) break;
             }
             finalize_level_nodes_kernel<<<grid_for(nn, kThreads), kThreads, 0, st>>>(ln.p, nn, t.nodes.p, t.n_cells,
                                                                                        dstat.p);
             BT_LAUNCH("finalize_level_nodes");
 
-            // A6: one scan over the level's cells
-            const bool child_ok = (level + 1) < t.depth_cap;
-            device_scan<CellScan>(CellIn{hist.p, t.s, child_ok}, CellOut{cpre.p, cid.p, cact.p}, ncells, dcs.p);
-            CellScan tot;
-            read_back({{dcs.p, &tot, sizeof(CellScan)}});
+            // A6: one scan over the level's cells (done above unless a node halved)
+            if (!scanned) {
+                device_scan<CellScan>(cin, CellOut{cpre.p, cid.p, cact.p}, ncells, dcs.p);
+                read_back({{dcs.p, &tot, sizeof(CellScan)}});
+            }
             const int64_t nn_next = tot.nnode, n_act_next = tot.actoff, nleaf = tot.nleaf;
+            ncells_next = tot.ncnext;
+            max_leaf_h = std::max<int64_t>(max_leaf_h, tot.maxleaf);
 
             // A8: emit children / leaves / cell table
             ln_next.alloc(nn_next > 0 ? nn_next : 1);
@@ -1030,37 +1065,32 @@ void build_tree(TreeDev &t, const double *pos) {
         leaf_rec_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
             t.leaf_box.p, t.leaf_begin.p, t.leaf_count.p, t.n_leaves, t.leaf_rec.p);
         BT_LAUNCH("leaf_rec");
-        DBuf<long long> dtot(1);
         // small leaves paired (runs of small leaves, pair by rank, box check)
         DBuf<int32_t> rs(t.n_leaves), merge(t.n_leaves);
         device_scan<MaxScan>(RunStartIn{t.leaf_count.p}, RunStartOut{rs.p}, t.n_leaves, (MaxScan *)nullptr);
         pair_leaves_kernel<<<grid_for(t.n_leaves, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
             t.leaf_count.p, t.leaf_box.p, rs.p, t.n_leaves, merge.p);
         BT_LAUNCH("pair_leaves");
-        // units: count first (to size the array), then write
-        device_scan<long long>(UnitsOfLeaf{t.leaf_count.p, merge.p}, NullOut{}, t.n_leaves, dtot.p);
-        long long nu = 0;
-        unsigned long long ml = 0;
-        read_back({{dtot.p, &nu, sizeof(long long)}, {dstat.p + 1, &ml, sizeof(ml)}});
         // leaves above kBigLeaf (depth cap): records in canonical order by a segmented sort
-        if (ml > (unsigned long long)kBigLeaf) order_big_leaves(t, fin.p, dflags.p + 2);
-        t.units.alloc(nu);
-        t.n_units = nu;
+        if (max_leaf_h > kBigLeaf) order_big_leaves(t, fin.p, dflags.p + 2);
+        // units, sized by their bound (<= ceil(q / kUnitQ) per leaf): the count
+        // stays on the device until the build's closing read
+        const int64_t nu_bound = t.n_leaves + n / kUnitQ + 1;
+        DBuf<int4> units_raw(nu_bound);
+        t.units.alloc(nu_bound);
         device_scan<long long>(UnitsOfLeaf{t.leaf_count.p, merge.p},
-                               UnitsOut{t.leaf_begin.p, t.leaf_count.p, merge.p, t.units.p}, t.n_leaves, dtot.p);
-        if (nu > 1) {  // Morton order of the units (walk locality)
-            DBuf<unsigned> key(nu);
+                               UnitsOut{t.leaf_begin.p, t.leaf_count.p, merge.p, units_raw.p}, t.n_leaves, dnu.p);
+        {  // Morton order of the units (walk locality)
+            DBuf<unsigned> key(nu_bound);
             DBuf<int32_t> bucket(1u << kMortonBits);
-            DBuf<int4> sorted(nu);
             BT_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(int32_t) << kMortonBits, st));
-            unit_key_kernel<<<grid_for(nu, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(t.units.p, nu, t.leaf_box.p,
-                                                                                       dbox.p, key.p, bucket.p);
+            unit_key_kernel<<<grid_for(nu_bound, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
+                units_raw.p, dnu.p, t.leaf_box.p, dbox.p, key.p, bucket.p);
             BT_LAUNCH("unit_key");
             device_scan<long long>(HistIn{bucket.p}, HistOut{bucket.p}, 1 << kMortonBits, (long long *)nullptr);
-            unit_scatter_kernel<<<grid_for(nu, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(t.units.p, nu, key.p,
-                                                                                           bucket.p, sorted.p);
+            unit_scatter_kernel<<<grid_for(nu_bound, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
+                units_raw.p, dnu.p, key.p, bucket.p, t.units.p);
             BT_LAUNCH("unit_scatter");
-            t.units = std::move(sorted);
         }
     }
     // the build's one closing control read: statistics, root box, root b, input check
@@ -1068,12 +1098,15 @@ void build_tree(TreeDev &t, const double *pos) {
     double hb[8];
     int hbad = 0;
     int32_t rb = 0;
+    long long nu = 0;
     if (t.root_is_leaf)
         read_back({{dstat.p, hstat, 4 * sizeof(unsigned long long)}, {dbox.p, hb, 7 * sizeof(double)},
-                   {dflags.p, &hbad, sizeof(int)}});
+                   {dflags.p, &hbad, sizeof(int)}, {dnu.p, &nu, sizeof(long long)}});
     else
         read_back({{dstat.p, hstat, 4 * sizeof(unsigned long long)}, {dbox.p, hb, 7 * sizeof(double)},
-                   {dflags.p, &hbad, sizeof(int)}, {&t.nodes.p[0].b, &rb, sizeof(int32_t)}});
+                   {dflags.p, &hbad, sizeof(int)}, {&t.nodes.p[0].b, &rb, sizeof(int32_t)},
+                   {dnu.p, &nu, sizeof(long long)}});
+    t.n_units = nu;
     if (hbad) throw Error(BT_ERR_INPUT, "bt_build: non-finite coordinate or |coordinate| > 1e150");
     for (int l = 0; l < 3; l++) {
         t.box_lo[l] = hb[l];
