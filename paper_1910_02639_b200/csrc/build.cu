@@ -611,9 +611,10 @@ __global__ void remap_cells_kernel(int32_t *cells, int64_t n_cells, const int32_
 // ---- walk unit order: Morton (Z-order) of the leaf centre ------------------
 // The walk processes units in array order; depth-first leaf order puts the
 // +z neighbour of a root cell b^2 cells later, so concurrently processed units
-// would not share candidate leaves in L2.  Units are bucketed by the top 21
-// bits of the 30-bit Morton code of their leaf centre (counting sort).
-constexpr int kMortonBits = 21;
+// would not share candidate leaves in L2.  Units are bucketed by the top
+// bits (about 2 buckets per unit, at most 21) of the 30-bit Morton code of
+// their leaf centre (counting sort).
+constexpr int kMortonBits = 21;  // at most; fewer for few units (about 2 buckets per unit)
 
 __device__ __forceinline__ unsigned spread3(unsigned v) {  // 10 bits -> every third bit
     v &= 0x3ffu;
@@ -684,7 +685,7 @@ __global__ void leaf_rec_kernel(const double *__restrict__ box, const int32_t *_
 }
 
 __global__ void unit_key_kernel(const int4 *__restrict__ units, const long long *__restrict__ dnu,
-                                const double *__restrict__ leaf_box, const double *__restrict__ box,
+                                const double *__restrict__ leaf_box, const double *__restrict__ box, int mbits,
                                 unsigned *__restrict__ key, int32_t *__restrict__ hist) {
     const int64_t nu = *dnu;  // (the unit count stays on the device: grids sized by its bound)
     for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < nu; u += (int64_t)gridDim.x * blockDim.x) {
@@ -696,7 +697,7 @@ __global__ void unit_key_kernel(const int4 *__restrict__ units, const long long 
             q[l] = (unsigned)fmin(1023.0, fmax(0.0, f * 1024.0));
         }
         const unsigned m = spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2);
-        const unsigned k = m >> (30 - kMortonBits);
+        const unsigned k = m >> (30 - mbits);
         key[u] = k;
         atomicAdd(&hist[k], 1);
     }
@@ -1082,12 +1083,14 @@ void build_tree(TreeDev &t, const double *pos) {
                                UnitsOut{t.leaf_begin.p, t.leaf_count.p, merge.p, units_raw.p}, t.n_leaves, dnu.p);
         {  // Morton order of the units (walk locality)
             DBuf<unsigned> key(nu_bound);
-            DBuf<int32_t> bucket(1u << kMortonBits);
-            BT_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(int32_t) << kMortonBits, st));
+            int mbits = 6;
+            while (mbits < kMortonBits && (int64_t(1) << mbits) < 2 * nu_bound) mbits++;
+            DBuf<int32_t> bucket(size_t(1) << mbits);
+            BT_CUDA(cudaMemsetAsync(bucket.p, 0, sizeof(int32_t) << mbits, st));
             unit_key_kernel<<<grid_for(nu_bound, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
-                units_raw.p, dnu.p, t.leaf_box.p, dbox.p, key.p, bucket.p);
+                units_raw.p, dnu.p, t.leaf_box.p, dbox.p, mbits, key.p, bucket.p);
             BT_LAUNCH("unit_key");
-            device_scan<long long>(HistIn{bucket.p}, HistOut{bucket.p}, 1 << kMortonBits, (long long *)nullptr);
+            device_scan<long long>(HistIn{bucket.p}, HistOut{bucket.p}, int64_t(1) << mbits, (long long *)nullptr);
             unit_scatter_kernel<<<grid_for(nu_bound, kThreads, (int64_t)sms * 8), kThreads, 0, st>>>(
                 units_raw.p, dnu.p, key.p, bucket.p, t.units.p);
             BT_LAUNCH("unit_scatter");

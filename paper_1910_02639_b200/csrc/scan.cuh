@@ -116,11 +116,36 @@ struct TileOut {
     __device__ void operator()(int64_t i, const T &exc, const T &) const { p[i] = exc; }
 };
 
+// one tile (n <= kScanTile): the whole scan in one block, one launch
+template <class T, class In, class Out>
+__global__ void __launch_bounds__(kScanThreads) scan_single_kernel(In in, Out out, int64_t n, T *total) {
+    const int64_t base = (int64_t)threadIdx.x * kScanItems;
+    T vals[kScanItems];
+    T acc{};
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        vals[k] = (base + k < n) ? in(base + k) : T{};
+        acc = acc + vals[k];
+    }
+    T tot;
+    T pre = block_exclusive(acc, tot);
+#pragma unroll
+    for (int k = 0; k < kScanItems; k++) {
+        if (base + k < n) out(base + k, pre, vals[k]);
+        pre = pre + vals[k];
+    }
+    if (threadIdx.x == 0 && total) *total = tot;
+}
+
 // Exclusive scan of n items; total (device pointer, may be null) receives the sum.
 template <class T, class In, class Out>
 void device_scan(In in, Out out, int64_t n, T *total) {
     int64_t ntiles = (n + kScanTile - 1) / kScanTile;
-    if (ntiles < 1) ntiles = 1;
+    if (ntiles <= 1) {
+        scan_single_kernel<T, In, Out><<<1, kScanThreads, 0, stream()>>>(in, out, n, total);
+        BT_LAUNCH("scan_single");
+        return;
+    }
     DBuf<T> tiles(ntiles);
     scan_reduce_kernel<T, In><<<(unsigned)ntiles, kScanThreads, 0, stream()>>>(in, n, tiles.p);
     BT_LAUNCH("scan_reduce");
