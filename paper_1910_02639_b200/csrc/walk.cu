@@ -1883,24 +1883,8 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
                 walk_kernel<false, kSym><<<g.w, kWalkThreads, 0, st>>>(a);
                 BT_LAUNCH(kSym ? "walk_test_sym" : "walk_test");
             }
-            read_counters(t, hc);
-            const bool fits = hc[C_CAND] <= a.cand_cap && hc[C_MASK] <= a.mask_cap;
-            if (!fits) throw Error(BT_ERR_CUDA, std::string(who) + ": internal: walk arena bound exceeded");
-            t.rec_valid = true;
-            t.rec_csum = hc[C_CSUM];
-            t.rec_h = h;
-            t.rec_hsum = hsum;
-            t.rec_exact = g_exact_only;
-            t.rec_sym = kSym;
-            t.rec_tree_order = t.tree_order;
+            // (the walk's counters are read with the offsets total below: one host read)
         }
-        t.staged = hc[C_STAGED];
-        t.loaded = hc[C_LOADED];
-        t.tests = hc[C_TESTS];
-        t.exact_tests = hc[C_EXACT];
-        t.mask_words = hc[C_MASK];
-        t.cand_slots = hc[C_CAND];
-        t.mask_words_nz = hc[C_NZW];
         cnt_now = cnt;
         if (count_pass) {
             DBuf<long long> dtot(1);
@@ -1915,12 +1899,30 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
             BT_LAUNCH("max_count");
         }
     }
-    int64_t total = 0, maxc = 0, over = 0;
-    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p + C_MAXC, &maxc, sizeof(int64_t)},
-               {t.counters.p + C_OVER, &over, sizeof(int64_t)}});
+    int64_t total = 0;
+    long long hw[C_N];
+    read_back({{offsets + n, &total, sizeof(int64_t)}, {t.counters.p, hw, C_N * sizeof(long long)}});
+    if (run_test) {
+        const bool fits = hw[C_CAND] <= (long long)t.arena_cands.n && hw[C_MASK] <= (long long)t.arena_masks.n;
+        if (!fits) throw Error(BT_ERR_CUDA, std::string(who) + ": internal: walk arena bound exceeded");
+        t.rec_valid = true;
+        t.rec_csum = hw[C_CSUM];
+        t.rec_h = h;
+        t.rec_hsum = hsum;
+        t.rec_exact = g_exact_only;
+        t.rec_sym = kSym;
+        t.rec_tree_order = t.tree_order;
+        t.staged = hw[C_STAGED];
+        t.loaded = hw[C_LOADED];
+        t.tests = hw[C_TESTS];
+        t.exact_tests = hw[C_EXACT];
+        t.mask_words = hw[C_MASK];
+        t.cand_slots = hw[C_CAND];
+        t.mask_words_nz = hw[C_NZW];
+    }
     if (count_pass) {
-        t.max_count = maxc;
-        t.rows_over_ngmax = over;
+        t.max_count = hw[C_MAXC];
+        t.rows_over_ngmax = hw[C_OVER];
     }
     t.total_pairs = total;
     if (!fill_pass || nbr_idx == nullptr) return;
