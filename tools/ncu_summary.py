@@ -98,7 +98,12 @@ def full(rep, out, traffic=None, key=None, config=None):
         except Exception:
             pass
         t.setdefault("kernels", {})
-        t["kernels"][key] = max(dram.values())
+        # bench.py's kernel keys -> the report's kernel of that name (first launch)
+        names = {"walk_desc": "desc_kernel", "walk_test": "walk_kernel", "walk_fill": "fill_kernel"}
+        for bk, kn in names.items():
+            hit = [v for (i, name), v in sorted(dram.items(), key=lambda kv: int(kv[0][0])) if kn in name]
+            if hit and (key in (None, "all") or key == bk):
+                t["kernels"][bk] = hit[0]
         t["config"] = int(config)
         t["source"] = f"ncu --set full dram__bytes_read.sum + dram__bytes_write.sum ({rep.split('/')[-1]})"
         json.dump(t, open(traffic, "w"), indent=1)
