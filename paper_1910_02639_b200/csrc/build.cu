@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kThreads) pack_bbox_kernel(const double *__res
         double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
         // finite and |x| <= 1e150 (keeps squared distances finite)
         if (!(fabs(x) <= 1e150) || !(fabs(y) <= 1e150) || !(fabs(z) <= 1e150)) badv = 1;
-        rec[i] = make_double4(x, y, z, __longlong_as_double((long long)i));
+        if (rec) rec[i] = make_double4(x, y, z, __longlong_as_double((long long)i));
         mn[0] = fmin(mn[0], x); mn[1] = fmin(mn[1], y); mn[2] = fmin(mn[2], z);
         mx[0] = fmax(mx[0], x); mx[1] = fmax(mx[1], y); mx[2] = fmax(mx[2], z);
     }
@@ -141,11 +141,6 @@ __global__ void __launch_bounds__(256) root_box_kernel(const double *partials, i
     root->cell_base = 0;
 }
 
-__global__ void copy_rec_kernel(const double4 *__restrict__ src, double4 *__restrict__ dst, int64_t n) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
-}
-
 // ---- A2: Eq. 1 --------------------------------------------------------------
 __host__ __device__ __forceinline__ int64_t ipow_k(int64_t b, int k) { return k == 3 ? b * b * b : b * b; }
 
@@ -194,8 +189,12 @@ __device__ __forceinline__ int64_t find_node(const LevelNode *ln, int64_t nn, in
 }
 
 // ---- A3 + A4: Eq. 2, Eq. 3, histogram ---------------------------------------
+// the root level (kRoot) reads the caller's positions directly: every
+// particle belongs to node 0 and its record is (pos, caller index)
+template <bool kRoot>
 __global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__restrict__ act, const int32_t *__restrict__ act_node,
-                                                            int64_t n_act, const LevelNode *__restrict__ ln,
+                                                            const double *__restrict__ pos, int64_t n_act,
+                                                            const LevelNode *__restrict__ ln,
                                                             const NodeRec *__restrict__ nodes, uint32_t *__restrict__ keys,
                                                             int32_t *__restrict__ hist, int round) {
     // (BT_SCATTER_UNROLL particles per thread: independent load chains in flight)
@@ -207,8 +206,13 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__res
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t p = p0 + u * stride;
-            node[u] = p < n_act ? act_node[p] : -1;
-            if (node[u] >= 0) r[u] = act[p];
+            if (kRoot) {
+                node[u] = p < n_act ? 0 : -1;
+                if (node[u] >= 0) r[u] = make_double4(pos[3 * p], pos[3 * p + 1], pos[3 * p + 2], 0.0);
+            } else {
+                node[u] = p < n_act ? act_node[p] : -1;
+                if (node[u] >= 0) r[u] = act[p];
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -391,7 +395,9 @@ __global__ void finalize_level_nodes_kernel(const LevelNode *ln, int64_t nn, Nod
 // Latency-bound per particle (node record -> cell -> returning atomic on the
 // cell cursor -> destination): kUnroll particles per thread keep that many
 // independent chains in flight.
-__global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__restrict__ act, int64_t n_act,
+template <bool kRoot>
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__restrict__ act, const double *__restrict__ pos,
+                                                           int64_t n_act,
                                                            const uint32_t *__restrict__ keys, int32_t *cursor,
                                                            double4 *__restrict__ out_final, double4 *__restrict__ act_next) {
     // cursor[g] (written by emit): the cell's next destination, bit 31 set
@@ -407,7 +413,8 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__rest
             const int64_t p = p0 + u * stride;
             if (p < n_act) {
                 d[u] = atomicAdd(&cursor[keys[p]], 1);
-                v[u] = act[p];
+                v[u] = kRoot ? make_double4(pos[3 * p], pos[3 * p + 1], pos[3 * p + 2], __longlong_as_double((long long)p))
+                             : act[p];
             }
         }
 #pragma unroll
@@ -869,8 +876,10 @@ void build_tree(TreeDev &t, const double *pos) {
     // A1: records in caller order + root box
     {
         Phase ph("build.bbox");
-        act[0].alloc(n);
-        pack_bbox_kernel<<<gridN, kThreads, 0, st>>>(pos, n, act[0].p, partials.p, dflags.p);
+        // records are written only for a root leaf (straight into the final
+        // array); otherwise the root level reads pos itself
+        const bool root_leaf = n <= t.s || t.depth_cap == 0;
+        pack_bbox_kernel<<<gridN, kThreads, 0, st>>>(pos, n, root_leaf ? fin.p : nullptr, partials.p, dflags.p);
         BT_LAUNCH("pack_bbox");
         root_box_kernel<<<1, 256, 0, st>>>(partials.p, (int)gridN, t.nodes.p, dbox.p);
         BT_LAUNCH("root_box");
@@ -887,8 +896,6 @@ void build_tree(TreeDev &t, const double *pos) {
         BT_CUDA(cudaMemcpyAsync(t.leaf_begin.p, &hl[0], 4, cudaMemcpyHostToDevice, st));
         BT_CUDA(cudaMemcpyAsync(t.leaf_count.p, &hl[1], 4, cudaMemcpyHostToDevice, st));
         BT_CUDA(cudaMemcpyAsync(t.leaf_depth.p, &hl[2], 4, cudaMemcpyHostToDevice, st));
-        copy_rec_kernel<<<gridN, kThreads, 0, st>>>(act[0].p, fin.p, n);
-        BT_LAUNCH("copy_rec");
         t.n_leaves = 1;
         t.n_nodes = 0;
         t.level_begin.clear();
@@ -897,8 +904,8 @@ void build_tree(TreeDev &t, const double *pos) {
     } else {
         t.root_is_leaf = false;
         max_leaf_h = 0;
-        act_node[0].alloc(n);
-        BT_CUDA(cudaMemsetAsync(act_node[0].p, 0, n * sizeof(int32_t), st));
+        act[0].alloc(n);
+        act_node[0].alloc(n);  // (level 0 reads pos and node 0: neither array)
         act[1].alloc(n);
         act_node[1].alloc(n);
         DBuf<uint32_t> keys(n);
@@ -960,8 +967,12 @@ void build_tree(TreeDev &t, const double *pos) {
                     zero_flagged_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells);
                     BT_LAUNCH("zero_flagged");
                 }
-                key_hist_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, n_act, ln.p, t.nodes.p, keys.p,
-                                                            hist.p, round);
+                if (level == 0)
+                    key_hist_kernel<true><<<gridA, kThreads, 0, st>>>(nullptr, nullptr, pos, n_act, ln.p, t.nodes.p,
+                                                                      keys.p, hist.p, round);
+                else
+                    key_hist_kernel<false><<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, nullptr, n_act, ln.p,
+                                                                       t.nodes.p, keys.p, hist.p, round);
                 BT_LAUNCH("key_hist");
                 if (t.octree) break;  // no ratio test for the octree policy
                 under_count_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, t.alpha * (double)t.s);
@@ -1008,7 +1019,11 @@ void build_tree(TreeDev &t, const double *pos) {
             // particles first grouped by coarse cell range so the scatter's
             // destination window stays L2-resident -- measured slower in round 2:
             // cfg 5 levels 3.9 -> 5.1 ms.)
-            scatter_kernel<<<gridA, kThreads, 0, st>>>(act[cur].p, n_act, keys.p, hist.p, fin.p, act[cur ^ 1].p);
+            if (level == 0)
+                scatter_kernel<true><<<gridA, kThreads, 0, st>>>(nullptr, pos, n_act, keys.p, hist.p, fin.p, act[cur ^ 1].p);
+            else
+                scatter_kernel<false><<<gridA, kThreads, 0, st>>>(act[cur].p, nullptr, n_act, keys.p, hist.p, fin.p,
+                                                                  act[cur ^ 1].p);
             BT_LAUNCH("scatter");
             if (nn_next > 0) {
                 node_ids_kernel<<<grid_for(nn_next * 32, kThreads, (int64_t)sms * 16), kThreads, 0, st>>>(
