@@ -179,7 +179,6 @@ struct TreeDev {
     DBuf<int32_t> ulist;                   // candidate leaf lists of all units
     DBuf<unsigned long long> arena_masks;  // neighbor masks per (64-candidate chunk, query)
     DBuf<int32_t> arena_cands;             // candidate caller indices per slot
-    DBuf<float4> scratch;                  // walk staging scratch (per resident warp)
     bool rec_valid = false;    // arena holds the test pass of (rec_h, rec_hsum, rec_exact)
     const double *rec_h = nullptr;
     long long rec_hsum = 0;

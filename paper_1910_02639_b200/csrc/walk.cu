@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kQ = 64;           // queries per unit (== build.cu kUnitQ)
 constexpr int kBlk = 128;        // staged candidates per test block
-constexpr int kScratch = 4096;   // staged candidates per warp scratch (global, L2-resident); multiple of kBlk
+constexpr int kStg = kBlk + 32;  // staged candidates per warp (shared memory): a block plus one window
 constexpr int kGroup = 32;       // candidate leaves per staging group (one per lane)
 constexpr int kGroupPos = 2048;  // positions a multi-leaf group may span (its leaf-start bitmap)
 constexpr int kFrontCap = 512;   // shared-memory descent frontier per level
@@ -112,11 +112,9 @@ struct WalkArgs {
     int64_t nbr_cap;          // int32 slots of nbr -- bounds checks
     unsigned long long *masks;
     long long mask_cap;
-    float4 *scratch;          // per walk warp: kScratch staged candidates (ax, ay, az, tree position)
     int desc_batch;           // units claimed per atomic by the descent warps
     const double *m_tree;     // density mode: masses in tree order
     double *rho;              // density mode: output, caller order
-    float *scrk;              // symmetric mode: per walk warp, kScratch staged -k Mid_j (candidate thresholds)
     const double *leaf_hmax;  // symmetric mode: max h per leaf
     const double *node_hmax;  // symmetric mode: max h per internal node subtree
 };
@@ -666,11 +664,9 @@ struct UnitSm {                     // per-warp unit state (shared memory)
     long long cand_base, mask_base;  // the unit's record bases
     Slab cs, ms;                     // the warp's candidate / mask slabs
     long long tests, exact, staged, loaded, nzw;  // warp totals
-    float4 *scr;                     // the warp's staging scratch (read from here: not rematerialised)
     int32_t *cand_ptr;               // the unit's candidate-index records (a.cands + cand_base)
     double c[3], E;                  // unit centre, coordinate bound (L4)
     double Ru, eps, tqmin;           // symmetric: R'_u, l4_eps(E), smallest query threshold
-    float *scrk;                     // symmetric: the staged candidates' -k Mid_j
     float4 box0, box1;               // fp32 query box relative to c: (lo xyz, cull2), (hi xyz, -)
     int q0, nq;                      // (8-byte aligned: read as one int2)
     float k;                         // band scale of the unit (power of two; 0: force)
@@ -688,6 +684,7 @@ struct WalkSmem {
     float4 loff[kGroup];            // group leaves: fl32(c_leaf - c), w = 1 compact / 0 fp64 records
     float lcull[kGroup];            // symmetric: group leaves' fp32 cull radius^2 (max(R'_u, R'(h_max)))
     float2 qm[kQ + 1];              // symmetric: -k Mid_i per query (packed pair); [kQ]: look-ahead pad
+    float4 stg[kStg];               // staged candidates: fp32 x, y, z relative to the unit centre, tree position
     UnitSm u;
 };
 
@@ -701,9 +698,17 @@ struct DensitySm<true> {
     float4 qraw[kQ];  // fp32 query coordinates relative to the unit centre
     float4 dc[kBlk];  // ax, ay, az (fp32, relative to the unit centre), m_j
 };
-template <bool kDensity>
+// symmetric mode: the staged candidates' -k Mid_j (candidate thresholds)
+template <bool kSym>
+struct SymSm {};
+template <>
+struct SymSm<true> {
+    float stk[kStg];
+};
+template <bool kDensity, bool kSym>
 struct WalkSmemT : WalkSmem {
     DensitySm<kDensity> d;
+    SymSm<kSym> y;
 };
 
 // fp32 square root on the SFU (sqrt.approx: relative error ~2^-22, sqrt(0) = 0)
@@ -718,15 +723,14 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // with |d'| <= 1 (all pairs when `force`; padding slots >= n are never
 // neighbors).  blk: the block's staged candidates (ax, ay, az, tree position).
 template <bool kSym>
-__device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int lane, const float4 *blk, int n,
+__device__ __noinline__ void resolve_band(WalkSmemT<false, kSym> &S, const WalkArgs &a, int lane, int b0, int n,
                                           long long &exact) {
+    const float4 *blk = S.stg + b0;
     const int nch = (n + 63) >> 6;
     const float inf = __int_as_float(0x7f800000);
     const float ku = S.u.k;
     const bool force = S.u.force != 0;  // (inf used for padding Ac)
     const int q0 = S.u.q0, nq = S.u.nq;
-    // symmetric: the block's -k Mid_j (scratch slots blk - scr)
-    const float *blkk = kSym ? S.u.scrk + (blk - S.u.scr) : nullptr;
     for (int k = 0; k < nch; k++) {
         float4 c[2];
         float ac[2], nk[2] = {0.f, 0.f};
@@ -735,10 +739,10 @@ __device__ __noinline__ void resolve_band(WalkSmem &S, const WalkArgs &a, int la
         for (int h = 0; h < 2; h++) {
             const int s = 64 * k + 32 * h + lane;
             real[h] = s < n;
-            c[h] = real[h] ? __ldcg(&blk[s]) : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
+            c[h] = real[h] ? blk[s] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
             const float nc = __fmaf_rn(c[h].z, c[h].z, __fmaf_rn(c[h].y, c[h].y, __fmul_rn(c[h].x, c[h].x)));
             ac[h] = real[h] ? __fmul_rn(ku, nc) : inf;  // identical to test_block
-            if (kSym) nk[h] = real[h] ? __ldcg(&blkk[s]) : 0.f;
+            if constexpr (kSym) nk[h] = real[h] ? S.y.stk[b0 + s] : 0.f;
         }
         for (int q = 0; q < nq; q++) {
             const float4 Q0 = S.q0[q], Q1 = S.q1[q];
@@ -801,8 +805,9 @@ __device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsig
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
-__device__ __forceinline__ void density_block(WalkSmemT<true> &S, const WalkArgs &a, int lane, const float4 *blk, int n,
+__device__ __forceinline__ void density_block(WalkSmemT<true, false> &S, const WalkArgs &a, int lane, int b0, int n,
                                               double (&dacc)[2]) {
+    const float4 *blk = S.stg + b0;
     float4 *P = S.d.dc;       // pair p: (x_2p, x_2p+1, y_2p, y_2p+1)
     float4 *Qz = S.d.dc + kBlk / 2;  // pair p: (z_2p, z_2p+1, m_2p, m_2p+1)
     float *Pf = reinterpret_cast<float *>(P), *Qf = reinterpret_cast<float *>(Qz);
@@ -812,7 +817,7 @@ __device__ __forceinline__ void density_block(WalkSmemT<true> &S, const WalkArgs
         float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
         float m = 0.f;  // padding: m = 0 (no contribution)
         if (sl < n) {
-            c = __ldcg(&blk[sl]);
+            c = blk[sl];
             m = (float)a.m_tree[__float_as_int(c.w)];
         }
         const int p = sl >> 1, o = sl & 1;
@@ -856,8 +861,9 @@ __device__ __forceinline__ void density_block(WalkSmemT<true> &S, const WalkArgs
 // the unit's queries and record the block's masks; returns this lane's count
 // increments for queries (lane, lane + 32).
 template <bool kDensity, bool kSym>
-__device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArgs &a, int lane, const float4 *blk,
-                                           int n, int us0, int b0, double (&dacc)[2]) {
+__device__ __forceinline__ int2 test_block(WalkSmemT<kDensity, kSym> &S, const WalkArgs &a, int lane, int n, int us0,
+                                           int b0, double (&dacc)[2]) {
+    const float4 *blk = S.stg + b0;
     const float inf = __int_as_float(0x7f800000);
     const int nch = (n + 63) >> 6;  // 1 or 2 chunks of 64
     const int nq = S.u.nq;
@@ -869,7 +875,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int s = 32 * j + lane;
-        c[j] = (s < n) ? __ldcg(&blk[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        c[j] = (s < n) ? blk[s] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float nc = __fmaf_rn(c[j].z, c[j].z, __fmaf_rn(c[j].y, c[j].y, __fmul_rn(c[j].x, c[j].x)));
         ac[j] = (s < n) ? __fmul_rn(ku, nc) : inf;  // k |c|^2 (exact scaling)
     }
@@ -901,7 +907,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const int sl = 32 * j + lane;
-            nk[j] = (sl < n) ? __ldcg(&S.u.scrk[b0 + sl]) : inf;  // (padding: u = +inf anyway)
+            if constexpr (kSym) nk[j] = (sl < n) ? S.y.stk[b0 + sl] : inf;  // (padding: u = +inf anyway)
         }
         const unsigned aqm = (unsigned)__cvta_generic_to_shared(&S.qm[0]);
         unsigned long long NM;
@@ -993,7 +999,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity> &S, const WalkArg
     const bool band = S.u.force != 0 || bmin <= 1.0f;
     __syncwarp();
     long long exact = 0;
-    if (__any_sync(0xffffffffu, band)) resolve_band<kSym>(S, a, lane, blk, n, exact);
+    if constexpr (!kDensity)
+        if (__any_sync(0xffffffffu, band)) resolve_band<kSym>(S, a, lane, b0, n, exact);
     // self is never its own neighbor (R12); counts; the final masks recorded
     // for the fill pass (chunk kk = us0 / 64 + k of the unit) straight from
     // the lanes that own the queries
@@ -1045,18 +1052,17 @@ __device__ __forceinline__ void locate(const WalkSmem &S, int total, bool single
 }
 
 // Stage the particles of the current leaf group from window w0 on (lemma L3
-// cull) into the warp's scratch at nst, until the group is done or the
-// scratch cannot take another window.  kMixed: some leaf of the group is
+// cull) into the warp's staging buffer at nst, until the group is done or a
+// whole block is staged.  kMixed: some leaf of the group is
 // staged from the fp64 records (a = fl32(fl64(x - c))).
 template <bool kMixed, bool kSym, bool kD>
-__device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int lane, int total, bool single,
+__device__ __forceinline__ void stage_group(WalkSmemT<kD, kSym> &S, const WalkArgs &a, int lane, int total, bool single,
                                             int &w0, int &nst, int slot0) {
     const unsigned lt = lanemask_lt(), le = lt | (1u << lane);
     const float4 *__restrict__ rec32 = a.rec32;
     const float4 B0 = S.u.box0, B1 = S.u.box1;
     const int2 qn = lds2iv(&S.u.q0);
     const bool rec_ok = S.u.rec_ok != 0;
-    float4 *const scr = S.u.scr;
     int32_t *const cands = S.u.cand_ptr + (unsigned)slot0;
     // record of position pos: the compact record, or (large leaf of a kMixed
     // group, `rel` set) the fp64 record already relative to the unit centre
@@ -1083,7 +1089,7 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
     float4 r = load(pos, mine, rel);
 #pragma unroll 1
     for (; w0 < total; w0 += 32) {
-        if (nst > kScratch - 32) break;  // full: the caller tests the staged blocks and resumes at w0
+        if (nst >= kBlk) break;  // a block is staged: the caller tests it and resumes at w0
         // the next window's record load is issued before this window is processed
         int pos_n = -1, mine_n = 0;
         bool rel_n = false;
@@ -1110,14 +1116,13 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
         const unsigned km = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             const int slot = nst + __popc(km & lt);
-            BT_DEV_CHECK(slot < kScratch && pos >= 0 && pos < a.n_rec);
+            BT_DEV_CHECK(slot < kStg && pos >= 0 && pos < a.n_rec);
             BT_DEV_CHECK(!rec_ok || S.u.cand_base + slot0 + slot < a.cand_cap);
-            __stcg(&scr[(unsigned)slot], make_float4(ax, ay, az, __int_as_float(pos)));  // L2-resident scratch
-            if (kSym) {  // -k Mid_j of the candidate threshold; +inf when it cannot decide (Tj <= Tqmin, L4s)
+            S.stg[slot] = make_float4(ax, ay, az, __int_as_float(pos));
+            if constexpr (kSym) {  // -k Mid_j of the candidate threshold; +inf when it cannot decide (Tj <= Tqmin, L4s)
                 const double tj = __dmul_rn(2.0, a.h_tree[pos]);
                 const double Tj = __dmul_rn(tj, tj);
-                __stcg(&S.u.scrk[(unsigned)slot],
-                       Tj > S.u.tqmin ? -S.u.k * __double2float_rn(Tj) : __int_as_float(0x7f800000));
+                S.y.stk[slot] = Tj > S.u.tqmin ? -S.u.k * __double2float_rn(Tj) : __int_as_float(0x7f800000);
             }
             if (rec_ok) __stcs(&cands[(unsigned)slot], a.tree_order ? pos : __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
@@ -1137,14 +1142,11 @@ __device__ __forceinline__ void stage_group(WalkSmem &S, const WalkArgs &a, int 
 // radius, each pair tested against both thresholds (lemma L4s)
 template <bool kDensity, bool kSym>
 __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(WalkArgs a) {
-    __shared__ WalkSmemT<kDensity> smem[kWalkThreads / 32];
+    __shared__ WalkSmemT<kDensity, kSym> smem[kWalkThreads / 32];
     const int lane = threadIdx.x & 31;
-    WalkSmemT<kDensity> &S = smem[threadIdx.x >> 5];
+    WalkSmemT<kDensity, kSym> &S = smem[threadIdx.x >> 5];
     const float inf = __int_as_float(0x7f800000);
-    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (lane == 0) {
-        S.u.scr = a.scratch + gwarp * kScratch;
-        if (kSym) S.u.scrk = a.scrk + gwarp * kScratch;
         S.u.cs = Slab();
         S.u.ms = Slab();
         S.u.tests = S.u.exact = S.u.staged = S.u.loaded = S.u.nzw = 0;
@@ -1263,11 +1265,11 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         long long loaded = 0;
         const int nleaf = R.nleaf;
         const long long list_off = R.list_off;
-        int nst = 0, slot0 = 0;            // candidates in the scratch; unit slot of scratch[0]
+        int nst = 0, slot0 = 0;            // candidates in the staging buffer; unit slot of stg[0]
         int g0 = 0, w0 = 0, total = 0, nl = 0;
         bool mixed = false, have_group = false;
         for (;;) {
-            // ---- staging phase: fill the scratch
+            // ---- staging phase: stage (at least) a block
             while (g0 < nleaf) {
                 if (!have_group) {
                     // the group's leaves: first position, count, offset of the centre
@@ -1336,7 +1338,7 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                     stage_group<true, kSym, kDensity>(S, a, lane, total, nl == 1, w0, nst, slot0);
                 else
                     stage_group<false, kSym, kDensity>(S, a, lane, total, nl == 1, w0, nst, slot0);
-                if (w0 < total) break;  // scratch full
+                if (w0 < total) break;  // a block is staged
                 loaded += total;
                 g0 += nl;
                 have_group = false;
@@ -1347,11 +1349,10 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             const int ntest = done ? nst : nst - nst % kBlk;
             for (int b0 = 0; b0 < ntest; b0 += kBlk) {
                 if constexpr (kDensity) {
-                    density_block(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0), dacc);
+                    density_block(S, a, lane, b0, min(kBlk, ntest - b0), dacc);
                     if (lane == 0) S.u.tests += (long long)min(kBlk, ntest - b0) * S.u.nq;
                 } else {
-                    const int2 inc = test_block<kDensity, kSym>(S, a, lane, S.u.scr + b0, min(kBlk, ntest - b0),
-                                                                slot0 + b0, b0, dacc);
+                    const int2 inc = test_block<kDensity, kSym>(S, a, lane, min(kBlk, ntest - b0), slot0 + b0, b0, dacc);
                     cnt0 += inc.x;
                     cnt1 += inc.y;
                 }
@@ -1360,12 +1361,11 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
                 slot0 += nst;
                 break;
             }
-            // move the partial block to the front of the scratch
+            // move the partial block to the front of the staging buffer (rest < 32 <= ntest: no overlap)
             const int rest = nst - ntest;
-            float4 *const scr = S.u.scr;
-            for (int i = lane; i < rest; i += 32) __stcg(&scr[i], __ldcg(&scr[ntest + i]));
+            if (lane < rest) S.stg[lane] = S.stg[ntest + lane];
             if constexpr (kSym)
-                for (int i = lane; i < rest; i += 32) __stcg(&S.u.scrk[i], __ldcg(&S.u.scrk[ntest + i]));
+                if (lane < rest) S.y.stk[lane] = S.y.stk[ntest + lane];
             slot0 += ntest;
             nst = rest;
             __syncwarp();
@@ -1870,13 +1870,6 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
             a.cand_cap = (long long)t.arena_cands.n;
             a.masks = t.arena_masks.p;
             a.mask_cap = (long long)t.arena_masks.n;
-            t.scratch.reserve(warps_w * kScratch, 0);
-            a.scratch = t.scratch.p;
-            DBuf<float> scrk;
-            if (kSym) {
-                scrk.alloc(warps_w * kScratch);
-                a.scrk = scrk.p;
-            }
             for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT, C_CSUM, C_NZW}) zero(c);
             {
                 Phase ph("search.count");
@@ -1979,9 +1972,6 @@ void density(TreeDev &t, const double *h, const double *mass, double *rho) {
     long long hc[C_N];
     t.rec_valid = false;  // the density walk records no masks
     run_descent<false>(t, a, g, hc);
-    const long long warps_w = (long long)g.w * (kWalkThreads / 32);
-    t.scratch.reserve(warps_w * kScratch, 0);
-    a.scratch = t.scratch.p;
     for (int c : {C_WORK3, C_CAND, C_MASK, C_STAGED, C_LOADED, C_TESTS, C_EXACT, C_CSUM, C_NZW}) zero_counter(t, c);
     {
         Phase ph("density.walk");
