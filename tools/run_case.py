@@ -34,10 +34,10 @@ counts = torch.empty(n, dtype=torch.int32, device=dev)
 offsets = torch.empty(n + 1, dtype=torch.int64, device=dev)
 nbr = torch.empty(n * args.ngmax, dtype=torch.int32, device=dev)
 P.set_exact_only(args.exact)
+per_rep = []
 for r in range(args.reps):
-    if r == args.reps - 1:
-        P.profile_reset()
-        P.profile_enable(True)
+    P.profile_reset()
+    P.profile_enable(True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     t = P.Tree(pos, 64, 0.5)
@@ -53,7 +53,8 @@ for r in range(args.reps):
     t.free()
     torch.cuda.synchronize()
     t1 = time.perf_counter()
+    per_rep.append({k: round(v[0], 3) for k, v in P.profile().items() if k.startswith("search.") or k == "build.total"})
 prof = P.profile()
-print(json.dumps({"n": n, "wall_ms_last": (t1 - t0) * 1e3, "stats": st,
+print(json.dumps({"n": n, "wall_ms_last": (t1 - t0) * 1e3, "stats": st, "per_rep": per_rep,
                   "phases_ms": {k: round(v[0], 4) for k, v in prof.items() if not k.startswith("kernel.")},
                   "launches": {k: v[1] for k, v in prof.items() if k.startswith("kernel.")}}, indent=1))
