@@ -709,17 +709,9 @@ struct DensitySm<true> {
     float4 qraw[kQ];  // fp32 query coordinates relative to the unit centre
     float4 dc[kBlk];  // ax, ay, az (fp32, relative to the unit centre), m_j
 };
-// symmetric mode: the staged candidates' -k Mid_j (candidate thresholds)
-template <bool kSym>
-struct SymSm {};
-template <>
-struct SymSm<true> {
-    float stk[kStg];
-};
 template <bool kDensity, bool kSym>
 struct WalkSmemT : WalkSmem {
     DensitySm<kDensity> d;
-    SymSm<kSym> y;
 };
 
 // fp32 square root on the SFU (sqrt.approx: relative error ~2^-22, sqrt(0) = 0)
@@ -733,6 +725,14 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // hot loop's fp32 operations and let the fp64 predicate decide every pair
 // with |d'| <= 1 (all pairs when `force`; padding slots >= n are never
 // neighbors).  blk: the block's staged candidates (ax, ay, az, tree position).
+// symmetric criterion: the candidate threshold term -k Mid_j of a staged
+// candidate (tree position tp), +inf when it cannot decide (Tj <= Tqmin, L4s)
+__device__ __forceinline__ float cand_thr(const WalkArgs &a, const UnitSm &u, int tp) {
+    const double tj = __dmul_rn(2.0, a.h_tree[tp]);
+    const double Tj = __dmul_rn(tj, tj);
+    return Tj > u.tqmin ? -u.k * __double2float_rn(Tj) : __int_as_float(0x7f800000);
+}
+
 template <bool kSym>
 __device__ __noinline__ void resolve_band(WalkSmemT<false, kSym> &S, const WalkArgs &a, int lane, int b0, int n,
                                           long long &exact) {
@@ -753,7 +753,7 @@ __device__ __noinline__ void resolve_band(WalkSmemT<false, kSym> &S, const WalkA
             c[h] = real[h] ? blk[s] : make_float4(0.f, 0.f, 0.f, __int_as_float(-1));
             const float nc = __fmaf_rn(c[h].z, c[h].z, __fmaf_rn(c[h].y, c[h].y, __fmul_rn(c[h].x, c[h].x)));
             ac[h] = real[h] ? __fmul_rn(ku, nc) : inf;  // identical to test_block
-            if constexpr (kSym) nk[h] = real[h] ? S.y.stk[b0 + s] : 0.f;
+            if constexpr (kSym) nk[h] = real[h] ? cand_thr(a, S.u, __float_as_int(c[h].w)) : 0.f;
         }
         for (int q = 0; q < nq; q++) {
             const float4 Q0 = S.q0[q], Q1 = S.q1[q];
@@ -918,7 +918,7 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity, kSym> &S, const W
 #pragma unroll
         for (int j = 0; j < 4; j++) {
             const int sl = 32 * j + lane;
-            if constexpr (kSym) nk[j] = (sl < n) ? S.y.stk[b0 + sl] : inf;  // (padding: u = +inf anyway)
+            nk[j] = (sl < n) ? cand_thr(a, S.u, __float_as_int(c[j].w)) : inf;  // (padding: u = +inf anyway)
         }
         const unsigned aqm = (unsigned)__cvta_generic_to_shared(&S.qm[0]);
         unsigned long long NM;
@@ -1130,11 +1130,6 @@ __device__ __forceinline__ void stage_group(WalkSmemT<kD, kSym> &S, const WalkAr
             BT_DEV_CHECK(slot < kStg && pos >= 0 && pos < a.n_rec);
             BT_DEV_CHECK(!rec_ok || S.u.cand_base + slot0 + slot < a.cand_cap);
             S.stg[slot] = make_float4(ax, ay, az, __int_as_float(pos));
-            if constexpr (kSym) {  // -k Mid_j of the candidate threshold; +inf when it cannot decide (Tj <= Tqmin, L4s)
-                const double tj = __dmul_rn(2.0, a.h_tree[pos]);
-                const double Tj = __dmul_rn(tj, tj);
-                S.y.stk[slot] = Tj > S.u.tqmin ? -S.u.k * __double2float_rn(Tj) : __int_as_float(0x7f800000);
-            }
             if (rec_ok) __stcs(&cands[(unsigned)slot], a.tree_order ? pos : __float_as_int(r.w));
             if ((unsigned)(pos - qn.x) < (unsigned)qn.y) S.self[pos - qn.x] = slot0 + slot;
         }
@@ -1375,8 +1370,6 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
             // move the partial block to the front of the staging buffer (rest < 32 <= ntest: no overlap)
             const int rest = nst - ntest;
             if (lane < rest) S.stg[lane] = S.stg[ntest + lane];
-            if constexpr (kSym)
-                if (lane < rest) S.y.stk[lane] = S.y.stk[ntest + lane];
             slot0 += ntest;
             nst = rest;
             __syncwarp();
