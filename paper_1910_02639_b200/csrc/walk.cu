@@ -26,6 +26,7 @@
 //   each neighbor's slot in its CSR row.
 #include <algorithm>
 #include <cfloat>
+#include <type_traits>
 
 #include "common.cuh"
 #include "scan.cuh"
@@ -868,6 +869,12 @@ __device__ __forceinline__ void density_block(WalkSmemT<true, false> &S, const W
     __syncwarp();
 }
 
+// units with at least BT_FUNNEL_Q queries record masks by funnel shifts (65: none)
+#ifndef BT_FUNNEL_Q
+#define BT_FUNNEL_Q 65
+#endif
+constexpr int kFunnelQ = BT_FUNNEL_Q;
+
 // Test n (<= kBlk) staged candidates (blk, unit slots us0 .. us0 + n) against
 // the unit's queries and record the block's masks; returns this lane's count
 // increments for queries (lane, lane + 32).
@@ -973,6 +980,67 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity, kSym> &S, const W
             }
         }
 #undef BT_SYM_LOOP
+    } else if (nq >= kFunnelQ) {
+        // (BT_FUNNEL_Q, off by default) masks by funnel shifts: the sign bit of
+        // each v shifted into a per-candidate word over up to 32 queries, then a
+        // 32 x 32 bit transpose (five shuffle rounds) so that lane q holds query
+        // q's ballot words.  Fewer instructions per query than four compares and
+        // ballots but ~40 per transpose: measured slower at cfg 5 (walk 17.6 ms
+        // with BT_FUNNEL_Q = 16 vs 15.5).  Compiled in, it also changes the
+        // register allocation of the ballot loops below: their 4 ballots land in
+        // the STS.128 quad directly (25 instead of 27.5 SASS per query; walk
+        // 15.85 -> 15.46 ms at cfg 5).
+        auto funnel = [&](auto two_chunks) {
+            constexpr bool kTwo = decltype(two_chunks)::value;
+            unsigned acc[4] = {0u, 0u, 0u, 0u};
+            for (int qb = 0; qb < nqp; qb += 32) {
+                const int qe = min(qb + 32, nqp);
+#pragma unroll 2
+                for (int q = qb; q < qe; q++) {
+                    const float4 Q0 = N0, Q1 = N1;
+                    ldq(q + 1, N0, N1);
+                    const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
+                                             bq = pk(Q1.z, Q1.w);
+                    const unsigned long long da = f2_fma(xa, qx, f2_fma(ya, qy, f2_fma(za, qz, f2_add(aa, bq))));
+                    acc[0] = __funnelshift_l(__float_as_uint(lo_f(da)), acc[0], 1);
+                    acc[1] = __funnelshift_l(__float_as_uint(hi_f(da)), acc[1], 1);
+                    if constexpr (kTwo) {
+                        const unsigned long long db =
+                            f2_fma(xb, qx, f2_fma(yb, qy, f2_fma(zb, qz, f2_add(ab, bq))));
+                        bmin = fminf(fminf(bmin, fminf(fabsf(lo_f(da)), fabsf(hi_f(da)))),
+                                     fminf(fabsf(lo_f(db)), fabsf(hi_f(db))));
+                        acc[2] = __funnelshift_l(__float_as_uint(lo_f(db)), acc[2], 1);
+                        acc[3] = __funnelshift_l(__float_as_uint(hi_f(db)), acc[3], 1);
+                    } else {
+                        bmin = fminf(bmin, fminf(fabsf(lo_f(da)), fabsf(hi_f(da))));
+                    }
+                }
+                const int sh = 32 - (qe - qb);
+                unsigned w[4];
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    unsigned x = __brev(acc[j]) >> sh;
+                    const unsigned masks[5] = {0x0000ffffu, 0x00ff00ffu, 0x0f0f0f0fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+                    for (int r = 0; r < 5; r++) {
+                        const int s2 = 16 >> r;
+                        const unsigned m = masks[r];
+                        const unsigned y = __shfl_xor_sync(0xffffffffu, x, s2);
+                        x = (lane & s2) ? ((x & ~m) | ((y >> s2) & m)) : ((x & m) | ((y << s2) & ~m));
+                    }
+                    w[j] = x;
+                }
+                if (lane < qe - qb) {
+                    if (kTwo)
+                        *reinterpret_cast<ulonglong2 *>(S.mask[qb + lane]) = make_ulonglong2(
+                            ((unsigned long long)w[1] << 32) | w[0], ((unsigned long long)w[3] << 32) | w[2]);
+                    else
+                        S.mask[qb + lane][0] = ((unsigned long long)w[1] << 32) | w[0];
+                }
+            }
+        };
+        if (nch == 2) funnel(std::true_type{});
+        else funnel(std::false_type{});
     } else if (nch == 2) {
 #pragma unroll 2
         for (int q = 0; q < nqp; q++) {
