@@ -708,7 +708,6 @@ template <>
 struct DensitySm<true> {
     float hinv[kQ];
     float4 qraw[kQ];  // fp32 query coordinates relative to the unit centre
-    float4 dc[kBlk];  // ax, ay, az (fp32, relative to the unit centre), m_j
 };
 template <bool kDensity, bool kSym>
 struct WalkSmemT : WalkSmem {
@@ -820,18 +819,30 @@ __device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsig
 __device__ __forceinline__ void density_block(WalkSmemT<true, false> &S, const WalkArgs &a, int lane, int b0, int n,
                                               double (&dacc)[2]) {
     const float4 *blk = S.stg + b0;
-    float4 *P = S.d.dc;       // pair p: (x_2p, x_2p+1, y_2p, y_2p+1)
-    float4 *Qz = S.d.dc + kBlk / 2;  // pair p: (z_2p, z_2p+1, m_2p, m_2p+1)
+    // the block's candidates with their masses, repacked in place over
+    // stg[0, kBlk) (read into registers first; a second block, b0 = kBlk,
+    // lies beyond the packed range)
+    float4 *P = S.stg;                // pair p: (x_2p, x_2p+1, y_2p, y_2p+1)
+    float4 *Qz = S.stg + kBlk / 2;    // pair p: (z_2p, z_2p+1, m_2p, m_2p+1)
     float *Pf = reinterpret_cast<float *>(P), *Qf = reinterpret_cast<float *>(Qz);
+    float4 cc[4];
+    float mm[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) {
         const int sl = 32 * j + lane;
-        float4 c = make_float4(0.f, 0.f, 0.f, 0.f);
-        float m = 0.f;  // padding: m = 0 (no contribution)
+        cc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        mm[j] = 0.f;  // padding: m = 0 (no contribution)
         if (sl < n) {
-            c = blk[sl];
-            m = (float)a.m_tree[__float_as_int(c.w)];
+            cc[j] = blk[sl];
+            mm[j] = (float)a.m_tree[__float_as_int(cc[j].w)];
         }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+        const int sl = 32 * j + lane;
+        const float4 c = cc[j];
+        const float m = mm[j];
         const int p = sl >> 1, o = sl & 1;
         Pf[4 * p + o] = c.x;
         Pf[4 * p + 2 + o] = c.y;
