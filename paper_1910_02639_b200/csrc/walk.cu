@@ -801,6 +801,64 @@ __device__ __noinline__ void resolve_band(WalkSmemT<false, kSym> &S, const WalkA
     __syncwarp();
 }
 
+// The band by candidate (round 2, third pass): the lanes in fl own every
+// candidate with a banded pair (a lane's bmin covers its four candidates and
+// all queries), so only their candidates are redone -- each broadcast to the
+// lanes, lanes = queries, with the hot loop's fp32 operations -- and the
+// pairs with |v| <= 1 (symmetric: |w| <= 1) decided by the fp64 predicate.
+// Not for `force` (every pair exact): resolve_band.
+constexpr int kBandLanes = 4;
+template <bool kSym>
+__device__ __noinline__ void resolve_band_lanes(WalkSmemT<false, kSym> &S, const WalkArgs &a, int lane, int b0, int n,
+                                                unsigned fl, long long &exact) {
+    const float ku = S.u.k;
+    const int q0 = S.u.q0, nq = S.u.nq;
+    int nex = 0;  // this lane's exact pairs (summed over the warp at the end)
+    while (fl) {
+        const int l = __ffs(fl) - 1;
+        fl &= fl - 1;
+#pragma unroll 1
+        for (int j = 0; j < 4; j++) {
+            const int s = 32 * j + l;  // block slot of the lane's j-th candidate
+            if (s >= n) break;
+            const float4 c = S.stg[b0 + s];
+            const float nc = __fmaf_rn(c.z, c.z, __fmaf_rn(c.y, c.y, __fmul_rn(c.x, c.x)));
+            const float ac = __fmul_rn(ku, nc);  // identical to test_block
+            const int tp = __float_as_int(c.w);
+            float nkc = 0.f;
+            if constexpr (kSym) nkc = cand_thr(a, S.u, tp);
+            const unsigned long long bit = 1ull << (s & 63);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int q = lane + 32 * h;
+                if (q >= nq) continue;
+                const float4 Q0 = S.q0[q], Q1 = S.q1[q];
+                // the hot loop's v, operation for operation
+                const float v = __fmaf_rn(c.x, Q0.x, __fmaf_rn(c.y, Q0.z, __fmaf_rn(c.z, Q1.x, __fadd_rn(ac, Q1.z))));
+                const float w = kSym ? __fadd_rn(v, fminf(S.qm[q].x, nkc)) : v;
+                if (!(fabsf(w) <= 1.0f)) continue;
+                const int qp = q0 + q;
+                bool e = false;
+                if (tp != qp) {
+                    const double t = __dmul_rn(2.0, a.h_tree[qp]);
+                    double T = __dmul_rn(t, t);
+                    if (kSym) {  // the pair's threshold: fl((2 max(h_i, h_j))^2) = max(T_i, T_j)
+                        const double tj = __dmul_rn(2.0, a.h_tree[tp]);
+                        T = fmax(T, __dmul_rn(tj, tj));
+                    }
+                    const double4 Qr = a.rec[qp];
+                    e = exact_pair(Qr.x, Qr.y, Qr.z, T, a.rec[tp]);
+                }
+                unsigned long long &mw = S.mask[q][s >> 6];
+                mw = e ? (mw | bit) : (mw & ~bit);
+                nex++;
+            }
+        }
+    }
+    exact += __reduce_add_sync(0xffffffffu, (unsigned)nex);
+    __syncwarp();
+}
+
 // Density mode (reading R21), round 2: the SPH sum needs
 // no neighbor masks.  The M4 shape vanishes at the support's edge (w(2) = 0,
 // w(2 - d) = d^3 / 4), so a pair decided differently by fp32 near r = 2h
@@ -1089,8 +1147,15 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity, kSym> &S, const W
     const bool band = S.u.force != 0 || bmin <= 1.0f;
     __syncwarp();
     long long exact = 0;
-    if constexpr (!kDensity)
-        if (__any_sync(0xffffffffu, band)) resolve_band<kSym>(S, a, lane, b0, n, exact);
+    if constexpr (!kDensity) {
+        // few banded candidate lanes (the common case): those lanes' candidates
+        // against the queries; else (or force) every query against the block
+        const unsigned fl = __ballot_sync(0xffffffffu, band);
+        if (fl) {
+            if (S.u.force == 0 && __popc(fl) <= kBandLanes) resolve_band_lanes<kSym>(S, a, lane, b0, n, fl, exact);
+            else resolve_band<kSym>(S, a, lane, b0, n, exact);
+        }
+    }
     // self is never its own neighbor (R12); counts; the final masks recorded
     // for the fill pass (chunk kk = us0 / 64 + k of the unit) straight from
     // the lanes that own the queries
