@@ -807,7 +807,10 @@ __device__ __noinline__ void resolve_band(WalkSmemT<false, kSym> &S, const WalkA
 // lanes, lanes = queries, with the hot loop's fp32 operations -- and the
 // pairs with |v| <= 1 (symmetric: |w| <= 1) decided by the fp64 predicate.
 // Not for `force` (every pair exact): resolve_band.
-constexpr int kBandLanes = 4;
+#ifndef BT_BAND_LANES
+#define BT_BAND_LANES 4
+#endif
+constexpr int kBandLanes = BT_BAND_LANES;
 template <bool kSym>
 __device__ __noinline__ void resolve_band_lanes(WalkSmemT<false, kSym> &S, const WalkArgs &a, int lane, int b0, int n,
                                                 unsigned fl, long long &exact) {
@@ -938,6 +941,11 @@ __device__ __forceinline__ void density_block(WalkSmemT<true, false> &S, const W
     __syncwarp();
 }
 
+// query loop unroll of the gather pair tests (queries padded to a multiple)
+#ifndef BT_TEST_UNROLL
+#define BT_TEST_UNROLL 2
+#endif
+constexpr int kTestUnroll = BT_TEST_UNROLL;
 // units with at least BT_FUNNEL_Q queries record masks by funnel shifts (65: none)
 #ifndef BT_FUNNEL_Q
 #define BT_FUNNEL_Q 65
@@ -971,6 +979,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity, kSym> &S, const W
     const unsigned long long xb = pk(c[2].x, c[3].x), yb = pk(c[2].y, c[3].y), zb = pk(c[2].z, c[3].z),
                              ab = pk(ac[2], ac[3]);
     const int nqp = (nq + 1) & ~1;  // padded to even (the pad query never matches)
+    // the gather loops: padded to a multiple of their unroll (pad queries never match)
+    const int nqu = (nq + kTestUnroll - 1) / kTestUnroll * kTestUnroll;
     // shared addresses of the query records (two LDS.128 per query)
     const unsigned aq0 = (unsigned)__cvta_generic_to_shared(&S.q0[0]);
     const unsigned aq1 = (unsigned)__cvta_generic_to_shared(&S.q1[0]);
@@ -1111,10 +1121,10 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity, kSym> &S, const W
         if (nch == 2) funnel(std::true_type{});
         else funnel(std::false_type{});
     } else if (nch == 2) {
-#pragma unroll 2
-        for (int q = 0; q < nqp; q++) {
+#pragma unroll kTestUnroll
+        for (int q = 0; q < nqu; q++) {
             const float4 Q0 = N0, Q1 = N1;
-            ldq(q + 1, N0, N1);  // q + 1 <= nqp <= 64: within the padded arrays
+            ldq(q + 1, N0, N1);  // q + 1 <= nqu <= 64: within the padded arrays
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
                                      bq = pk(Q1.z, Q1.w);
             // v = k (|c - q|^2 - Mid) expanded: one add + three FMA per packed pair (lemma L4)
@@ -1131,8 +1141,8 @@ __device__ __forceinline__ int2 test_block(WalkSmemT<kDensity, kSym> &S, const W
             }
         }
     } else {
-#pragma unroll 2
-        for (int q = 0; q < nqp; q++) {
+#pragma unroll kTestUnroll
+        for (int q = 0; q < nqu; q++) {
             const float4 Q0 = N0, Q1 = N1;
             ldq(q + 1, N0, N1);
             const unsigned long long qx = pk(Q0.x, Q0.y), qy = pk(Q0.z, Q0.w), qz = pk(Q1.x, Q1.y),
