@@ -138,6 +138,13 @@ struct UnitRun {             // per walk unit, written by the walk kernels
     double rmax;            // symmetric criterion: largest cull radius max(R'_u, R'(h_max of a kept leaf))
 };
 
+struct UnitPrep {            // gather walk: a unit's geometry, prepared by the descent (A10)
+    double c[3], E;         // unit centre, coordinate bound (L4)
+    float4 box0, box1;      // fp32 query box relative to c: (lo xyz, cull2), (hi xyz, -)
+    float k;                // band scale (power of two; 0: force)
+    int pad;
+};
+
 struct TreeDev {
     int64_t n = 0;
     int32_t s = 64;
@@ -176,6 +183,8 @@ struct TreeDev {
     DBuf<double> leaf_hmax, node_hmax;  // symmetric criterion: max h per leaf / per node subtree
     DBuf<double> m_tree;       // masses in tree order (density consumer)
     DBuf<UnitRun> urun;                    // per-unit walk record
+    DBuf<UnitPrep> uprep;                  // gather walk: per-unit geometry from the descent
+    DBuf<float4> qrec;                     // gather walk: per-query record (-2k q, fl32(k(|q|^2 - Mid))) by tree position
     DBuf<int32_t> ulist;                   // candidate leaf lists of all units
     DBuf<unsigned long long> arena_masks;  // neighbor masks per (64-candidate chunk, query)
     DBuf<int32_t> arena_cands;             // candidate caller indices per slot

@@ -100,6 +100,8 @@ struct WalkArgs {
     int32_t *front;           // big-unit pass: per-warp frontier scratch, 2 x front_cap node ids
     int64_t front_cap;
     UnitRun *urun;
+    UnitPrep *uprep;          // gather count pass: the descent prepares each unit's walk geometry and
+    float4 *qrec;             //   query records (tree positions), the walk loads them
     int32_t *ulist;
     long long list_cap;
     int32_t *counts;
@@ -575,6 +577,72 @@ __device__ __forceinline__ DescOut descend(const WalkArgs &a, const double (&qlo
     return r;
 }
 
+// The gather walk's unit geometry and query records (round 2, third pass:
+// computed by the descent, which holds the unit's query box and R'_u already,
+// instead of by the issue-bound walk): the same operations as unit_setup and
+// the walk's setup -- c = (lo + hi) / 2, E, the band scale k = min over the
+// queries of l4_band's (0 = force), per query (-2k a, fl32(k (|a|^2 - Mid)))
+// with a = fl32(x - c), the fp32 query box and cull radius -- so the walk's
+// decisions are bit-identical either way.
+__device__ __forceinline__ void prep_gather_unit(const WalkArgs &a, const int4 &UU, long long uid, int lane,
+                                                 const double (&lo)[3], const double (&hi)[3], double Ru) {
+    const int q0 = UU.y, nq = UU.z;
+    double c[3], E = 0.0, Mu = 0.0;
+    for (int l = 0; l < 3; l++) {
+        c[l] = 0.5 * (lo[l] + hi[l]);
+        E = fmax(E, 0.5 * (hi[l] - lo[l]));
+        Mu = fmax(Mu, fmax(fabs(lo[l]), fabs(hi[l])));
+    }
+    E = (E + Ru) * 1.0001 + 4.0 * 0x1p-53 * Mu;  // (Rx = R'_u: the gather walk)
+    const double eps = l4_eps(E);
+    float kq[2] = {INFINITY, INFINITY}, mid[2] = {0.0f, 0.0f};
+    float ax[2] = {0.f, 0.f}, ay[2] = {0.f, 0.f}, az[2] = {0.f, 0.f};
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int k = lane + 32 * h;
+        if (k < nq) {
+            const double4 r = a.rec[q0 + k];  // (reloaded: values kept from unit_box cost the descent registers)
+            const double t = __dmul_rn(2.0, a.h_tree[q0 + k]);  // 2h (exact)
+            l4_band(__dmul_rn(t, t), t, E, eps, a.exact_only != 0, kq[h], mid[h]);
+            ax[h] = __double2float_rn(__dsub_rn(r.x, c[0]));
+            ay[h] = __double2float_rn(__dsub_rn(r.y, c[1]));
+            az[h] = __double2float_rn(__dsub_rn(r.z, c[2]));
+        }
+    }
+    float ku = fminf(kq[0], kq[1]);
+    for (int d = 16; d; d >>= 1) ku = fminf(ku, __shfl_xor_sync(0xffffffffu, ku, d));
+    const bool force = ku == 0.0f;
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        const int k = lane + 32 * h;
+        if (k < nq) {
+            const float m2k = -2.0f * ku;
+            const double qq = (double)ax[h] * ax[h] + (double)ay[h] * ay[h] + (double)az[h] * az[h];
+            const float bq = force ? 0.0f : __double2float_rn((double)ku * (qq - (double)mid[h]));
+            a.qrec[q0 + k] = make_float4(m2k * ax[h], m2k * ay[h], m2k * az[h], bq);
+        }
+    }
+    if (lane == 0) {
+        float blo[3], bhi[3];
+        for (int l = 0; l < 3; l++) {
+            blo[l] = __double2float_rn(__dsub_rn(lo[l], c[l]));
+            bhi[l] = __double2float_rn(__dsub_rn(hi[l], c[l]));
+        }
+        const double rc = (Ru + 4.0 * eps) * (1.0 + 0x1p-20);
+        const double rc2 = rc * rc * (1.0 + 0x1p-40);
+        UnitPrep P;
+        P.c[0] = c[0];
+        P.c[1] = c[1];
+        P.c[2] = c[2];
+        P.E = E;
+        P.box0 = make_float4(blo[0], blo[1], blo[2], (rc2 < 3.0e38) ? __double2float_ru(rc2) : INFINITY);
+        P.box1 = make_float4(bhi[0], bhi[1], bhi[2], 0.0f);
+        P.k = ku;
+        P.pad = 0;
+        a.uprep[uid] = P;
+    }
+}
+
 // exact arena bounds of the walk (a unit stages at most `loaded` candidates),
 // summed per warp (lane 0) and added once per warp at the end of the pass
 // (two same-address atomics per unit cost the cfg 2 descent 0.18 -> 0.13 ms)
@@ -626,6 +694,7 @@ __global__ void __launch_bounds__(kDescThreads) desc_kernel(WalkArgs a) {
         const int4 U = a.units[uid];
         double qlo[3], qhi[3], Ru;
         unit_box(a, U, lane, qlo, qhi, Ru, hsum, hbad);
+        if (!kBig && !kSym && a.uprep) prep_gather_unit(a, U, uid, lane, qlo, qhi, Ru);
         UnitRun &R = a.urun[uid];
         if (!kBig) {
             const bool ok = slab_reserve(ls, kListReserve, kListSlab, a.list_cap, &a.ctr[C_LIST], lane);
@@ -1320,7 +1389,51 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
         const UnitRun R = a.urun[uid];
         int32_t qo[2];
         int nq, q0;
-        {
+        if (!kSym && !kDensity && a.uprep) {
+            // the gather count pass: geometry and query records prepared by the descent
+            const int4 UU = a.units[uid];
+            q0 = UU.y;
+            nq = UU.z;
+            const UnitPrep P = a.uprep[uid];
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int k = lane + 32 * h;
+                qo[h] = 0;
+                if (k < nq) {
+                    const float4 r = a.qrec[q0 + k];
+                    qo[h] = a.tree_order ? q0 + k : a.perm[q0 + k];
+                    S.q0[k] = make_float4(r.x, r.x, r.y, r.y);
+                    S.q1[k] = make_float4(r.z, r.z, r.w, r.w);
+                } else {  // padding query: v = Ac + 2 >= 2 (never a neighbor, never banded)
+                    S.q0[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    S.q1[k] = make_float4(0.f, 0.f, 2.f, 2.f);
+                }
+                S.self[k] = -1;
+            }
+            Slab cs = S.u.cs, ms = S.u.ms;
+            const long long need_c = R.loaded, need_m = (long long)((R.loaded + 63) >> 6) * nq;
+            const bool okc = slab_reserve(cs, need_c, kCandSlab, a.cand_cap, &a.ctr[C_CAND], lane);
+            const bool okm = slab_reserve(ms, need_m, kMaskSlab, a.mask_cap, &a.ctr[C_MASK], lane);
+            __syncwarp();
+            if (lane == 0) {
+                S.u.cs = cs;
+                S.u.ms = ms;
+                S.u.cand_base = cs.cur;
+                S.u.cand_ptr = a.cands + cs.cur;
+                S.u.mask_base = ms.cur;
+                S.u.c[0] = P.c[0];
+                S.u.c[1] = P.c[1];
+                S.u.c[2] = P.c[2];
+                S.u.E = P.E;
+                S.u.q0 = q0;
+                S.u.nq = nq;
+                S.u.rec_ok = okc && okm;
+                S.u.force = P.k == 0.0f;
+                S.u.k = P.k;
+                S.u.box0 = P.box0;
+                S.u.box1 = P.box1;
+            }
+        } else {
             UnitGeom G;
             unit_setup(a, a.units[uid], lane, G, kSym ? R.rmax : 0.0);
             nq = G.nq;
@@ -2014,6 +2127,13 @@ void search(TreeDev &t, const double *h, int32_t *counts, int64_t *offsets, int3
         if (fuse) {
             a.h_src = h;
             a.h_out = t.h_tree.p;
+        }
+        if (!kSym) {  // the descent prepares the gather walk's unit geometry and query records
+            const int64_t u0 = t.n_units * t.part / t.nparts;
+            t.uprep.reserve(t.n_units, 0);
+            t.qrec.reserve(n, 0);
+            a.uprep = t.uprep.p + u0;
+            a.qrec = t.qrec.p;
         }
         run_descent<kSym>(t, a, g, hc);
         if (fuse) {
