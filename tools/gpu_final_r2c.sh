@@ -1,8 +1,8 @@
 # round-2 closing evidence (third pass, final: shared-memory staging, per-warp arena bounds,
-# symmetric thresholds in the test block, exact band by candidate): parity suite, per-config
-# bench lines, launch lists, ncu --set full of the search kernels (cfg 5 and 2), density / symmetric / tree-order cases
-mkdir -p gpurun_out/final5
-O=gpurun_out/final5
+# symmetric thresholds in the test block, exact band by candidate, unit preparation in the
+# descent): parity suite, per-config bench lines, launch lists, ncu --set full of the search kernels (cfg 5 and 2), density / symmetric / tree-order cases
+mkdir -p gpurun_out/final7
+O=gpurun_out/final7
 timeout 1500 python -m pytest tests -m gpu -x -q > $O/gpu_tests.log 2>&1; echo "tests rc=$?" >> $O/gpu_tests.log
 for c in 5 1 2 3 4; do
   timeout 900 python bench.py --config $c --steps 10 --warmup 3 > $O/bench_cfg$c.json 2> $O/bench_cfg$c.err
