@@ -1707,6 +1707,21 @@ struct FillSmem {
     unsigned long long mask[kFillChunks * kQ];   // the round's masks, [k][q]
 };
 
+// CSR row store of the fill (BT_FILL_ST: 0 streaming st.global.cs, 1 plain
+// st.global, 2 st.global with an L2 evict_last policy -- A/B knob)
+#ifndef BT_FILL_ST
+#define BT_FILL_ST 2
+#endif
+__device__ __forceinline__ void row_store(int32_t *p, int32_t v, unsigned long long pol) {
+#if BT_FILL_ST == 0
+    __stcs(p, v);
+#elif BT_FILL_ST == 1
+    *p = v;
+#else
+    asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+#endif
+}
+
 __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     __shared__ FillSmem fsm[kFillWarps];
     const int lane = threadIdx.x & 31;
@@ -1715,6 +1730,10 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
     WorkBatch wb;
     const int32_t *__restrict__ cands = a.cands;
     const unsigned long long *__restrict__ masks = a.masks;
+    unsigned long long pol = 0;
+#if BT_FILL_ST == 2
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
     for (;;) {
         const long long u = next_unit(wb, &a.ctr[C_WORK2], a.n_units, 1, lane);
         if (u >= a.n_units) break;
@@ -1749,8 +1768,8 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
                     if (!(lo | hi)) continue;
                     const int plo = __popc(lo);
                     BT_DEV_CHECK(dst - a.nbr + o + plo + __popc(hi) <= a.nbr_cap);
-                    if (lo & lanebit) __stcs(&dst[o + __popc(lo & lt)], c0[k]);
-                    if (hi & lanebit) __stcs(&dst[o + plo + __popc(hi & lt)], c1[k]);
+                    if (lo & lanebit) row_store(&dst[o + __popc(lo & lt)], c0[k], pol);
+                    if (hi & lanebit) row_store(&dst[o + plo + __popc(hi & lt)], c1[k], pol);
                     o += plo + __popc(hi);
                 }
                 if (lane == 0 && o) F.row[q] = dst + o;
