@@ -32,6 +32,12 @@ namespace bt {
 namespace {
 
 constexpr int kThreads = 256;
+// BT_RANK_HIST: the histogram's atomic returns each particle's rank in its
+// cell and the scatter adds it to the cell's start (one atomic per particle
+// and round instead of one in the histogram and one in the scatter) -- A/B knob
+#ifndef BT_RANK_HIST
+#define BT_RANK_HIST 0
+#endif
 #ifndef BT_SCATTER_UNROLL
 #define BT_SCATTER_UNROLL 4  // particles per thread in flight in key_hist / scatter
 #endif
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__res
                                                             const double *__restrict__ pos, int64_t n_act,
                                                             const LevelNode *__restrict__ ln,
                                                             const NodeRec *__restrict__ nodes, uint32_t *__restrict__ keys,
-                                                            int32_t *__restrict__ hist, int round) {
+                                                            int32_t *__restrict__ hist, int32_t *__restrict__ rank, int round) {
     // (BT_SCATTER_UNROLL particles per thread: independent load chains in flight)
     constexpr int U = BT_SCATTER_UNROLL;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -227,7 +233,11 @@ __global__ void __launch_bounds__(kThreads) key_hist_kernel(const double4 *__res
             const int c3 = cell_coord_fast(r[u].z, nr.lo[2], nr.ext[2], L.bx[2], bz_of(b, L.kz));
             const uint32_t j = (uint32_t)c1 + (uint32_t)c2 * (uint32_t)b + (uint32_t)c3 * (uint32_t)b * (uint32_t)b;
             keys[p0 + u * stride] = (uint32_t)(L.cell_base + j);  // the level's cell index (< 2^32)
+#if BT_RANK_HIST
+            rank[p0 + u * stride] = atomicAdd(&hist[L.cell_base + j], 1);  // the particle's slot in its cell
+#else
             atomicAdd(&hist[L.cell_base + j], 1);
+#endif
         }
     }
 }
@@ -399,6 +409,7 @@ template <bool kRoot>
 __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__restrict__ act, const double *__restrict__ pos,
                                                            int64_t n_act,
                                                            const uint32_t *__restrict__ keys, int32_t *cursor,
+                                                           const int32_t *__restrict__ rank,
                                                            double4 *__restrict__ out_final, double4 *__restrict__ act_next) {
     // cursor[g] (written by emit): the cell's next destination, bit 31 set
     // for a child-node cell (next level's active array) -- one returning
@@ -412,7 +423,11 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const double4 *__rest
         for (int u = 0; u < U; u++) {
             const int64_t p = p0 + u * stride;
             if (p < n_act) {
+#if BT_RANK_HIST
+                d[u] = (int32_t)((unsigned)__ldg(&cursor[keys[p]]) + (unsigned)rank[p]);  // cell start + histogram rank
+#else
                 d[u] = atomicAdd(&cursor[keys[p]], 1);
+#endif
                 v[u] = kRoot ? make_double4(pos[3 * p], pos[3 * p + 1], pos[3 * p + 2], __longlong_as_double((long long)p))
                              : act[p];
             }
@@ -909,6 +924,7 @@ void build_tree(TreeDev &t, const double *pos) {
         act[1].alloc(n);
         act_node[1].alloc(n);
         DBuf<uint32_t> keys(n);
+        DBuf<int32_t> ranks(BT_RANK_HIST ? n : 1);
         DBuf<LevelNode> ln(1), ln_next;
         {
             LevelNode r{};
@@ -969,10 +985,10 @@ void build_tree(TreeDev &t, const double *pos) {
                 }
                 if (level == 0)
                     key_hist_kernel<true><<<gridA, kThreads, 0, st>>>(nullptr, nullptr, pos, n_act, ln.p, t.nodes.p,
-                                                                      keys.p, hist.p, round);
+                                                                      keys.p, hist.p, ranks.p, round);
                 else
                     key_hist_kernel<false><<<gridA, kThreads, 0, st>>>(act[cur].p, act_node[cur].p, nullptr, n_act, ln.p,
-                                                                       t.nodes.p, keys.p, hist.p, round);
+                                                                       t.nodes.p, keys.p, hist.p, ranks.p, round);
                 BT_LAUNCH("key_hist");
                 if (t.octree) break;  // no ratio test for the octree policy
                 under_count_kernel<<<gridC, kThreads, 0, st>>>(ln.p, nn, hist.p, ncells, t.alpha * (double)t.s);
@@ -1020,9 +1036,10 @@ void build_tree(TreeDev &t, const double *pos) {
             // destination window stays L2-resident -- measured slower in round 2:
             // cfg 5 levels 3.9 -> 5.1 ms.)
             if (level == 0)
-                scatter_kernel<true><<<gridA, kThreads, 0, st>>>(nullptr, pos, n_act, keys.p, hist.p, fin.p, act[cur ^ 1].p);
+                scatter_kernel<true><<<gridA, kThreads, 0, st>>>(nullptr, pos, n_act, keys.p, hist.p, ranks.p, fin.p,
+                                                                 act[cur ^ 1].p);
             else
-                scatter_kernel<false><<<gridA, kThreads, 0, st>>>(act[cur].p, nullptr, n_act, keys.p, hist.p, fin.p,
+                scatter_kernel<false><<<gridA, kThreads, 0, st>>>(act[cur].p, nullptr, n_act, keys.p, hist.p, ranks.p, fin.p,
                                                                   act[cur ^ 1].p);
             BT_LAUNCH("scatter");
             if (nn_next > 0) {
