@@ -73,8 +73,20 @@ def full(rep, out, traffic=None, key=None, config=None):
     rr = list(csv.reader(raw.splitlines()))
     h2 = rr[0]
     dram = {}
+    pipes = {}
     for r in rr[2:]:
         d = dict(zip(h2, r))
+        # execution pipes at >= 10 % of their sustained peak (XU = POPC / conversions, quarter rate)
+        pp = []
+        for name, val in d.items():
+            if name.startswith("sm__inst_executed_pipe_") and name.endswith(".avg.pct_of_peak_sustained_active"):
+                try:
+                    v = float(val.replace(",", ""))
+                except ValueError:
+                    continue
+                if v >= 10.0:
+                    pp.append((v, name[len("sm__inst_executed_pipe_"):-len(".avg.pct_of_peak_sustained_active")]))
+        pipes[(d.get("ID"), d.get("Kernel Name", "")[:60])] = ", ".join(f"{n} {v:.1f} %" for v, n in sorted(pp, reverse=True))
         try:
             rd = float(d.get("dram__bytes_read.sum", "0").replace(",", ""))
             wr = float(d.get("dram__bytes_write.sum", "0").replace(",", ""))
@@ -89,6 +101,8 @@ def full(rep, out, traffic=None, key=None, config=None):
         lines += ["    " + x for x in v]
         if k in dram:
             lines.append(f"    dram bytes (read + write): {dram[k]:.4g}")
+        if pipes.get(k):
+            lines.append(f"    pipes (inst executed, % of sustained peak while active): {pipes[k]}")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
     if traffic and dram:
