@@ -43,7 +43,10 @@ constexpr int kGroupPos = 2048;  // positions a multi-leaf group may span (its l
 constexpr int kFrontCap = 512;   // shared-memory descent frontier per level
 constexpr int kDescThreads = 128;
 constexpr int kWalkThreads = 128;
-constexpr int kFillThreads = 256;
+#ifndef BT_FILL_THREADS
+#define BT_FILL_THREADS 256
+#endif
+constexpr int kFillThreads = BT_FILL_THREADS;
 constexpr int kFillChunks = 6;   // 64-candidate chunks per fill round (measured: 4 -> 6 is 4 % faster at cfg 5, 7 slower)
 constexpr long long kListSlab = 8192;     // leaf-list entries per warp allocation
 constexpr long long kListReserve = 2048;  // more candidate leaves -> big-unit pass
@@ -1702,9 +1705,20 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
 constexpr int kFillWarps = kFillThreads / 32;
 constexpr int kCsrThreads = kFillThreads;
 
+// BT_FILL_PRE: each round's row offsets are scanned once per query (lanes =
+// queries: entries before word k in the round, and the low half's popcount,
+// 15 bits) so the replay loop carries no running offset and issues two POPC
+// per mask word (the lane ranks) instead of four -- A/B knob
+#ifndef BT_FILL_PRE
+#define BT_FILL_PRE 1
+#endif
+
 struct FillSmem {
     int32_t *row[kQ];                            // next write address of each query's row
     unsigned long long mask[kFillChunks * kQ];   // the round's masks, [k][q]
+#if BT_FILL_PRE
+    unsigned short pre[kFillChunks * kQ];        // (entries of the round before word k) << 6 | popc(low half), [k][q]
+#endif
 };
 
 // CSR row store of the fill (BT_FILL_ST: 0 streaming st.global.cs, 1 plain
@@ -1722,7 +1736,10 @@ __device__ __forceinline__ void row_store(int32_t *p, int32_t v, unsigned long l
 #endif
 }
 
-__global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
+#ifndef BT_FILL_MIN_BLOCKS
+#define BT_FILL_MIN_BLOCKS 5   // 48 registers: 40 warps per SM (forced to 40 registers the replay is 18 % slower)
+#endif
+__global__ void __launch_bounds__(kFillThreads, BT_FILL_MIN_BLOCKS) fill_kernel(WalkArgs a) {
     __shared__ FillSmem fsm[kFillWarps];
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt(), lanebit = 1u << lane;
@@ -1757,6 +1774,46 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
             BT_DEV_CHECK(R.mask_base + (long long)(kk0 + nk) * nq <= a.mask_cap && R.cand_base + R.nstaged <= a.cand_cap);
             for (int w = lane; w < nk * nq; w += 32) F.mask[w] = __ldcs(&src[w]);
             __syncwarp();
+#if BT_FILL_PRE
+            int tot[kQ / 32];
+#pragma unroll
+            for (int t = 0; t < kQ / 32; t++) {
+                const int q = lane + 32 * t;
+                int o = 0;
+                if (q < nq) {
+#pragma unroll
+                    for (int k = 0; k < kFillChunks; k++) {
+                        if (k >= nk) break;
+                        const unsigned long long m = F.mask[k * nq + q];
+                        const int plo = __popc((unsigned)m);
+                        F.pre[k * nq + q] = (unsigned short)((o << 6) | plo);
+                        o += plo + __popc((unsigned)(m >> 32));
+                    }
+                }
+                tot[t] = o;
+            }
+            __syncwarp();
+            for (int q = 0; q < nq; q++) {
+                int32_t *const dst = F.row[q];
+#pragma unroll
+                for (int k = 0; k < kFillChunks; k++) {
+                    if (k >= nk) break;
+                    const unsigned long long m = F.mask[k * nq + q];
+                    const unsigned lo = (unsigned)m, hi = (unsigned)(m >> 32);
+                    if (!(lo | hi)) continue;
+                    const unsigned pk = F.pre[k * nq + q];
+                    const int o = (int)(pk >> 6), plo = (int)(pk & 63u);
+                    BT_DEV_CHECK(dst - a.nbr + o + plo + __popc(hi) <= a.nbr_cap);
+                    if (lo & lanebit) row_store(&dst[o + __popc(lo & lt)], c0[k], pol);
+                    if (hi & lanebit) row_store(&dst[o + plo + __popc(hi & lt)], c1[k], pol);
+                }
+            }
+            __syncwarp();
+#pragma unroll
+            for (int t = 0; t < kQ / 32; t++)
+                if (lane + 32 * t < nq) F.row[lane + 32 * t] += tot[t];
+            __syncwarp();
+#else
             for (int q = 0; q < nq; q++) {
                 int32_t *const dst = F.row[q];
                 int o = 0;  // entries of this round written to the row
@@ -1775,6 +1832,7 @@ __global__ void __launch_bounds__(kFillThreads) fill_kernel(WalkArgs a) {
                 if (lane == 0 && o) F.row[q] = dst + o;
             }
             __syncwarp();
+#endif
         }
     }
 }
