@@ -3,6 +3,7 @@ CSV) and, for a --set full report, the headline metrics + DRAM bytes per launch.
 
   python tools/ncu_summary.py launches <launches.csv> <out.txt>
   python tools/ncu_summary.py full <report.ncu-rep> <out.txt> [<traffic.json> <kernel-key> <config>]
+  python tools/ncu_summary.py headline <out.txt> <traffic.json>
 """
 import csv
 import json
@@ -123,8 +124,51 @@ def full(rep, out, traffic=None, key=None, config=None):
         json.dump(t, open(traffic, "w"), indent=1)
 
 
+def headline(summary, traffic):
+    """The "ncu" block of dram_traffic.json (bench.py's roofline.ncu) from a `full` summary file."""
+    import re
+    t = json.load(open(traffic))
+    out, cur = {}, None
+    for line in open(summary):
+        m = re.match(r"\[\d+\] .*?(desc_kernel|walk_kernel|fill_kernel)", line)
+        if m:
+            cur = out.setdefault(m.group(1), {}) if m.group(1) not in out else None
+            continue
+        if cur is None or not line.startswith("    "):
+            continue
+        k, _, v = line.strip().partition(": ")
+        if k.startswith("pipes"):
+            cur["pipes_pct"] = {p.split()[0]: float(p.split()[1]) for p in v.split(", ")}
+            continue
+        num = re.match(r"([\d.,e+]+)\s*(\S*)", v)
+        if not num:
+            continue
+        x, unit = float(num.group(1).replace(",", "")), num.group(2)
+        if k == "Duration":
+            cur["duration_ms"] = x * {"us": 1e-3, "ms": 1.0, "s": 1e3}.get(unit, 1.0)
+        elif k == "L2 Hit Rate":
+            cur["l2_hit_pct"] = x
+        elif k == "Issue Slots Busy":
+            cur["issue_slots_busy_pct"] = x
+        elif k == "Executed Ipc Active":
+            cur["ipc"] = x
+        elif k == "Achieved Occupancy":
+            cur["occupancy_pct"] = x
+        elif k.startswith("dram bytes"):
+            cur["dram_bytes"] = x
+    for d in out.values():
+        if "dram_bytes" in d and d.get("duration_ms"):
+            d["dram_GBps"] = d["dram_bytes"] / d["duration_ms"] / 1e6
+    out["source"] = summary
+    t["ncu"] = out
+    json.dump(t, open(traffic, "w"), indent=1)
+    print(json.dumps(out, indent=1))
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "headline":
+        headline(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         full(*sys.argv[2:])
