@@ -1694,9 +1694,11 @@ __global__ void __launch_bounds__(kWalkThreads, BT_WALK_MIN_BLOCKS) walk_kernel(
 // Fill pass (A13, Alg. 2 "Add q to NeighborsOf(p)" P:294): replay the
 // recorded masks into the CSR rows.  (Bounded by the DRAM cost of writing
 // rows at random CSR positions: tools/probe_csr.py measured a plain
-// warp-per-row writer of the same rows at 8.7 ms of this pass's 11.1 ms at
-// cfg 5; fewer instructions per mask word did not
-// shorten it.)  Per unit, rounds
+// warp-per-row writer of the same rows at 8.7 ms of this pass's 10.7 ms at
+// cfg 5; POPC runs on the quarter-rate XU pipe, which
+// ncu had at 71 % of its peak with four POPC per mask word -- hence the
+// per-round prefix packs below; fewer ALU instructions per mask word did not
+// shorten it in caller order.)  Per unit, rounds
 // of up to kFillChunks (6) chunks: the chunks' candidate indices in registers (chunk k,
 // lane l -> slots 64k + l, 64k + 32 + l), their masks in shared memory; for
 // each (query, chunk) mask word __popc(mask & lanemask_lt) gives each
