@@ -47,7 +47,10 @@ constexpr int kWalkThreads = 128;
 #define BT_FILL_THREADS 256
 #endif
 constexpr int kFillThreads = BT_FILL_THREADS;
-constexpr int kFillChunks = 6;   // 64-candidate chunks per fill round (measured: 4 -> 6 is 4 % faster at cfg 5, 7 slower)
+#ifndef BT_FILL_CHUNKS
+#define BT_FILL_CHUNKS 6
+#endif
+constexpr int kFillChunks = BT_FILL_CHUNKS;   // 64-candidate chunks per fill round (cfg 5 fill, with the prefix packs: 4 chunks 11.45 ms, 5 11.84, 6 10.66, 8 11.04)
 constexpr long long kListSlab = 8192;     // leaf-list entries per warp allocation
 constexpr long long kListReserve = 2048;  // more candidate leaves -> big-unit pass
 constexpr long long kCandSlab = 16384;    // candidate slots per warp allocation
